@@ -1,0 +1,11 @@
+"""B200-native BDDC-preconditioned CG (arXiv 2410.14786 hot path).
+
+Host C++ setup + hand-written sm_100a CUDA kernels behind the C-ABI in
+include/bddc_b200.h; this package is the thin Python mirror of the reference API.
+"""
+from ._lib import BddcError, InvalidArgument, OutOfRange, lib  # noqa: F401
+from .solver import (HostSetup, Preconditioner, Problem, SolveReport, SolverOptions,  # noqa: F401
+                     pcg)
+
+__all__ = ["Problem", "Preconditioner", "HostSetup", "SolverOptions", "SolveReport", "pcg",
+           "BddcError", "InvalidArgument", "OutOfRange", "lib"]

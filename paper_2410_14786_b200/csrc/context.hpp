@@ -1,0 +1,97 @@
+// Device context: owns the uploaded device image, scratch vectors and the stream;
+// runs the BDDC apply and the device-resident PCG loop. No CUDA types leak out of
+// this header (the C-ABI layer in capi.cpp includes it from plain C++).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "host/problem.hpp"
+#include "host/setup.hpp"
+
+namespace bddc_b200 {
+
+struct GpuOptions {
+    int device = 0;
+    int workers = 0;              // host setup threads (0 = hardware concurrency)
+    int coarse_mode = 0;          // 0: dense replicated A_c^{-1}; 1: reference-faithful coarse CG
+    double coarse_rtol = 1e-12;   // reference preconditioner.hpp:42
+    double coarse_atol = 0.0;
+    int coarse_max_iterations = 500;
+    int leaf_size = 16;
+    int local_blocks = 4;         // CTAs per subdomain for the K_i GEMV
+    bool profile = false;         // record per-kernel CUDA events in apply()
+};
+
+struct SolverOpts {
+    double rel_tolerance = 1e-8;
+    double abs_tolerance = 0.0;
+    int max_iterations = 1000;
+    bool record_history = false;
+};
+
+struct SolveResult {
+    int iterations = 0;
+    double final_relative_residual = 0.0;
+    std::vector<double> history;
+    std::optional<double> condition_estimate;
+    bool converged = false;
+};
+
+struct ProblemData {
+    Decomposition decomposition;
+    ConstraintSet constraints;
+    CsrMatrix global_matrix;
+    std::vector<CsrMatrix> local_matrices;
+    std::vector<index_t> coords;  // optional (empty => graph ordering)
+};
+
+struct KernelTimes {
+    double interior_ms = 0.0;   // both interior solves
+    double iface_ms = 0.0;      // restrict + coarse + local
+    double apply_ms = 0.0;
+    std::int64_t applies = 0;
+};
+
+enum class Stage : int { interior = 0, coarse = 1, local = 2, static_condensation = 3 };
+
+class GpuContext {
+public:
+    GpuContext(ProblemData problem, const GpuOptions& opt);
+    ~GpuContext();
+    GpuContext(const GpuContext&) = delete;
+    GpuContext& operator=(const GpuContext&) = delete;
+
+    index_t n() const;
+    // Device pointers (n doubles each) on the context's device; stream may be null.
+    void apply_device(const double* r, double* z, void* stream);
+    void apply_host(const double* r, double* z);
+    SolveResult pcg_host(const double* b, const SolverOpts& o, double* x, bool precondition);
+    SolveResult pcg_device(const double* b, const SolverOpts& o, double* x, bool precondition,
+                           void* stream);
+    void stage_host(Stage st, const double* in0, const double* in1, const double* in2, double* out);
+
+    const BddcSetup& setup() const;
+    const ProblemData& problem() const;
+    double setup_seconds() const;
+    std::int64_t apply_bytes() const;       // algorithmic FP64 bytes per apply
+    std::int64_t interior_pass_bytes() const;  // bytes of one interior solve (fwd + bwd)
+    std::int64_t factor_values() const;
+    KernelTimes kernel_times() const;
+    void reset_kernel_times();
+    void set_profile(bool on);
+    int device() const;
+    void synchronize();
+
+private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+};
+
+std::optional<double> condition_estimate(const std::vector<double>& alphas,
+                                         const std::vector<double>& betas);
+
+}  // namespace bddc_b200

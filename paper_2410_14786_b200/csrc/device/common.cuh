@@ -1,0 +1,55 @@
+// Shared device helpers for the sm_100a BDDC kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../device_format.hpp"
+
+namespace bddc_b200 {
+
+#define BDDC_CUDA(call)                                                                        \
+    do {                                                                                       \
+        cudaError_t err__ = (call);                                                            \
+        if (err__ != cudaSuccess)                                                              \
+            throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(err__) + \
+                                     " at " + __FILE__ + ":" + std::to_string(__LINE__));      \
+    } while (0)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum (fixed tree); all threads receive the result.
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* scratch /* THREADS/32 */) {
+    v = warp_sum(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = lane < THREADS / 32 ? scratch[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) scratch[0] = t;
+    }
+    __syncthreads();
+    t = scratch[0];
+    __syncthreads();
+    return t;
+}
+
+// Streaming (read-once) global load: non-coherent path, no L1 allocation.
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+}  // namespace bddc_b200

@@ -1,0 +1,542 @@
+// GpuContext: uploads the device image and orchestrates the apply / PCG on one B200.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <thread>
+
+#include "../context.hpp"
+#include "../host/program.hpp"
+#include "iface.cuh"
+#include "pcg.cuh"
+#include "solve.cuh"
+
+namespace bddc_b200 {
+namespace {
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { if (p) cudaFree(p); }
+    void alloc(std::size_t count) {
+        if (p) { cudaFree(p); p = nullptr; }
+        n = count;
+        if (count) BDDC_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void upload(const std::vector<T>& v) {
+        alloc(std::max<std::size_t>(v.size(), 1));
+        if (!v.empty()) BDDC_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    }
+};
+
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { BDDC_CUDA(cudaEventCreate(&e)); }
+    ~Event() { if (e) cudaEventDestroy(e); }
+};
+
+void ensure_finite(const double* x, index_t n, const char* context) {
+    for (index_t i = 0; i < n; ++i)
+        if (!std::isfinite(x[i]))
+            throw std::invalid_argument(std::string(context) + ": non-finite entry at index " +
+                                        std::to_string(i));
+}
+
+// pcg.cpp:21-36
+void sampled_symmetry_check(const CsrMatrix& A) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("pcg: matrix must be square");
+    const index_t stride = std::max<index_t>(1, A.nrows / 16);
+    for (index_t i = 0; i < A.nrows; i += stride) {
+        if (A.row_offsets[i] == A.row_offsets[i + 1]) continue;
+        const index_t p = A.row_offsets[i];
+        const index_t j = A.col_indices[p];
+        const double a = A.values[p];
+        double b = 0.0;
+        for (index_t q = A.row_offsets[j]; q < A.row_offsets[j + 1]; ++q)
+            if (A.col_indices[q] == i) { b = A.values[q]; break; }
+        if (std::abs(a - b) > 1e-12 * (std::abs(a) + std::abs(b)) + 1e-300)
+            throw std::invalid_argument("pcg: matrix is not symmetric");
+    }
+}
+
+}  // namespace
+
+struct GpuContext::Impl {
+    ProblemData pb;
+    GpuOptions opt;
+    BddcSetup setup;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;  // apply() is const-callable concurrently in the reference; serialise here
+
+    // image
+    DBuf<SubdomainDesc> subs;
+    DBuf<double> stream_data;
+    DBuf<TileTask> tasks;
+    DBuf<std::int32_t> phases, idx, gmap, couple_ptr, couple_gamma, iface_dof, iface_gid,
+        iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col, gi_own_ptr, gi_own_ref,
+        c_own_ptr, c_own_ref;
+    DBuf<double> couple_val, iface_w, kmat, phig, phi, gi_row_val, coarse_inv;
+    // global matrix
+    DBuf<std::int32_t> A_ptr, A_col;
+    DBuf<double> A_val;
+    // scratch
+    DBuf<double> U, gbuf, hbuf, cbuf, xc, vin, vout, vtmp, vtmp2;
+    // pcg
+    DBuf<double> x, r, z, p, q, part_a, part_b, rho, alpha, beta, hist, scal;
+    DBuf<int> flag;
+    double* pinned = nullptr;  // host mirror of scal
+    int max_it_alloc = 0;
+
+    std::int32_t max_interior = 0, max_iface = 0, max_primal = 0, n_coarse = 0;
+    std::size_t solve_smem = 0;
+    std::int64_t fwd_values = 0, bwd_values = 0, factor_vals = 0;
+    std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0, n_iface_total = 0;
+
+    KernelTimes times;
+    Event ev[6];
+
+    SolveParams solve_params(const double* in, double* out) const {
+        SolveParams P{};
+        P.subs = subs.p;
+        P.first_subdomain = 0;
+        P.stream = stream_data.p;
+        P.tasks = tasks.p;
+        P.phases = phases.p;
+        P.idx = idx.p;
+        P.gmap = gmap.p;
+        P.couple_ptr = couple_ptr.p;
+        P.couple_gamma = couple_gamma.p;
+        P.couple_val = couple_val.p;
+        P.iface_gid = iface_gid.p;
+        P.iface_dof = iface_dof.p;
+        P.iface_writer = iface_writer.p;
+        P.gi_own_ptr = gi_own_ptr.p;
+        P.gi_own_ref = gi_own_ref.p;
+        P.hbuf = hbuf.p;
+        P.in = in;
+        P.out = out;
+        return P;
+    }
+
+    IfaceParams iface_params() const {
+        IfaceParams P{};
+        P.subs = subs.p;
+        P.n_subdomains = pb.decomposition.n_subdomains;
+        P.max_iface = max_iface;
+        P.max_primal = max_primal;
+        P.iface_dof = iface_dof.p;
+        P.iface_w = iface_w.p;
+        P.iface_gid = iface_gid.p;
+        P.gi_row_ptr = gi_row_ptr.p;
+        P.gi_row_col = gi_row_col.p;
+        P.gi_row_val = gi_row_val.p;
+        P.kmat = kmat.p;
+        P.phig = phig.p;
+        P.primal = primal.p;
+        P.n_coarse = n_coarse;
+        P.c_own_ptr = c_own_ptr.p;
+        P.c_own_ref = c_own_ref.p;
+        P.coarse_inv = coarse_inv.p;
+        P.gbuf = gbuf.p;
+        P.hbuf = hbuf.p;
+        P.cbuf = cbuf.p;
+        P.xc = xc.p;
+        return P;
+    }
+
+    void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
+        const int nsub = pb.decomposition.n_subdomains;
+        const bool prof = opt.profile;
+        if (prof) BDDC_CUDA(cudaEventRecord(ev[0].e, s));
+        launch_interior_solve(solve_params(r_dev, U.p), 0, nsub, solve_smem, s);
+        if (prof) BDDC_CUDA(cudaEventRecord(ev[1].e, s));
+        const IfaceParams ip = iface_params();
+        launch_iface_restrict(ip, r_dev, U.p, s);
+        if (opt.coarse_mode == 0) launch_coarse_direct(ip, s);
+        else throw std::runtime_error("coarse CG mode not available in this build");
+        launch_iface_local(ip, opt.local_blocks, s);
+        if (prof) BDDC_CUDA(cudaEventRecord(ev[2].e, s));
+        launch_interior_solve(solve_params(r_dev, z_dev), 1, nsub, solve_smem, s);
+        if (prof) {
+            BDDC_CUDA(cudaEventRecord(ev[3].e, s));
+            BDDC_CUDA(cudaEventSynchronize(ev[3].e));
+            float a = 0, b = 0, c = 0, t = 0;
+            BDDC_CUDA(cudaEventElapsedTime(&a, ev[0].e, ev[1].e));
+            BDDC_CUDA(cudaEventElapsedTime(&b, ev[1].e, ev[2].e));
+            BDDC_CUDA(cudaEventElapsedTime(&c, ev[2].e, ev[3].e));
+            BDDC_CUDA(cudaEventElapsedTime(&t, ev[0].e, ev[3].e));
+            times.interior_ms += a + c;
+            times.iface_ms += b;
+            times.apply_ms += t;
+            times.applies += 1;
+        }
+    }
+
+    void ensure_pcg(int max_it) {
+        const index_t n = pb.decomposition.global_dofs;
+        if (!x.p) {
+            for (DBuf<double>* b : {&x, &r, &z, &p, &q}) b->alloc(n);
+            const int g = pcg_grid_for(n);
+            part_a.alloc(g);
+            part_b.alloc(g);
+            scal.alloc(8);
+            BDDC_CUDA(cudaMallocHost(&pinned, sizeof(double) * 8));
+        }
+        if (max_it > max_it_alloc) {
+            rho.alloc(max_it + 1);
+            alpha.alloc(max_it);
+            beta.alloc(max_it);
+            hist.alloc(max_it + 1);
+            max_it_alloc = max_it;
+        }
+    }
+
+    PcgDevice pcg_device(const SolverOpts& o, double* xd, double* rd, double* zd) const {
+        PcgDevice D{};
+        D.n = pb.decomposition.global_dofs;
+        D.grid = pcg_grid_for(D.n);
+        D.A_ptr = A_ptr.p;
+        D.A_col = A_col.p;
+        D.A_val = A_val.p;
+        D.x = xd;
+        D.r = rd;
+        D.z = zd;
+        D.p = p.p;
+        D.q = q.p;
+        D.part_a = part_a.p;
+        D.part_b = part_b.p;
+        D.rho = rho.p;
+        D.alpha = alpha.p;
+        D.beta = beta.p;
+        D.hist = hist.p;
+        D.scal = scal.p;
+        D.rtol = o.rel_tolerance;
+        D.atol = o.abs_tolerance;
+        return D;
+    }
+
+    // pcg.cpp:40-109 with every vector on the device; b and x are device pointers.
+    SolveResult pcg(const double* b, const SolverOpts& o, double* xout, bool precondition,
+                    cudaStream_t s) {
+        if (!(o.rel_tolerance > 0.0) || o.abs_tolerance < 0.0)
+            throw std::invalid_argument("pcg: tolerances must be positive");
+        if (o.max_iterations < 1) throw std::invalid_argument("pcg: max_iterations must be at least 1");
+        sampled_symmetry_check(pb.global_matrix);
+        const index_t n = pb.decomposition.global_dofs;
+        ensure_pcg(o.max_iterations);
+        SolveResult rep;
+        double* xd = xout;
+        double* rd = r.p;
+        double* zd = precondition ? z.p : r.p;
+        PcgDevice D = pcg_device(o, xd, rd, zd);
+        BDDC_CUDA(cudaMemsetAsync(xd, 0, sizeof(double) * n, s));
+        BDDC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(double) * 8, s));
+        BDDC_CUDA(cudaMemcpyAsync(rd, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        pcg_dot(D, b, b, part_b.p, s);
+        pcg_finalize(D, part_b.p, 0, true, s);
+        BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        const double normb = pinned[0];
+        if (!std::isfinite(normb)) {
+            int* idxd = nullptr;
+            BDDC_CUDA(cudaMalloc(&idxd, sizeof(int)));
+            device_first_nonfinite(n, b, idxd, s);
+            int bad = 0;
+            BDDC_CUDA(cudaMemcpyAsync(&bad, idxd, sizeof(int), cudaMemcpyDeviceToHost, s));
+            BDDC_CUDA(cudaStreamSynchronize(s));
+            cudaFree(idxd);
+            throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(bad));
+        }
+        if (o.record_history) rep.history.push_back(1.0);
+        if (normb == 0.0) {
+            rep.converged = true;
+            return rep;
+        }
+        if (precondition) apply(rd, zd, s);
+        pcg_dot(D, rd, zd, part_a.p, s);
+        pcg_init_rho(D, s);
+        int it = 1;
+        double rel = 1.0;
+        for (; it <= o.max_iterations; ++it) {
+            pcg_spmv_dot(D, s);
+            pcg_update(D, it, s);
+            pcg_check(D, it, s);
+            BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+            BDDC_CUDA(cudaStreamSynchronize(s));
+            if (pinned[3] == 1.0) throw std::runtime_error("matrix not SPD");
+            if (pinned[3] == 2.0) throw std::invalid_argument("bddc apply: non-finite entry in residual");
+            rel = pinned[1];
+            rep.iterations = it;
+            if (pinned[2] != 0.0) { rep.converged = true; break; }
+            if (it == o.max_iterations) break;
+            if (precondition) apply(rd, zd, s);
+            pcg_dot(D, rd, zd, part_a.p, s);
+            pcg_xpay(D, it, s);
+        }
+        rep.final_relative_residual = rel;
+        const int k = rep.iterations;
+        std::vector<double> al(k), be(std::max(0, k - 1));
+        if (k) BDDC_CUDA(cudaMemcpyAsync(al.data(), alpha.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        if (k > 1) BDDC_CUDA(cudaMemcpyAsync(be.data(), beta.p, sizeof(double) * (k - 1), cudaMemcpyDeviceToHost, s));
+        if (o.record_history && k) {
+            rep.history.resize(k + 1);
+            BDDC_CUDA(cudaMemcpyAsync(rep.history.data() + 1, hist.p + 1, sizeof(double) * k,
+                                      cudaMemcpyDeviceToHost, s));
+        }
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        rep.condition_estimate = condition_estimate(al, be);
+        return rep;
+    }
+};
+
+GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new Impl) {
+    Impl& I = *impl_;
+    I.pb = std::move(problem);
+    I.opt = opt;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
+    if (opt.device < 0 || opt.device >= ndev) throw std::invalid_argument("bad device index");
+    I.device = opt.device;
+    BDDC_CUDA(cudaSetDevice(I.device));
+    const Decomposition& d = I.pb.decomposition;
+    if (static_cast<index_t>(I.pb.local_matrices.size()) != d.n_subdomains ||
+        static_cast<index_t>(I.pb.constraints.constraint_matrices.size()) != d.n_subdomains)
+        throw std::invalid_argument("bddc setup: subdomain count mismatch");
+    const int workers = opt.workers > 0 ? opt.workers
+                                        : std::max(1u, std::thread::hardware_concurrency());
+    FactorOptions fo;
+    fo.leaf_size = opt.leaf_size;
+    I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints,
+                         I.pb.coords.empty() ? nullptr : I.pb.coords.data(), workers, fo);
+    const DeviceImage img = build_device_image(d, I.pb.constraints, I.pb.local_matrices,
+                                               I.pb.global_matrix, I.setup);
+    I.max_interior = img.max_interior;
+    I.max_iface = img.max_iface;
+    I.max_primal = img.max_primal;
+    I.n_coarse = img.n_coarse;
+    I.fwd_values = img.fwd_values;
+    I.bwd_values = img.bwd_values;
+    I.factor_vals = img.factor_values;
+    I.k_values = static_cast<std::int64_t>(img.kmat.size());
+    I.phig_values = static_cast<std::int64_t>(img.phig.size());
+    I.ginnz = static_cast<std::int64_t>(img.gi_row_val.size());
+    I.couple_nnz = static_cast<std::int64_t>(img.couple_val.size());
+    I.n_iface_total = static_cast<std::int64_t>(img.iface_dof.size());
+    I.solve_smem = interior_solve_smem(img.max_interior, img.max_iface);
+    int max_smem = 0;
+    BDDC_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, I.device));
+    if (I.solve_smem > static_cast<std::size_t>(max_smem))
+        throw std::runtime_error("subdomain interior (" + std::to_string(img.max_interior) +
+                                 " dofs) exceeds the shared-memory solve capacity");
+
+    BDDC_CUDA(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
+    {
+        std::vector<SubdomainDesc> subs = img.subs;
+        I.subs.alloc(subs.size());
+        BDDC_CUDA(cudaMemcpy(I.subs.p, subs.data(), sizeof(SubdomainDesc) * subs.size(), cudaMemcpyHostToDevice));
+    }
+    I.stream_data.upload(img.stream);
+    {
+        I.tasks.alloc(std::max<std::size_t>(img.tasks.size(), 1));
+        if (!img.tasks.empty())
+            BDDC_CUDA(cudaMemcpy(I.tasks.p, img.tasks.data(), sizeof(TileTask) * img.tasks.size(),
+                                 cudaMemcpyHostToDevice));
+    }
+    I.phases.upload(img.phases);
+    I.idx.upload(img.idx);
+    I.gmap.upload(img.gmap);
+    I.couple_ptr.upload(img.couple_ptr);
+    I.couple_gamma.upload(img.couple_gamma);
+    I.couple_val.upload(img.couple_val);
+    I.iface_dof.upload(img.iface_dof);
+    I.iface_w.upload(img.iface_w);
+    I.iface_gid.upload(img.iface_gid);
+    I.iface_writer.upload(img.iface_writer);
+    I.kmat.upload(img.kmat);
+    I.phig.upload(img.phig);
+    I.phi.upload(img.phi);
+    I.primal.upload(img.primal);
+    I.local_dofs.upload(img.local_dofs);
+    I.gi_dof.upload(img.gi_dof);
+    I.gi_row_ptr.upload(img.gi_row_ptr);
+    I.gi_row_col.upload(img.gi_row_col);
+    I.gi_row_val.upload(img.gi_row_val);
+    I.gi_own_ptr.upload(img.gi_own_ptr);
+    I.gi_own_ref.upload(img.gi_own_ref);
+    I.c_own_ptr.upload(img.c_own_ptr);
+    I.c_own_ref.upload(img.c_own_ref);
+    I.coarse_inv.upload(img.coarse_inv);
+    I.A_ptr.upload(I.pb.global_matrix.row_offsets);
+    I.A_col.upload(I.pb.global_matrix.col_indices);
+    I.A_val.upload(I.pb.global_matrix.values);
+    const std::size_t n = d.global_dofs;
+    I.U.alloc(n);
+    BDDC_CUDA(cudaMemset(I.U.p, 0, sizeof(double) * n));
+    I.gbuf.alloc(std::max<std::int64_t>(img.hbuf_total, 1));
+    I.hbuf.alloc(std::max<std::int64_t>(img.hbuf_total, 1));
+    I.cbuf.alloc(std::max<std::int64_t>(img.cbuf_total, 1));
+    I.xc.alloc(std::max(img.n_coarse, 1));
+    I.vin.alloc(n);
+    I.vout.alloc(n);
+    I.vtmp.alloc(n);
+    I.vtmp2.alloc(n);
+    BDDC_CUDA(cudaDeviceSynchronize());
+}
+
+GpuContext::~GpuContext() {
+    if (impl_) {
+        cudaSetDevice(impl_->device);
+        if (impl_->pinned) cudaFreeHost(impl_->pinned);
+        if (impl_->stream) cudaStreamDestroy(impl_->stream);
+    }
+}
+
+index_t GpuContext::n() const { return impl_->pb.decomposition.global_dofs; }
+
+void GpuContext::apply_device(const double* r, double* z, void* stream) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    BDDC_CUDA(cudaSetDevice(impl_->device));
+    impl_->apply(r, z, stream ? static_cast<cudaStream_t>(stream) : impl_->stream);
+}
+
+void GpuContext::apply_host(const double* r, double* z) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    Impl& I = *impl_;
+    const index_t n = I.pb.decomposition.global_dofs;
+    ensure_finite(r, n, "bddc apply");
+    BDDC_CUDA(cudaSetDevice(I.device));
+    BDDC_CUDA(cudaMemcpyAsync(I.vin.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+    I.apply(I.vin.p, I.vout.p, I.stream);
+    BDDC_CUDA(cudaMemcpyAsync(z, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, I.stream));
+    BDDC_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x, bool precondition) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    Impl& I = *impl_;
+    const index_t n = I.pb.decomposition.global_dofs;
+    ensure_finite(b, n, "pcg rhs");
+    BDDC_CUDA(cudaSetDevice(I.device));
+    BDDC_CUDA(cudaMemcpyAsync(I.vin.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+    SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);
+    BDDC_CUDA(cudaMemcpyAsync(x, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, I.stream));
+    BDDC_CUDA(cudaStreamSynchronize(I.stream));
+    return rep;
+}
+
+SolveResult GpuContext::pcg_device(const double* b, const SolverOpts& o, double* x, bool precondition,
+                                   void* stream) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    BDDC_CUDA(cudaSetDevice(impl_->device));
+    return impl_->pcg(b, o, x, precondition, stream ? static_cast<cudaStream_t>(stream) : impl_->stream);
+}
+
+void GpuContext::stage_host(Stage st, const double* in0, const double* in1, const double* in2,
+                            double* out) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    Impl& I = *impl_;
+    const index_t n = I.pb.decomposition.global_dofs;
+    BDDC_CUDA(cudaSetDevice(I.device));
+    cudaStream_t s = I.stream;
+    const int nsub = I.pb.decomposition.n_subdomains;
+    switch (st) {
+        case Stage::interior:
+            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+            BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
+            launch_interior_solve(I.solve_params(I.vin.p, I.vout.p), 0, nsub, I.solve_smem, s);
+            break;
+        case Stage::static_condensation: {
+            // interior_correction(r - A (v1 + v2))  (preconditioner.cpp:215-223)
+            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in1, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+            BDDC_CUDA(cudaMemcpyAsync(I.vtmp.p, in2, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+            device_axpby(n, 1.0, I.vin.p, 1.0, I.vtmp.p, I.vtmp2.p, s);
+            device_spmv(n, I.A_ptr.p, I.A_col.p, I.A_val.p, I.vtmp2.p, I.vtmp.p, s);
+            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+            device_axpby(n, 1.0, I.vin.p, -1.0, I.vtmp.p, I.vtmp2.p, s);
+            BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
+            launch_interior_solve(I.solve_params(I.vtmp2.p, I.vout.p), 0, nsub, I.solve_smem, s);
+            break;
+        }
+        default:
+            throw std::invalid_argument("stage not available in this build");
+    }
+    BDDC_CUDA(cudaMemcpyAsync(out, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    BDDC_CUDA(cudaStreamSynchronize(s));
+}
+
+const BddcSetup& GpuContext::setup() const { return impl_->setup; }
+const ProblemData& GpuContext::problem() const { return impl_->pb; }
+double GpuContext::setup_seconds() const { return impl_->setup.seconds; }
+std::int64_t GpuContext::factor_values() const { return impl_->factor_vals; }
+std::int64_t GpuContext::interior_pass_bytes() const {
+    return 8 * (impl_->fwd_values + impl_->bwd_values);
+}
+std::int64_t GpuContext::apply_bytes() const {
+    const Impl& I = *impl_;
+    const std::int64_t n = I.pb.decomposition.global_dofs;
+    // 2 interior solves + K_i + Phi_G (x2: restrict and prolong) + coarse inverse
+    // + interface rows/coupling + vector traffic (r read twice, z written once, u0 once)
+    return 2 * interior_pass_bytes() + 8 * (I.k_values + 2 * I.phig_values +
+                                            static_cast<std::int64_t>(I.n_coarse) * I.n_coarse +
+                                            I.ginnz + I.couple_nnz + 4 * n);
+}
+KernelTimes GpuContext::kernel_times() const { return impl_->times; }
+void GpuContext::reset_kernel_times() { impl_->times = KernelTimes{}; }
+void GpuContext::set_profile(bool on) { impl_->opt.profile = on; }
+int GpuContext::device() const { return impl_->device; }
+void GpuContext::synchronize() { BDDC_CUDA(cudaStreamSynchronize(impl_->stream)); }
+
+// pcg.cpp:111-173 (host; O(iterations))
+std::optional<double> condition_estimate(const std::vector<double>& alphas,
+                                         const std::vector<double>& betas) {
+    const std::size_t k = alphas.size();
+    if (k < 2 || betas.size() + 1 < k) return std::nullopt;
+    std::vector<double> diag(k), off(k - 1);
+    for (std::size_t i = 0; i < k; ++i) {
+        diag[i] = 1.0 / alphas[i];
+        if (i > 0) diag[i] += betas[i - 1] / alphas[i - 1];
+        if (i + 1 < k) off[i] = std::sqrt(betas[i]) / alphas[i];
+    }
+    const std::size_t n = k;
+    double lo = diag[0], hi = diag[0];
+    for (std::size_t i = 0; i < n; ++i) {
+        double radius = 0.0;
+        if (i > 0) radius += std::abs(off[i - 1]);
+        if (i + 1 < n) radius += std::abs(off[i]);
+        lo = std::min(lo, diag[i] - radius);
+        hi = std::max(hi, diag[i] + radius);
+    }
+    auto count_below = [&](double x) {
+        std::size_t count = 0;
+        double qv = 1.0;
+        for (std::size_t i = 0; i < n; ++i) {
+            const double off2 = i > 0 ? off[i - 1] * off[i - 1] : 0.0;
+            qv = diag[i] - x - off2 / qv;
+            if (qv == 0.0) qv = 1e-300;
+            if (qv < 0.0) ++count;
+        }
+        return count;
+    };
+    auto bisect = [&](std::size_t target) {
+        double a = lo, b = hi;
+        for (int step = 0; step < 200 && b - a > 1e-15 * std::max(1.0, std::abs(b)); ++step) {
+            const double mid = 0.5 * (a + b);
+            if (count_below(mid) >= target) b = mid;
+            else a = mid;
+        }
+        return 0.5 * (a + b);
+    };
+    const double l = bisect(1), h = bisect(n);
+    if (!(l > 0.0)) return std::nullopt;
+    return h / l;
+}
+
+}  // namespace bddc_b200

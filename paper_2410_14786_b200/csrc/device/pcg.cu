@@ -1,0 +1,171 @@
+// PCG vector kernels (reference src/pcg.cpp:40-109): SpMV fused with p.q, the
+// x/r update fused with ||r||^2, deterministic grid-partial reductions.
+#include "pcg.cuh"
+
+namespace bddc_b200 {
+namespace {
+
+__device__ __forceinline__ double sum_partials(const double* part, int n, double* scratch) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
+    return block_sum<kVecThreads>(v, scratch);
+}
+
+__global__ void __launch_bounds__(kVecThreads) dot_kernel(int n, const double* __restrict__ a,
+                                                          const double* __restrict__ b, double* part) {
+    __shared__ double scratch[kVecThreads / 32];
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        acc = fma(a[i], b[i], acc);
+    acc = block_sum<kVecThreads>(acc, scratch);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kVecThreads) finalize_kernel(const double* part, int n, double* out,
+                                                               int take_sqrt) {
+    __shared__ double scratch[kVecThreads / 32];
+    const double v = sum_partials(part, n, scratch);
+    if (threadIdx.x == 0) *out = take_sqrt ? sqrt(v) : v;
+}
+
+__global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D) {
+    __shared__ double scratch[kVecThreads / 32];
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+        double y = 0.0;
+        for (int e = D.A_ptr[i]; e < D.A_ptr[i + 1]; ++e) y += D.A_val[e] * D.p[D.A_col[e]];
+        D.q[i] = y;
+        acc = fma(D.p[i], y, acc);
+    }
+    acc = block_sum<kVecThreads>(acc, scratch);
+    if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int it) {
+    __shared__ double scratch[kVecThreads / 32];
+    const double pq = sum_partials(D.part_a, D.grid, scratch);
+    if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
+        if (blockIdx.x == 0 && threadIdx.x == 0) D.scal[3] = 1.0;
+        return;
+    }
+    const double alpha = D.rho[it - 1] / pq;
+    if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[it - 1] = alpha;
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+        D.x[i] += alpha * D.p[i];
+        const double ri = D.r[i] - alpha * D.q[i];
+        D.r[i] = ri;
+        acc = fma(ri, ri, acc);
+    }
+    acc = block_sum<kVecThreads>(acc, scratch);
+    if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int it) {
+    __shared__ double scratch[kVecThreads / 32];
+    if (D.scal[3] != 0.0) return;
+    const double rr = sum_partials(D.part_b, D.grid, scratch);
+    if (threadIdx.x == 0) {
+        const double normb = D.scal[0];
+        const double rel = sqrt(rr) / normb;
+        D.hist[it] = rel;
+        D.scal[1] = rel;
+        if (!isfinite(rel)) D.scal[3] = 2.0;
+        if (rel <= D.rtol || (D.atol > 0.0 && rel * normb <= D.atol)) D.scal[2] = 1.0;
+    }
+}
+
+__global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {
+    __shared__ double scratch[kVecThreads / 32];
+    const double rz = sum_partials(D.part_a, D.grid, scratch);
+    if (blockIdx.x == 0 && threadIdx.x == 0) D.rho[0] = rz;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+        D.p[i] = D.z[i];
+}
+
+__global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int it) {
+    __shared__ double scratch[kVecThreads / 32];
+    const double rz = sum_partials(D.part_a, D.grid, scratch);
+    const double beta = rz / D.rho[it - 1];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+        D.p[i] = D.z[i] + beta * D.p[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        D.beta[it - 1] = beta;
+        D.rho[it] = rz;
+    }
+}
+
+__global__ void __launch_bounds__(kVecThreads) spmv_kernel(int n, const std::int32_t* __restrict__ ptr,
+                                                           const std::int32_t* __restrict__ col,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ x, double* y) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int e = ptr[i]; e < ptr[i + 1]; ++e) acc += val[e] * x[col[e]];
+        y[i] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(kVecThreads) axpby_kernel(int n, double a, const double* x, double b,
+                                                            const double* y, double* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = a * x[i] + b * y[i];
+}
+
+__global__ void __launch_bounds__(kVecThreads) nonfinite_kernel(int n, const double* x, int* res) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) atomicMin(res, i);
+}
+
+int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecThreads, 148 * 8)); }
+
+}  // namespace
+
+void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s) {
+    dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D.n, a, b, part);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s) {
+    finalize_kernel<<<1, kVecThreads, 0, s>>>(part, D.grid, D.scal + slot, take_sqrt ? 1 : 0);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
+    spmv_dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_update(const PcgDevice& D, int it, cudaStream_t s) {
+    update_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_check(const PcgDevice& D, int it, cudaStream_t s) {
+    check_kernel<<<1, kVecThreads, 0, s>>>(D, it);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_init_rho(const PcgDevice& D, cudaStream_t s) {
+    init_rho_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    BDDC_CUDA(cudaGetLastError());
+}
+void pcg_xpay(const PcgDevice& D, int it, cudaStream_t s) {
+    xpay_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
+    BDDC_CUDA(cudaGetLastError());
+}
+void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
+                 const double* x, double* y, cudaStream_t s) {
+    spmv_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, x, y);
+    BDDC_CUDA(cudaGetLastError());
+}
+void device_axpby(int n, double a, const double* x, double b, const double* y, double* out,
+                  cudaStream_t s) {
+    axpby_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, a, x, b, y, out);
+    BDDC_CUDA(cudaGetLastError());
+}
+void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_t s) {
+    const int init = 0x7fffffff;
+    BDDC_CUDA(cudaMemcpyAsync(dev_result, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+    nonfinite_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, x, dev_result);
+    BDDC_CUDA(cudaGetLastError());
+}
+
+int pcg_grid_for(int n) { return vec_grid(n); }
+
+}  // namespace bddc_b200

@@ -1,0 +1,48 @@
+#pragma once
+
+#include "common.cuh"
+
+namespace bddc_b200 {
+
+// Device-resident CG state. Scalars live in device memory; kernels derive alpha/beta
+// from fixed-order partial sums, so results are deterministic run to run.
+struct PcgDevice {
+    int n;
+    int grid;                 // blocks of the vector kernels (fixed => fixed reduction order)
+    const std::int32_t* A_ptr;
+    const std::int32_t* A_col;
+    const double* A_val;
+    double* x;
+    double* r;
+    double* z;
+    double* p;
+    double* q;
+    double* part_a;   // grid partials
+    double* part_b;
+    double* rho;      // [max_it + 1]
+    double* alpha;    // [max_it]
+    double* beta;     // [max_it]
+    double* hist;     // [max_it + 1]
+    double* scal;     // [0]=||b||, [1]=rel, [2]=converged flag, [3]=error code
+    double rtol, atol;
+};
+
+constexpr int kVecThreads = 256;
+
+void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s);
+// scal[slot] = sqrt(sum part) (sqrt=true) or sum part
+void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s);
+void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s);           // q = A p ; part_a = p.q
+void pcg_update(const PcgDevice& D, int it, cudaStream_t s);     // x += a p ; r -= a q ; part_b = r.r
+void pcg_check(const PcgDevice& D, int it, cudaStream_t s);      // hist[it], converged flag
+void pcg_init_rho(const PcgDevice& D, cudaStream_t s);           // rho[0] = sum part_a ; p = z
+void pcg_xpay(const PcgDevice& D, int it, cudaStream_t s);       // beta from part_a ; p = z + beta p
+void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
+                 const double* x, double* y, cudaStream_t s);
+void device_axpby(int n, double a, const double* x, double b, const double* y, double* out,
+                  cudaStream_t s);  // out = a x + b y
+int pcg_grid_for(int n);
+// Smallest index of a non-finite entry, or -1 (writes to *dev_result).
+void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_t s);
+
+}  // namespace bddc_b200
