@@ -87,6 +87,7 @@ typedef struct {
     int32_t coarse_max_iterations; /* 500 */
     int32_t leaf_size;             /* nested-dissection leaf size (default 16) */
     int32_t local_blocks;          /* CTAs per subdomain for the K_i GEMV (default 4) */
+    int32_t solve_parts;           /* CTAs (cluster size) per subdomain in the interior solve: 0 auto, 1, 2 */
 } bddc_gpu_options;
 
 /* Reference SolverOptions (include/bddc/pcg.hpp:17-22). */
@@ -175,6 +176,10 @@ int bddc_gpu_get_stats(const bddc_gpu_ctx* ctx, bddc_stats* stats);
 int bddc_gpu_set_profile(bddc_gpu_ctx* ctx, int32_t on);
 int bddc_gpu_kernel_times(const bddc_gpu_ctx* ctx, bddc_kernel_times* times, int32_t reset);
 int bddc_gpu_synchronize(bddc_gpu_ctx* ctx);
+/* Diagnostics: per-CTA, per-warp cycle accounting {total, wait, barrier, units} of the last
+ * interior solve; only recorded when the context was created with BDDC_SOLVE_STATS set.
+ * Returns the number of int64 values written (0 when not recorded). */
+int64_t bddc_gpu_solve_profile(bddc_gpu_ctx* ctx, int64_t* out, int64_t capacity);
 const char* bddc_gpu_last_error(const bddc_gpu_ctx* ctx);
 void bddc_gpu_destroy(bddc_gpu_ctx* ctx);
 

@@ -47,7 +47,8 @@ class ProblemView(C.Structure):
 class GpuOptions(C.Structure):
     _fields_ = [("device", i32), ("workers", i32), ("coarse_mode", i32),
                 ("coarse_rel_tolerance", f64), ("coarse_abs_tolerance", f64),
-                ("coarse_max_iterations", i32), ("leaf_size", i32), ("local_blocks", i32)]
+                ("coarse_max_iterations", i32), ("leaf_size", i32), ("local_blocks", i32),
+                ("solve_parts", i32)]
 
 
 class SolverOptions(C.Structure):
@@ -100,6 +101,7 @@ SIGNATURES = {
     "bddc_gpu_set_profile": (C.c_int, [vp, i32]),
     "bddc_gpu_kernel_times": (C.c_int, [vp, P(KernelTimes), i32]),
     "bddc_gpu_synchronize": (C.c_int, [vp]),
+    "bddc_gpu_solve_profile": (i64, [vp, P(i64), i64]),
     "bddc_gpu_last_error": (C.c_char_p, [vp]),
     "bddc_gpu_destroy": (None, [vp]),
 }

@@ -153,6 +153,7 @@ GpuOptions to_gpu(const bddc_gpu_options* o) {
         g.coarse_max_iterations = o->coarse_max_iterations;
         if (o->leaf_size > 0) g.leaf_size = o->leaf_size;
         if (o->local_blocks > 0) g.local_blocks = o->local_blocks;
+        if (o->solve_parts > 0) g.solve_parts = o->solve_parts;
     }
     return g;
 }
@@ -187,6 +188,7 @@ void bddc_default_gpu_options(bddc_gpu_options* o) {
     o->coarse_max_iterations = 500;
     o->leaf_size = 16;
     o->local_blocks = 4;
+    o->solve_parts = 0;
 }
 
 void bddc_default_solver_options(bddc_solver_options* o) {
@@ -469,6 +471,15 @@ int bddc_gpu_synchronize(bddc_gpu_ctx* c) {
         if (!c) throw std::invalid_argument("null context");
         c->ctx->synchronize();
     }, c);
+}
+
+int64_t bddc_gpu_solve_profile(bddc_gpu_ctx* c, int64_t* out, int64_t cap) {
+    std::int64_t n = 0;
+    const int rc = guarded([&] {
+        if (!c || !out) throw std::invalid_argument("null argument");
+        n = c->ctx->solve_profile(out, cap);
+    }, c);
+    return rc == BDDC_OK ? n : -1;
 }
 
 const char* bddc_gpu_last_error(const bddc_gpu_ctx* c) { return c ? c->last_error.c_str() : g_last_error.c_str(); }

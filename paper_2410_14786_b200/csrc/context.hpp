@@ -23,6 +23,7 @@ struct GpuOptions {
     int coarse_max_iterations = 500;
     int leaf_size = 16;
     int local_blocks = 4;         // CTAs per subdomain for the K_i GEMV
+    int solve_parts = 0;          // CTAs per subdomain in the interior solve (0 = auto)
     bool profile = false;         // record per-kernel CUDA events in apply()
 };
 
@@ -78,13 +79,15 @@ public:
     const ProblemData& problem() const;
     double setup_seconds() const;
     std::int64_t apply_bytes() const;       // algorithmic FP64 bytes per apply
-    std::int64_t interior_pass_bytes() const;  // bytes of one interior solve (fwd + bwd)
+    std::int64_t interior_pass_bytes() const;  // stream bytes of one batched interior solve
+    int solve_parts() const;
     std::int64_t factor_values() const;
     KernelTimes kernel_times() const;
     void reset_kernel_times();
     void set_profile(bool on);
     int device() const;
     void synchronize();
+    std::int64_t solve_profile(std::int64_t* out, std::int64_t cap);
 
 private:
     struct Impl;

@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -44,8 +46,7 @@ struct Event {
 void ensure_finite(const double* x, index_t n, const char* context) {
     for (index_t i = 0; i < n; ++i)
         if (!std::isfinite(x[i]))
-            throw std::invalid_argument(std::string(context) + ": non-finite entry at index " +
-                                        std::to_string(i));
+            throw std::invalid_argument(std::string(context) + ": non-finite entry at index " + std::to_string(i));
 }
 
 // pcg.cpp:21-36
@@ -73,43 +74,47 @@ struct GpuContext::Impl {
     BddcSetup setup;
     int device = 0;
     cudaStream_t stream = nullptr;
-    std::mutex mu;  // apply() is const-callable concurrently in the reference; serialise here
+    std::mutex mu;  // the reference apply() is callable concurrently; serialise here
 
-    // image
+    // interior-solve program
+    DBuf<PartDesc> parts;
+    DBuf<double> sstream;
+    DBuf<std::int32_t> units;
+    DBuf<std::int32_t> phases, gmap, couple_ptr, couple_gamma;
+    DBuf<double> couple_val;
+    SolveLaunch launch;
+    // interface data
     DBuf<SubdomainDesc> subs;
-    DBuf<double> stream_data;
-    DBuf<TileTask> tasks;
-    DBuf<std::int32_t> phases, idx, gmap, couple_ptr, couple_gamma, iface_dof, iface_gid,
-        iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col, gi_own_ptr, gi_own_ref,
-        c_own_ptr, c_own_ref;
-    DBuf<double> couple_val, iface_w, kmat, phig, phi, gi_row_val, coarse_inv;
+    DBuf<std::int32_t> iface_dof, iface_gid, iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col,
+        gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col;
+    DBuf<double> iface_w, kmat, phig, phi, gi_row_val, coarse_inv, lrow_val, weights_local;
+    // coarse matrix (CG mode)
+    DBuf<std::int32_t> Ac_ptr, Ac_col;
+    DBuf<double> Ac_val, coarse_status;
     // global matrix
     DBuf<std::int32_t> A_ptr, A_col;
     DBuf<double> A_val;
     // scratch
-    DBuf<double> U, gbuf, hbuf, cbuf, xc, vin, vout, vtmp, vtmp2;
+    DBuf<double> U, gbuf, hbuf, cbuf, xc, lbuf, vin, vout, vtmp, vtmp2;
     // pcg
     DBuf<double> x, r, z, p, q, part_a, part_b, rho, alpha, beta, hist, scal;
-    DBuf<int> flag;
-    double* pinned = nullptr;  // host mirror of scal
+    double* pinned = nullptr;
     int max_it_alloc = 0;
 
-    std::int32_t max_interior = 0, max_iface = 0, max_primal = 0, n_coarse = 0;
-    std::size_t solve_smem = 0;
-    std::int64_t fwd_values = 0, bwd_values = 0, factor_vals = 0;
-    std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0, n_iface_total = 0;
+    std::int32_t max_iface = 0, max_primal = 0, n_coarse = 0, n_gi = 0;
+    std::int64_t solve_stream_bytes = 0, factor_vals = 0;
+    std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
-    Event ev[6];
+    Event ev[4];
 
     SolveParams solve_params(const double* in, double* out) const {
         SolveParams P{};
+        P.parts = parts.p;
         P.subs = subs.p;
-        P.first_subdomain = 0;
-        P.stream = stream_data.p;
-        P.tasks = tasks.p;
+        P.stream = sstream.p;
+        P.units = units.p;
         P.phases = phases.p;
-        P.idx = idx.p;
         P.gmap = gmap.p;
         P.couple_ptr = couple_ptr.p;
         P.couple_gamma = couple_gamma.p;
@@ -122,8 +127,18 @@ struct GpuContext::Impl {
         P.hbuf = hbuf.p;
         P.in = in;
         P.out = out;
+        P.max_loc = max_loc;
+        P.max_top = max_top;
+        P.max_iface = max_iface;
+        P.debug = debug_solve;
+        P.l2_ahead = l2_ahead;
+        P.dbg = dbg_buf.p;
         return P;
     }
+    std::int32_t max_loc = 0, max_top = 0;
+    int debug_solve = std::getenv("BDDC_DEBUG_SOLVE") ? std::atoi(std::getenv("BDDC_DEBUG_SOLVE")) : 0;
+    DBuf<long long> dbg_buf;
+    int l2_ahead = std::getenv("BDDC_L2_AHEAD") ? std::atoi(std::getenv("BDDC_L2_AHEAD")) : 6;
 
     IfaceParams iface_params() const {
         IfaceParams P{};
@@ -151,19 +166,78 @@ struct GpuContext::Impl {
         return P;
     }
 
+    StageParams stage_params() const {
+        StageParams P{};
+        P.subs = subs.p;
+        P.n_subdomains = pb.decomposition.n_subdomains;
+        P.n_vector = pb.decomposition.global_dofs;
+        P.max_primal = max_primal;
+        P.local_dofs = local_dofs.p;
+        P.phi = phi.p;
+        P.iface_w = iface_w.p;
+        P.iface_dof = iface_dof.p;
+        P.gi_dof = gi_dof.p;
+        P.n_gi = n_gi;
+        P.gi_own_ptr = gi_own_ptr.p;
+        P.gi_own_ref = gi_own_ref.p;
+        P.dof_own_ptr = dof_own_ptr.p;
+        P.dof_own_ref = dof_own_ref.p;
+        P.lrow_ptr = lrow_ptr.p;
+        P.lrow_col = lrow_col.p;
+        P.lrow_val = lrow_val.p;
+        P.primal = primal.p;
+        P.weights_local = weights_local.p;
+        P.lbuf = lbuf.p;
+        P.gbuf = gbuf.p;
+        P.cbuf = cbuf.p;
+        P.xc = xc.p;
+        return P;
+    }
+
+    void coarse_solve(cudaStream_t s) {
+        if (opt.coarse_mode == 0) {
+            launch_coarse_direct(iface_params(), s);
+        } else {
+            CoarseCgParams C{};
+            C.n = n_coarse;
+            C.ptr = Ac_ptr.p;
+            C.col = Ac_col.p;
+            C.val = Ac_val.p;
+            C.c_own_ptr = c_own_ptr.p;
+            C.c_own_ref = c_own_ref.p;
+            C.cbuf = cbuf.p;
+            C.xc = xc.p;
+            C.status = coarse_status.p;
+            C.rtol = opt.coarse_rtol;
+            C.atol = opt.coarse_atol;
+            C.max_it = opt.coarse_max_iterations;
+            launch_coarse_cg(C, s);
+        }
+    }
+
+    // Reference-faithful coarse CG: surface non-convergence like preconditioner.cpp:152-157.
+    void check_coarse(cudaStream_t s) {
+        if (opt.coarse_mode == 0) return;
+        double st[3];
+        BDDC_CUDA(cudaMemcpyAsync(st, coarse_status.p, sizeof st, cudaMemcpyDeviceToHost, s));
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        if (st[0] < 0) throw std::runtime_error("matrix not SPD");
+        if (st[2] == 0.0)
+            throw std::runtime_error("coarse CG did not converge: " + std::to_string(static_cast<int>(st[0])) +
+                                     " iterations, relative residual " + std::to_string(st[1]));
+    }
+
     void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
-        const int nsub = pb.decomposition.n_subdomains;
         const bool prof = opt.profile;
         if (prof) BDDC_CUDA(cudaEventRecord(ev[0].e, s));
-        launch_interior_solve(solve_params(r_dev, U.p), 0, nsub, solve_smem, s);
+        launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
         if (prof) BDDC_CUDA(cudaEventRecord(ev[1].e, s));
         const IfaceParams ip = iface_params();
         launch_iface_restrict(ip, r_dev, U.p, s);
-        if (opt.coarse_mode == 0) launch_coarse_direct(ip, s);
-        else throw std::runtime_error("coarse CG mode not available in this build");
-        launch_iface_local(ip, opt.local_blocks, s);
+        coarse_solve(s);
+        launch_iface_local(ip, opt.local_blocks, s, true);
         if (prof) BDDC_CUDA(cudaEventRecord(ev[2].e, s));
-        launch_interior_solve(solve_params(r_dev, z_dev), 1, nsub, solve_smem, s);
+        launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
         if (prof) {
             BDDC_CUDA(cudaEventRecord(ev[3].e, s));
             BDDC_CUDA(cudaEventSynchronize(ev[3].e));
@@ -223,8 +297,7 @@ struct GpuContext::Impl {
     }
 
     // pcg.cpp:40-109 with every vector on the device; b and x are device pointers.
-    SolveResult pcg(const double* b, const SolverOpts& o, double* xout, bool precondition,
-                    cudaStream_t s) {
+    SolveResult pcg(const double* b, const SolverOpts& o, double* xout, bool precondition, cudaStream_t s) {
         if (!(o.rel_tolerance > 0.0) || o.abs_tolerance < 0.0)
             throw std::invalid_argument("pcg: tolerances must be positive");
         if (o.max_iterations < 1) throw std::invalid_argument("pcg: max_iterations must be at least 1");
@@ -245,38 +318,50 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaStreamSynchronize(s));
         const double normb = pinned[0];
         if (!std::isfinite(normb)) {
-            int* idxd = nullptr;
-            BDDC_CUDA(cudaMalloc(&idxd, sizeof(int)));
-            device_first_nonfinite(n, b, idxd, s);
-            int bad = 0;
-            BDDC_CUDA(cudaMemcpyAsync(&bad, idxd, sizeof(int), cudaMemcpyDeviceToHost, s));
+            DBuf<int> bad;
+            bad.alloc(1);
+            device_first_nonfinite(n, b, bad.p, s);
+            int idx = 0;
+            BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             BDDC_CUDA(cudaStreamSynchronize(s));
-            cudaFree(idxd);
-            throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(bad));
+            throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(idx));
         }
         if (o.record_history) rep.history.push_back(1.0);
         if (normb == 0.0) {
             rep.converged = true;
             return rep;
         }
-        if (precondition) apply(rd, zd, s);
+        if (precondition) {
+            apply(rd, zd, s);
+            check_coarse(s);
+        }
         pcg_dot(D, rd, zd, part_a.p, s);
         pcg_init_rho(D, s);
-        int it = 1;
         double rel = 1.0;
-        for (; it <= o.max_iterations; ++it) {
+        for (int it = 1; it <= o.max_iterations; ++it) {
             pcg_spmv_dot(D, s);
             pcg_update(D, it, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
             BDDC_CUDA(cudaStreamSynchronize(s));
             if (pinned[3] == 1.0) throw std::runtime_error("matrix not SPD");
-            if (pinned[3] == 2.0) throw std::invalid_argument("bddc apply: non-finite entry in residual");
+            if (pinned[3] == 2.0) {
+                DBuf<int> bad;
+                bad.alloc(1);
+                device_first_nonfinite(n, rd, bad.p, s);
+                int idx = 0;
+                BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                BDDC_CUDA(cudaStreamSynchronize(s));
+                throw std::invalid_argument("bddc apply: non-finite entry at index " + std::to_string(idx));
+            }
             rel = pinned[1];
             rep.iterations = it;
             if (pinned[2] != 0.0) { rep.converged = true; break; }
             if (it == o.max_iterations) break;
-            if (precondition) apply(rd, zd, s);
+            if (precondition) {
+                apply(rd, zd, s);
+                check_coarse(s);
+            }
             pcg_dot(D, rd, zd, part_a.p, s);
             pcg_xpay(D, it, s);
         }
@@ -287,8 +372,7 @@ struct GpuContext::Impl {
         if (k > 1) BDDC_CUDA(cudaMemcpyAsync(be.data(), beta.p, sizeof(double) * (k - 1), cudaMemcpyDeviceToHost, s));
         if (o.record_history && k) {
             rep.history.resize(k + 1);
-            BDDC_CUDA(cudaMemcpyAsync(rep.history.data() + 1, hist.p + 1, sizeof(double) * k,
-                                      cudaMemcpyDeviceToHost, s));
+            BDDC_CUDA(cudaMemcpyAsync(rep.history.data() + 1, hist.p + 1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
         }
         BDDC_CUDA(cudaStreamSynchronize(s));
         rep.condition_estimate = condition_estimate(al, be);
@@ -310,52 +394,64 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     if (static_cast<index_t>(I.pb.local_matrices.size()) != d.n_subdomains ||
         static_cast<index_t>(I.pb.constraints.constraint_matrices.size()) != d.n_subdomains)
         throw std::invalid_argument("bddc setup: subdomain count mismatch");
-    const int workers = opt.workers > 0 ? opt.workers
-                                        : std::max(1u, std::thread::hardware_concurrency());
+    const int workers = opt.workers > 0 ? opt.workers : std::max(1u, std::thread::hardware_concurrency());
     FactorOptions fo;
     fo.leaf_size = opt.leaf_size;
-    I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints,
-                         I.pb.coords.empty() ? nullptr : I.pb.coords.data(), workers, fo);
-    const DeviceImage img = build_device_image(d, I.pb.constraints, I.pb.local_matrices,
-                                               I.pb.global_matrix, I.setup);
-    I.max_interior = img.max_interior;
+    I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, I.pb.coords.empty() ? nullptr : I.pb.coords.data(),
+                         workers, fo);
+    int nsm = 148;
+    BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
+    const int parts = opt.solve_parts > 0 ? opt.solve_parts : (d.n_subdomains <= nsm ? 2 : 1);
+    // largest per-warp TMA unit whose double-buffered rings fit next to the vectors
+    const int max_smem = max_solve_smem(I.device);
+    DeviceImage img;
+    int unit = 4096;
+    for (;; unit /= 2) {
+        img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit);
+        if (interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit) <=
+            static_cast<std::size_t>(max_smem))
+            break;
+        if (unit <= 1024)
+            throw std::runtime_error("subdomain interior (" + std::to_string(img.solve.max_loc) +
+                                     " dofs per CTA) exceeds the shared-memory solve capacity");
+    }
     I.max_iface = img.max_iface;
     I.max_primal = img.max_primal;
     I.n_coarse = img.n_coarse;
-    I.fwd_values = img.fwd_values;
-    I.bwd_values = img.bwd_values;
+    I.n_gi = static_cast<std::int32_t>(img.gi_dof.size());
+    I.max_loc = img.solve.max_loc;
+    I.max_top = img.solve.max_top;
     I.factor_vals = img.factor_values;
+    for (const PartDesc& pd : img.solve.parts) I.solve_stream_bytes += pd.stream_bytes;
     I.k_values = static_cast<std::int64_t>(img.kmat.size());
     I.phig_values = static_cast<std::int64_t>(img.phig.size());
     I.ginnz = static_cast<std::int64_t>(img.gi_row_val.size());
-    I.couple_nnz = static_cast<std::int64_t>(img.couple_val.size());
-    I.n_iface_total = static_cast<std::int64_t>(img.iface_dof.size());
-    I.solve_smem = interior_solve_smem(img.max_interior, img.max_iface);
-    int max_smem = 0;
-    BDDC_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, I.device));
-    if (I.solve_smem > static_cast<std::size_t>(max_smem))
-        throw std::runtime_error("subdomain interior (" + std::to_string(img.max_interior) +
-                                 " dofs) exceeds the shared-memory solve capacity");
+    for (const auto& v : img.solve.couple_val) (void)v;
+    I.couple_nnz = static_cast<std::int64_t>(img.solve.couple_val.size());
+    I.launch.n_parts = static_cast<int>(img.solve.parts.size());
+    I.launch.cluster = parts;
+    I.launch.unit_bytes = unit;
+    I.launch.smem = interior_solve_smem(I.max_loc, I.max_top, I.max_iface, unit);
 
     BDDC_CUDA(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
-    {
-        std::vector<SubdomainDesc> subs = img.subs;
-        I.subs.alloc(subs.size());
-        BDDC_CUDA(cudaMemcpy(I.subs.p, subs.data(), sizeof(SubdomainDesc) * subs.size(), cudaMemcpyHostToDevice));
+    auto upload_pod = [](auto& buf, const auto& vec) {
+        using T = typename std::decay_t<decltype(vec)>::value_type;
+        buf.alloc(std::max<std::size_t>(vec.size(), 1));
+        if (!vec.empty()) BDDC_CUDA(cudaMemcpy(buf.p, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice));
+    };
+    upload_pod(I.parts, img.solve.parts);
+    I.units.upload(img.solve.units);
+    if (std::getenv("BDDC_SOLVE_STATS")) {
+        I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 4);
+        BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));
     }
-    I.stream_data.upload(img.stream);
-    {
-        I.tasks.alloc(std::max<std::size_t>(img.tasks.size(), 1));
-        if (!img.tasks.empty())
-            BDDC_CUDA(cudaMemcpy(I.tasks.p, img.tasks.data(), sizeof(TileTask) * img.tasks.size(),
-                                 cudaMemcpyHostToDevice));
-    }
-    I.phases.upload(img.phases);
-    I.idx.upload(img.idx);
-    I.gmap.upload(img.gmap);
-    I.couple_ptr.upload(img.couple_ptr);
-    I.couple_gamma.upload(img.couple_gamma);
-    I.couple_val.upload(img.couple_val);
+    upload_pod(I.subs, img.subs);
+    I.sstream.upload(img.solve.stream);
+    I.phases.upload(img.solve.phases);
+    I.gmap.upload(img.solve.gmap);
+    I.couple_ptr.upload(img.solve.couple_ptr);
+    I.couple_gamma.upload(img.solve.couple_gamma);
+    I.couple_val.upload(img.solve.couple_val);
     I.iface_dof.upload(img.iface_dof);
     I.iface_w.upload(img.iface_w);
     I.iface_gid.upload(img.iface_gid);
@@ -365,15 +461,29 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     I.phi.upload(img.phi);
     I.primal.upload(img.primal);
     I.local_dofs.upload(img.local_dofs);
+    I.lrow_ptr.upload(img.lrow_ptr);
+    I.lrow_col.upload(img.lrow_col);
+    I.lrow_val.upload(img.lrow_val);
     I.gi_dof.upload(img.gi_dof);
     I.gi_row_ptr.upload(img.gi_row_ptr);
     I.gi_row_col.upload(img.gi_row_col);
     I.gi_row_val.upload(img.gi_row_val);
     I.gi_own_ptr.upload(img.gi_own_ptr);
     I.gi_own_ref.upload(img.gi_own_ref);
+    I.dof_own_ptr.upload(img.dof_own_ptr);
+    I.dof_own_ref.upload(img.dof_own_ref);
     I.c_own_ptr.upload(img.c_own_ptr);
     I.c_own_ref.upload(img.c_own_ref);
     I.coarse_inv.upload(img.coarse_inv);
+    {
+        std::vector<double> wl;
+        for (const auto& w : d.weights) wl.insert(wl.end(), w.begin(), w.end());
+        I.weights_local.upload(wl);
+    }
+    I.Ac_ptr.upload(I.setup.coarse_matrix.row_offsets);
+    I.Ac_col.upload(I.setup.coarse_matrix.col_indices);
+    I.Ac_val.upload(I.setup.coarse_matrix.values);
+    I.coarse_status.alloc(4);
     I.A_ptr.upload(I.pb.global_matrix.row_offsets);
     I.A_col.upload(I.pb.global_matrix.col_indices);
     I.A_val.upload(I.pb.global_matrix.values);
@@ -383,6 +493,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     I.gbuf.alloc(std::max<std::int64_t>(img.hbuf_total, 1));
     I.hbuf.alloc(std::max<std::int64_t>(img.hbuf_total, 1));
     I.cbuf.alloc(std::max<std::int64_t>(img.cbuf_total, 1));
+    I.lbuf.alloc(std::max<std::int64_t>(img.local_total, 1));
     I.xc.alloc(std::max(img.n_coarse, 1));
     I.vin.alloc(n);
     I.vout.alloc(n);
@@ -404,7 +515,9 @@ index_t GpuContext::n() const { return impl_->pb.decomposition.global_dofs; }
 void GpuContext::apply_device(const double* r, double* z, void* stream) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     BDDC_CUDA(cudaSetDevice(impl_->device));
-    impl_->apply(r, z, stream ? static_cast<cudaStream_t>(stream) : impl_->stream);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : impl_->stream;
+    impl_->apply(r, z, s);
+    impl_->check_coarse(s);
 }
 
 void GpuContext::apply_host(const double* r, double* z) {
@@ -415,6 +528,7 @@ void GpuContext::apply_host(const double* r, double* z) {
     BDDC_CUDA(cudaSetDevice(I.device));
     BDDC_CUDA(cudaMemcpyAsync(I.vin.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
     I.apply(I.vin.p, I.vout.p, I.stream);
+    I.check_coarse(I.stream);
     BDDC_CUDA(cudaMemcpyAsync(z, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, I.stream));
     BDDC_CUDA(cudaStreamSynchronize(I.stream));
 }
@@ -432,41 +546,58 @@ SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x
     return rep;
 }
 
-SolveResult GpuContext::pcg_device(const double* b, const SolverOpts& o, double* x, bool precondition,
-                                   void* stream) {
+SolveResult GpuContext::pcg_device(const double* b, const SolverOpts& o, double* x, bool precondition, void* stream) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     BDDC_CUDA(cudaSetDevice(impl_->device));
     return impl_->pcg(b, o, x, precondition, stream ? static_cast<cudaStream_t>(stream) : impl_->stream);
 }
 
-void GpuContext::stage_host(Stage st, const double* in0, const double* in1, const double* in2,
-                            double* out) {
+void GpuContext::stage_host(Stage st, const double* in0, const double* in1, const double* in2, double* out) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
     const index_t n = I.pb.decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
     cudaStream_t s = I.stream;
-    const int nsub = I.pb.decomposition.n_subdomains;
+    const StageParams sp = I.stage_params();
+    auto h2d = [&](double* dst, const double* src) {
+        BDDC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    };
     switch (st) {
-        case Stage::interior:
-            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        case Stage::interior:  // preconditioner.cpp:194-213
+            h2d(I.vin.p, in0);
             BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
-            launch_interior_solve(I.solve_params(I.vin.p, I.vout.p), 0, nsub, I.solve_smem, s);
+            launch_interior_solve(I.solve_params(I.vin.p, I.vout.p), I.launch, 0, s);
             break;
-        case Stage::static_condensation: {
-            // interior_correction(r - A (v1 + v2))  (preconditioner.cpp:215-223)
-            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in1, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-            BDDC_CUDA(cudaMemcpyAsync(I.vtmp.p, in2, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-            device_axpby(n, 1.0, I.vin.p, 1.0, I.vtmp.p, I.vtmp2.p, s);
-            device_spmv(n, I.A_ptr.p, I.A_col.p, I.A_val.p, I.vtmp2.p, I.vtmp.p, s);
-            BDDC_CUDA(cudaMemcpyAsync(I.vin.p, in0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-            device_axpby(n, 1.0, I.vin.p, -1.0, I.vtmp.p, I.vtmp2.p, s);
+        case Stage::coarse:  // preconditioner.cpp:129-171
+            h2d(I.vin.p, in0);
+            launch_stage_phi_restrict(sp, I.vin.p, s);
+            I.coarse_solve(s);
+            I.check_coarse(s);
+            launch_stage_phi_prolong(sp, s);
+            launch_stage_gather_local(sp, I.vout.p, s);
+            break;
+        case Stage::local: {  // preconditioner.cpp:173-192, saddle solve by interior/interface blocks
+            h2d(I.vin.p, in0);
+            BDDC_CUDA(cudaMemsetAsync(I.vtmp.p, 0, sizeof(double) * n, s));
+            launch_interior_solve(I.solve_params(I.vin.p, I.vtmp.p), I.launch, 0, s);  // y = A_II^-1 f_I
+            launch_stage_local_g(sp, I.vin.p, I.vtmp.p, s);                             // g = f_G - A_GI y
+            launch_iface_local(I.iface_params(), I.opt.local_blocks, s, false);         // z_G = K g
             BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
-            launch_interior_solve(I.solve_params(I.vtmp2.p, I.vout.p), 0, nsub, I.solve_smem, s);
+            launch_interior_solve(I.solve_params(I.vin.p, I.vout.p), I.launch, 2, s);  // z_I
+            launch_stage_iface_gather(sp, I.hbuf.p, I.vout.p, s);                       // sum_i w z_G
             break;
         }
-        default:
-            throw std::invalid_argument("stage not available in this build");
+        case Stage::static_condensation: {  // preconditioner.cpp:215-223
+            h2d(I.vin.p, in1);
+            h2d(I.vtmp.p, in2);
+            device_axpby(n, 1.0, I.vin.p, 1.0, I.vtmp.p, I.vtmp2.p, s);
+            device_spmv(n, I.A_ptr.p, I.A_col.p, I.A_val.p, I.vtmp2.p, I.vtmp.p, s);
+            h2d(I.vin.p, in0);
+            device_axpby(n, 1.0, I.vin.p, -1.0, I.vtmp.p, I.vtmp2.p, s);
+            BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
+            launch_interior_solve(I.solve_params(I.vtmp2.p, I.vout.p), I.launch, 0, s);
+            break;
+        }
     }
     BDDC_CUDA(cudaMemcpyAsync(out, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     BDDC_CUDA(cudaStreamSynchronize(s));
@@ -476,27 +607,33 @@ const BddcSetup& GpuContext::setup() const { return impl_->setup; }
 const ProblemData& GpuContext::problem() const { return impl_->pb; }
 double GpuContext::setup_seconds() const { return impl_->setup.seconds; }
 std::int64_t GpuContext::factor_values() const { return impl_->factor_vals; }
-std::int64_t GpuContext::interior_pass_bytes() const {
-    return 8 * (impl_->fwd_values + impl_->bwd_values);
-}
+std::int64_t GpuContext::interior_pass_bytes() const { return impl_->solve_stream_bytes; }
+int GpuContext::solve_parts() const { return impl_->launch.cluster; }
 std::int64_t GpuContext::apply_bytes() const {
     const Impl& I = *impl_;
     const std::int64_t n = I.pb.decomposition.global_dofs;
-    // 2 interior solves + K_i + Phi_G (x2: restrict and prolong) + coarse inverse
-    // + interface rows/coupling + vector traffic (r read twice, z written once, u0 once)
-    return 2 * interior_pass_bytes() + 8 * (I.k_values + 2 * I.phig_values +
-                                            static_cast<std::int64_t>(I.n_coarse) * I.n_coarse +
-                                            I.ginnz + I.couple_nnz + 4 * n);
+    // algorithmic FP64 bytes: two interior solves (forward + backward over every factor
+    // value), K_i, Phi_G (restrict + prolong), the coarse inverse, interface rows and
+    // coupling, plus vector traffic (r read twice, u0 written/read, z written)
+    return 8 * (4 * I.factor_vals + I.k_values + 2 * I.phig_values +
+                static_cast<std::int64_t>(I.n_coarse) * I.n_coarse + I.ginnz + I.couple_nnz + 5 * n);
 }
 KernelTimes GpuContext::kernel_times() const { return impl_->times; }
 void GpuContext::reset_kernel_times() { impl_->times = KernelTimes{}; }
 void GpuContext::set_profile(bool on) { impl_->opt.profile = on; }
 int GpuContext::device() const { return impl_->device; }
 void GpuContext::synchronize() { BDDC_CUDA(cudaStreamSynchronize(impl_->stream)); }
+std::int64_t GpuContext::solve_profile(std::int64_t* out, std::int64_t cap) {
+    Impl& I = *impl_;
+    if (!I.dbg_buf.p) return 0;
+    const std::int64_t n = std::min<std::int64_t>(cap, static_cast<std::int64_t>(I.dbg_buf.n));
+    BDDC_CUDA(cudaDeviceSynchronize());
+    BDDC_CUDA(cudaMemcpy(out, I.dbg_buf.p, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+    return n;
+}
 
 // pcg.cpp:111-173 (host; O(iterations))
-std::optional<double> condition_estimate(const std::vector<double>& alphas,
-                                         const std::vector<double>& betas) {
+std::optional<double> condition_estimate(const std::vector<double>& alphas, const std::vector<double>& betas) {
     const std::size_t k = alphas.size();
     if (k < 2 || betas.size() + 1 < k) return std::nullopt;
     std::vector<double> diag(k), off(k - 1);
@@ -514,12 +651,12 @@ std::optional<double> condition_estimate(const std::vector<double>& alphas,
         lo = std::min(lo, diag[i] - radius);
         hi = std::max(hi, diag[i] + radius);
     }
-    auto count_below = [&](double x) {
+    auto count_below = [&](double xv) {
         std::size_t count = 0;
         double qv = 1.0;
         for (std::size_t i = 0; i < n; ++i) {
             const double off2 = i > 0 ? off[i - 1] * off[i - 1] : 0.0;
-            qv = diag[i] - x - off2 / qv;
+            qv = diag[i] - xv - off2 / qv;
             if (qv == 0.0) qv = 1e-300;
             if (qv < 0.0) ++count;
         }

@@ -10,6 +10,8 @@
 //   z_G  = sum_i R_i^T h_i  (ascending i, fused into the second interior solve)
 #include "iface.cuh"
 
+#include <algorithm>
+
 namespace bddc_b200 {
 namespace {
 
@@ -67,7 +69,7 @@ coarse_direct_kernel(const IfaceParams P) {
 constexpr int kLocalThreads = 256;
 
 __global__ void __launch_bounds__(kLocalThreads)
-iface_local_kernel(const IfaceParams P, int blocks_per_sub) {
+iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     extern __shared__ double sm[];
     const int sub = blockIdx.x / blocks_per_sub, part = blockIdx.x % blocks_per_sub;
     const SubdomainDesc& sd = P.subs[sub];
@@ -75,7 +77,8 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub) {
     double* g = sm;
     double* xl = sm + ((ng + 1) & ~1);
     for (int k = threadIdx.x; k < ng; k += blockDim.x) g[k] = P.gbuf[sd.hbuf + k];
-    for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
+    if (with_coarse)
+        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
     __syncthreads();
     const int rows_per = (ng + blocks_per_sub - 1) / blocks_per_sub;
     const int r0 = part * rows_per, r1 = min(ng, r0 + rows_per);
@@ -93,13 +96,181 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub) {
         if (k < ng) a0 = fma(ld_stream(krow + k), g[k], a0);
         double acc = warp_sum(a0 + a1);
         if (lane == 0) {
-            double coarse = 0.0;
-            for (int j = 0; j < np; ++j) coarse = fma(phig[row * np + j], xl[j], coarse);
-            P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (coarse + acc);
+            if (with_coarse) {
+                double coarse = 0.0;
+                for (int j = 0; j < np; ++j) coarse = fma(phig[row * np + j], xl[j], coarse);
+                P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (coarse + acc);
+            } else {
+                P.hbuf[sd.hbuf + row] = acc;
+            }
         }
     }
 }
 
+
+// ---------------------------------------------------------------- stage hooks
+constexpr int kStageThreads = 256;
+
+// c_i = Phi_i^T (W_i R_i r)   (coarse_correction restriction, preconditioner.cpp:135-140)
+__global__ void __launch_bounds__(kStageThreads) stage_phi_restrict_kernel(const StageParams P, const double* r) {
+    const SubdomainDesc& sd = P.subs[blockIdx.x];
+    const int nl = sd.n_local, np = sd.n_primal;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* phi = P.phi + sd.phi;
+    for (int j = warp; j < np; j += kStageThreads / 32) {
+        double acc = 0.0;
+        for (int l = lane; l < nl; l += 32)
+            acc = fma(phi[l * np + j], P.weights_local[sd.local_dofs + l] * r[P.local_dofs[sd.local_dofs + l]], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) P.cbuf[sd.cbuf + j] = acc;
+    }
+}
+
+// lbuf_i = W_i Phi_i x_c[map_i]   (preconditioner.cpp:159-167)
+__global__ void __launch_bounds__(kStageThreads) stage_phi_prolong_kernel(const StageParams P) {
+    const SubdomainDesc& sd = P.subs[blockIdx.x];
+    const int nl = sd.n_local, np = sd.n_primal;
+    const double* phi = P.phi + sd.phi;
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < np; ++j) acc += phi[l * np + j] * P.xc[P.primal[sd.primal + j]];
+        P.lbuf[sd.local_dofs + l] = P.weights_local[sd.local_dofs + l] * acc;
+    }
+}
+
+// out[g] = sum over owners (ascending subdomain) of lbuf   (prolong_add loop order)
+__global__ void __launch_bounds__(kStageThreads) stage_gather_local_kernel(const StageParams P, double* out) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < P.n_vector; g += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int o = P.dof_own_ptr[g]; o < P.dof_own_ptr[g + 1]; ++o) acc += P.lbuf[P.dof_own_ref[o]];
+        out[g] = acc;
+    }
+}
+
+// g_i = W_G r_G - A_GI^(i) y_I   (interface rhs of the local saddle solve)
+__global__ void __launch_bounds__(kStageThreads) stage_local_g_kernel(const StageParams P, const double* r,
+                                                                    const double* y) {
+    const SubdomainDesc& sd = P.subs[blockIdx.x];
+    const int ng = sd.n_iface;
+    const std::int32_t* rp = P.lrow_ptr + sd.lrow_ptr;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+        double acc = 0.0;
+        for (int e = rp[g]; e < rp[g + 1]; ++e) acc += P.lrow_val[e] * y[P.lrow_col[e]];
+        P.gbuf[sd.hbuf + g] = P.iface_w[sd.iface + g] * r[P.iface_dof[sd.iface + g]] - acc;
+    }
+}
+
+// out[G] = sum over owners of w * h   (local_correction interface prolongation)
+__global__ void __launch_bounds__(kStageThreads) stage_iface_gather_kernel(const StageParams P, const double* h,
+                                                                         double* out) {
+    for (int gid = blockIdx.x * blockDim.x + threadIdx.x; gid < P.n_gi; gid += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int o = P.gi_own_ptr[gid]; o < P.gi_own_ptr[gid + 1]; ++o) {
+            const int slot = P.gi_own_ref[o];
+            acc += P.iface_w[slot] * h[slot];
+        }
+        out[P.gi_dof[gid]] = acc;
+    }
+}
+
+constexpr int kCgThreads = 1024;
+
+__global__ void __launch_bounds__(kCgThreads) coarse_cg_kernel(const CoarseCgParams P) {
+    extern __shared__ double sh[];
+    __shared__ double scratch[kCgThreads / 32];
+    const int n = P.n;
+    const int ld = (n + 1) & ~1;
+    double* x = sh;
+    double* r = x + ld;
+    double* p = r + ld;
+    double* q = p + ld;
+    double bb = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double acc = 0.0;
+        for (int o = P.c_own_ptr[i]; o < P.c_own_ptr[i + 1]; ++o) acc += P.cbuf[P.c_own_ref[o]];
+        r[i] = acc;
+        p[i] = acc;
+        x[i] = 0.0;
+        bb += acc * acc;
+    }
+    const double norm_b = sqrt(block_sum<kCgThreads>(bb, scratch));
+    int iterations = 0;
+    double rel = 1.0;
+    bool converged = false;
+    if (norm_b == 0.0) {
+        converged = true;
+    } else {
+        double rho = block_sum<kCgThreads>(bb, scratch);
+        for (int it = 1; it <= P.max_it; ++it) {
+            double pq = 0.0;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                double acc = 0.0;
+                for (int e = P.ptr[i]; e < P.ptr[i + 1]; ++e) acc += P.val[e] * p[P.col[e]];
+                q[i] = acc;
+                pq += p[i] * acc;
+            }
+            pq = block_sum<kCgThreads>(pq, scratch);
+            if (!(pq > 0.0)) { iterations = -it; break; }
+            const double alpha = rho / pq;
+            double rr = 0.0;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                x[i] += alpha * p[i];
+                r[i] -= alpha * q[i];
+                rr += r[i] * r[i];
+            }
+            rr = block_sum<kCgThreads>(rr, scratch);
+            rel = sqrt(rr) / norm_b;
+            iterations = it;
+            if (rel <= P.rtol || (P.atol > 0.0 && rel * norm_b <= P.atol)) { converged = true; break; }
+            if (it == P.max_it) break;
+            const double beta = rr / rho;
+            rho = rr;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = r[i] + beta * p[i];
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) P.xc[i] = x[i];
+    if (threadIdx.x == 0) {
+        P.status[0] = iterations;
+        P.status[1] = rel;
+        P.status[2] = converged ? 1.0 : 0.0;
+    }
+}
+
+}  // namespace
+
+void launch_coarse_cg(const CoarseCgParams& P, cudaStream_t s) {
+    const std::size_t smem = sizeof(double) * 4 * ((P.n + 1) & ~1);
+    if (smem > 48 * 1024)
+        BDDC_CUDA(cudaFuncSetAttribute(coarse_cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coarse_cg_kernel<<<1, kCgThreads, smem, s>>>(P);
+    BDDC_CUDA(cudaGetLastError());
+}
+
+static int stage_grid(int n) { return std::max(1, std::min((n + kStageThreads - 1) / kStageThreads, 148 * 8)); }
+
+void launch_stage_phi_restrict(const StageParams& P, const double* r, cudaStream_t s) {
+    stage_phi_restrict_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P, r);
+    BDDC_CUDA(cudaGetLastError());
+}
+void launch_stage_phi_prolong(const StageParams& P, cudaStream_t s) {
+    stage_phi_prolong_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P);
+    BDDC_CUDA(cudaGetLastError());
+}
+void launch_stage_gather_local(const StageParams& P, double* out, cudaStream_t s) {
+    stage_gather_local_kernel<<<stage_grid(P.n_vector), kStageThreads, 0, s>>>(P, out);
+    BDDC_CUDA(cudaGetLastError());
+}
+void launch_stage_local_g(const StageParams& P, const double* r, const double* y, cudaStream_t s) {
+    stage_local_g_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P, r, y);
+    BDDC_CUDA(cudaGetLastError());
+}
+void launch_stage_iface_gather(const StageParams& P, const double* h, double* out, cudaStream_t s) {
+    stage_iface_gather_kernel<<<stage_grid(P.n_gi), kStageThreads, 0, s>>>(P, h, out);
+    BDDC_CUDA(cudaGetLastError());
+}
+
+namespace {
 }  // namespace
 
 void launch_iface_restrict(const IfaceParams& P, const double* r, const double* u0, cudaStream_t s) {
@@ -121,12 +292,13 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
     BDDC_CUDA(cudaGetLastError());
 }
 
-void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s) {
+void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, bool with_coarse) {
     const std::size_t smem = sizeof(double) * (P.max_iface + P.max_primal + 4);
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub);
+    iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub,
+                                                                                 with_coarse ? 1 : 0);
     BDDC_CUDA(cudaGetLastError());
 }
 

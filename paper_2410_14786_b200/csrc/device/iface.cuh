@@ -32,11 +32,62 @@ struct IfaceParams {
     double* xc;     // coarse solution
 };
 
+struct StageParams {
+    const SubdomainDesc* subs;
+    int n_subdomains;
+    int n_vector;
+    int max_primal;
+    const std::int32_t* local_dofs;
+    const double* phi;
+    const double* iface_w;     // per local interface slot
+    const std::int32_t* iface_dof;
+    const std::int32_t* gi_dof;
+    int n_gi;
+    const std::int32_t* gi_own_ptr;
+    const std::int32_t* gi_own_ref;
+    const std::int32_t* dof_own_ptr;
+    const std::int32_t* dof_own_ref;
+    const std::int32_t* lrow_ptr;
+    const std::int32_t* lrow_col;
+    const double* lrow_val;
+    const std::int32_t* primal;
+    const double* weights_local;  // per local slot
+    double* lbuf;                 // per local slot
+    double* gbuf;
+    double* cbuf;
+    const double* xc;
+};
+
+// Reference-faithful coarse CG on A_c (src/preconditioner.cpp:149-157 + pcg.cpp:40-109,
+// no preconditioner). status: [0]=iterations, [1]=relative residual, [2]=converged.
+struct CoarseCgParams {
+    int n;
+    const std::int32_t* ptr;
+    const std::int32_t* col;
+    const double* val;
+    const std::int32_t* c_own_ptr;
+    const std::int32_t* c_own_ref;
+    const double* cbuf;
+    double* xc;
+    double* status;
+    double rtol, atol;
+    int max_it;
+};
+void launch_coarse_cg(const CoarseCgParams& P, cudaStream_t s);
+
+// Stage hooks (not on the hot path): general-r coarse/local corrections.
+void launch_stage_phi_restrict(const StageParams& P, const double* r, cudaStream_t s);
+void launch_stage_phi_prolong(const StageParams& P, cudaStream_t s);
+void launch_stage_gather_local(const StageParams& P, double* out, cudaStream_t s);
+void launch_stage_local_g(const StageParams& P, const double* r, const double* y, cudaStream_t s);
+void launch_stage_iface_gather(const StageParams& P, const double* h, double* out, cudaStream_t s);
+
 // K3: g_i = W_i (r_G - A_GI u0_I) restricted to subdomain i, c_i = Phi_Gi^T g_i.
 void launch_iface_restrict(const IfaceParams& P, const double* r, const double* u0, cudaStream_t s);
 // K4: x_c = A_c^{-1} r_c with r_c = sum_i R_ci^T c_i (ascending i).
 void launch_coarse_direct(const IfaceParams& P, cudaStream_t s);
 // K5: h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i); rows split over blocks_per_sub CTAs.
-void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s);
+// with_coarse = false: h_i = K_i g_i (unweighted; local_correction stage)
+void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, bool with_coarse = true);
 
 }  // namespace bddc_b200

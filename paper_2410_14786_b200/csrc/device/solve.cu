@@ -1,148 +1,323 @@
-// Batched interior solve A_II^{-1} b for every subdomain: one CTA per subdomain,
-// the whole permuted interior vector resident in shared memory (two arrays T, X),
-// the supernodal factor streamed once per sweep as coalesced column-major tiles.
+// Batched interior solve A_II^{-1} b for every subdomain (replaces reference
+// interior_correction, src/preconditioner.cpp:194-213, and the lu_solve it calls,
+// src/sparse_lu.cpp:203-237).
 //
-// Replaces reference interior_correction (src/preconditioner.cpp:194-213) and the
-// lu_solve it calls (src/sparse_lu.cpp:203-237).
+// One CTA per part (a cluster of P CTAs per subdomain). Each of the 16 warps owns a
+// double-buffered shared-memory ring: lane 0 streams the warp's own tile units from HBM
+// with cp.async.bulk (TMA bulk copies, mbarrier completion), one unit ahead, so streaming
+// never waits for other warps and keeps going across phase barriers. Vectors T/X live in
+// shared memory; every output chunk of a phase is owned by one warp (deterministic).
+// With P = 2 the two CTAs of a cluster each own one half of the nested-dissection tree
+// and exchange the partial sums into the separator chain above the split through
+// distributed shared memory.
 #include "solve.cuh"
 
 namespace bddc_b200 {
 namespace {
 
-struct PassArgs {
-    const double* stream;
-    const TileTask* tasks;
-    const std::int32_t* phases;  // (kSolveWarps+1) per phase
-    int n_phases;
-    const std::int32_t* idx;
-};
+constexpr int kThreads = kSolveWarps * 32;
+constexpr int kMaxRegEntries = 96;  // per-warp phase / unit tables held in registers (3 per lane)
 
-// One sweep. own/other: see device_format.hpp (forward own=T, backward own=X).
-__device__ __forceinline__ void run_pass(const PassArgs a, double* __restrict__ own,
-                                         double* __restrict__ other) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int ph = 0; ph < a.n_phases; ++ph) {
-        const std::int32_t* tab = a.phases + ph * (kSolveWarps + 1);
-        const int t0 = tab[warp], t1 = tab[warp + 1];
-        double acc = 0.0;
-        for (int t = t0; t < t1; ++t) {
-            const int4 raw = __ldg(reinterpret_cast<const int4*>(a.tasks) + t);
-            TileTask task;
-            *reinterpret_cast<int4*>(&task) = raw;
-            if (task.flags & kTaskFirst) acc = 0.0;
-            const double* in = (task.flags & kTaskDiag) ? own : other;
-            const int row = lane - task.lane_off;
-            const int nrows = task.nrows, ncols = task.ncols;
-            if (row >= 0 && row < nrows) {
-                const double* M = a.stream + task.m_off + row;
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                int j = 0;
-                if (task.flags & kTaskInIndexed) {
-                    const std::int32_t* ix = a.idx + task.in_ref;
-                    for (; j + 4 <= ncols; j += 4) {
-                        const double m0 = ld_stream(M + (j + 0) * nrows);
-                        const double m1 = ld_stream(M + (j + 1) * nrows);
-                        const double m2 = ld_stream(M + (j + 2) * nrows);
-                        const double m3 = ld_stream(M + (j + 3) * nrows);
-                        s0 = fma(m0, in[__ldg(ix + j + 0)], s0);
-                        s1 = fma(m1, in[__ldg(ix + j + 1)], s1);
-                        s2 = fma(m2, in[__ldg(ix + j + 2)], s2);
-                        s3 = fma(m3, in[__ldg(ix + j + 3)], s3);
-                    }
-                    for (; j < ncols; ++j) s0 = fma(ld_stream(M + j * nrows), in[__ldg(ix + j)], s0);
-                } else {
-                    const double* v = in + task.in_ref;
-                    for (; j + 4 <= ncols; j += 4) {
-                        const double m0 = ld_stream(M + (j + 0) * nrows);
-                        const double m1 = ld_stream(M + (j + 1) * nrows);
-                        const double m2 = ld_stream(M + (j + 2) * nrows);
-                        const double m3 = ld_stream(M + (j + 3) * nrows);
-                        s0 = fma(m0, v[j + 0], s0);
-                        s1 = fma(m1, v[j + 1], s1);
-                        s2 = fma(m2, v[j + 2], s2);
-                        s3 = fma(m3, v[j + 3], s3);
-                    }
-                    for (; j < ncols; ++j) s0 = fma(ld_stream(M + j * nrows), v[j], s0);
-                }
-                acc += (s0 + s1) + (s2 + s3);
-            }
-            if (task.flags & kTaskLast) {
-                if (lane < task.nvalid) {
-                    if (task.flags & kTaskDiag) other[task.out_base + lane] = acc;
-                    else own[task.out_base + lane] -= acc;
-                }
-            }
-        }
-        __syncthreads();
-    }
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double ld_dsmem(const double* local, std::uint32_t rank) {
+    std::uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+    return v;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kSolveWarps * 32, 1)
-interior_solve_kernel(const SolveParams P) {
-    extern __shared__ double smem[];
-    const int sub = blockIdx.x + P.first_subdomain;
-    const SubdomainDesc& sd = P.subs[sub];
-    const int nI = sd.n_interior;
-    const int ldn = (nI + 1) & ~1;
-    double* T = smem;
-    double* X = smem + ldn;
-    double* ZG = X + ldn;  // interface values (MODE 1)
-    const std::int32_t* gmap = P.gmap + sd.gmap;
+// Per-warp table spread over the lanes' registers: entry i lives in lane i % 32, slot i / 32;
+// entries beyond kMaxRegEntries fall back to global memory.
+struct RegTable {
+    int v[kMaxRegEntries / 32];
+    __device__ __forceinline__ int get(int i, const int* fallback, int stride) const {
+        if (i >= kMaxRegEntries) return __ldg(fallback + static_cast<std::int64_t>(i) * stride);
+        const int slot = i >> 5;
+        const int mine = slot == 0 ? v[0] : (slot == 1 ? v[1] : v[2]);
+        return __shfl_sync(0xffffffffu, mine, i & 31);
+    }
+};
 
-    for (int p = threadIdx.x; p < nI; p += blockDim.x) T[p] = P.in[gmap[p]];
-    if (MODE == 1) {
-        // z_G = sum over the subdomains sharing each interface dof of their h
-        // contributions, ascending subdomain (reference prolong_add order,
-        // preconditioner.cpp:168-169,189-190); writes the interface part of z.
+template <int MODE, int CLUSTER>
+__global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const PartDesc& pdr = S.parts[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int unit = S.unit_bytes;
+
+    // ---- shared memory carve-up
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);  // [warp][kUnitSlots]
+    const int ldn = (S.max_loc + 64 + 1) & ~1;
+    double* T = reinterpret_cast<double*>(bars + kSolveWarps * kUnitSlots);
+    double* X = T + ldn;
+    double* Q = X + ldn;
+    double* ZG = Q + ((S.max_top + 1) & ~1);
+    unsigned char* ring = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<std::uintptr_t>(ZG + ((S.max_iface + 1) & ~1)) + 127) & ~std::uintptr_t(127));
+    unsigned char* my_ring = ring + static_cast<std::size_t>(warp) * kUnitSlots * unit;
+    std::uint64_t* my_bars = bars + warp * kUnitSlots;
+
+    const int n_phases = pdr.n_phases;
+    const int ubase = pdr.warp_base[warp];
+    const int nunits = pdr.warp_base[warp + 1] - ubase;
+    const int* units = S.units + 2 * (pdr.units + ubase);  // {offset16, bytes} pairs
+    const std::int32_t* gtable = S.phases + pdr.phases;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(S.stream + pdr.stream);
+
+    if (lane < kUnitSlots) mbar_init(&my_bars[lane], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+
+    // per-warp registers: unit offsets / bytes, the end unit and kind of each phase
+    RegTable uoff, ubytes, uend, pkind;
+#pragma unroll
+    for (int q = 0; q < kMaxRegEntries / 32; ++q) {
+        const int i = q * 32 + lane;
+        int2 e = make_int2(0, 0);
+        if (i < nunits) e = __ldg(reinterpret_cast<const int2*>(units) + i);
+        uoff.v[q] = e.x;
+        ubytes.v[q] = e.y;
+        uend.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + kSolveWarps + warp) : 0;
+        pkind.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + 2 * kSolveWarps) : 0;
+    }
+    auto prefetch_l2 = [&](int u) {  // whole warp calls; stage unit u in L2 ahead of its smem fill
+        if (u >= nunits) return;
+        const int o16 = uoff.get(u, units, 2);
+        const int nb = ubytes.get(u, units + 1, 2);
+        if (lane == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + static_cast<std::int64_t>(o16) * 16),
+                         "r"(nb)
+                         : "memory");
+    };
+    auto fetch = [&](int u) {  // whole warp calls; lane 0 issues unit u into its slot
+        const int o16 = uoff.get(u, units, 2);
+        const int nb = ubytes.get(u, units + 1, 2);
+        if (lane == 0) {
+            const int s = u % kUnitSlots;
+            mbar_expect_tx(&my_bars[s], static_cast<std::uint32_t>(nb));
+            bulk_g2s(my_ring + s * unit, src + static_cast<std::int64_t>(o16) * 16, static_cast<std::uint32_t>(nb),
+                     &my_bars[s]);
+        }
+        prefetch_l2(u + S.l2_ahead);
+    };
+    for (int u = kUnitSlots; u < kUnitSlots + S.l2_ahead - 1; ++u) prefetch_l2(u);
+    for (int u = 0; u < kUnitSlots && u < nunits; ++u) fetch(u);
+
+    // ---- right-hand side (and, in MODE 1/2, the interface coupling)
+    const std::int32_t* gmap = S.gmap + pdr.gmap;
+    const int n_loc = pdr.n_loc, n_top = pdr.n_top;
+    for (int l = tid; l < ldn; l += kThreads) {
+        T[l] = l < n_loc ? S.in[gmap[l]] : 0.0;
+        X[l] = 0.0;  // padded columns of a tile read finite zeros
+    }
+    for (int l = tid; l < n_top; l += kThreads) Q[l] = 0.0;
+    if (MODE != 0) {
+        const SubdomainDesc& sd = S.subs[pdr.sub];
         const int ng = sd.n_iface;
-        for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-            const int gid = P.iface_gid[sd.iface + g];
-            double z = 0.0;
-            for (int o = P.gi_own_ptr[gid]; o < P.gi_own_ptr[gid + 1]; ++o) z += P.hbuf[P.gi_own_ref[o]];
+        for (int g = tid; g < ng; g += kThreads) {
+            double z;
+            if (MODE == 1) {
+                // z_G = sum over the subdomains sharing the dof of their h, ascending
+                // subdomain (reference prolong_add order, preconditioner.cpp:168-169,189-190)
+                const int gid = S.iface_gid[sd.iface + g];
+                z = 0.0;
+                for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) z += S.hbuf[S.gi_own_ref[o]];
+                if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) S.out[S.iface_dof[sd.iface + g]] = z;
+            } else {
+                z = S.hbuf[sd.hbuf + g];
+            }
             ZG[g] = z;
-            if (P.iface_writer[sd.iface + g]) P.out[P.iface_dof[sd.iface + g]] = z;
         }
         __syncthreads();
-        // b_I = r_I - A_IG z_G
-        const std::int32_t* cp = P.couple_ptr + sd.couple_ptr;
-        for (int p = threadIdx.x; p < nI; p += blockDim.x) {
+        const std::int32_t* cp = S.couple_ptr + pdr.couple_ptr;
+        for (int l = tid; l < n_loc; l += kThreads) {
             double acc = 0.0;
-            for (int e = cp[p]; e < cp[p + 1]; ++e)
-                acc += P.couple_val[sd.couple_ent + e] * ZG[P.couple_gamma[sd.couple_ent + e]];
-            T[p] -= acc;
+            for (int e = cp[l]; e < cp[l + 1]; ++e)
+                acc += S.couple_val[pdr.couple_ent + e] * ZG[S.couple_gamma[pdr.couple_ent + e]];
+            T[l] -= acc;
         }
     }
     __syncthreads();
 
-    const PassArgs fwd{P.stream + sd.fwd_stream, P.tasks + sd.fwd_tasks, P.phases + sd.fwd_phases,
-                       sd.n_fwd_phases, P.idx + sd.idx_base};
-    run_pass(fwd, T, X);
-    const PassArgs bwd{P.stream + sd.bwd_stream, P.tasks + sd.bwd_tasks, P.phases + sd.bwd_phases,
-                       sd.n_bwd_phases, P.idx + sd.idx_base};
-    run_pass(bwd, X, T);
+    double acc = 0.0;
+    int u = 0;  // next unit of this warp
+    long long t_wait = 0, t_bar = 0, t_start = clock64();
+    for (int ph = 0; ph < n_phases; ++ph) {
+        const int kind = pkind.get(ph, gtable + 2 * kSolveWarps, kPhaseStride);
+        const int u_end = uend.get(ph, gtable + kSolveWarps + warp, kPhaseStride);
+        double* own = (kind & kPhaseBackward) ? X : T;
+        double* other = (kind & kPhaseBackward) ? T : X;
+        for (; u < u_end; ++u) {
+            const int s = u % kUnitSlots;
+            const long long tw0 = clock64();
+            mbar_wait(&my_bars[s], (u / kUnitSlots) & 1);
+            t_wait += clock64() - tw0;
+            const unsigned char* ubuf = my_ring + s * unit;
+            std::uint32_t cur = 0;
+            while (cur != kNoTask) {
+                const unsigned char* hdr = ubuf + (cur << 4);
+                TileTask task;
+                *reinterpret_cast<int4*>(&task) = *reinterpret_cast<const int4*>(hdr);
+                cur = task.next;
+                const bool indexed = task.flags & kTaskInIndexed;
+                const int k = task.nrows, G = task.groups, kG = k * G;
+                const int iters = (task.ncols + G - 1) / G;
+                const int vbytes = (iters * kG * 8 + 15) & ~15;
+                const int ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
+                if (task.flags & kTaskFirst) acc = 0.0;
+                // flattened mapping: lane = g*k + r, columns j = t*G + g
+                const int g = lane / k;
+                const unsigned char* tile = hdr + 16;
+                double s0 = 0.0, s1 = 0.0;
+                if (lane < kG && S.debug != 1) {
+                    const double* M = reinterpret_cast<const double*>(tile) + lane;
+                    const double* in = (task.flags & kTaskDiag) ? own : other;
+                    int t = 0;
+                    if (indexed) {
+                        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
+                        for (; t + 2 <= iters; t += 2) {
+                            s0 = fma(M[t * kG], in[ix[t * G]], s0);
+                            s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
+                        }
+                        if (t < iters) s0 = fma(M[t * kG], in[ix[t * G]], s0);
+                    } else {
+                        const double* v = in + task.in_ref + g;
+                        for (; t + 2 <= iters; t += 2) {
+                            s0 = fma(M[t * kG], v[t * G], s0);
+                            s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
+                        }
+                        if (t < iters) s0 = fma(M[t * kG], v[t * G], s0);
+                    }
+                }
+                double tot = s0 + s1;
+                for (int off = 1; off < G; off <<= 1) {
+                    const double o = __shfl_down_sync(0xffffffffu, tot, off * k);
+                    if (g + off < G) tot += o;
+                }
+                acc += tot;  // meaningful in lanes r < k (g == 0)
+                if (task.flags & kTaskLast) {
+                    if (task.flags & kTaskPush) {
+                        if (lane < k) {
+                            const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes)[lane];
+                            if (task.flags & kTaskPartial) Q[o] += acc;
+                            else own[o] -= acc;
+                        }
+                    } else if (lane < task.nvalid) {
+                        if (task.flags & kTaskDiag) other[task.out_base + lane] = acc;
+                        else own[task.out_base + lane] -= acc;
+                    }
+                }
+            }
+            // slot consumed: refill it with the unit kUnitSlots ahead
+            if (u + kUnitSlots < nunits) {
+                __syncwarp();
+                if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                fetch(u + kUnitSlots);
+            }
+        }
+        const long long tb0 = clock64();
+        __syncthreads();
+        t_bar += clock64() - tb0;
+        if (CLUSTER > 1 && (kind & kPhaseCombine)) {
+            cluster_sync_all();
+            // t_top = (t - Q_rank0) - Q_rank1 : identical arithmetic in both CTAs
+            const int cb = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 1);
+            const int ce = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 2);
+            for (int l = cb + tid; l < ce; l += kThreads) {
+                const int qi = l - pdr.n_group;
+                const double q0 = pdr.rank == 0 ? Q[qi] : ld_dsmem(&Q[qi], 0);
+                const double q1 = pdr.rank == 1 ? Q[qi] : ld_dsmem(&Q[qi], 1);
+                T[l] = (T[l] - q0) - q1;
+            }
+            __syncthreads();
+        }
+    }
 
-    for (int p = threadIdx.x; p < nI; p += blockDim.x) P.out[gmap[p]] = T[p];
+    if (S.dbg && lane == 0) {  // instrumentation (debug builds of the timing experiments)
+        long long* d = S.dbg + (static_cast<long long>(blockIdx.x) * kSolveWarps + warp) * 4;
+        d[0] = clock64() - t_start;
+        d[1] = t_wait;
+        d[2] = t_bar;
+        d[3] = nunits;
+    }
+    for (int l = tid; l < pdr.n_write; l += kThreads) S.out[gmap[l]] = T[l];
+    if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
+}
+
+template <int MODE, int CLUSTER>
+void launch_one(const SolveParams& P, const SolveLaunch& L, cudaStream_t stream) {
+    auto kern = interior_solve_kernel<MODE, CLUSTER>;
+    BDDC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.n_parts);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BDDC_CUDA(cudaLaunchKernelEx(&cfg, kern, P));
 }
 
 }  // namespace
 
-std::size_t interior_solve_smem(int max_interior, int max_iface) {
-    const int ldn = (max_interior + 1) & ~1;
-    return sizeof(double) * (2 * static_cast<std::size_t>(ldn) + max_iface + 2);
+std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes) {
+    return static_cast<std::size_t>(kSolveWarps) * kUnitSlots * 8 +
+           8 * (2 * static_cast<std::size_t>((max_loc + 64 + 1) & ~1) + ((max_top + 1) & ~1) +
+                ((max_iface + 1) & ~1)) +
+           128 + static_cast<std::size_t>(kSolveWarps) * kUnitSlots * unit_bytes;
 }
 
-void launch_interior_solve(const SolveParams& P, int mode, int n_subdomains, std::size_t smem,
-                           cudaStream_t stream) {
-    if (n_subdomains <= 0) return;
-    if (mode == 0) {
-        BDDC_CUDA(cudaFuncSetAttribute(interior_solve_kernel<0>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        interior_solve_kernel<0><<<n_subdomains, kSolveWarps * 32, smem, stream>>>(P);
+int max_solve_smem(int device) {
+    int max_smem = 0;
+    BDDC_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    return max_smem;
+}
+
+void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaStream_t stream) {
+    if (L.n_parts <= 0) return;
+    P.unit_bytes = L.unit_bytes;
+    if (L.cluster == 2) {
+        if (mode == 0) launch_one<0, 2>(P, L, stream);
+        else if (mode == 1) launch_one<1, 2>(P, L, stream);
+        else launch_one<2, 2>(P, L, stream);
     } else {
-        BDDC_CUDA(cudaFuncSetAttribute(interior_solve_kernel<1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        interior_solve_kernel<1><<<n_subdomains, kSolveWarps * 32, smem, stream>>>(P);
+        if (mode == 0) launch_one<0, 1>(P, L, stream);
+        else if (mode == 1) launch_one<1, 1>(P, L, stream);
+        else launch_one<2, 1>(P, L, stream);
     }
     BDDC_CUDA(cudaGetLastError());
 }

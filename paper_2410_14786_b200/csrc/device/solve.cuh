@@ -5,12 +5,11 @@
 namespace bddc_b200 {
 
 struct SolveParams {
+    const PartDesc* parts;
     const SubdomainDesc* subs;
-    int first_subdomain;
     const double* stream;
-    const TileTask* tasks;
+    const std::int32_t* units;   // {offset16, bytes} pairs
     const std::int32_t* phases;
-    const std::int32_t* idx;
     const std::int32_t* gmap;
     // MODE 1 (second interior solve of the apply): coupling + interface gather
     const std::int32_t* couple_ptr;
@@ -22,13 +21,29 @@ struct SolveParams {
     const std::int32_t* gi_own_ptr;
     const std::int32_t* gi_own_ref;
     const double* hbuf;
-    // vectors
     const double* in;
     double* out;
+    int unit_bytes;  // set by the launcher
+    int max_loc;
+    int max_top;
+    int max_iface;
+    int debug;     // timing experiments only: 1 = skip tile math
+    int l2_ahead;  // units staged in L2 ahead of the smem fill
+    long long* dbg;  // optional per-warp cycle accounting [part][warp][4]
 };
 
-std::size_t interior_solve_smem(int max_interior, int max_iface);
-void launch_interior_solve(const SolveParams& P, int mode, int n_subdomains, std::size_t smem,
-                           cudaStream_t stream);
+struct SolveLaunch {
+    int n_parts = 0;      // CTAs
+    int cluster = 1;      // parts per subdomain (1 or 2)
+    std::size_t smem = 0;
+    int unit_bytes = 0;
+};
+
+std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes);
+int max_solve_smem(int device);
+// mode 0: out[I] = A_II^{-1} in[I]
+// mode 1: z_G = sum of h over owners (written to out), out[I] = A_II^{-1}(in_I - A_IG z_G)
+// mode 2: out[I] = A_II^{-1}(in_I - A_IG h_own)   (local saddle solve, stage hook)
+void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaStream_t stream);
 
 }  // namespace bddc_b200

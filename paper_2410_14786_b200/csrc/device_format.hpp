@@ -1,71 +1,115 @@
-// Layout contract between the host program builder (host/program.cpp) and the
-// sm_100a kernels (device/*.cu). Plain structs only: no torch / STL types.
+// Layout contract between the host program builder (host/solve_program.cpp,
+// host/program.cpp) and the sm_100a kernels (device/*.cu). Plain structs only.
 //
-// Interior solve "program": each subdomain's supernodal L (nested dissection order)
-// is compiled into two streams of column-major FP64 tiles — one for the forward
-// sweep L x = b, one for the backward sweep L^T y = x — laid out in consumption
-// order, plus per-warp task lists per phase. Every task is the same warp op:
+// Interior solve "program"
+// ------------------------
+// A subdomain's supernodal Cholesky factor L of A_II (nested-dissection order) is
+// compiled into P "parts" (P = 1, or 2 = a CTA pair in one thread-block cluster:
+// each CTA owns one half of the elimination tree; the separator chain above the split
+// is processed redundantly by both after one exchange of partial sums through
+// distributed shared memory). Each part is
+//   * per warp, a sequence of "units" in HBM (<= unit_bytes each, whole tiles with their
+//     16-byte headers, one phase per unit); every warp prefetches its own units into a
+//     private double-buffered shared-memory ring with cp.async.bulk (TMA bulk copies)
+//     and its own mbarriers, so streaming never waits on other warps and continues
+//     across the phase barriers;
+//   * a phase table giving each warp's unit range per phase (phases are separated by
+//     CTA barriers).
 //
-//     acc[lane] += sum_j  M[(lane - lane_off) + j*nrows] * in[col(j)]
+// Every task is one warp-level tile GEMV with a flattened lane mapping: a tile has k
+// rows (k <= 32) and ncols columns; lane l < k*G (G = floor(32/k) column groups) owns
+// row r = l % k and columns j = t*G + l/k for t = 0, 1, ...; the tile values are stored
+// iteration-major, value(r, t*G + g) at [t*k*G + g*k + r], so each iteration is one
+// contiguous, conflict-free shared-memory read. Partial sums are reduced across the G
+// groups with shuffles; lane r then holds the row total. Accumulators persist across
+// consecutive tasks of the same output (FIRST/LAST flags).
 //
-// with lanes mapped to output rows (no shuffles, coalesced tile-column loads), the
-// accumulator kept in registers across consecutive tasks of one 32-row output chunk
-// (FIRST/LAST flags), and each output chunk owned by exactly one warp per phase
-// (deterministic, race-free; host balances chunks across warps).
-//
-// Phase kinds (two per elimination-tree height):
-//   A (gather):  own[out]   -= acc   (forward: t -= L_{s,d} x_d ; backward: u = x - B^T y)
-//   B (diag):    other[out]  = acc   (forward: x_s = L_ss^{-1} t_s ; backward: y_s = L_ss^{-T} u_s)
-// Forward: own = T, other = X.  Backward: own = X, other = T.  Both in shared memory.
+// Task kinds (forward: own = T, other = X; backward: own = X, other = T):
+//   DIAG : other[out_base + r]  = acc     x_s = L_ss^{-1} t_s     /  y_s = L_ss^{-T} u_s
+//   PUSH : own[outidx[r]]      -= acc     t[R_d] -= L_{R_d,d} x_d (forward off-diagonal)
+//          Q[outidx[r]]        += acc     (PARTIAL: this CTA's contribution into the top)
+//   PULL : own[out_base + r]   -= acc     u_s = x_s - L_{R_s,s}^T y[R_s] (backward)
+// Input column j is in[in_ref + j] (contiguous) or in[idx[j]] (IN_INDEXED).
+// Pushes of one phase never share a target row (supernodes are coloured per height).
 #pragma once
 
 #include <cstdint>
 
 namespace bddc_b200 {
 
-constexpr int kSolveWarps = 16;  // warps per interior-solve CTA (one CTA per subdomain)
+constexpr int kSolveWarps = 16;          // consumer warps per interior-solve CTA
+constexpr int kUnitSlots = 2;            // ring slots per warp (double buffering)
+constexpr int kPhaseStride = 2 * kSolveWarps + 3;
 
 enum TaskFlags : std::uint8_t {
-    kTaskInIndexed = 1,  // input column j read at position idx[in_ref + j], else in_ref + j
+    kTaskInIndexed = 1,  // input column j at idx[j] (int32 list after the values)
     kTaskFirst = 2,      // start a new accumulator
-    kTaskLast = 4,       // flush the accumulator to the output chunk
-    kTaskDiag = 8,       // phase-B store (other[out] = acc) instead of own[out] -= acc
+    kTaskLast = 4,       // flush the accumulator
+    kTaskDiag = 8,       // other[out_base + r] = acc
+    kTaskPush = 16,      // own[outidx[r]] -= acc (outidx after the values / index list)
+    kTaskPartial = 32,   // with PUSH: Q[outidx[r]] += acc
 };
 
+enum PhaseKind : std::int32_t { kPhaseNormal = 0, kPhaseCombine = 1, kPhaseBackward = 2 };
+
+// Each tile in a unit is preceded by its 16-byte header; `next` links the tiles of one
+// unit (offset in 16-byte units from the unit start), kNoTask ends the unit.
+constexpr std::uint32_t kNoTask = 0xffffffffu;
 struct TileTask {
-    std::uint32_t m_off;    // tile offset (doubles) within the subdomain's pass stream
-    std::uint32_t in_ref;   // contiguous input start position, or offset into the index list
-    std::uint16_t out_base; // first row (position) of the 32-row output chunk
-    std::uint16_t ncols;    // tile columns (input length)
-    std::uint8_t nrows;     // tile rows (leading dimension), <= 32
-    std::uint8_t lane_off;  // tile row i is lane i + lane_off
+    std::uint32_t next;     // offset (16-byte units, from the unit start) of the next tile, or kNoTask
+    std::uint32_t in_ref;   // first input local index (contiguous inputs)
+    std::uint16_t out_base; // output chunk start (DIAG / PULL)
+    std::uint16_t ncols;    // tile columns (inputs)
+    std::uint8_t nrows;     // k, <= 32
+    std::uint8_t groups;    // G = floor(32 / k)
     std::uint8_t flags;
-    std::uint8_t nvalid;    // valid lanes of the output chunk on flush
+    std::uint8_t nvalid;    // rows written on flush
 };
 static_assert(sizeof(TileTask) == 16, "TileTask must stay 16 bytes");
 
-// Per-subdomain descriptor for the interior solve and the interface steps.
+// Bytes of one tile in the stream (16-byte aligned sections).
+inline constexpr int tile_iters(int ncols, int groups) { return (ncols + groups - 1) / groups; }
+inline constexpr int tile_value_bytes(int nrows, int ncols, int groups) {
+    return tile_iters(ncols, groups) * nrows * groups * 8;
+}
+inline constexpr int pad16i(int b) { return (b + 15) & ~15; }
+
+// Phase table entry (kPhaseStride int32):
+//   [0 .. W-1]      first unit of each warp in this phase (index into the warp's unit list)
+//   [W .. 2W-1]     end unit (exclusive)
+//   [2W]            kind (PhaseKind bits)
+//   [2W+1, 2W+2]    combine range of local rows [begin, end) (kPhaseCombine, runs after the phase)
+// Unit list of a part: for warp w, entries [warp_base[w], warp_base[w+1]) of int2
+// {offset in 16-byte units from the part stream start, bytes}.
+struct PartDesc {
+    std::int64_t stream;        // offset (doubles) of this part's stream in the pool
+    std::int64_t stream_bytes;  // multiple of 16
+    std::int64_t units;         // offset (int2 entries) of the part's unit list
+    std::int32_t warp_base[kSolveWarps + 1];  // per-warp unit ranges within the part's list
+    std::int64_t gmap;          // local index -> vector index
+    std::int64_t couple_ptr;    // coupling rows per local index (n_loc + 1)
+    std::int64_t couple_ent;    // coupling entries (gamma, value)
+    std::int32_t phases;        // offset (int32) into the phase pool
+    std::int32_t n_phases;
+    std::int32_t n_loc;         // local indices: group rows then top rows
+    std::int32_t n_group;
+    std::int32_t n_top;
+    std::int32_t n_write;       // locals written on output (rank 0 also writes the top)
+    std::int32_t sub;           // subdomain
+    std::int32_t rank;          // 0 .. P-1 within the cluster
+};
+
+// Per-subdomain descriptor for the interface steps and stage hooks.
 struct SubdomainDesc {
-    std::int64_t fwd_stream;   // offset (doubles) of the forward tile stream in the pool
-    std::int64_t bwd_stream;   // offset (doubles) of the backward tile stream
-    std::int64_t fwd_tasks;    // offset of the forward task list
-    std::int64_t bwd_tasks;
-    std::int32_t fwd_phases;   // offset into the phase table (kSolveWarps+1 entries per phase)
-    std::int32_t bwd_phases;
-    std::int32_t n_fwd_phases;
-    std::int32_t n_bwd_phases;
-    std::int64_t idx_base;     // offset of this subdomain's index lists
-    std::int64_t gmap;         // offset: permuted interior position -> vector index
-    std::int64_t couple_ptr;   // offset of coupling CSR row pointers (n_interior+1 entries)
-    std::int64_t couple_ent;   // offset of coupling entries (gamma index, value)
     std::int64_t iface;        // offset: gamma -> vector index / weight / global iface id
-    std::int64_t kmat;         // offset of K_i (n_iface x n_iface, row-major)
-    std::int64_t phig;         // offset of Phi_G (n_iface x n_primal, row-major)
-    std::int64_t phi;          // offset of the full Phi (n_local x n_primal, row-major)
-    std::int64_t primal;       // offset into the primal map pool
-    std::int64_t hbuf;         // offset of this subdomain's h / g scratch (n_iface)
-    std::int64_t cbuf;         // offset of this subdomain's coarse contribution (n_primal)
-    std::int64_t local_dofs;   // offset: local dof -> vector index (stage hooks)
+    std::int64_t kmat;         // K_i (n_iface x n_iface, row-major)
+    std::int64_t phig;         // Phi_G (n_iface x n_primal, row-major)
+    std::int64_t phi;          // full Phi (n_local x n_primal, row-major)
+    std::int64_t primal;       // primal map
+    std::int64_t hbuf;         // h / g scratch (n_iface)
+    std::int64_t cbuf;         // coarse contribution (n_primal)
+    std::int64_t local_dofs;   // local dof -> vector index
+    std::int64_t lrow_ptr;     // local A_GI rows (n_iface + 1) -> (vector index, value)
     std::int32_t n_interior;
     std::int32_t n_iface;
     std::int32_t n_primal;

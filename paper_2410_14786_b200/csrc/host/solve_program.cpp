@@ -1,0 +1,419 @@
+#include "solve_program.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+
+namespace bddc_b200 {
+namespace {
+
+inline std::int64_t pad16(std::int64_t b) { return (b + 15) & ~std::int64_t(15); }
+
+struct Tile {
+    TileTask t{};
+    std::vector<double> vals;
+    std::vector<std::int32_t> idx;     // input index list (IN_INDEXED)
+    std::vector<std::int32_t> outidx;  // output rows (PUSH, last piece)
+    std::int64_t bytes() const {
+        return pad16(static_cast<std::int64_t>(vals.size()) * 8) + pad16(static_cast<std::int64_t>(idx.size()) * 4) +
+               pad16(static_cast<std::int64_t>(outidx.size()) * 4);
+    }
+};
+
+// One output unit (a 32-row chunk of a supernode, or a row chunk of a push), owned by
+// one warp; its pieces accumulate in registers.
+struct Chunk {
+    std::vector<Tile> tiles;
+    std::int64_t cost = 0;
+};
+
+struct Phase {
+    std::vector<Chunk> chunks;
+    std::int32_t kind = kPhaseNormal;
+    std::int32_t comb_begin = 0, comb_end = 0;
+};
+
+// Build the flattened-mapping pieces of one output unit.
+template <typename Val, typename InIdx>
+Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx in_idx, int in_start, int out_base,
+                 int nvalid, std::uint8_t flags, const std::vector<std::int32_t>* outidx) {
+    Chunk ch;
+    if (k < 1 || k > 32 || ncols < 1) throw std::logic_error("solve program: bad tile shape");
+    const int G = 32 / k;
+    // iterations per piece so that header + values + index list + output rows fit a unit
+    const int room = unit_bytes - 16 - 128 - 32;
+    const int per_iter = 8 * k * G + (indexed ? 4 * G : 0);
+    const int per = std::max(1, room / per_iter) * G;  // columns per piece (multiple of G)
+    for (int j0 = 0; j0 < ncols; j0 += per) {
+        const int jn = std::min(per, ncols - j0);
+        const int iters = tile_iters(jn, G);
+        Tile T;
+        T.t.in_ref = indexed ? 0u : static_cast<std::uint32_t>(in_start + j0);
+        T.t.out_base = static_cast<std::uint16_t>(out_base);
+        T.t.ncols = static_cast<std::uint16_t>(jn);
+        T.t.nrows = static_cast<std::uint8_t>(k);
+        T.t.groups = static_cast<std::uint8_t>(G);
+        T.t.nvalid = static_cast<std::uint8_t>(nvalid);
+        T.t.flags = flags | (indexed ? kTaskInIndexed : 0) | (j0 == 0 ? kTaskFirst : 0) |
+                    (j0 + jn >= ncols ? kTaskLast : 0);
+        T.vals.assign(static_cast<std::size_t>(iters) * k * G, 0.0);
+        for (int t = 0; t < iters; ++t)
+            for (int g = 0; g < G; ++g) {
+                const int j = t * G + g;
+                if (j >= jn) continue;
+                for (int r = 0; r < k; ++r)
+                    T.vals[static_cast<std::size_t>(t) * k * G + g * k + r] = val(r, j0 + j);
+            }
+        if (indexed) {
+            T.idx.resize(static_cast<std::size_t>(iters) * G);
+            for (int j = 0; j < iters * G; ++j) T.idx[j] = in_idx(j0 + std::min(j, jn - 1));
+        }
+        if (outidx && (T.t.flags & kTaskLast)) T.outidx = *outidx;
+        ch.cost += iters + 12;
+        ch.tiles.push_back(std::move(T));
+    }
+    return ch;
+}
+
+}  // namespace
+
+void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std::vector<index_t>& l2v, int sub,
+                         int P, int unit_bytes, SolvePools& pools) {
+    const auto& sn = F.snodes;
+    const index_t nsn = static_cast<index_t>(sn.size());
+    const index_t nI = F.n_interior;
+    if (P < 1 || P > 2) throw std::invalid_argument("solve program: parts must be 1 or 2");
+
+    // ---- tree and group assignment (P = 2: halves below the top separator chain)
+    std::vector<std::vector<index_t>> children(nsn);
+    std::vector<index_t> roots;
+    for (index_t s = 0; s < nsn; ++s) {
+        if (sn[s].parent >= 0) children[sn[s].parent].push_back(s);
+        else roots.push_back(s);
+    }
+    std::vector<std::int64_t> weight(nsn, 0);
+    for (index_t s = 0; s < nsn; ++s) {
+        const std::int64_t ns = sn[s].size();
+        weight[s] += ns * (ns + 1) + 2 * ns * sn[s].n_interior_rows;
+        if (sn[s].parent >= 0) weight[sn[s].parent] += weight[s];
+    }
+    std::vector<int> group(nsn, 0);
+    if (P == 2) {
+        std::vector<index_t> tops, split_children;
+        if (roots.size() == 1) {
+            index_t cur = roots[0];
+            while (true) {
+                tops.push_back(cur);
+                if (children[cur].size() == 1) { cur = children[cur][0]; continue; }
+                split_children = children[cur];
+                break;
+            }
+        } else {
+            split_children = roots;
+        }
+        std::sort(split_children.begin(), split_children.end(),
+                  [&](index_t a, index_t b) { return weight[a] != weight[b] ? weight[a] > weight[b] : a < b; });
+        std::int64_t load[2] = {0, 0};
+        std::vector<int> gsub(nsn, -2);
+        for (index_t c : split_children) {
+            const int g = load[0] <= load[1] ? 0 : 1;
+            load[g] += weight[c];
+            gsub[c] = g;
+        }
+        for (index_t t : tops) gsub[t] = -1;
+        for (index_t s = nsn - 1; s >= 0; --s) {
+            if (gsub[s] != -2) { group[s] = gsub[s]; continue; }
+            const index_t p = sn[s].parent;
+            if (p < 0 || group[p] < 0) throw std::logic_error("solve program: supernode without a group");
+            group[s] = group[p];
+        }
+    }
+    std::vector<index_t> top;
+    for (index_t s = 0; s < nsn; ++s)
+        if (group[s] < 0) top.push_back(s);
+    std::vector<index_t> owner(nI, -1);
+    for (index_t s = 0; s < nsn; ++s)
+        for (index_t c = sn[s].col_begin; c < sn[s].col_end; ++c) owner[c] = s;
+
+    for (int part = 0; part < P; ++part) {
+        // local index space: group positions ascending, then top positions ascending
+        std::vector<std::int32_t> loc(nI, -1);
+        std::vector<index_t> locpos;
+        for (index_t p = 0; p < nI; ++p)
+            if (group[owner[p]] == part) { loc[p] = static_cast<std::int32_t>(locpos.size()); locpos.push_back(p); }
+        const std::int32_t n_group = static_cast<std::int32_t>(locpos.size());
+        for (index_t p = 0; p < nI; ++p)
+            if (group[owner[p]] < 0) { loc[p] = static_cast<std::int32_t>(locpos.size()); locpos.push_back(p); }
+        const std::int32_t n_loc = static_cast<std::int32_t>(locpos.size());
+        const std::int32_t n_top = n_loc - n_group;
+        if (n_loc + 64 > 65535) throw std::runtime_error("subdomain interior too large for the solve kernel");
+
+        auto in_group = [&](index_t s) { return group[s] == part; };
+        std::vector<index_t> heights;
+        for (index_t s = 0; s < nsn; ++s)
+            if (in_group(s)) heights.push_back(sn[s].height);
+        std::sort(heights.begin(), heights.end());
+        heights.erase(std::unique(heights.begin(), heights.end()), heights.end());
+
+        auto diag_fwd = [&](index_t s, Phase& ph) {
+            const Supernode& S = sn[s];
+            const index_t ns = S.size();
+            for (index_t r0 = 0; r0 < ns; r0 += 32) {
+                const int nr = static_cast<int>(std::min<index_t>(32, ns - r0));
+                ph.chunks.push_back(make_chunk(unit_bytes, 
+                    nr, static_cast<int>(r0 + nr),
+                    [&](int r, int j) { return j <= r0 + r ? S.Linv[static_cast<std::size_t>(r0 + r) * ns + j] : 0.0; },
+                    false, [](int) { return 0; }, loc[S.col_begin], loc[S.col_begin + r0], nr, kTaskDiag, nullptr));
+            }
+        };
+        auto diag_bwd = [&](index_t s, Phase& ph) {
+            const Supernode& S = sn[s];
+            const index_t ns = S.size();
+            for (index_t q0 = 0; q0 < ns; q0 += 32) {
+                const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
+                ph.chunks.push_back(make_chunk(unit_bytes, 
+                    nq, static_cast<int>(ns - q0),
+                    [&](int r, int j) {
+                        return j >= r ? S.Linv[static_cast<std::size_t>(q0 + j) * ns + q0 + r] : 0.0;
+                    },
+                    false, [](int) { return 0; }, loc[S.col_begin + q0], loc[S.col_begin + q0], nq, kTaskDiag,
+                    nullptr));
+            }
+        };
+        auto pull_bwd = [&](index_t s, Phase& ph) {
+            const Supernode& S = sn[s];
+            const index_t ns = S.size(), mI = S.n_interior_rows;
+            if (mI == 0) return;
+            for (index_t q0 = 0; q0 < ns; q0 += 32) {
+                const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
+                ph.chunks.push_back(make_chunk(unit_bytes, 
+                    nq, static_cast<int>(mI),
+                    [&](int r, int j) { return S.B[static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
+                    [&](int j) {
+                        const std::int32_t l = loc[S.rows[j]];
+                        if (l < 0) throw std::logic_error("solve program: ancestor row not local");
+                        return l;
+                    },
+                    0, loc[S.col_begin + q0], nq, 0, nullptr));
+            }
+        };
+        // t[R_d] -= L_{R_d,d} x_d : rows in the own group (or own top) -> own T, rows in the
+        // shared top from a group supernode -> Q (partial).
+        auto push_fwd = [&](index_t d, Phase& ph, bool from_top) {
+            const Supernode& D = sn[d];
+            const index_t nd = D.size(), mI = D.n_interior_rows;
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool to_top = pass == 1;
+                if (from_top && to_top) continue;
+                std::vector<index_t> rows;  // indices a into R_d
+                for (index_t a = 0; a < mI; ++a) {
+                    const std::int32_t l = loc[D.rows[a]];
+                    if (l < 0) throw std::logic_error("solve program: push target not local");
+                    const bool is_top = !from_top && l >= n_group;
+                    if (is_top == to_top) rows.push_back(a);
+                }
+                for (std::size_t c0 = 0; c0 < rows.size(); c0 += 32) {
+                    const int k = static_cast<int>(std::min<std::size_t>(32, rows.size() - c0));
+                    std::vector<std::int32_t> out(k);
+                    for (int r = 0; r < k; ++r) {
+                        const std::int32_t l = loc[D.rows[rows[c0 + r]]];
+                        out[r] = to_top ? l - n_group : l;
+                    }
+                    ph.chunks.push_back(make_chunk(unit_bytes, 
+                        k, static_cast<int>(nd),
+                        [&](int r, int j) { return D.B[static_cast<std::size_t>(rows[c0 + r]) * nd + j]; }, false,
+                        [](int) { return 0; }, loc[D.col_begin], 0, k,
+                        static_cast<std::uint8_t>(kTaskPush | (to_top ? kTaskPartial : 0)), &out));
+                }
+            }
+        };
+
+        std::vector<Phase> phases;
+        // ---------------- forward sweep: own group, by height
+        for (index_t h : heights) {
+            Phase b;
+            for (index_t s = 0; s < nsn; ++s)
+                if (in_group(s) && sn[s].height == h) diag_fwd(s, b);
+            phases.push_back(std::move(b));
+            // colour the pushes of this height so one phase never writes a row twice
+            std::vector<std::vector<char>> used;
+            std::vector<std::vector<index_t>> classes;
+            for (index_t d = 0; d < nsn; ++d) {
+                if (!in_group(d) || sn[d].height != h || sn[d].n_interior_rows == 0) continue;
+                std::size_t c = 0;
+                for (; c < used.size(); ++c) {
+                    bool clash = false;
+                    for (index_t a = 0; a < sn[d].n_interior_rows && !clash; ++a) clash = used[c][sn[d].rows[a]];
+                    if (!clash) break;
+                }
+                if (c == used.size()) {
+                    used.emplace_back(nI, 0);
+                    classes.emplace_back();
+                }
+                for (index_t a = 0; a < sn[d].n_interior_rows; ++a) used[c][sn[d].rows[a]] = 1;
+                classes[c].push_back(d);
+            }
+            for (const auto& cls : classes) {
+                Phase ph;
+                for (index_t d : cls) push_fwd(d, ph, false);
+                phases.push_back(std::move(ph));
+            }
+        }
+        // ---------------- exchange the partial sums into the shared top (P = 2)
+        if (P == 2) {
+            Phase comb;
+            comb.kind = kPhaseCombine;
+            comb.comb_begin = n_group;
+            comb.comb_end = n_loc;
+            phases.push_back(std::move(comb));
+        }
+        // ---------------- forward sweep: shared top chain (identical in every part)
+        for (index_t s : top) {
+            Phase b, ps;
+            diag_fwd(s, b);
+            push_fwd(s, ps, true);
+            phases.push_back(std::move(b));
+            phases.push_back(std::move(ps));
+        }
+        // ---------------- backward sweep: top chain, then own group by height
+        for (auto it = top.rbegin(); it != top.rend(); ++it) {
+            Phase a, b;
+            a.kind = b.kind = kPhaseBackward;
+            pull_bwd(*it, a);
+            diag_bwd(*it, b);
+            phases.push_back(std::move(a));
+            phases.push_back(std::move(b));
+        }
+        for (auto hit = heights.rbegin(); hit != heights.rend(); ++hit) {
+            Phase a, b;
+            a.kind = b.kind = kPhaseBackward;
+            for (index_t s = 0; s < nsn; ++s)
+                if (in_group(s) && sn[s].height == *hit) {
+                    pull_bwd(s, a);
+                    diag_bwd(s, b);
+                }
+            phases.push_back(std::move(a));
+            phases.push_back(std::move(b));
+        }
+        {
+            std::vector<Phase> kept;
+            for (Phase& ph : phases)
+                if (!ph.chunks.empty() || (ph.kind & kPhaseCombine)) kept.push_back(std::move(ph));
+            phases.swap(kept);
+        }
+
+        // ---------------- emit: LPT warp assignment, then each warp's tiles of a phase are
+        // packed into units of <= unit_bytes (whole tiles, headers linked within the unit)
+        PartDesc pd{};
+        pd.sub = sub;
+        pd.rank = part;
+        pd.n_loc = n_loc;
+        pd.n_group = n_group;
+        pd.n_top = n_top;
+        pd.n_write = part == 0 ? n_loc : n_group;
+        pd.stream = static_cast<std::int64_t>(pools.stream.size());
+        pd.phases = static_cast<std::int32_t>(pools.phases.size());
+        pd.n_phases = static_cast<std::int32_t>(phases.size());
+        std::int64_t pos = 0;
+        std::vector<std::int32_t> table(phases.size() * kPhaseStride, 0);
+        std::vector<std::vector<std::int32_t>> wunits(kSolveWarps);  // per warp: {offset16, bytes} pairs
+        auto ensure = [&](std::int64_t bytes) {
+            const std::size_t need = static_cast<std::size_t>(pd.stream + (bytes + 7) / 8);
+            if (pools.stream.size() < need) pools.stream.resize(need, 0.0);
+        };
+        for (std::size_t pi = 0; pi < phases.size(); ++pi) {
+            Phase& ph = phases[pi];
+            std::vector<index_t> order(ph.chunks.size());
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(),
+                             [&](index_t a, index_t b) { return ph.chunks[a].cost > ph.chunks[b].cost; });
+            std::vector<std::int64_t> load(kSolveWarps, 0);
+            std::vector<std::vector<index_t>> per_warp(kSolveWarps);
+            for (index_t c : order) {
+                const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+                load[w] += ph.chunks[c].cost;
+                per_warp[w].push_back(c);
+            }
+            std::int32_t* row = &table[pi * kPhaseStride];
+            for (int w = 0; w < kSolveWarps; ++w) {
+                std::sort(per_warp[w].begin(), per_warp[w].end());
+                row[w] = static_cast<std::int32_t>(wunits[w].size() / 2);
+                std::int64_t ustart = -1, uused = 0, last_hdr = -1;
+                auto close_unit = [&]() {
+                    if (ustart < 0) return;
+                    wunits[w].push_back(static_cast<std::int32_t>(ustart / 16));
+                    wunits[w].push_back(static_cast<std::int32_t>(uused));
+                    pos = ustart + pad16(uused);
+                    ustart = -1;
+                };
+                for (index_t c : per_warp[w])
+                    for (Tile& t : ph.chunks[c].tiles) {
+                        const std::int64_t nb = 16 + t.bytes();
+                        if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
+                        if (ustart >= 0 && uused + nb > unit_bytes) close_unit();
+                        if (ustart < 0) { ustart = pos; uused = 0; last_hdr = -1; }
+                        ensure(ustart + uused + nb);
+                        char* base = reinterpret_cast<char*>(pools.stream.data() + pd.stream);
+                        char* dst = base + ustart + uused;
+                        TileTask hdr = t.t;
+                        hdr.next = kNoTask;
+                        std::memcpy(dst, &hdr, 16);
+                        std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
+                        std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
+                        if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
+                        off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
+                        if (!t.outidx.empty()) std::memcpy(dst + off, t.outidx.data(), t.outidx.size() * 4);
+                        if (last_hdr >= 0)
+                            reinterpret_cast<TileTask*>(base + ustart + last_hdr)->next =
+                                static_cast<std::uint32_t>(uused / 16);
+                        last_hdr = uused;
+                        uused += nb;
+                        pools.tile_values += static_cast<std::int64_t>(t.vals.size());
+                        ++pools.n_tiles;
+                    }
+                close_unit();
+                row[kSolveWarps + w] = static_cast<std::int32_t>(wunits[w].size() / 2);
+            }
+            row[2 * kSolveWarps] = ph.kind;
+            row[2 * kSolveWarps + 1] = ph.comb_begin;
+            row[2 * kSolveWarps + 2] = ph.comb_end;
+        }
+        const std::int64_t total = pad16(pos);
+        pools.stream.resize(static_cast<std::size_t>(pd.stream + total / 8), 0.0);
+        pd.stream_bytes = total;
+        if (total / 16 > (std::int64_t(1) << 31) - 1) throw std::runtime_error("solve program: part stream too large");
+        pools.phases.insert(pools.phases.end(), table.begin(), table.end());
+        pd.units = static_cast<std::int64_t>(pools.units.size() / 2);
+        pd.warp_base[0] = 0;
+        for (int w = 0; w < kSolveWarps; ++w) {
+            pools.units.insert(pools.units.end(), wunits[w].begin(), wunits[w].end());
+            pd.warp_base[w + 1] = pd.warp_base[w] + static_cast<std::int32_t>(wunits[w].size() / 2);
+            pools.max_units = std::max<std::int32_t>(pools.max_units, static_cast<std::int32_t>(wunits[w].size() / 2));
+        }
+
+        pd.gmap = static_cast<std::int64_t>(pools.gmap.size());
+        for (index_t l = 0; l < n_loc; ++l) pools.gmap.push_back(l2v[F.perm[locpos[l]]]);
+        pd.couple_ptr = static_cast<std::int64_t>(pools.couple_ptr.size());
+        pd.couple_ent = static_cast<std::int64_t>(pools.couple_gamma.size());
+        std::int32_t cnt = 0;
+        pools.couple_ptr.push_back(0);
+        for (index_t l = 0; l < n_loc; ++l) {
+            const index_t v = F.perm[locpos[l]];
+            for (index_t q = A.row_offsets[v]; q < A.row_offsets[v + 1]; ++q)
+                if (A.col_indices[q] >= nI) {
+                    pools.couple_gamma.push_back(A.col_indices[q] - nI);
+                    pools.couple_val.push_back(A.values[q]);
+                    ++cnt;
+                }
+            pools.couple_ptr.push_back(cnt);
+        }
+        pools.max_loc = std::max(pools.max_loc, n_loc);
+        pools.max_top = std::max(pools.max_top, n_top);
+        pools.max_phases = std::max(pools.max_phases, pd.n_phases);
+        pools.parts.push_back(pd);
+    }
+}
+
+}  // namespace bddc_b200

@@ -1,0 +1,33 @@
+// Compiles one subdomain's supernodal factor into the streamed interior-solve
+// program consumed by device/solve.cu (format: device_format.hpp).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "../device_format.hpp"
+#include "factor.hpp"
+
+namespace bddc_b200 {
+
+struct SolvePools {
+    std::vector<double> stream;  // tile values (+ int32 index lists packed in place)
+    std::vector<std::int32_t> units;  // per part, per warp: {offset16, bytes} pairs
+    std::vector<std::int32_t> phases;
+    std::vector<std::int32_t> gmap;
+    std::vector<std::int32_t> couple_ptr, couple_gamma;
+    std::vector<double> couple_val;
+    std::vector<PartDesc> parts;
+    std::int64_t tile_values = 0;   // FP64 values in all tiles (incl. explicit zeros of diag tiles)
+    std::int64_t n_tiles = 0;
+    std::int32_t max_loc = 0, max_top = 0, max_phases = 0, max_units = 0;
+};
+
+// local_to_vec: local dof index (interior first) -> device vector index.
+// parts: 1 (one CTA per subdomain) or 2 (CTA pair in a cluster); unit_bytes: size of the
+// per-warp TMA units (and of each ring slot).
+void build_solve_program(const InteriorFactor& F, const CsrMatrix& A_local,
+                         const std::vector<index_t>& local_to_vec, int sub, int parts, int unit_bytes,
+                         SolvePools& pools);
+
+}  // namespace bddc_b200

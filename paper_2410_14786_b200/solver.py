@@ -146,7 +146,7 @@ class Problem:
 
 
 def gpu_options(device=0, workers=0, coarse_mode="direct", coarse_options: SolverOptions | None = None,
-                leaf_size=16, local_blocks=4) -> L.GpuOptions:
+                leaf_size=16, local_blocks=4, solve_parts=0) -> L.GpuOptions:
     o = L.GpuOptions()
     L.lib().bddc_default_gpu_options(C.byref(o))
     o.device, o.workers = device, workers
@@ -155,7 +155,7 @@ def gpu_options(device=0, workers=0, coarse_mode="direct", coarse_options: Solve
         o.coarse_rel_tolerance = coarse_options.rel_tolerance
         o.coarse_abs_tolerance = coarse_options.abs_tolerance
         o.coarse_max_iterations = coarse_options.max_iterations
-    o.leaf_size, o.local_blocks = leaf_size, local_blocks
+    o.leaf_size, o.local_blocks, o.solve_parts = leaf_size, local_blocks, solve_parts
     return o
 
 
@@ -204,11 +204,12 @@ class Preconditioner:
     """B200 BDDC preconditioner (reference bddc::Preconditioner semantics)."""
 
     def __init__(self, problem: Problem, device: int = 0, workers: int = 0, coarse_mode: str = "direct",
-                 coarse_options: SolverOptions | None = None, leaf_size: int = 16, local_blocks: int = 4):
+                 coarse_options: SolverOptions | None = None, leaf_size: int = 16, local_blocks: int = 4,
+                 solve_parts: int = 0):
         self.problem = problem
         self.n = problem.global_dofs
         h = C.c_void_p()
-        opts = gpu_options(device, workers, coarse_mode, coarse_options, leaf_size, local_blocks)
+        opts = gpu_options(device, workers, coarse_mode, coarse_options, leaf_size, local_blocks, solve_parts)
         L.check(L.lib().bddc_gpu_create(problem.handle, C.byref(opts), C.byref(h)))
         self._h = h
 
@@ -273,6 +274,13 @@ class Preconditioner:
         t = L.KernelTimes()
         L.check(L.lib().bddc_gpu_kernel_times(self._h, C.byref(t), 1 if reset else 0))
         return {k: getattr(t, k) for k, _ in L.KernelTimes._fields_}
+
+    def solve_profile(self) -> np.ndarray:
+        """Per-CTA, per-warp cycle accounting of the last interior solve (diagnostics)."""
+        cap = 1 << 20
+        out = np.zeros(cap, dtype=np.int64)
+        n = L.lib().bddc_gpu_solve_profile(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), cap)
+        return out[:max(n, 0)].reshape(-1, 4)
 
     def synchronize(self) -> None:
         L.check(L.lib().bddc_gpu_synchronize(self._h), self._h)

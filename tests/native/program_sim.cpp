@@ -1,0 +1,207 @@
+// TEST-ONLY: sequential CPU interpreter of the interior-solve program produced by
+// build_device_image (device_format.hpp). Lets the CPU test suite validate the
+// program builder (phase order, tile layout, cluster split, combine steps) without a
+// GPU. It is compiled into tests/native/libbddc_sim.so, never into the product library,
+// and executes exactly the task semantics of device/solve.cu.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "../../paper_2410_14786_b200/csrc/context.hpp"
+#include "../../paper_2410_14786_b200/csrc/host/program.hpp"
+
+using namespace bddc_b200;
+
+namespace {
+
+struct PartState {
+    const PartDesc* pd;
+    std::vector<double> T, X, Q;
+    int ph = 0;
+};
+
+void run_phase(const SolvePools& sp, PartState& st) {
+    const PartDesc& pd = *st.pd;
+    const std::int32_t* row = &sp.phases[pd.phases + st.ph * kPhaseStride];
+    const int kind = row[2 * kSolveWarps];
+    std::vector<double>& own = (kind & kPhaseBackward) ? st.X : st.T;
+    std::vector<double>& other = (kind & kPhaseBackward) ? st.T : st.X;
+    const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
+    for (int w = 0; w < kSolveWarps; ++w) {
+        double acc[32] = {0};
+        const int ua = st.ph == 0 ? 0 : sp.phases[pd.phases + (st.ph - 1) * kPhaseStride + kSolveWarps + w];
+        const int ub = row[kSolveWarps + w];
+        for (int u = ua; u < ub; ++u)
+        for (std::uint32_t cur = 0; cur != kNoTask;) {
+            const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + u)];
+            const char* ubase = base + std::int64_t(ue[0]) * 16;
+            TileTask task;
+            std::memcpy(&task, ubase + std::int64_t(cur) * 16, 16);
+            const char* tb = ubase + std::int64_t(cur) * 16 + 16;
+            cur = task.next;
+            const int k = task.nrows, G = task.groups, iters = tile_iters(task.ncols, G);
+            const double* M = reinterpret_cast<const double*>(tb);
+            const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + pad16i(iters * k * G * 8));
+            const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(
+                tb + pad16i(iters * k * G * 8) + ((task.flags & kTaskInIndexed) ? pad16i(iters * G * 4) : 0));
+            if (task.flags & kTaskFirst)
+                for (double& a : acc) a = 0.0;
+            const std::vector<double>& in = (task.flags & kTaskDiag) ? own : other;
+            for (int r = 0; r < k; ++r) {
+                double s = 0.0;
+                for (int it = 0; it < iters; ++it)
+                    for (int g = 0; g < G; ++g) {
+                        const int j = it * G + g;
+                        const double v = (task.flags & kTaskInIndexed) ? in.at(ix[j]) : in.at(task.in_ref + j);
+                        s += M[it * k * G + g * k + r] * v;
+                    }
+                acc[r] += s;
+            }
+            if (task.flags & kTaskLast)
+                for (int r = 0; r < task.nvalid; ++r) {
+                    if (task.flags & kTaskDiag) other.at(task.out_base + r) = acc[r];
+                    else if (task.flags & kTaskPush) {
+                        if (task.flags & kTaskPartial) st.Q.at(ox[r]) += acc[r];
+                        else own.at(ox[r]) -= acc[r];
+                    } else own.at(task.out_base + r) -= acc[r];
+                }
+        }
+    }
+}
+
+}  // namespace
+
+// Task-shape statistics of the program (development aid).
+extern "C" int bddc_sim_program_stats(int cells, int k, int parts, int leaf_size) {
+    PoissonProblem pp = assemble_poisson(cells, cells, k, k);
+    ProblemData pb;
+    pb.constraints = build_constraints(pp.decomposition);
+    pb.decomposition = std::move(pp.decomposition);
+    pb.global_matrix = std::move(pp.global_matrix);
+    pb.local_matrices = std::move(pp.local_matrices);
+    pb.coords = std::move(pp.coords);
+    FactorOptions fo;
+    fo.leaf_size = leaf_size;
+    const BddcSetup setup = bddc_setup(pb.local_matrices, pb.decomposition, pb.constraints, pb.coords.data(), 8, fo);
+    const DeviceImage img = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
+                                               pb.global_matrix, setup, parts);
+    const SolvePools& sp = img.solve;
+    const PartDesc& pd = sp.parts[parts * (pb.decomposition.n_subdomains / 2)];  // an interior subdomain
+    long cnt[4] = {0}, elems[4] = {0}, iters[4] = {0}, flat[4] = {0};
+    long rows_hist[33] = {0};
+    long critical = 0;
+    for (int ph = 0; ph < pd.n_phases; ++ph) {
+        const std::int32_t* row = &sp.phases[pd.phases + ph * kPhaseStride];
+        const bool bwd = row[2 * kSolveWarps] & kPhaseBackward;
+        const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
+        long crit = 0;
+        for (int w = 0; w < kSolveWarps; ++w) {
+          long wl = 0;
+          const int ua = ph == 0 ? 0 : sp.phases[pd.phases + (ph - 1) * kPhaseStride + kSolveWarps + w];
+          const int ub = row[kSolveWarps + w];
+          for (int u = ua; u < ub; ++u)
+          for (std::uint32_t cur = 0; cur != kNoTask;) {
+            const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + u)];
+            TileTask tk;
+            std::memcpy(&tk, base + std::int64_t(ue[0]) * 16 + std::int64_t(cur) * 16, 16);
+            cur = tk.next;
+            wl += tile_iters(tk.ncols, tk.groups) + 12;
+            const int kind = (bwd ? 2 : 0) + ((tk.flags & kTaskDiag) ? 1 : 0);
+            cnt[kind]++;
+            elems[kind] += tk.nrows * tk.ncols;
+            iters[kind] += tile_iters(tk.ncols, tk.groups);
+            const int g = 32 / tk.nrows;
+            flat[kind] += tk.nrows * tk.groups * tile_iters(tk.ncols, tk.groups); (void)g;
+            rows_hist[tk.nrows]++;
+          }
+          crit = std::max(crit, wl);
+        }
+        critical += crit;
+    }
+    std::printf("critical path (sum over phases of the busiest warp's iterations+overhead): %ld\n", critical);
+    const char* names[4] = {"fwd-A", "fwd-B", "bwd-A", "bwd-B"};
+    std::printf("part stream %ld bytes, phases %d, tasks %ld\n", (long)pd.stream_bytes, pd.n_phases,
+                cnt[0] + cnt[1] + cnt[2] + cnt[3]);
+    for (int i = 0; i < 4; ++i)
+        std::printf("%s: tasks %ld elems %ld iters %ld lane-slots %ld lane-eff %.2f\n", names[i],
+                    cnt[i], elems[i], iters[i], flat[i], flat[i] ? double(elems[i]) / (32.0 * iters[i]) : 0.0);
+    std::printf("rows histogram:");
+    for (int r = 1; r <= 32; ++r)
+        if (rows_hist[r]) std::printf(" %d:%ld", r, rows_hist[r]);
+    std::printf("\n");
+    return 0;
+}
+
+extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
+                                       int use_coords, const double* in, double* out, char* err, int errlen) {
+    try {
+        PoissonProblem pp = assemble_poisson(cells_x, cells_y, kx, ky);
+        ProblemData pb;
+        pb.constraints = build_constraints(pp.decomposition);
+        pb.decomposition = std::move(pp.decomposition);
+        pb.global_matrix = std::move(pp.global_matrix);
+        pb.local_matrices = std::move(pp.local_matrices);
+        if (use_coords) pb.coords = std::move(pp.coords);
+        FactorOptions fo;
+        fo.leaf_size = leaf_size;
+        const BddcSetup setup = bddc_setup(pb.local_matrices, pb.decomposition, pb.constraints,
+                                           pb.coords.empty() ? nullptr : pb.coords.data(), 4, fo);
+        const DeviceImage img = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
+                                                   pb.global_matrix, setup, parts);
+        const SolvePools& sp = img.solve;
+        for (std::size_t i0 = 0; i0 < sp.parts.size(); i0 += parts) {
+            std::vector<PartState> st(parts);
+            for (int c = 0; c < parts; ++c) {
+                const PartDesc& pd = sp.parts[i0 + c];
+                st[c].pd = &pd;
+                st[c].T.resize(pd.n_loc);
+                st[c].X.assign(pd.n_loc + 64, 0.0);
+                st[c].T.resize(pd.n_loc + 64, 0.0);
+                st[c].Q.assign(pd.n_top, 0.0);
+                for (int l = 0; l < pd.n_loc; ++l) st[c].T[l] = in[sp.gmap[pd.gmap + l]];
+            }
+            bool progress = true;
+            while (progress) {
+                progress = false;
+                // run every part up to (and including) its next combine phase
+                std::vector<int> at_combine(parts, -1);
+                for (int c = 0; c < parts; ++c) {
+                    PartState& s = st[c];
+                    while (s.ph < s.pd->n_phases) {
+                        const std::int32_t* row = &sp.phases[s.pd->phases + s.ph * kPhaseStride];
+                        run_phase(sp, s);
+                        ++s.ph;
+                        progress = true;
+                        if (parts > 1 && (row[2 * kSolveWarps] & kPhaseCombine)) {
+                            at_combine[c] = s.ph - 1;
+                            break;
+                        }
+                    }
+                }
+                if (parts > 1 && at_combine[0] >= 0) {
+                    if (at_combine[1] < 0) throw std::logic_error("parts disagree on combine phases");
+                    std::vector<std::vector<double>> Qs = {st[0].Q, st[1].Q};
+                    for (int c = 0; c < parts; ++c) {
+                        const std::int32_t* row = &sp.phases[st[c].pd->phases + at_combine[c] * kPhaseStride];
+                        const int cb = row[2 * kSolveWarps + 1], ce = row[2 * kSolveWarps + 2];
+                        for (int l = cb; l < ce; ++l) {
+                            const int qi = l - st[c].pd->n_group;
+                            st[c].T[l] = (st[c].T[l] - Qs[0][qi]) - Qs[1][qi];
+                        }
+                    }
+                }
+            }
+            for (int c = 0; c < parts; ++c)
+                for (int l = 0; l < st[c].pd->n_write; ++l) out[sp.gmap[st[c].pd->gmap + l]] = st[c].T[l];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 1;
+    }
+}

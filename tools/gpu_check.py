@@ -27,9 +27,11 @@ def run(name, k, m, reps=20, leaf=16):
         out["apply_rel_err"] = float(np.abs(z - g["apply_rhs"]).max() / np.abs(g["apply_rhs"]).max())
     import torch
 
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     rd = torch.tensor(b, device="cuda")
     zd = torch.empty_like(rd)
-    s = torch.cuda.current_stream().cuda_stream
+    s = stream.cuda_stream
     for _ in range(3):
         pre.apply_device(rd.data_ptr(), zd.data_ptr(), s)
     torch.cuda.synchronize()
@@ -41,6 +43,9 @@ def run(name, k, m, reps=20, leaf=16):
     torch.cuda.synchronize()
     out["apply_ms"] = e0.elapsed_time(e1) / reps
     out["apply_GBps"] = st["apply_bytes"] / (out["apply_ms"] * 1e-3) / 1e9
+    za = zd.cpu().numpy()
+    if "apply_rhs" in g:
+        out["apply_dev_rel_err"] = float(np.abs(za - g["apply_rhs"]).max() / np.abs(g["apply_rhs"]).max())
     pre.set_profile(True)
     for _ in range(reps):
         pre.apply_device(rd.data_ptr(), zd.data_ptr(), s)
@@ -65,10 +70,8 @@ def run(name, k, m, reps=20, leaf=16):
 
 
 if __name__ == "__main__":
-    import __graft_entry__ as ge
-
-    ge.smoke()
     leaf = int(os.environ.get("LEAF", "16"))
-    run("k4m8", 4, 8, leaf=leaf)
-    run("c1", 4, 64, leaf=leaf)
-    run("c2", 8, 100, leaf=leaf)
+    cfgs = {"k4m8": (4, 8), "c1": (4, 64), "c2": (8, 100)}
+    names = sys.argv[1:] or list(cfgs)
+    for nm in names:
+        run(nm, *cfgs[nm], leaf=leaf)
