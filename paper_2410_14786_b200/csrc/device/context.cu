@@ -79,7 +79,7 @@ struct GpuContext::Impl {
     // interior-solve program
     DBuf<PartDesc> parts;
     DBuf<double> sstream;
-    DBuf<std::int32_t> units;
+    DBuf<std::int32_t> units, order;
     DBuf<std::int32_t> phases, gmap, couple_ptr, couple_gamma;
     DBuf<double> couple_val;
     SolveLaunch launch;
@@ -131,8 +131,6 @@ struct GpuContext::Impl {
         P.max_top = max_top;
         P.max_iface = max_iface;
         P.debug = debug_solve;
-        P.l2_ahead = l2_ahead;
-        P.dbg = dbg_buf.p;
         return P;
     }
     std::int32_t max_loc = 0, max_top = 0;
@@ -402,15 +400,21 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     int nsm = 148;
     BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
     const int parts = opt.solve_parts > 0 ? opt.solve_parts : (d.n_subdomains <= nsm ? 2 : 1);
-    // largest per-warp TMA unit whose double-buffered rings fit next to the vectors
+    // TMA unit size: the largest for which every warp gets at least two ring slots next to
+    // the vectors (BDDC_UNIT_BYTES overrides, for experiments)
     const int max_smem = max_solve_smem(I.device);
     DeviceImage img;
-    int unit = 4096;
+    int unit = std::getenv("BDDC_UNIT_BYTES") ? std::atoi(std::getenv("BDDC_UNIT_BYTES")) : 4096;
+    int spw = 0;
     for (;; unit /= 2) {
         img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit);
-        if (interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit) <=
-            static_cast<std::size_t>(max_smem))
-            break;
+        const std::size_t fixed = interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit, 0);
+        spw = 0;
+        if (fixed < static_cast<std::size_t>(max_smem)) {
+            const std::size_t fit = (max_smem - fixed) / (static_cast<std::size_t>(kSolveWarps) * unit);
+            spw = fit >= 8 ? 8 : fit >= 4 ? 4 : fit >= 2 ? 2 : 0;
+        }
+        if (spw >= 2) break;
         if (unit <= 1024)
             throw std::runtime_error("subdomain interior (" + std::to_string(img.solve.max_loc) +
                                      " dofs per CTA) exceeds the shared-memory solve capacity");
@@ -431,7 +435,8 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     I.launch.n_parts = static_cast<int>(img.solve.parts.size());
     I.launch.cluster = parts;
     I.launch.unit_bytes = unit;
-    I.launch.smem = interior_solve_smem(I.max_loc, I.max_top, I.max_iface, unit);
+    I.launch.slot_shift = spw == 8 ? 3 : spw == 4 ? 2 : 1;
+    I.launch.smem = interior_solve_smem(I.max_loc, I.max_top, I.max_iface, unit, spw);
 
     BDDC_CUDA(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
     auto upload_pod = [](auto& buf, const auto& vec) {
@@ -441,6 +446,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new I
     };
     upload_pod(I.parts, img.solve.parts);
     I.units.upload(img.solve.units);
+    I.order.upload(img.solve.order);
     if (std::getenv("BDDC_SOLVE_STATS")) {
         I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 4);
         BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));

@@ -17,6 +17,7 @@ namespace {
 
 constexpr int kThreads = kSolveWarps * 32;
 constexpr int kMaxRegEntries = 96;  // per-warp phase / unit tables held in registers (3 per lane)
+constexpr int kMaxWarpSlots = 8;    // ring slots per warp (power of two, <= 8)
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -75,16 +76,19 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     const int unit = S.unit_bytes;
 
     // ---- shared memory carve-up
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);  // [warp][kUnitSlots]
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);  // [warp][kMaxWarpSlots]
     const int ldn = (S.max_loc + 64 + 1) & ~1;
-    double* T = reinterpret_cast<double*>(bars + kSolveWarps * kUnitSlots);
+    double* T = reinterpret_cast<double*>(bars + kSolveWarps * kMaxWarpSlots);
     double* X = T + ldn;
     double* Q = X + ldn;
     double* ZG = Q + ((S.max_top + 1) & ~1);
+    unsigned char* glut = reinterpret_cast<unsigned char*>(ZG + ((S.max_iface + 1) & ~1));  // lane / k, k = 1..32
     unsigned char* ring = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<std::uintptr_t>(ZG + ((S.max_iface + 1) & ~1)) + 127) & ~std::uintptr_t(127));
-    unsigned char* my_ring = ring + static_cast<std::size_t>(warp) * kUnitSlots * unit;
-    std::uint64_t* my_bars = bars + warp * kUnitSlots;
+        (reinterpret_cast<std::uintptr_t>(glut + 33 * 32) + 127) & ~std::uintptr_t(127));
+    const int nsl = 1 << S.slot_shift;  // ring slots per warp
+    const int slot_shift = S.slot_shift;
+    unsigned char* my_ring = ring + static_cast<std::size_t>(warp) * nsl * unit;
+    std::uint64_t* my_bars = bars + warp * kMaxWarpSlots;
 
     const int n_phases = pdr.n_phases;
     const int ubase = pdr.warp_base[warp];
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     const std::int32_t* gtable = S.phases + pdr.phases;
     const unsigned char* src = reinterpret_cast<const unsigned char*>(S.stream + pdr.stream);
 
-    if (lane < kUnitSlots) mbar_init(&my_bars[lane], 1);
+    if (lane < nsl) mbar_init(&my_bars[lane], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
 
@@ -109,28 +113,17 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         uend.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + kSolveWarps + warp) : 0;
         pkind.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + 2 * kSolveWarps) : 0;
     }
-    auto prefetch_l2 = [&](int u) {  // whole warp calls; stage unit u in L2 ahead of its smem fill
-        if (u >= nunits) return;
-        const int o16 = uoff.get(u, units, 2);
-        const int nb = ubytes.get(u, units + 1, 2);
-        if (lane == 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + static_cast<std::int64_t>(o16) * 16),
-                         "r"(nb)
-                         : "memory");
-    };
     auto fetch = [&](int u) {  // whole warp calls; lane 0 issues unit u into its slot
         const int o16 = uoff.get(u, units, 2);
         const int nb = ubytes.get(u, units + 1, 2);
         if (lane == 0) {
-            const int s = u % kUnitSlots;
+            const int s = u & (nsl - 1);
             mbar_expect_tx(&my_bars[s], static_cast<std::uint32_t>(nb));
             bulk_g2s(my_ring + s * unit, src + static_cast<std::int64_t>(o16) * 16, static_cast<std::uint32_t>(nb),
                      &my_bars[s]);
         }
-        prefetch_l2(u + S.l2_ahead);
     };
-    for (int u = kUnitSlots; u < kUnitSlots + S.l2_ahead - 1; ++u) prefetch_l2(u);
-    for (int u = 0; u < kUnitSlots && u < nunits; ++u) fetch(u);
+    for (int u = 0; u < nsl && u < nunits; ++u) fetch(u);
 
     // ---- right-hand side (and, in MODE 1/2, the interface coupling)
     const std::int32_t* gmap = S.gmap + pdr.gmap;
@@ -140,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         X[l] = 0.0;  // padded columns of a tile read finite zeros
     }
     for (int l = tid; l < n_top; l += kThreads) Q[l] = 0.0;
+    for (int i = tid; i < 33 * 32; i += kThreads) glut[i] = static_cast<unsigned char>(i >> 5 ? (i & 31) / (i >> 5) : 0);
     if (MODE != 0) {
         const SubdomainDesc& sd = S.subs[pdr.sub];
         const int ng = sd.n_iface;
@@ -170,17 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
 
     double acc = 0.0;
     int u = 0;  // next unit of this warp
-    long long t_wait = 0, t_bar = 0, t_start = clock64();
     for (int ph = 0; ph < n_phases; ++ph) {
         const int kind = pkind.get(ph, gtable + 2 * kSolveWarps, kPhaseStride);
         const int u_end = uend.get(ph, gtable + kSolveWarps + warp, kPhaseStride);
         double* own = (kind & kPhaseBackward) ? X : T;
         double* other = (kind & kPhaseBackward) ? T : X;
         for (; u < u_end; ++u) {
-            const int s = u % kUnitSlots;
-            const long long tw0 = clock64();
-            mbar_wait(&my_bars[s], (u / kUnitSlots) & 1);
-            t_wait += clock64() - tw0;
+            const int s = u & (nsl - 1);
+            mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
             const unsigned char* ubuf = my_ring + s * unit;
             std::uint32_t cur = 0;
             while (cur != kNoTask) {
@@ -190,35 +181,39 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 cur = task.next;
                 const bool indexed = task.flags & kTaskInIndexed;
                 const int k = task.nrows, G = task.groups, kG = k * G;
-                const int iters = (task.ncols + G - 1) / G;
+                const int iters = task.iters;
                 const int vbytes = (iters * kG * 8 + 15) & ~15;
                 const int ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
                 if (task.flags & kTaskFirst) acc = 0.0;
                 // flattened mapping: lane = g*k + r, columns j = t*G + g
-                const int g = lane / k;
+                const int g = glut[(k << 5) + lane];
                 const unsigned char* tile = hdr + 16;
-                double s0 = 0.0, s1 = 0.0;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 if (lane < kG && S.debug != 1) {
                     const double* M = reinterpret_cast<const double*>(tile) + lane;
                     const double* in = (task.flags & kTaskDiag) ? own : other;
                     int t = 0;
                     if (indexed) {
                         const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
-                        for (; t + 2 <= iters; t += 2) {
+                        for (; t + 4 <= iters; t += 4) {
                             s0 = fma(M[t * kG], in[ix[t * G]], s0);
                             s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
+                            s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
+                            s3 = fma(M[(t + 3) * kG], in[ix[(t + 3) * G]], s3);
                         }
-                        if (t < iters) s0 = fma(M[t * kG], in[ix[t * G]], s0);
+                        for (; t < iters; ++t) s0 = fma(M[t * kG], in[ix[t * G]], s0);
                     } else {
                         const double* v = in + task.in_ref + g;
-                        for (; t + 2 <= iters; t += 2) {
+                        for (; t + 4 <= iters; t += 4) {
                             s0 = fma(M[t * kG], v[t * G], s0);
                             s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
+                            s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
+                            s3 = fma(M[(t + 3) * kG], v[(t + 3) * G], s3);
                         }
-                        if (t < iters) s0 = fma(M[t * kG], v[t * G], s0);
+                        for (; t < iters; ++t) s0 = fma(M[t * kG], v[t * G], s0);
                     }
                 }
-                double tot = s0 + s1;
+                double tot = (s0 + s1) + (s2 + s3);
                 for (int off = 1; off < G; off <<= 1) {
                     const double o = __shfl_down_sync(0xffffffffu, tot, off * k);
                     if (g + off < G) tot += o;
@@ -235,18 +230,17 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                         if (task.flags & kTaskDiag) other[task.out_base + lane] = acc;
                         else own[task.out_base + lane] -= acc;
                     }
+                    __syncwarp();  // later tiles of this warp's job read what was just written
                 }
             }
-            // slot consumed: refill it with the unit kUnitSlots ahead
-            if (u + kUnitSlots < nunits) {
+            // slot consumed: refill it with the unit nsl ahead
+            if (u + nsl < nunits) {
                 __syncwarp();
                 if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                fetch(u + kUnitSlots);
+                fetch(u + nsl);
             }
         }
-        const long long tb0 = clock64();
         __syncthreads();
-        t_bar += clock64() - tb0;
         if (CLUSTER > 1 && (kind & kPhaseCombine)) {
             cluster_sync_all();
             // t_top = (t - Q_rank0) - Q_rank1 : identical arithmetic in both CTAs
@@ -262,13 +256,6 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
     }
 
-    if (S.dbg && lane == 0) {  // instrumentation (debug builds of the timing experiments)
-        long long* d = S.dbg + (static_cast<long long>(blockIdx.x) * kSolveWarps + warp) * 4;
-        d[0] = clock64() - t_start;
-        d[1] = t_wait;
-        d[2] = t_bar;
-        d[3] = nunits;
-    }
     for (int l = tid; l < pdr.n_write; l += kThreads) S.out[gmap[l]] = T[l];
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
 }
@@ -294,11 +281,11 @@ void launch_one(const SolveParams& P, const SolveLaunch& L, cudaStream_t stream)
 
 }  // namespace
 
-std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes) {
-    return static_cast<std::size_t>(kSolveWarps) * kUnitSlots * 8 +
+std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes, int slots_per_warp) {
+    return static_cast<std::size_t>(kSolveWarps) * kMaxWarpSlots * 8 +
            8 * (2 * static_cast<std::size_t>((max_loc + 64 + 1) & ~1) + ((max_top + 1) & ~1) +
                 ((max_iface + 1) & ~1)) +
-           128 + static_cast<std::size_t>(kSolveWarps) * kUnitSlots * unit_bytes;
+           33 * 32 + 128 + static_cast<std::size_t>(kSolveWarps) * slots_per_warp * unit_bytes;
 }
 
 int max_solve_smem(int device) {
@@ -310,6 +297,7 @@ int max_solve_smem(int device) {
 void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaStream_t stream) {
     if (L.n_parts <= 0) return;
     P.unit_bytes = L.unit_bytes;
+    P.slot_shift = L.slot_shift;
     if (L.cluster == 2) {
         if (mode == 0) launch_one<0, 2>(P, L, stream);
         else if (mode == 1) launch_one<1, 2>(P, L, stream);

@@ -24,12 +24,11 @@ struct SolveParams {
     const double* in;
     double* out;
     int unit_bytes;  // set by the launcher
+    int slot_shift;  // log2(ring slots per warp)
     int max_loc;
     int max_top;
     int max_iface;
     int debug;     // timing experiments only: 1 = skip tile math
-    int l2_ahead;  // units staged in L2 ahead of the smem fill
-    long long* dbg;  // optional per-warp cycle accounting [part][warp][4]
 };
 
 struct SolveLaunch {
@@ -37,9 +36,10 @@ struct SolveLaunch {
     int cluster = 1;      // parts per subdomain (1 or 2)
     std::size_t smem = 0;
     int unit_bytes = 0;
+    int slot_shift = 1;
 };
 
-std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes);
+std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int unit_bytes, int slots_per_warp);
 int max_solve_smem(int device);
 // mode 0: out[I] = A_II^{-1} in[I]
 // mode 1: z_G = sum of h over owners (written to out), out[I] = A_II^{-1}(in_I - A_IG z_G)

@@ -38,7 +38,7 @@
 namespace bddc_b200 {
 
 constexpr int kSolveWarps = 16;          // consumer warps per interior-solve CTA
-constexpr int kUnitSlots = 2;            // ring slots per warp (double buffering)
+constexpr int kMaxSlots = 64;            // max ring slots per CTA (shared slot pool)
 constexpr int kPhaseStride = 2 * kSolveWarps + 3;
 
 enum TaskFlags : std::uint8_t {
@@ -59,7 +59,7 @@ struct TileTask {
     std::uint32_t next;     // offset (16-byte units, from the unit start) of the next tile, or kNoTask
     std::uint32_t in_ref;   // first input local index (contiguous inputs)
     std::uint16_t out_base; // output chunk start (DIAG / PULL)
-    std::uint16_t ncols;    // tile columns (inputs)
+    std::uint16_t iters;    // ceil(columns / groups): inner-loop trip count
     std::uint8_t nrows;     // k, <= 32
     std::uint8_t groups;    // G = floor(32 / k)
     std::uint8_t flags;
@@ -80,12 +80,16 @@ inline constexpr int pad16i(int b) { return (b + 15) & ~15; }
 //   [2W]            kind (PhaseKind bits)
 //   [2W+1, 2W+2]    combine range of local rows [begin, end) (kPhaseCombine, runs after the phase)
 // Unit list of a part: for warp w, entries [warp_base[w], warp_base[w+1]) of int2
-// {offset in 16-byte units from the part stream start, bytes}.
+// {offset in 16-byte units from the part stream start, bytes}. The producer streams the
+// part's units in `order` (phase-major, warps interleaved by bytes): int4 entries
+// {offset16, bytes, warp | phase << 8, index of the unit within its warp's list}.
 struct PartDesc {
     std::int64_t stream;        // offset (doubles) of this part's stream in the pool
     std::int64_t stream_bytes;  // multiple of 16
     std::int64_t units;         // offset (int2 entries) of the part's unit list
     std::int32_t warp_base[kSolveWarps + 1];  // per-warp unit ranges within the part's list
+    std::int64_t order;         // offset (int4 entries) of the producer's unit order
+    std::int32_t n_units;
     std::int64_t gmap;          // local index -> vector index
     std::int64_t couple_ptr;    // coupling rows per local index (n_loc + 1)
     std::int64_t couple_ent;    // coupling entries (gamma, value)

@@ -1,6 +1,7 @@
 #include "solve_program.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -30,7 +31,7 @@ struct Chunk {
 };
 
 struct Phase {
-    std::vector<Chunk> chunks;
+    std::vector<std::vector<Chunk>> jobs;  // each job: ordered chunks owned by one warp
     std::int32_t kind = kPhaseNormal;
     std::int32_t comb_begin = 0, comb_end = 0;
 };
@@ -52,7 +53,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         Tile T;
         T.t.in_ref = indexed ? 0u : static_cast<std::uint32_t>(in_start + j0);
         T.t.out_base = static_cast<std::uint16_t>(out_base);
-        T.t.ncols = static_cast<std::uint16_t>(jn);
+        T.t.iters = static_cast<std::uint16_t>(iters);
         T.t.nrows = static_cast<std::uint8_t>(k);
         T.t.groups = static_cast<std::uint8_t>(G);
         T.t.nvalid = static_cast<std::uint8_t>(nvalid);
@@ -71,7 +72,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
             for (int j = 0; j < iters * G; ++j) T.idx[j] = in_idx(j0 + std::min(j, jn - 1));
         }
         if (outidx && (T.t.flags & kTaskLast)) T.outidx = *outidx;
-        ch.cost += iters + 12;
+        ch.cost += iters + 16;  // ~16 iterations' worth of per-tile overhead
         ch.tiles.push_back(std::move(T));
     }
     return ch;
@@ -151,29 +152,25 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         if (n_loc + 64 > 65535) throw std::runtime_error("subdomain interior too large for the solve kernel");
 
         auto in_group = [&](index_t s) { return group[s] == part; };
-        std::vector<index_t> heights;
-        for (index_t s = 0; s < nsn; ++s)
-            if (in_group(s)) heights.push_back(sn[s].height);
-        std::sort(heights.begin(), heights.end());
-        heights.erase(std::unique(heights.begin(), heights.end()), heights.end());
 
-        auto diag_fwd = [&](index_t s, Phase& ph) {
+        using Chunks = std::vector<Chunk>;
+        auto diag_fwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size();
             for (index_t r0 = 0; r0 < ns; r0 += 32) {
                 const int nr = static_cast<int>(std::min<index_t>(32, ns - r0));
-                ph.chunks.push_back(make_chunk(unit_bytes, 
+                out.push_back(make_chunk(unit_bytes,
                     nr, static_cast<int>(r0 + nr),
                     [&](int r, int j) { return j <= r0 + r ? S.Linv[static_cast<std::size_t>(r0 + r) * ns + j] : 0.0; },
                     false, [](int) { return 0; }, loc[S.col_begin], loc[S.col_begin + r0], nr, kTaskDiag, nullptr));
             }
         };
-        auto diag_bwd = [&](index_t s, Phase& ph) {
+        auto diag_bwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size();
             for (index_t q0 = 0; q0 < ns; q0 += 32) {
                 const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
-                ph.chunks.push_back(make_chunk(unit_bytes, 
+                out.push_back(make_chunk(unit_bytes,
                     nq, static_cast<int>(ns - q0),
                     [&](int r, int j) {
                         return j >= r ? S.Linv[static_cast<std::size_t>(q0 + j) * ns + q0 + r] : 0.0;
@@ -182,13 +179,13 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     nullptr));
             }
         };
-        auto pull_bwd = [&](index_t s, Phase& ph) {
+        auto pull_bwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size(), mI = S.n_interior_rows;
             if (mI == 0) return;
             for (index_t q0 = 0; q0 < ns; q0 += 32) {
                 const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
-                ph.chunks.push_back(make_chunk(unit_bytes, 
+                out.push_back(make_chunk(unit_bytes,
                     nq, static_cast<int>(mI),
                     [&](int r, int j) { return S.B[static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
                     [&](int j) {
@@ -199,9 +196,10 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     0, loc[S.col_begin + q0], nq, 0, nullptr));
             }
         };
-        // t[R_d] -= L_{R_d,d} x_d : rows in the own group (or own top) -> own T, rows in the
-        // shared top from a group supernode -> Q (partial).
-        auto push_fwd = [&](index_t d, Phase& ph, bool from_top) {
+        // t[R_d] -= L_{R_d,d} x_d restricted to the target rows accepted by `take`: rows in the
+        // own group (or own top) go to own T, rows in the shared top from a group supernode
+        // go to Q (partial).
+        auto push_fwd = [&](index_t d, Chunks& out, bool from_top, auto take) {
             const Supernode& D = sn[d];
             const index_t nd = D.size(), mI = D.n_interior_rows;
             for (int pass = 0; pass < 2; ++pass) {
@@ -209,6 +207,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 if (from_top && to_top) continue;
                 std::vector<index_t> rows;  // indices a into R_d
                 for (index_t a = 0; a < mI; ++a) {
+                    if (!take(D.rows[a])) continue;
                     const std::int32_t l = loc[D.rows[a]];
                     if (l < 0) throw std::logic_error("solve program: push target not local");
                     const bool is_top = !from_top && l >= n_group;
@@ -216,49 +215,139 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 }
                 for (std::size_t c0 = 0; c0 < rows.size(); c0 += 32) {
                     const int k = static_cast<int>(std::min<std::size_t>(32, rows.size() - c0));
-                    std::vector<std::int32_t> out(k);
+                    std::vector<std::int32_t> outidx(k);
                     for (int r = 0; r < k; ++r) {
                         const std::int32_t l = loc[D.rows[rows[c0 + r]]];
-                        out[r] = to_top ? l - n_group : l;
+                        outidx[r] = to_top ? l - n_group : l;
                     }
-                    ph.chunks.push_back(make_chunk(unit_bytes, 
+                    out.push_back(make_chunk(unit_bytes,
                         k, static_cast<int>(nd),
                         [&](int r, int j) { return D.B[static_cast<std::size_t>(rows[c0 + r]) * nd + j]; }, false,
                         [](int) { return 0; }, loc[D.col_begin], 0, k,
-                        static_cast<std::uint8_t>(kTaskPush | (to_top ? kTaskPartial : 0)), &out));
+                        static_cast<std::uint8_t>(kTaskPush | (to_top ? kTaskPartial : 0)), &outidx));
                 }
             }
         };
+        auto all_rows = [](index_t) { return true; };
+        auto singles = [](Chunks&& cs) {  // level-synchronous phase: every chunk is its own job
+            Phase ph;
+            for (Chunk& c : cs) {
+                ph.jobs.emplace_back();
+                ph.jobs.back().push_back(std::move(c));
+            }
+            return ph;
+        };
 
-        std::vector<Phase> phases;
-        // ---------------- forward sweep: own group, by height
-        for (index_t h : heights) {
-            Phase b;
+        // ---- subtree-to-warp mapping: below the cut every warp solves whole subtrees ("jobs")
+        // sequentially with no CTA barrier; only the levels above the cut are level-synchronous.
+        std::vector<char> local(nsn, 0);
+        std::vector<index_t> job_roots;
+        {
+            std::int64_t total = 0;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && sn[s].height == h) diag_fwd(s, b);
-            phases.push_back(std::move(b));
-            // colour the pushes of this height so one phase never writes a row twice
+                if (in_group(s) && (sn[s].parent < 0 || !in_group(sn[s].parent))) total += weight[s];
+            // subtree jobs per warp (BDDC_JOBS_PER_WARP); off by default: measured on B200 the
+            // serial per-warp chain of a subtree costs more than the level barriers it saves
+            const char* jpw_env = std::getenv("BDDC_JOBS_PER_WARP");
+            const double jpw = jpw_env ? std::atof(jpw_env) : 0.0;
+            const std::int64_t tau = jpw > 0 ? std::max<std::int64_t>(1, static_cast<std::int64_t>(total / (jpw * kSolveWarps))) : 0;
+            for (index_t s = nsn - 1; s >= 0; --s) {  // parents before children
+                if (!in_group(s)) continue;
+                const index_t p = sn[s].parent;
+                const bool parent_local = p >= 0 && in_group(p) && local[p];
+                if (parent_local) { local[s] = 1; continue; }
+                if (weight[s] <= tau) { local[s] = 1; job_roots.push_back(s); }
+            }
+            std::sort(job_roots.begin(), job_roots.end());
+        }
+        std::vector<index_t> job_of(nsn, -1);
+        std::vector<std::vector<index_t>> job_nodes(job_roots.size());  // postorder
+        for (std::size_t j = 0; j < job_roots.size(); ++j) job_of[job_roots[j]] = static_cast<index_t>(j);
+        for (index_t s = nsn - 1; s >= 0; --s)
+            if (local[s] && job_of[s] < 0) job_of[s] = job_of[sn[s].parent];
+        for (index_t s = 0; s < nsn; ++s)
+            if (local[s]) job_nodes[job_of[s]].push_back(s);
+        std::vector<index_t> heights;  // above the cut
+        for (index_t s = 0; s < nsn; ++s)
+            if (in_group(s) && !local[s]) heights.push_back(sn[s].height);
+        std::sort(heights.begin(), heights.end());
+        heights.erase(std::unique(heights.begin(), heights.end()), heights.end());
+
+        // greedy colouring of jobs whose target-row sets intersect
+        auto colour = [&](const std::vector<std::vector<index_t>>& targets) {
             std::vector<std::vector<char>> used;
-            std::vector<std::vector<index_t>> classes;
-            for (index_t d = 0; d < nsn; ++d) {
-                if (!in_group(d) || sn[d].height != h || sn[d].n_interior_rows == 0) continue;
+            std::vector<std::vector<std::size_t>> classes;
+            for (std::size_t j = 0; j < targets.size(); ++j) {
+                if (targets[j].empty()) continue;
                 std::size_t c = 0;
                 for (; c < used.size(); ++c) {
                     bool clash = false;
-                    for (index_t a = 0; a < sn[d].n_interior_rows && !clash; ++a) clash = used[c][sn[d].rows[a]];
+                    for (index_t r : targets[j])
+                        if (used[c][r]) { clash = true; break; }
                     if (!clash) break;
                 }
                 if (c == used.size()) {
                     used.emplace_back(nI, 0);
                     classes.emplace_back();
                 }
-                for (index_t a = 0; a < sn[d].n_interior_rows; ++a) used[c][sn[d].rows[a]] = 1;
-                classes[c].push_back(d);
+                for (index_t r : targets[j]) used[c][r] = 1;
+                classes[c].push_back(j);
             }
-            for (const auto& cls : classes) {
-                Phase ph;
-                for (index_t d : cls) push_fwd(d, ph, false);
-                phases.push_back(std::move(ph));
+            return classes;
+        };
+
+        std::vector<Phase> phases;
+        // ---------------- forward sweep
+        {
+            // (1) warp-local subtrees: diag + pushes inside the subtree, postorder
+            Phase ph;
+            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
+                Chunks job;
+                for (index_t s : job_nodes[j]) {
+                    diag_fwd(s, job);
+                    push_fwd(s, job, false, [&](index_t r) { return local[owner[r]] && job_of[owner[r]] == (index_t)j; });
+                }
+                ph.jobs.push_back(std::move(job));
+            }
+            phases.push_back(std::move(ph));
+            // (2) pushes leaving each subtree, jobs coloured by target rows
+            std::vector<std::vector<index_t>> targets(job_nodes.size());
+            std::vector<Chunks> ext(job_nodes.size());
+            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
+                auto outside = [&](index_t r) { return !(local[owner[r]] && job_of[owner[r]] == (index_t)j); };
+                for (index_t s : job_nodes[j]) {
+                    push_fwd(s, ext[j], false, outside);
+                    for (index_t a = 0; a < sn[s].n_interior_rows; ++a)
+                        if (outside(sn[s].rows[a])) targets[j].push_back(sn[s].rows[a]);
+                }
+            }
+            for (const auto& cls : colour(targets)) {
+                Phase pe;
+                for (std::size_t j : cls) pe.jobs.push_back(std::move(ext[j]));
+                phases.push_back(std::move(pe));
+            }
+        }
+        // (3) levels above the cut, level-synchronous
+        for (index_t h : heights) {
+            Chunks b;
+            std::vector<index_t> nodes;
+            for (index_t s = 0; s < nsn; ++s)
+                if (in_group(s) && !local[s] && sn[s].height == h) {
+                    diag_fwd(s, b);
+                    nodes.push_back(s);
+                }
+            phases.push_back(singles(std::move(b)));
+            std::vector<std::vector<index_t>> targets;
+            std::vector<Chunks> pushes;
+            for (index_t d : nodes) {
+                targets.emplace_back(sn[d].rows.begin(), sn[d].rows.begin() + sn[d].n_interior_rows);
+                pushes.emplace_back();
+                push_fwd(d, pushes.back(), false, all_rows);
+            }
+            for (const auto& cls : colour(targets)) {
+                Phase pp;
+                for (std::size_t j : cls) pp.jobs.push_back(std::move(pushes[j]));
+                phases.push_back(std::move(pp));
             }
         }
         // ---------------- exchange the partial sums into the shared top (P = 2)
@@ -271,36 +360,53 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         // ---------------- forward sweep: shared top chain (identical in every part)
         for (index_t s : top) {
-            Phase b, ps;
+            Chunks b, ps;
             diag_fwd(s, b);
-            push_fwd(s, ps, true);
-            phases.push_back(std::move(b));
-            phases.push_back(std::move(ps));
+            push_fwd(s, ps, true, all_rows);
+            phases.push_back(singles(std::move(b)));
+            Phase pp;
+            pp.jobs.push_back(std::move(ps));
+            phases.push_back(std::move(pp));
         }
-        // ---------------- backward sweep: top chain, then own group by height
+        // ---------------- backward sweep: top chain, levels above the cut, then subtrees
         for (auto it = top.rbegin(); it != top.rend(); ++it) {
-            Phase a, b;
-            a.kind = b.kind = kPhaseBackward;
+            Chunks a, b;
             pull_bwd(*it, a);
             diag_bwd(*it, b);
-            phases.push_back(std::move(a));
-            phases.push_back(std::move(b));
+            Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
+            pa.kind = pb2.kind = kPhaseBackward;
+            phases.push_back(std::move(pa));
+            phases.push_back(std::move(pb2));
         }
         for (auto hit = heights.rbegin(); hit != heights.rend(); ++hit) {
-            Phase a, b;
-            a.kind = b.kind = kPhaseBackward;
+            Chunks a, b;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && sn[s].height == *hit) {
+                if (in_group(s) && !local[s] && sn[s].height == *hit) {
                     pull_bwd(s, a);
                     diag_bwd(s, b);
                 }
-            phases.push_back(std::move(a));
-            phases.push_back(std::move(b));
+            Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
+            pa.kind = pb2.kind = kPhaseBackward;
+            phases.push_back(std::move(pa));
+            phases.push_back(std::move(pb2));
+        }
+        {
+            Phase ph;
+            ph.kind = kPhaseBackward;
+            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
+                Chunks job;
+                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it) {
+                    pull_bwd(*it, job);
+                    diag_bwd(*it, job);
+                }
+                ph.jobs.push_back(std::move(job));
+            }
+            phases.push_back(std::move(ph));
         }
         {
             std::vector<Phase> kept;
             for (Phase& ph : phases)
-                if (!ph.chunks.empty() || (ph.kind & kPhaseCombine)) kept.push_back(std::move(ph));
+                if (!ph.jobs.empty() || (ph.kind & kPhaseCombine)) kept.push_back(std::move(ph));
             phases.swap(kept);
         }
 
@@ -319,21 +425,24 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         std::int64_t pos = 0;
         std::vector<std::int32_t> table(phases.size() * kPhaseStride, 0);
         std::vector<std::vector<std::int32_t>> wunits(kSolveWarps);  // per warp: {offset16, bytes} pairs
+        std::vector<std::int32_t> porder;                             // producer order (int4 entries)
         auto ensure = [&](std::int64_t bytes) {
             const std::size_t need = static_cast<std::size_t>(pd.stream + (bytes + 7) / 8);
             if (pools.stream.size() < need) pools.stream.resize(need, 0.0);
         };
         for (std::size_t pi = 0; pi < phases.size(); ++pi) {
             Phase& ph = phases[pi];
-            std::vector<index_t> order(ph.chunks.size());
+            std::vector<std::int64_t> jcost(ph.jobs.size(), 0);
+            for (std::size_t j = 0; j < ph.jobs.size(); ++j)
+                for (const Chunk& c : ph.jobs[j]) jcost[j] += c.cost;
+            std::vector<index_t> order(ph.jobs.size());
             std::iota(order.begin(), order.end(), 0);
-            std::stable_sort(order.begin(), order.end(),
-                             [&](index_t a, index_t b) { return ph.chunks[a].cost > ph.chunks[b].cost; });
+            std::stable_sort(order.begin(), order.end(), [&](index_t a, index_t b) { return jcost[a] > jcost[b]; });
             std::vector<std::int64_t> load(kSolveWarps, 0);
             std::vector<std::vector<index_t>> per_warp(kSolveWarps);
             for (index_t c : order) {
                 const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-                load[w] += ph.chunks[c].cost;
+                load[w] += jcost[c];
                 per_warp[w].push_back(c);
             }
             std::int32_t* row = &table[pi * kPhaseStride];
@@ -349,7 +458,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     ustart = -1;
                 };
                 for (index_t c : per_warp[w])
-                    for (Tile& t : ph.chunks[c].tiles) {
+                    for (Chunk& ch : ph.jobs[c])
+                    for (Tile& t : ch.tiles) {
                         const std::int64_t nb = 16 + t.bytes();
                         if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
                         if (ustart >= 0 && uused + nb > unit_bytes) close_unit();
@@ -376,6 +486,25 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 close_unit();
                 row[kSolveWarps + w] = static_cast<std::int32_t>(wunits[w].size() / 2);
             }
+            // producer order for this phase: warps' units interleaved by cumulative bytes
+            {
+                std::vector<std::int32_t> cur(kSolveWarps), endu(kSolveWarps);
+                std::vector<std::int64_t> done_bytes(kSolveWarps, 0);
+                for (int w = 0; w < kSolveWarps; ++w) { cur[w] = row[w]; endu[w] = row[kSolveWarps + w]; }
+                while (true) {
+                    int best = -1;
+                    for (int w = 0; w < kSolveWarps; ++w)
+                        if (cur[w] < endu[w] && (best < 0 || done_bytes[w] < done_bytes[best])) best = w;
+                    if (best < 0) break;
+                    const std::int32_t k = cur[best]++;
+                    const std::int32_t off16 = wunits[best][2 * k], nb = wunits[best][2 * k + 1];
+                    porder.push_back(off16);
+                    porder.push_back(nb);
+                    porder.push_back(best | (static_cast<std::int32_t>(pi) << 8));
+                    porder.push_back(k);
+                    done_bytes[best] += nb;
+                }
+            }
             row[2 * kSolveWarps] = ph.kind;
             row[2 * kSolveWarps + 1] = ph.comb_begin;
             row[2 * kSolveWarps + 2] = ph.comb_end;
@@ -386,6 +515,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         if (total / 16 > (std::int64_t(1) << 31) - 1) throw std::runtime_error("solve program: part stream too large");
         pools.phases.insert(pools.phases.end(), table.begin(), table.end());
         pd.units = static_cast<std::int64_t>(pools.units.size() / 2);
+        pd.order = static_cast<std::int64_t>(pools.order.size() / 4);
+        pd.n_units = static_cast<std::int32_t>(porder.size() / 4);
+        pools.order.insert(pools.order.end(), porder.begin(), porder.end());
         pd.warp_base[0] = 0;
         for (int w = 0; w < kSolveWarps; ++w) {
             pools.units.insert(pools.units.end(), wunits[w].begin(), wunits[w].end());

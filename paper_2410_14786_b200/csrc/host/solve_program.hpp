@@ -13,6 +13,7 @@ namespace bddc_b200 {
 struct SolvePools {
     std::vector<double> stream;  // tile values (+ int32 index lists packed in place)
     std::vector<std::int32_t> units;  // per part, per warp: {offset16, bytes} pairs
+    std::vector<std::int32_t> order;  // per part: producer order, int4 {offset16, bytes, warp|phase<<8, k}
     std::vector<std::int32_t> phases;
     std::vector<std::int32_t> gmap;
     std::vector<std::int32_t> couple_ptr, couple_gamma;

@@ -1,4 +1,4 @@
 # timing experiments for the interior solve (dev tool)
-for a in 1 3 12; do
-  echo "l2_ahead=$a"; BDDC_L2_AHEAD=$a timeout 60 python tools/gpu_check.py c2 2>&1 | grep -o "'kernel_times': {[^}]*}"
+for j in 0.5 1 2 4; do
+  echo "jpw=$j"; BDDC_JOBS_PER_WARP=$j timeout 60 python tools/gpu_check.py c2 2>&1 | grep -o "'kernel_times': {[^}]*}\|'hist_rel_err': [0-9.e-]*"
 done
