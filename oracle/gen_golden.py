@@ -43,6 +43,17 @@ CONFIGS = {
     "c2": (8, 100, 1, "history", ["--no-stages"]),
 }
 
+# Problems the reference cannot assemble itself (rectangular layouts, heterogeneous
+# coefficients) reach it through its own bundle ingestion (src/bundle.cpp:113-290): the
+# bundle is written by this repo's exporter, solved by the unmodified reference.
+# name -> (cells_x, cells_y, kx, ky, kappa_decades, kappa_seed, rhs_seed, kind)
+BUNDLES = {
+    "r4x2m8": (32, 16, 4, 2, 0.0, 0, 1, "full"),
+    "h4m8": (32, 32, 4, 4, 2.0, 0x5EED, 1, "full"),
+    "r16x8m8": (128, 64, 16, 8, 0.0, 0, 1, "solve"),
+    "c5": (352, 352, 8, 8, 2.0, 0x5EED, 1, "history"),
+}
+
 MAP_ARRAYS = ("subdomain_dofs", "subdomain_dofs_off", "interior_counts", "class_kind",
               "class_entity", "multiplicity", "primal_maps", "primal_maps_off",
               "A_rowptr", "A_cols", "A_vals", "weights", "constraints_vals",
@@ -55,12 +66,28 @@ def digest(a: np.ndarray) -> str:
 
 
 def run(name: str) -> None:
-    k, m, seed, kind, flags = CONFIGS[name]
-    with tempfile.TemporaryDirectory() as tmp:
-        cmd = [DRIVER, "dump", str(k), str(m), str(seed), tmp, str(min(8, os.cpu_count() or 1))] + flags
-        out = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
-        arrays = {f[:-4]: np.load(os.path.join(tmp, f)) for f in os.listdir(tmp) if f.endswith(".npy")}
-    keep: dict[str, np.ndarray] = {"config": np.array([k, m, seed], dtype=np.int64)}
+    workers = str(min(8, os.cpu_count() or 1))
+    if name in BUNDLES:
+        cx, cy, kx, ky, dec, kseed, seed, kind = BUNDLES[name]
+        flags = ["--plain"]
+        sys.path.insert(0, REPO)
+        from paper_2410_14786_b200 import Problem
+
+        with tempfile.TemporaryDirectory() as bdir, tempfile.TemporaryDirectory() as tmp:
+            prob = Problem.poisson(cx, kx, cy, ky, kappa_decades=dec, kappa_seed=kseed, rhs_seed=seed)
+            manifest = prob.export_bundle(bdir)
+            cmd = [DRIVER, "dumpb", manifest, tmp, workers] + flags
+            out = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
+            arrays = {f[:-4]: np.load(os.path.join(tmp, f)) for f in os.listdir(tmp) if f.endswith(".npy")}
+        config = np.array([cx, cy, kx, ky, int(dec * 1000), kseed, seed], dtype=np.int64)
+    else:
+        k, m, seed, kind, flags = CONFIGS[name]
+        with tempfile.TemporaryDirectory() as tmp:
+            cmd = [DRIVER, "dump", str(k), str(m), str(seed), tmp, workers] + flags
+            out = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
+            arrays = {f[:-4]: np.load(os.path.join(tmp, f)) for f in os.listdir(tmp) if f.endswith(".npy")}
+        config = np.array([k, m, seed], dtype=np.int64)
+    keep: dict[str, np.ndarray] = {"config": config}
     if kind == "full":
         keep.update(arrays)
     else:
@@ -89,7 +116,7 @@ def run(name: str) -> None:
 def main(argv: list[str]) -> None:
     if not os.path.exists(DRIVER):
         subprocess.run(["make", "-C", HERE, "-j8"], check=True)
-    names = argv or list(CONFIGS)
+    names = argv or (list(CONFIGS) + list(BUNDLES))
     for n in names:
         run(n)
 

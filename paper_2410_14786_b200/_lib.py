@@ -132,8 +132,8 @@ _lib = None
 
 def header_symbols() -> list[str]:
     """Every function the public header declares (for the export check)."""
-    text = open(HEADER_PATH).read()
-    return sorted(set(re.findall(r"^[a-z_0-9 ]*?\b(bddc_[a-z_0-9]+)\s*\(", text, flags=re.M)))
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER_PATH).read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(bddc_[a-z_0-9]+)\s*\(", text)))
 
 
 def lib() -> C.CDLL:

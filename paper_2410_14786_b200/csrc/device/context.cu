@@ -378,14 +378,16 @@ struct GpuContext::Impl {
     }
 };
 
-GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) : impl_(new Impl) {
-    Impl& I = *impl_;
-    I.pb = std::move(problem);
-    I.opt = opt;
+GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
     if (opt.device < 0 || opt.device >= ndev) throw std::invalid_argument("bad device index");
+    BDDC_CUDA(cudaSetDevice(opt.device));
+    impl_.reset(new Impl);
+    Impl& I = *impl_;
+    I.pb = std::move(problem);
+    I.opt = opt;
     I.device = opt.device;
     BDDC_CUDA(cudaSetDevice(I.device));
     const Decomposition& d = I.pb.decomposition;

@@ -72,6 +72,61 @@ class Problem:
                                              kappa_seed, rhs_seed, C.byref(h)))
         return cls(h.value)
 
+    @classmethod
+    def from_arrays(cls, global_matrix, local_matrices, subdomain_dofs, interior_counts, weights,
+                    constraint_matrices, primal_maps, n_coarse, class_kind=None, class_entity=None,
+                    multiplicity=None, rhs=None, coords=None) -> "Problem":
+        """Drop-in path for externally decomposed problems (the reference's in-memory
+        Decomposition + ConstraintSet + matrices). CSR arguments are (nrows, ncols, rowptr,
+        cols, vals) tuples; everything is deep-copied by the library."""
+        keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a
+
+        def csr(m):
+            nr, nc, rp, ci, va = m
+            rp, ci, va = arr(rp, np.int32), arr(ci, np.int32), arr(va, np.float64)
+            return L.CsrView(int(nr), int(nc), rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                             ci.ctypes.data_as(C.POINTER(C.c_int32)), va.ctypes.data_as(C.POINTER(C.c_double)))
+
+        ns = len(local_matrices)
+        v = L.ProblemView()
+        v.n_subdomains, v.global_dofs, v.n_coarse = ns, int(global_matrix[0]), int(n_coarse)
+        v.global_matrix = csr(global_matrix)
+        locs = (L.CsrView * ns)(*[csr(m) for m in local_matrices])
+        cons = (L.CsrView * ns)(*[csr(m) for m in constraint_matrices])
+        keep += [locs, cons]
+        v.local_matrices, v.constraint_matrices = locs, cons
+        doff = arr(np.concatenate([[0], np.cumsum([len(d) for d in subdomain_dofs])]), np.int64)
+        poff = arr(np.concatenate([[0], np.cumsum([len(p) for p in primal_maps])]), np.int64)
+        ptr = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+        v.dof_offsets = ptr(doff, C.c_int64)
+        v.subdomain_dofs = ptr(arr(np.concatenate(subdomain_dofs), np.int32), C.c_int32)
+        v.weights = ptr(arr(np.concatenate(weights), np.float64), C.c_double)
+        v.interior_counts = ptr(arr(interior_counts, np.int32), C.c_int32)
+        v.primal_offsets = ptr(poff, C.c_int64)
+        v.primal_maps = ptr(arr(np.concatenate(primal_maps), np.int32), C.c_int32)
+        if class_kind is not None:
+            v.class_kind = ptr(arr(class_kind, np.uint8), C.c_uint8)
+        if class_entity is not None:
+            v.class_entity = ptr(arr(class_entity, np.int32), C.c_int32)
+        if multiplicity is not None:
+            v.multiplicity = ptr(arr(multiplicity, np.int32), C.c_int32)
+        if rhs is not None:
+            v.rhs = ptr(arr(rhs, np.float64), C.c_double)
+        if coords is not None:
+            v.coords = ptr(arr(coords, np.int32), C.c_int32)
+        h = C.c_void_p()
+        L.check(L.lib().bddc_problem_from_view(C.byref(v), C.byref(h)))
+        return cls(h.value)
+
+    def coords(self):
+        v = self._view
+        return self._arr(v.coords, 2 * v.global_dofs) if v.coords else None
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and h.value:

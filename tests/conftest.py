@@ -32,3 +32,12 @@ def gpu():
     if not has_gpu():
         pytest.fail("GPU test selected but no CUDA device is visible (no CPU fallback exists)")
     return 0
+
+
+def history_err(h, ref) -> float:
+    """Max elementwise difference of two relative-residual histories, relative to
+    max(ref, 1e-6): relative for the entries that carry information, absolute (scaled)
+    for entries already at round-off level. Parity target (BASELINE.json): <= 1e-10."""
+    h, ref = np.asarray(h, dtype=float), np.asarray(ref, dtype=float)
+    n = min(h.size, ref.size)
+    return float(np.max(np.abs(h[:n] - ref[:n]) / np.maximum(ref[:n], 1e-6)))

@@ -1,0 +1,134 @@
+"""Host setup (C++; no GPU): coarse bases, multipliers, coarse blocks and the coarse
+matrix against the reference (tests/golden), plus the reference's setup identities
+(test_bddc.cpp:56-125, 371-402) and the device-program builder via its CPU simulator."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import bddc_oracle as o
+from conftest import ROOT, golden
+from paper_2410_14786_b200 import BddcError, HostSetup, InvalidArgument, Problem
+from paper_2410_14786_b200 import _lib
+
+
+@pytest.mark.parametrize("name", ["k2m4", "k3m4", "k3m6", "k4m8", "r4x2m8", "h4m8"])
+def test_blocks_match_reference(name):
+    g = golden(name)
+    cfg = [int(v) for v in g["config"]]
+    if len(cfg) == 3:
+        k, m, seed = cfg
+        p = Problem.poisson(k * m, k, rhs_seed=seed)
+    else:
+        cx, cy, kx, ky, dm, ks, seed = cfg
+        p = Problem.poisson(cx, kx, cy, ky, kappa_decades=dm / 1000.0, kappa_seed=ks, rhs_seed=seed)
+    s = HostSetup(p, workers=4)
+    phi = np.concatenate([s.blocks(i)[0].ravel() for i in range(p.n_subdomains)])
+    lam = np.concatenate([s.blocks(i)[1].ravel() for i in range(p.n_subdomains)])
+    aci = np.concatenate([s.blocks(i)[2].ravel() for i in range(p.n_subdomains)])
+    scale = max(1.0, np.abs(g["aci"]).max())
+    assert np.abs(phi - g["phi"]).max() < 1e-11
+    assert np.abs(lam - g["lambda"]).max() < 1e-11 * scale
+    assert np.abs(aci - g["aci"]).max() < 1e-11 * scale
+    rp, ci, v = s.coarse_matrix()
+    assert np.array_equal(rp, g["Ac_rowptr"]) and np.array_equal(ci, g["Ac_cols"])
+    assert np.abs(v - g["Ac_vals"]).max() < 1e-11 * scale
+
+
+def test_saddle_identities():
+    # test_bddc.cpp:56-91: C Phi = I, A Phi + C^T Lambda = 0, A_ci symmetric
+    p = Problem.poisson(12, 3)
+    s = HostSetup(p)
+    for i in range(p.n_subdomains):
+        phi, lam, aci = s.blocks(i)
+        A = o.Csr(*p.local_matrix(i)).dense()
+        Cm = o.Csr(*p.constraint_matrix(i)).dense()
+        assert np.abs(Cm @ phi - np.eye(Cm.shape[0])).max() <= 1e-10
+        assert np.abs(A @ phi + Cm.T @ lam).max() <= 1e-10 * np.abs(A).sum(1).max()
+        assert np.abs(aci - aci.T).max() <= 1e-12
+
+
+def test_floating_subdomain_coarse_block():
+    # test_bddc.cpp:93-107: centre subdomain block is PSD with constants in its null space
+    p = Problem.poisson(12, 3)
+    s = HostSetup(p)
+    aci = s.blocks(4)[2]
+    assert aci.shape == (8, 8)
+    eig = np.linalg.eigvalsh(aci)
+    assert abs(eig[0]) <= 1e-10 and eig[1] > 1e-6
+    assert np.abs(aci @ np.ones(8)).max() <= 1e-10
+    assert np.linalg.eigvalsh(s.blocks(0)[2])[0] > 1e-8
+
+
+def test_interior_factor_solves():
+    p = Problem.poisson(24, 3)
+    s = HostSetup(p, leaf_size=8)
+    for i in (0, 4):
+        ni = int(p.interior_counts()[i])
+        A = o.Csr(*p.local_matrix(i)).dense()[:ni, :ni]
+        b = np.random.default_rng(i).standard_normal(ni)
+        x = s.interior_solve(i, b)
+        assert np.abs(A @ x - b).max() <= 1e-12 * np.abs(b).max() * 10
+
+
+def test_setup_error_names_subdomain():
+    # test_bddc.cpp:371-402: duplicated constraint rows make subdomain 0 singular
+    p = Problem.poisson(8, 2)
+    cons = [p.constraint_matrix(i) for i in range(p.n_subdomains)]
+    nr, nc, rp, ci, va = cons[0]
+    row0 = slice(rp[0], rp[1])
+    dup = (2, nc, np.array([0, rp[1] - rp[0], 2 * (rp[1] - rp[0])]), np.concatenate([ci[row0], ci[row0]]),
+           np.concatenate([va[row0], va[row0]]))
+    pm = p.primal_maps()
+    pm[0] = np.array([0, 1])
+    broken = Problem.from_arrays(p.global_matrix(), [p.local_matrix(i) for i in range(p.n_subdomains)],
+                                 p.subdomain_dofs(), p.interior_counts(), p.weights(), [dup] + cons[1:], pm,
+                                 p.n_coarse, *p.classes(), p.multiplicity(), p.rhs())
+    with pytest.raises(BddcError, match="bddc setup: subdomain 0"):
+        HostSetup(broken)
+
+
+def test_from_arrays_round_trip():
+    p = Problem.poisson(16, 2)
+    q = Problem.from_arrays(p.global_matrix(), [p.local_matrix(i) for i in range(4)], p.subdomain_dofs(),
+                            p.interior_counts(), p.weights(), [p.constraint_matrix(i) for i in range(4)],
+                            p.primal_maps(), p.n_coarse, *p.classes(), p.multiplicity(), p.rhs())
+    a, b = HostSetup(p), HostSetup(q)  # q has no coords: graph nested dissection
+    for i in range(4):
+        assert np.abs(a.blocks(i)[0] - b.blocks(i)[0]).max() < 1e-12
+    with pytest.raises(InvalidArgument):
+        bad = [p.local_matrix(i) for i in range(4)]
+        nr, nc, rp, ci, va = bad[0]
+        bad[0] = (nr, nc, rp, ci[::-1].copy(), va)  # unsorted columns
+        Problem.from_arrays(p.global_matrix(), bad, p.subdomain_dofs(), p.interior_counts(), p.weights(),
+                            [p.constraint_matrix(i) for i in range(4)], p.primal_maps(), p.n_coarse)
+
+
+# ---- device-program builder, executed by the test-only CPU interpreter (tests/native)
+SIM = os.path.join(ROOT, "tests", "native", "libbddc_sim.so")
+
+
+@pytest.fixture(scope="module")
+def sim():
+    import subprocess
+
+    _lib.lib()
+    subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "native"), "-s"], check=True)
+    return C.CDLL(SIM)
+
+
+@pytest.mark.parametrize("k,m,parts,leaf,coords", [(2, 4, 1, 16, 1), (3, 6, 2, 16, 1), (4, 8, 2, 4, 1),
+                                                   (4, 16, 2, 16, 1), (4, 16, 2, 8, 0), (3, 32, 1, 16, 0),
+                                                   (3, 32, 2, 16, 1)])
+def test_device_program_reproduces_interior_solve(sim, k, m, parts, leaf, coords):
+    prob, cs, b = o.poisson_setup(k, m)
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    ref = P.interior_correction(b)
+    out = np.zeros_like(b)
+    err = C.create_string_buffer(512)
+    dp = C.POINTER(C.c_double)
+    rc = sim.bddc_sim_interior_solve(k * m, k * m, k, k, parts, leaf, coords, b.ctypes.data_as(dp),
+                                     out.ctypes.data_as(dp), err, 512)
+    assert rc == 0, err.value
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()

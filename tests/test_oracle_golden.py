@@ -1,0 +1,109 @@
+"""Pins the CPU oracle (oracle/bddc_oracle.py) to the unmodified reference.
+
+Fixtures in tests/golden/ were produced by oracle/gen_golden.py running the reference
+library compiled from /root/reference/proj/src (oracle/Makefile). Mirrors the reference's
+own tests: map KATs (test_decomposition.cpp), PCG KATs (test_krylov.cpp), acceptance
+iteration counts (proj/test_output.txt:15).
+"""
+import numpy as np
+import pytest
+
+import bddc_oracle as o
+from conftest import golden, history_err
+
+SMALL = ["k2m4", "k3m4", "k3m6", "k4m8"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_problem_layer_bit_exact(name):
+    g = golden(name)
+    k, m, seed = (int(v) for v in g["config"])
+    prob, cs, b = o.poisson_setup(k, m, seed=seed)
+    d = prob.decomposition
+    assert np.array_equal(np.concatenate(d.subdomain_dofs), g["subdomain_dofs"])
+    assert np.array_equal(d.interior_counts, g["interior_counts"])
+    assert np.array_equal(d.kind, g["class_kind"])
+    assert np.array_equal(d.entity, g["class_entity"])
+    assert np.array_equal(d.multiplicity, g["multiplicity"])
+    assert np.array_equal(np.concatenate(d.weights), g["weights"])
+    assert np.array_equal(np.concatenate(cs.primal_maps), g["primal_maps"])
+    assert np.array_equal(np.concatenate([c.vals for c in cs.constraint_matrices]), g["constraints_vals"])
+    A = prob.global_matrix
+    assert np.array_equal(A.rowptr, g["A_rowptr"]) and np.array_equal(A.cols, g["A_cols"])
+    assert np.array_equal(A.vals, g["A_vals"])  # same summation order => bit-identical
+    assert np.array_equal(np.concatenate([L.vals for L in prob.local_matrices]), g["locals_vals"])
+    assert np.array_equal(b, g["rhs"])
+
+
+def test_study_rhs_matches_libstdcxx():
+    g = golden("c2")
+    b = o.study_rhs(799 * 799, 1)
+    stride = int(g["pcg_x_sample_stride"][0])
+    assert np.array_equal(b[::stride], g["rhs_sample"])
+
+
+def test_q1_element_matrix_kat():
+    # test_decomposition.cpp:15-27: (1/6)[[4,-1,-2,-1],...]
+    K = o.q1_element_matrix()
+    ref = np.array([[4, -1, -2, -1], [-1, 4, -1, -2], [-2, -1, 4, -1], [-1, -2, -1, 4]]) / 6.0
+    assert np.abs(K - ref).max() < 1e-15
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_setup_and_apply(name):
+    g = golden(name)
+    k, m, seed = (int(v) for v in g["config"])
+    prob, cs, b = o.poisson_setup(k, m, seed=seed)
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    assert np.abs(np.concatenate([p.ravel() for p in P.phi]) - g["phi"]).max() < 1e-12
+    assert np.abs(P.Ac.vals - g["Ac_vals"]).max() < 1e-12
+    z = P.apply(b)
+    assert np.abs(z - g["apply_rhs"]).max() <= 1e-12 * np.abs(g["apply_rhs"]).max()
+    for stage in ("u0", "v1", "v2", "v3"):
+        pass  # stage vectors are checked against the GPU in test_gpu_parity.py
+    cond = g["stage_condensed"]
+    assert np.abs(P.coarse_correction(cond) - g["stage_v1"]).max() < 1e-10
+    assert np.abs(P.local_correction(cond) - g["stage_v2"]).max() < 1e-10
+    assert np.abs(P.interior_correction(b) - g["stage_u0"]).max() < 1e-10
+
+
+@pytest.mark.parametrize("name", SMALL + ["k2m32", "k3m32"])
+def test_oracle_pcg_matches_reference(name):
+    g = golden(name)
+    k, m, seed = (int(v) for v in g["config"])
+    prob, cs, b = o.poisson_setup(k, m, seed=seed)
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    x, rep = o.pcg(prob.global_matrix, b, P.apply, 1e-8, 0.0, 10000, True)
+    assert rep.iterations == int(g["pcg_report"][0])
+    h = np.array(rep.residual_history)
+    assert history_err(h, g["pcg_history"]) < 1e-9
+    assert np.abs(x - g["pcg_x"]).max() <= 1e-10 * np.abs(g["pcg_x"]).max()
+
+
+def test_acceptance_iteration_kats():
+    # proj/test_output.txt:15: bddc={5,8,9,9,9,9}, plain={134,204,265,335,399,529}
+    bddc = [int(golden(f"k{k}m32")["pcg_report"][0]) for k in (2, 3, 4, 5, 6, 8)]
+    plain = [int(golden(f"k{k}m32")["plain_report"][0]) for k in (2, 3, 4, 5, 6, 8)]
+    assert bddc == [5, 8, 9, 9, 9, 9]
+    assert plain == [134, 204, 265, 335, 399, 529]
+
+
+def test_dense_oracle_full_matches_reference_apply():
+    # acceptance criterion 2 (acceptance.cpp:250-267): densified apply == B + (I-BA)C(I-AB)
+    g = golden("k2m4")
+    prob, cs, b = o.poisson_setup(2, 4)
+    M = o.dense_oracle_full(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    assert np.abs(M @ b - g["apply_rhs"]).max() < 1e-12
+
+
+def test_pcg_kats():
+    # test_krylov.cpp:35-44: 3x3 Laplacian -> x = (0.75, 0.5, 0.25)
+    A = o.csr_from_triplets(3, 3, [0, 0, 1, 1, 1, 2, 2], [0, 1, 0, 1, 2, 1, 2], [2, -1, -1, 2, -1, -1, 2])
+    x, rep = o.pcg(A, np.array([1.0, 0.0, 0.0]), None, 1e-12, 0, 100, True)
+    assert np.abs(x - [0.75, 0.5, 0.25]).max() < 1e-12
+    # zero rhs: converged, zero iterations (test_krylov.cpp:113-120)
+    x, rep = o.pcg(A, np.zeros(3), None, 1e-8, 0, 10, True)
+    assert rep.converged and rep.iterations == 0 and not x.any()
+    with pytest.raises(RuntimeError, match="matrix not SPD"):
+        N = o.csr_from_triplets(2, 2, [0, 1], [0, 1], [1.0, -1.0])
+        o.pcg(N, np.array([0.0, 1.0]), None, 1e-8, 0, 10)
