@@ -119,10 +119,12 @@ typedef struct {
     int32_t unique_subdomains;    /* distinct setup problems after exact deduplication */
     int32_t max_interior;
     int32_t max_interface;
+    int64_t interior_dofs;        /* sum of n_I over subdomains */
 } bddc_stats;
 
 typedef struct {
     double interior_ms; /* summed over profiled applies: both batched interior solves */
+    int64_t interior_launches;
     double iface_ms;    /* interface restrict + coarse + local */
     double apply_ms;
     int64_t applies;
@@ -134,6 +136,8 @@ typedef struct bddc_gpu_ctx bddc_gpu_ctx;
 
 const char* bddc_last_error(void);
 int32_t bddc_abi_version(void);
+/* Kernel launches issued by this library in this process so far (all contexts). */
+int64_t bddc_kernel_launches(void);
 void bddc_default_gpu_options(bddc_gpu_options* opt);
 void bddc_default_solver_options(bddc_solver_options* opt);
 

@@ -64,11 +64,11 @@ class SolveReport(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("setup_seconds", f64), ("factor_values", i64), ("interior_solve_bytes", i64),
                 ("apply_bytes", i64), ("n_subdomains", i32), ("global_dofs", i32), ("n_coarse", i32),
-                ("unique_subdomains", i32), ("max_interior", i32), ("max_interface", i32)]
+                ("unique_subdomains", i32), ("max_interior", i32), ("max_interface", i32), ("interior_dofs", i64)]
 
 
 class KernelTimes(C.Structure):
-    _fields_ = [("interior_ms", f64), ("iface_ms", f64), ("apply_ms", f64), ("applies", i64)]
+    _fields_ = [("interior_ms", f64), ("interior_launches", i64), ("iface_ms", f64), ("apply_ms", f64), ("applies", i64)]
 
 
 vp = C.c_void_p
@@ -76,6 +76,7 @@ pd = P(f64)
 SIGNATURES = {
     "bddc_last_error": (C.c_char_p, []),
     "bddc_abi_version": (i32, []),
+    "bddc_kernel_launches": (i64, []),
     "bddc_default_gpu_options": (None, [P(GpuOptions)]),
     "bddc_default_solver_options": (None, [P(SolverOptions)]),
     "bddc_problem_poisson": (C.c_int, [i32, i32, i32, i32, f64, u64, u64, P(vp)]),

@@ -176,7 +176,9 @@ void copy_coarse(const CsrMatrix& A, int32_t* nnz, int32_t* rp, int32_t* ci, dou
 extern "C" {
 
 const char* bddc_last_error(void) { return g_last_error.c_str(); }
-int32_t bddc_abi_version(void) { return 1; }
+int32_t bddc_abi_version(void) { return 2; }
+
+int64_t bddc_kernel_launches(void) { return g_kernel_launches.load(); }
 
 void bddc_default_gpu_options(bddc_gpu_options* o) {
     if (!o) return;
@@ -346,6 +348,7 @@ int bddc_host_setup_stats(const bddc_host_setup* s, bddc_stats* st) {
         st->setup_seconds = s->setup.seconds;
         for (const auto& sub : s->setup.subs) {
             st->factor_values += sub.factor.factor_values();
+            st->interior_dofs += sub.n_interior;
             st->max_interior = std::max(st->max_interior, sub.n_interior);
             st->max_interface = std::max(st->max_interface, sub.n_iface);
         }
@@ -441,6 +444,7 @@ int bddc_gpu_get_stats(const bddc_gpu_ctx* c, bddc_stats* st) {
         st->n_coarse = g.problem().constraints.n_coarse;
         st->unique_subdomains = g.setup().unique_subdomains;
         for (const auto& sub : g.setup().subs) {
+            st->interior_dofs += sub.n_interior;
             st->max_interior = std::max(st->max_interior, sub.n_interior);
             st->max_interface = std::max(st->max_interface, sub.n_iface);
         }
@@ -457,12 +461,14 @@ int bddc_gpu_set_profile(bddc_gpu_ctx* c, int32_t on) {
 int bddc_gpu_kernel_times(const bddc_gpu_ctx* c, bddc_kernel_times* t, int32_t reset) {
     return guarded([&] {
         if (!c || !t) throw std::invalid_argument("null argument");
-        const KernelTimes k = c->ctx->kernel_times();
+        GpuContext& g = const_cast<GpuContext&>(*c->ctx);
+        const KernelTimes k = g.kernel_times();
         t->interior_ms = k.interior_ms;
+        t->interior_launches = k.interior_launches;
         t->iface_ms = k.iface_ms;
         t->apply_ms = k.apply_ms;
         t->applies = k.applies;
-        if (reset) const_cast<GpuContext&>(*c->ctx).reset_kernel_times();
+        if (reset) g.reset_kernel_times();
     });
 }
 

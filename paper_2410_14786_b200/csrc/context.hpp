@@ -3,6 +3,7 @@
 // this header (the C-ABI layer in capi.cpp includes it from plain C++).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -13,6 +14,9 @@
 #include "host/setup.hpp"
 
 namespace bddc_b200 {
+
+// Kernel launches issued by this library in this process (defined in device/context.cu).
+extern std::atomic<std::int64_t> g_kernel_launches;
 
 struct GpuOptions {
     int device = 0;
@@ -52,6 +56,7 @@ struct ProblemData {
 
 struct KernelTimes {
     double interior_ms = 0.0;   // both interior solves
+    std::int64_t interior_launches = 0;
     double iface_ms = 0.0;      // restrict + coarse + local
     double apply_ms = 0.0;
     std::int64_t applies = 0;
@@ -82,7 +87,7 @@ public:
     std::int64_t interior_pass_bytes() const;  // stream bytes of one batched interior solve
     int solve_parts() const;
     std::int64_t factor_values() const;
-    KernelTimes kernel_times() const;
+    KernelTimes kernel_times();
     void reset_kernel_times();
     void set_profile(bool on);
     int device() const;

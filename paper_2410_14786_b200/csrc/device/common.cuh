@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -17,6 +18,16 @@ namespace bddc_b200 {
         if (err__ != cudaSuccess)                                                              \
             throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(err__) + \
                                      " at " + __FILE__ + ":" + std::to_string(__LINE__));      \
+    } while (0)
+
+// Kernel launches issued by this library in this process (bench.py's gpu_launches).
+extern std::atomic<std::int64_t> g_kernel_launches;
+
+// Every launch site is followed by exactly one BDDC_LAUNCHED(): checks the launch and counts it.
+#define BDDC_LAUNCHED()                                                    \
+    do {                                                                   \
+        BDDC_CUDA(cudaGetLastError());                                     \
+        ::bddc_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     } while (0)
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -16,6 +16,9 @@
 #include "solve.cuh"
 
 namespace bddc_b200 {
+
+std::atomic<std::int64_t> g_kernel_launches{0};
+
 namespace {
 
 template <typename T>
@@ -106,7 +109,6 @@ struct GpuContext::Impl {
     std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
-    Event ev[4];
 
     SolveParams solve_params(const double* in, double* out) const {
         SolveParams P{};
@@ -225,30 +227,50 @@ struct GpuContext::Impl {
                                      " iterations, relative residual " + std::to_string(st[1]));
     }
 
-    void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
-        const bool prof = opt.profile;
-        if (prof) BDDC_CUDA(cudaEventRecord(ev[0].e, s));
-        launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
-        if (prof) BDDC_CUDA(cudaEventRecord(ev[1].e, s));
-        const IfaceParams ip = iface_params();
-        launch_iface_restrict(ip, r_dev, U.p, s);
-        coarse_solve(s);
-        launch_iface_local(ip, opt.local_blocks, s, true);
-        if (prof) BDDC_CUDA(cudaEventRecord(ev[2].e, s));
-        launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
-        if (prof) {
-            BDDC_CUDA(cudaEventRecord(ev[3].e, s));
-            BDDC_CUDA(cudaEventSynchronize(ev[3].e));
+    // Profiling: CUDA events recorded on the launching stream around the two interior
+    // solves and the interface steps of every apply, without synchronising; they are
+    // resolved lazily (kernel_times()), so profiling does not perturb the timed region.
+    struct ApplyEvents {
+        Event e[4];
+    };
+    std::vector<std::unique_ptr<ApplyEvents>> ev_pool;
+    std::size_t ev_used = 0;
+
+    void resolve_events() {
+        for (std::size_t i = 0; i < ev_used; ++i) {
+            ApplyEvents& E = *ev_pool[i];
+            BDDC_CUDA(cudaEventSynchronize(E.e[3].e));
             float a = 0, b = 0, c = 0, t = 0;
-            BDDC_CUDA(cudaEventElapsedTime(&a, ev[0].e, ev[1].e));
-            BDDC_CUDA(cudaEventElapsedTime(&b, ev[1].e, ev[2].e));
-            BDDC_CUDA(cudaEventElapsedTime(&c, ev[2].e, ev[3].e));
-            BDDC_CUDA(cudaEventElapsedTime(&t, ev[0].e, ev[3].e));
+            BDDC_CUDA(cudaEventElapsedTime(&a, E.e[0].e, E.e[1].e));
+            BDDC_CUDA(cudaEventElapsedTime(&b, E.e[1].e, E.e[2].e));
+            BDDC_CUDA(cudaEventElapsedTime(&c, E.e[2].e, E.e[3].e));
+            BDDC_CUDA(cudaEventElapsedTime(&t, E.e[0].e, E.e[3].e));
             times.interior_ms += a + c;
+            times.interior_launches += 2;
             times.iface_ms += b;
             times.apply_ms += t;
             times.applies += 1;
         }
+        ev_used = 0;
+    }
+
+    void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
+        ApplyEvents* E = nullptr;
+        if (opt.profile) {
+            if (ev_used == 4096) resolve_events();
+            if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
+            E = ev_pool[ev_used++].get();
+        }
+        if (E) BDDC_CUDA(cudaEventRecord(E->e[0].e, s));
+        launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
+        if (E) BDDC_CUDA(cudaEventRecord(E->e[1].e, s));
+        const IfaceParams ip = iface_params();
+        launch_iface_restrict(ip, r_dev, U.p, s);
+        coarse_solve(s);
+        launch_iface_local(ip, opt.local_blocks, s, true);
+        if (E) BDDC_CUDA(cudaEventRecord(E->e[2].e, s));
+        launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
+        if (E) BDDC_CUDA(cudaEventRecord(E->e[3].e, s));
     }
 
     void ensure_pcg(int max_it) {
@@ -626,8 +648,17 @@ std::int64_t GpuContext::apply_bytes() const {
     return 8 * (4 * I.factor_vals + I.k_values + 2 * I.phig_values +
                 static_cast<std::int64_t>(I.n_coarse) * I.n_coarse + I.ginnz + I.couple_nnz + 5 * n);
 }
-KernelTimes GpuContext::kernel_times() const { return impl_->times; }
-void GpuContext::reset_kernel_times() { impl_->times = KernelTimes{}; }
+KernelTimes GpuContext::kernel_times() {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    BDDC_CUDA(cudaSetDevice(impl_->device));
+    impl_->resolve_events();
+    return impl_->times;
+}
+void GpuContext::reset_kernel_times() {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    impl_->resolve_events();
+    impl_->times = KernelTimes{};
+}
 void GpuContext::set_profile(bool on) { impl_->opt.profile = on; }
 int GpuContext::device() const { return impl_->device; }
 void GpuContext::synchronize() { BDDC_CUDA(cudaStreamSynchronize(impl_->stream)); }

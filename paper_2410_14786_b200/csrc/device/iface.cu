@@ -244,30 +244,30 @@ void launch_coarse_cg(const CoarseCgParams& P, cudaStream_t s) {
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(coarse_cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     coarse_cg_kernel<<<1, kCgThreads, smem, s>>>(P);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 static int stage_grid(int n) { return std::max(1, std::min((n + kStageThreads - 1) / kStageThreads, 148 * 8)); }
 
 void launch_stage_phi_restrict(const StageParams& P, const double* r, cudaStream_t s) {
     stage_phi_restrict_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P, r);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void launch_stage_phi_prolong(const StageParams& P, cudaStream_t s) {
     stage_phi_prolong_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void launch_stage_gather_local(const StageParams& P, double* out, cudaStream_t s) {
     stage_gather_local_kernel<<<stage_grid(P.n_vector), kStageThreads, 0, s>>>(P, out);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void launch_stage_local_g(const StageParams& P, const double* r, const double* y, cudaStream_t s) {
     stage_local_g_kernel<<<P.n_subdomains, kStageThreads, 0, s>>>(P, r, y);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void launch_stage_iface_gather(const StageParams& P, const double* h, double* out, cudaStream_t s) {
     stage_iface_gather_kernel<<<stage_grid(P.n_gi), kStageThreads, 0, s>>>(P, h, out);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 namespace {
@@ -279,7 +279,7 @@ void launch_iface_restrict(const IfaceParams& P, const double* r, const double* 
         BDDC_CUDA(cudaFuncSetAttribute(iface_restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     iface_restrict_kernel<<<P.n_subdomains, kRestrictThreads, smem, s>>>(P, r, u0);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
@@ -289,7 +289,7 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
         BDDC_CUDA(cudaFuncSetAttribute(coarse_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     coarse_direct_kernel<<<blocks, kCoarseThreads, smem, s>>>(P);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, bool with_coarse) {
@@ -299,7 +299,7 @@ void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s
                                        (int)smem));
     iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub,
                                                                                  with_coarse ? 1 : 0);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 }  // namespace bddc_b200

@@ -123,47 +123,47 @@ int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecTh
 
 void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s) {
     dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D.n, a, b, part);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s) {
     finalize_kernel<<<1, kVecThreads, 0, s>>>(part, D.grid, D.scal + slot, take_sqrt ? 1 : 0);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
     spmv_dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s) {
     update_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_check(const PcgDevice& D, int it, cudaStream_t s) {
     check_kernel<<<1, kVecThreads, 0, s>>>(D, it);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_init_rho(const PcgDevice& D, cudaStream_t s) {
     init_rho_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void pcg_xpay(const PcgDevice& D, int it, cudaStream_t s) {
     xpay_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
                  const double* x, double* y, cudaStream_t s) {
     spmv_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, x, y);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void device_axpby(int n, double a, const double* x, double b, const double* y, double* out,
                   cudaStream_t s) {
     axpby_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, a, x, b, y, out);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_t s) {
     const int init = 0x7fffffff;
     BDDC_CUDA(cudaMemcpyAsync(dev_result, &init, sizeof(int), cudaMemcpyHostToDevice, s));
     nonfinite_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, x, dev_result);
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 int pcg_grid_for(int n) { return vec_grid(n); }

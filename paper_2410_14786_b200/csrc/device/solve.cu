@@ -307,7 +307,7 @@ void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaSt
         else if (mode == 1) launch_one<1, 1>(P, L, stream);
         else launch_one<2, 1>(P, L, stream);
     }
-    BDDC_CUDA(cudaGetLastError());
+    BDDC_LAUNCHED();
 }
 
 }  // namespace bddc_b200

@@ -1,6 +1,9 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <utility>
+
+#include "distribute.hpp"
 #include <stdexcept>
 #include <string>
 
@@ -8,7 +11,7 @@ namespace bddc_b200 {
 
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
-                               const BddcSetup& setup, int parts, int unit_bytes) {
+                               const BddcSetup& setup, int parts, int unit_bytes, const RankPlan* plan) {
     DeviceImage img;
     const index_t nsub = d.n_subdomains;
     img.parts = parts;
@@ -34,7 +37,8 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
         }
         img.gi_row_ptr.push_back(static_cast<std::int32_t>(img.gi_row_col.size()));
     }
-    std::vector<std::vector<std::int32_t>> gi_owners(img.gi_dof.size());
+    // (global subdomain id, hbuf slot): sorted by subdomain before flattening
+    std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>> gi_owners(img.gi_dof.size());
     std::vector<std::vector<std::int32_t>> dof_owners(d.global_dofs);
     std::vector<std::vector<std::int32_t>> c_owners(cs.n_coarse);
 
@@ -68,15 +72,16 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
             if (gid < 0) throw std::runtime_error("interface dof classified interior");
             img.iface_gid.push_back(gid);
             img.iface_writer.push_back(gi_owners[gid].empty() ? 1 : 0);
-            gi_owners[gid].push_back(static_cast<std::int32_t>(img.hbuf_total + gmm));
+            const std::int32_t gsub = plan ? plan->subdomains[i] : i;
+            gi_owners[gid].push_back({gsub, static_cast<std::int32_t>(img.hbuf_total + gmm)});
         }
         img.hbuf_total += ng;
-        sd.cbuf = img.cbuf_total;
+        sd.cbuf = plan ? plan->cbuf_offset[plan->subdomains[i]] : img.cbuf_total;
         sd.primal = static_cast<std::int64_t>(img.primal.size());
         for (index_t j = 0; j < np; ++j) {
             const index_t q = cs.primal_maps[i][j];
             img.primal.push_back(q);
-            c_owners[q].push_back(static_cast<std::int32_t>(img.cbuf_total + j));
+            if (!plan) c_owners[q].push_back(static_cast<std::int32_t>(img.cbuf_total + j));
         }
         img.cbuf_total += np;
 
@@ -105,6 +110,29 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
         build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.solve);
     }
 
+    if (plan) {
+        // remote interface contributions (filled by the interface exchange) and the
+        // gathered coarse buffer of all ranks
+        if (img.hbuf_total != plan->n_local_slots) throw std::logic_error("rank plan: hbuf slot layout mismatch");
+        for (index_t l = 0; l < plan->n_rows; ++l)
+            for (const auto& [gsub, k] : plan->remote_owners[l]) {
+                const std::int32_t gid = gid_of[l];
+                if (gid < 0) throw std::logic_error("rank plan: remote owner of an interior dof");
+                gi_owners[gid].push_back({gsub, static_cast<std::int32_t>(plan->n_local_slots + k)});
+            }
+        img.hbuf_total += plan->n_remote_slots;
+        for (std::size_t j = 0; j < plan->primal_all.size(); ++j)
+            for (std::size_t t = 0; t < plan->primal_all[j].size(); ++t)
+                c_owners[plan->primal_all[j][t]].push_back(static_cast<std::int32_t>(plan->cbuf_offset[j] + t));
+        img.cbuf_total = static_cast<std::int64_t>(plan->world) * plan->cbuf_pad;
+    }
+    for (auto& o : gi_owners) std::stable_sort(o.begin(), o.end());
+    img.gi_own_ptr.assign(1, 0);
+    for (const auto& o : gi_owners) {
+        for (const auto& e : o) img.gi_own_ref.push_back(e.second);
+        img.gi_own_ptr.push_back(static_cast<std::int32_t>(img.gi_own_ref.size()));
+    }
+
     auto flatten = [](const std::vector<std::vector<std::int32_t>>& lists, std::vector<std::int32_t>& ptr,
                       std::vector<std::int32_t>& ref) {
         ptr.assign(1, 0);
@@ -113,7 +141,6 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
             ptr.push_back(static_cast<std::int32_t>(ref.size()));
         }
     };
-    flatten(gi_owners, img.gi_own_ptr, img.gi_own_ref);
     flatten(dof_owners, img.dof_own_ptr, img.dof_own_ref);
     flatten(c_owners, img.c_own_ptr, img.c_own_ref);
     img.coarse_inv = setup.coarse_inverse;

@@ -1,5 +1,9 @@
 // Compiles the host setup (supernodal factors, K_i, Phi_i, coarse inverse) into the
 // flat device image the sm_100a kernels consume (layout: device_format.hpp).
+// With a RankPlan (multi-GPU, host/distribute.hpp) the image describes one rank: interface
+// sums also read the remote slots filled by the interface exchange, and the coarse
+// residual is summed from the gathered c_i of every subdomain, both in ascending global
+// subdomain order.
 #pragma once
 
 #include <cstdint>
@@ -10,6 +14,8 @@
 #include "solve_program.hpp"
 
 namespace bddc_b200 {
+
+struct RankPlan;
 
 struct DeviceImage {
     std::vector<SubdomainDesc> subs;
@@ -42,6 +48,7 @@ struct DeviceImage {
 
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
-                               const BddcSetup& setup, int parts, int unit_bytes = 4096);
+                               const BddcSetup& setup, int parts, int unit_bytes = 4096,
+                               const RankPlan* plan = nullptr);
 
 }  // namespace bddc_b200
