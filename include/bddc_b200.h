@@ -24,6 +24,12 @@
  *   bddc_gpu_subdomain_blocks   SubdomainData::coarse_basis / multipliers / coarse_block
  *                               (include/bddc/preconditioner.hpp:27-35)
  *   bddc_gpu_coarse_matrix      Preconditioner::coarse().matrix (include/bddc/preconditioner.hpp:92)
+ *   bddc_gpu_create_dist        Preconditioner ctor, one rank per B200: the reference's only
+ *                               parallelism is the parallel_for worker pool over subdomains
+ *                               (include/bddc/parallel.hpp:19-45, src/preconditioner.cpp:114-123);
+ *                               here subdomain blocks go to ranks and cross-subdomain sums keep its
+ *                               ascending-subdomain order (src/preconditioner.cpp:141-147,168-169)
+ *   bddc_rank_plan_*            host-only view of one rank's partition (CPU tests, tooling)
  */
 #ifndef BDDC_B200_H
 #define BDDC_B200_H
@@ -133,6 +139,42 @@ typedef struct {
 typedef struct bddc_problem bddc_problem;
 typedef struct bddc_host_setup bddc_host_setup;
 typedef struct bddc_gpu_ctx bddc_gpu_ctx;
+typedef struct bddc_rank_plan bddc_rank_plan;
+
+/* Multi-GPU: this process is `rank` of `world` (one process per B200, NCCL over NVLink). */
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    uint8_t nccl_id[128];            /* from bddc_dist_unique_id() on rank 0, broadcast by the caller */
+    const int32_t* subdomain_rank;   /* optional [n_subdomains]; NULL = rectangular blocks */
+} bddc_dist_options;
+
+/* One rank's partition. Rank-local vector layout: [0, n_owned) owned dofs (dot products),
+ * [0, n_rows) every dof of the rank's subdomains, [n_rows, n_local) halo. */
+typedef struct {
+    int32_t rank, world, n_local, n_rows, n_owned, n_subdomains_global;
+    const int32_t* local_to_global;  /* [n_local] */
+    const int32_t* subdomain_rank;   /* [n_subdomains_global] */
+    int32_t n_local_subdomains;
+    const int32_t* subdomains;       /* global ids, ascending */
+    int32_t n_halo_peers;
+    const int32_t* halo_peers;       /* ranks */
+    const int32_t* halo_send_off;    /* [n_halo_peers+1] into halo_send_idx */
+    const int32_t* halo_send_idx;    /* rank-local indices packed per peer */
+    const int32_t* halo_recv_off;    /* [n_halo_peers+1]: received into n_rows + off */
+    int32_t n_iface_peers;
+    const int32_t* iface_peers;
+    const int32_t* iface_send_off;   /* [n_iface_peers+1] into iface_send_slot */
+    const int32_t* iface_send_slot;  /* local h slots (subdomain-major, interface order) */
+    const int32_t* iface_recv_off;   /* [n_iface_peers+1]: remote slot ranges */
+    int32_t n_local_slots, n_remote_slots;
+    const int32_t* remote_ptr;       /* [n_rows+1]: remote interface owners per local row */
+    const int32_t* remote_subdomain; /* global subdomain of each remote owner */
+    const int32_t* remote_slot;      /* its remote slot */
+    int32_t cbuf_pad;                /* gathered coarse contributions: rank q at q*cbuf_pad */
+    const int32_t* cbuf_offset;      /* [n_subdomains_global] */
+    const bddc_problem* local_problem; /* rank-local problem (borrowed; lives with the plan) */
+} bddc_rank_plan_view;
 
 const char* bddc_last_error(void);
 int32_t bddc_abi_version(void);
@@ -160,7 +202,22 @@ int bddc_host_setup_interior_solve(const bddc_host_setup* s, int32_t subdomain, 
 int bddc_host_setup_stats(const bddc_host_setup* s, bddc_stats* stats);
 void bddc_host_setup_destroy(bddc_host_setup* s);
 
-/* ---- GPU hot path ---- */
+/* ---- multi-GPU ---- */
+int bddc_dist_unique_id(uint8_t* id128);
+int bddc_gpu_create_dist(const bddc_problem* global_problem, const bddc_gpu_options* opt,
+                         const bddc_dist_options* dist, bddc_gpu_ctx** out);
+/* Device vector layout of a context (identity on one GPU); local_to_global may be NULL. */
+int bddc_gpu_layout(const bddc_gpu_ctx* ctx, int32_t* n_local, int32_t* n_rows, int32_t* n_owned,
+                    int32_t* local_to_global);
+int bddc_rank_plan_create(const bddc_problem* p, int32_t rank, int32_t world,
+                          const int32_t* subdomain_rank, bddc_rank_plan** out);
+int bddc_rank_plan_get_view(const bddc_rank_plan* plan, bddc_rank_plan_view* view);
+void bddc_rank_plan_destroy(bddc_rank_plan* plan);
+
+/* ---- GPU hot path ----
+ * On a distributed context the host entry points take GLOBAL vectors and each rank writes
+ * the entries of its own subdomains; the *_device entry points take rank-local vectors
+ * (bddc_gpu_layout). Every rank must make the same calls in the same order. */
 int bddc_gpu_create(const bddc_problem* p, const bddc_gpu_options* opt, bddc_gpu_ctx** out);
 int bddc_gpu_apply(bddc_gpu_ctx* ctx, const double* r, double* z);
 int bddc_gpu_apply_device(bddc_gpu_ctx* ctx, const double* r_dev, double* z_dev, void* cuda_stream);

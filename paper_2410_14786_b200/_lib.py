@@ -51,6 +51,23 @@ class GpuOptions(C.Structure):
                 ("solve_parts", i32)]
 
 
+class DistOptions(C.Structure):
+    _fields_ = [("rank", i32), ("world", i32), ("nccl_id", C.c_uint8 * 128), ("subdomain_rank", P(i32))]
+
+
+class RankPlanView(C.Structure):
+    _fields_ = [("rank", i32), ("world", i32), ("n_local", i32), ("n_rows", i32), ("n_owned", i32),
+                ("n_subdomains_global", i32), ("local_to_global", P(i32)), ("subdomain_rank", P(i32)),
+                ("n_local_subdomains", i32), ("subdomains", P(i32)),
+                ("n_halo_peers", i32), ("halo_peers", P(i32)), ("halo_send_off", P(i32)),
+                ("halo_send_idx", P(i32)), ("halo_recv_off", P(i32)),
+                ("n_iface_peers", i32), ("iface_peers", P(i32)), ("iface_send_off", P(i32)),
+                ("iface_send_slot", P(i32)), ("iface_recv_off", P(i32)),
+                ("n_local_slots", i32), ("n_remote_slots", i32), ("remote_ptr", P(i32)),
+                ("remote_subdomain", P(i32)), ("remote_slot", P(i32)),
+                ("cbuf_pad", i32), ("cbuf_offset", P(i32)), ("local_problem", C.c_void_p)]
+
+
 class SolverOptions(C.Structure):
     _fields_ = [("rel_tolerance", f64), ("abs_tolerance", f64), ("max_iterations", i32),
                 ("record_history", i32)]
@@ -91,6 +108,12 @@ SIGNATURES = {
     "bddc_host_setup_stats": (C.c_int, [vp, P(Stats)]),
     "bddc_host_setup_destroy": (None, [vp]),
     "bddc_gpu_create": (C.c_int, [vp, P(GpuOptions), P(vp)]),
+    "bddc_dist_unique_id": (C.c_int, [P(C.c_uint8)]),
+    "bddc_gpu_create_dist": (C.c_int, [vp, P(GpuOptions), P(DistOptions), P(vp)]),
+    "bddc_gpu_layout": (C.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
+    "bddc_rank_plan_create": (C.c_int, [vp, i32, i32, P(i32), P(vp)]),
+    "bddc_rank_plan_get_view": (C.c_int, [vp, P(RankPlanView)]),
+    "bddc_rank_plan_destroy": (None, [vp]),
     "bddc_gpu_apply": (C.c_int, [vp, pd, pd]),
     "bddc_gpu_apply_device": (C.c_int, [vp, vp, vp, vp]),
     "bddc_gpu_stage": (C.c_int, [vp, i32, pd, pd, pd, pd]),

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "context.hpp"
+#include "host/distribute.hpp"
 #include "host/problem.hpp"
 #include "host/setup.hpp"
 
@@ -58,6 +59,12 @@ struct bddc_problem {
 struct bddc_host_setup {
     BddcSetup setup;
     const bddc_problem* problem;
+};
+
+struct bddc_rank_plan {
+    RankPlan plan;
+    bddc_problem local;  // the rank-local problem, viewable like any bddc_problem
+    std::vector<std::int32_t> remote_ptr, remote_sub, remote_slot;
 };
 
 struct bddc_gpu_ctx {
@@ -369,6 +376,113 @@ int bddc_gpu_create(const bddc_problem* p, const bddc_gpu_options* opt, bddc_gpu
         *out = c.release();
     });
 }
+
+int bddc_dist_unique_id(uint8_t* id) {
+    return guarded([&] {
+        if (!id) throw std::invalid_argument("bddc_dist_unique_id: null argument");
+        char buf[128];
+        dist_nccl_id(buf);
+        std::memcpy(id, buf, 128);
+    });
+}
+
+int bddc_gpu_create_dist(const bddc_problem* p, const bddc_gpu_options* opt, const bddc_dist_options* dist,
+                         bddc_gpu_ctx** out) {
+    return guarded([&] {
+        if (!p || !dist || !out) throw std::invalid_argument("bddc_gpu_create_dist: null argument");
+        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+            throw std::invalid_argument("bddc_gpu_create_dist: bad rank / world");
+        DistSpec spec;
+        spec.rank = dist->rank;
+        spec.world = dist->world;
+        std::memcpy(spec.nccl_id, dist->nccl_id, 128);
+        if (dist->subdomain_rank)
+            spec.sub_rank.assign(dist->subdomain_rank, dist->subdomain_rank + p->data.decomposition.n_subdomains);
+        auto c = std::make_unique<bddc_gpu_ctx>();
+        c->ctx = std::make_unique<GpuContext>(p->data, to_gpu(opt), &spec);
+        *out = c.release();
+    });
+}
+
+int bddc_gpu_layout(const bddc_gpu_ctx* c, int32_t* n_local, int32_t* n_rows, int32_t* n_owned,
+                    int32_t* local_to_global) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("bddc_gpu_layout: null context");
+        const GpuContext& g = *c->ctx;
+        if (n_local) *n_local = g.n();
+        if (n_rows) *n_rows = g.n_rows();
+        if (n_owned) *n_owned = g.n_owned();
+        if (local_to_global) {
+            const auto& l2g = g.local_to_global();
+            if (l2g.empty())
+                for (index_t l = 0; l < g.n(); ++l) local_to_global[l] = l;
+            else
+                std::memcpy(local_to_global, l2g.data(), sizeof(int32_t) * l2g.size());
+        }
+    });
+}
+
+int bddc_rank_plan_create(const bddc_problem* p, int32_t rank, int32_t world, const int32_t* subdomain_rank,
+                          bddc_rank_plan** out) {
+    return guarded([&] {
+        if (!p || !out) throw std::invalid_argument("bddc_rank_plan_create: null argument");
+        auto r = std::make_unique<bddc_rank_plan>();
+        r->plan = make_rank_plan(p->data, rank, world, subdomain_rank);
+        r->local.data = std::move(r->plan.local);
+        r->plan.local = ProblemData{};
+        r->local.rhs.resize(r->local.data.decomposition.global_dofs);
+        if (!p->rhs.empty())
+            for (index_t l = 0; l < r->plan.n_local; ++l) r->local.rhs[l] = p->rhs[r->plan.local_to_global[l]];
+        r->local.flatten();
+        r->remote_ptr.assign(1, 0);
+        for (const auto& lst : r->plan.remote_owners) {
+            for (const auto& [gsub, k] : lst) {
+                r->remote_sub.push_back(gsub);
+                r->remote_slot.push_back(k);
+            }
+            r->remote_ptr.push_back(static_cast<std::int32_t>(r->remote_sub.size()));
+        }
+        *out = r.release();
+    });
+}
+
+int bddc_rank_plan_get_view(const bddc_rank_plan* r, bddc_rank_plan_view* v) {
+    return guarded([&] {
+        if (!r || !v) throw std::invalid_argument("bddc_rank_plan_get_view: null argument");
+        const RankPlan& P = r->plan;
+        std::memset(v, 0, sizeof *v);
+        v->rank = P.rank;
+        v->world = P.world;
+        v->n_local = P.n_local;
+        v->n_rows = P.n_rows;
+        v->n_owned = P.n_owned;
+        v->n_subdomains_global = static_cast<int32_t>(P.sub_rank.size());
+        v->local_to_global = P.local_to_global.data();
+        v->subdomain_rank = P.sub_rank.data();
+        v->n_local_subdomains = static_cast<int32_t>(P.subdomains.size());
+        v->subdomains = P.subdomains.data();
+        v->n_halo_peers = static_cast<int32_t>(P.halo_peers.size());
+        v->halo_peers = P.halo_peers.data();
+        v->halo_send_off = P.halo_send_off.data();
+        v->halo_send_idx = P.halo_send_idx.data();
+        v->halo_recv_off = P.halo_recv_off.data();
+        v->n_iface_peers = static_cast<int32_t>(P.iface_peers.size());
+        v->iface_peers = P.iface_peers.data();
+        v->iface_send_off = P.iface_send_off.data();
+        v->iface_send_slot = P.iface_send_slot.data();
+        v->iface_recv_off = P.iface_recv_off.data();
+        v->n_local_slots = P.n_local_slots;
+        v->n_remote_slots = P.n_remote_slots;
+        v->remote_ptr = r->remote_ptr.data();
+        v->remote_subdomain = r->remote_sub.data();
+        v->remote_slot = r->remote_slot.data();
+        v->cbuf_pad = P.cbuf_pad;
+        v->cbuf_offset = P.cbuf_offset.data();
+        v->local_problem = &r->local;
+    });
+}
+
+void bddc_rank_plan_destroy(bddc_rank_plan* r) { delete r; }
 
 int bddc_gpu_apply(bddc_gpu_ctx* c, const double* r, double* z) {
     return guarded([&] {

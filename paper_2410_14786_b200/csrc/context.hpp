@@ -62,17 +62,38 @@ struct KernelTimes {
     std::int64_t applies = 0;
 };
 
+// Multi-GPU: this process is rank `rank` of `world` (one per B200); the context is built
+// from the GLOBAL problem and keeps the rank's block of subdomains (host/distribute.hpp).
+struct DistSpec {
+    int rank = 0;
+    int world = 1;
+    char nccl_id[128] = {};     // ncclUniqueId from rank 0, broadcast by the caller
+    std::vector<int> sub_rank;  // optional subdomain -> rank (empty: rectangular blocks)
+};
+
+// 128-byte ncclUniqueId for a new distributed job (rank 0 calls this).
+void dist_nccl_id(char out[128]);
+
 enum class Stage : int { interior = 0, coarse = 1, local = 2, static_condensation = 3 };
 
 class GpuContext {
 public:
-    GpuContext(ProblemData problem, const GpuOptions& opt);
+    GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpec* dist = nullptr);
     ~GpuContext();
     GpuContext(const GpuContext&) = delete;
     GpuContext& operator=(const GpuContext&) = delete;
 
-    index_t n() const;
-    // Device pointers (n doubles each) on the context's device; stream may be null.
+    index_t n() const;         // device vector length (distributed: the rank-local layout)
+    index_t n_global() const;  // host vector length of apply_host / pcg_host
+    // distributed layout: [0, n_owned) owned, [0, n_rows) the rank's dofs, then the halo
+    index_t n_owned() const;
+    index_t n_rows() const;
+    int rank() const;
+    int world() const;
+    const std::vector<index_t>& local_to_global() const;  // empty on one GPU
+    // Device pointers (n() doubles each) on the context's device; stream may be null.
+    // Host entry points take global vectors; a distributed rank reads and writes only
+    // the entries of its own subdomains.
     void apply_device(const double* r, double* z, void* stream);
     void apply_host(const double* r, double* z);
     SolveResult pcg_host(const double* b, const SolverOpts& o, double* x, bool precondition);

@@ -10,7 +10,9 @@
 #include <thread>
 
 #include "../context.hpp"
+#include "../host/distribute.hpp"
 #include "../host/program.hpp"
+#include "comm.cuh"
 #include "iface.cuh"
 #include "pcg.cuh"
 #include "solve.cuh"
@@ -109,6 +111,41 @@ struct GpuContext::Impl {
     std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
+
+    // ---- multi-GPU (null / unused on one GPU)
+    std::unique_ptr<RankPlan> plan;
+    std::unique_ptr<Comm> comm;
+    DBuf<std::int32_t> halo_idx, iface_idx;
+    DBuf<double> halo_send, iface_send, gath_a, gath_b;
+    std::vector<std::int32_t> halo_soff, halo_roff, iface_soff, iface_roff;
+    index_t n_global = 0, n_rows = 0, n_owned = 0;
+    std::string symmetry_error;  // distributed: global symmetry check done once at creation
+    DBuf<double> hx_in, hx_out;  // host-entry staging (rank-local layout)
+
+    bool dist() const { return static_cast<bool>(comm); }
+
+    // u0 / p halo: owners send their entries, the halo region [n_rows, n) is overwritten
+    void halo_exchange(double* v, cudaStream_t s) {
+        if (!dist()) return;
+        launch_pack(static_cast<int>(plan->halo_send_idx.size()), halo_idx.p, v, halo_send.p, s);
+        comm->exchange(plan->halo_peers, halo_send.p, halo_soff, v + n_rows, halo_roff, s);
+    }
+    // h_i of interface dofs shared with other ranks -> remote hbuf slots
+    void iface_exchange(cudaStream_t s) {
+        if (!dist()) return;
+        launch_pack(static_cast<int>(plan->iface_send_slot.size()), iface_idx.p, hbuf.p, iface_send.p, s);
+        comm->exchange(plan->iface_peers, iface_send.p, iface_soff, hbuf.p + plan->n_local_slots, iface_roff, s);
+    }
+    // every rank's c_i (padded blocks, rank order) for the ordered r_c sum
+    void gather_cbuf(cudaStream_t s) {
+        if (dist()) comm->allgather_inplace(cbuf.p, static_cast<std::size_t>(plan->cbuf_pad), s);
+    }
+    // part[0..grid) -> gath[rank], then gathered over ranks (consumers sum in rank order)
+    void gather_partial(const double* part, int grid, double* gath, cudaStream_t s) {
+        if (!dist()) return;
+        launch_reduce_to(part, grid, gath + comm->rank(), false, s);
+        comm->allgather_inplace(gath, 1, s);
+    }
 
     SolveParams solve_params(const double* in, double* out) const {
         SolveParams P{};
@@ -264,10 +301,13 @@ struct GpuContext::Impl {
         if (E) BDDC_CUDA(cudaEventRecord(E->e[0].e, s));
         launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
         if (E) BDDC_CUDA(cudaEventRecord(E->e[1].e, s));
+        halo_exchange(U.p, s);
         const IfaceParams ip = iface_params();
         launch_iface_restrict(ip, r_dev, U.p, s);
+        gather_cbuf(s);
         coarse_solve(s);
         launch_iface_local(ip, opt.local_blocks, s, true);
+        iface_exchange(s);
         if (E) BDDC_CUDA(cudaEventRecord(E->e[2].e, s));
         launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
         if (E) BDDC_CUDA(cudaEventRecord(E->e[3].e, s));
@@ -277,9 +317,11 @@ struct GpuContext::Impl {
         const index_t n = pb.decomposition.global_dofs;
         if (!x.p) {
             for (DBuf<double>* b : {&x, &r, &z, &p, &q}) b->alloc(n);
-            const int g = pcg_grid_for(n);
+            const int g = pcg_grid_for(dist() ? n_rows : n);
             part_a.alloc(g);
             part_b.alloc(g);
+            gath_a.alloc(dist() ? comm->world() : 1);
+            gath_b.alloc(dist() ? comm->world() : 1);
             scal.alloc(8);
             BDDC_CUDA(cudaMallocHost(&pinned, sizeof(double) * 8));
         }
@@ -294,7 +336,8 @@ struct GpuContext::Impl {
 
     PcgDevice pcg_device(const SolverOpts& o, double* xd, double* rd, double* zd) const {
         PcgDevice D{};
-        D.n = pb.decomposition.global_dofs;
+        D.n = dist() ? n_rows : pb.decomposition.global_dofs;
+        D.n_dot = dist() ? n_owned : D.n;
         D.grid = pcg_grid_for(D.n);
         D.A_ptr = A_ptr.p;
         D.A_col = A_col.p;
@@ -306,6 +349,10 @@ struct GpuContext::Impl {
         D.q = q.p;
         D.part_a = part_a.p;
         D.part_b = part_b.p;
+        D.red_a = dist() ? gath_a.p : part_a.p;
+        D.red_a_n = dist() ? comm->world() : D.grid;
+        D.red_b = dist() ? gath_b.p : part_b.p;
+        D.red_b_n = dist() ? comm->world() : D.grid;
         D.rho = rho.p;
         D.alpha = alpha.p;
         D.beta = beta.p;
@@ -316,12 +363,21 @@ struct GpuContext::Impl {
         return D;
     }
 
+    index_t global_index(int local) const {
+        return dist() && local >= 0 && local < static_cast<int>(plan->local_to_global.size()) ? plan->local_to_global[local]
+                                                                                               : local;
+    }
+
     // pcg.cpp:40-109 with every vector on the device; b and x are device pointers.
     SolveResult pcg(const double* b, const SolverOpts& o, double* xout, bool precondition, cudaStream_t s) {
         if (!(o.rel_tolerance > 0.0) || o.abs_tolerance < 0.0)
             throw std::invalid_argument("pcg: tolerances must be positive");
         if (o.max_iterations < 1) throw std::invalid_argument("pcg: max_iterations must be at least 1");
-        sampled_symmetry_check(pb.global_matrix);
+        if (dist()) {
+            if (!symmetry_error.empty()) throw std::invalid_argument(symmetry_error);
+        } else {
+            sampled_symmetry_check(pb.global_matrix);
+        }
         const index_t n = pb.decomposition.global_dofs;
         ensure_pcg(o.max_iterations);
         SolveResult rep;
@@ -333,7 +389,12 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(double) * 8, s));
         BDDC_CUDA(cudaMemcpyAsync(rd, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         pcg_dot(D, b, b, part_b.p, s);
-        pcg_finalize(D, part_b.p, 0, true, s);
+        if (dist()) {
+            gather_partial(part_b.p, D.grid, gath_b.p, s);
+            launch_reduce_to(gath_b.p, comm->world(), scal.p, true, s);
+        } else {
+            pcg_finalize(D, part_b.p, 0, true, s);
+        }
         BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
         BDDC_CUDA(cudaStreamSynchronize(s));
         const double normb = pinned[0];
@@ -344,7 +405,7 @@ struct GpuContext::Impl {
             int idx = 0;
             BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             BDDC_CUDA(cudaStreamSynchronize(s));
-            throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(idx));
+            throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(global_index(idx)));
         }
         if (o.record_history) rep.history.push_back(1.0);
         if (normb == 0.0) {
@@ -356,11 +417,15 @@ struct GpuContext::Impl {
             check_coarse(s);
         }
         pcg_dot(D, rd, zd, part_a.p, s);
+        gather_partial(part_a.p, D.grid, gath_a.p, s);
         pcg_init_rho(D, s);
+        halo_exchange(p.p, s);
         double rel = 1.0;
         for (int it = 1; it <= o.max_iterations; ++it) {
             pcg_spmv_dot(D, s);
+            gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_update(D, it, s);
+            gather_partial(part_b.p, D.grid, gath_b.p, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
             BDDC_CUDA(cudaStreamSynchronize(s));
@@ -372,7 +437,7 @@ struct GpuContext::Impl {
                 int idx = 0;
                 BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
                 BDDC_CUDA(cudaStreamSynchronize(s));
-                throw std::invalid_argument("bddc apply: non-finite entry at index " + std::to_string(idx));
+                throw std::invalid_argument("bddc apply: non-finite entry at index " + std::to_string(global_index(idx)));
             }
             rel = pinned[1];
             rep.iterations = it;
@@ -383,7 +448,9 @@ struct GpuContext::Impl {
                 check_coarse(s);
             }
             pcg_dot(D, rd, zd, part_a.p, s);
+            gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_xpay(D, it, s);
+            halo_exchange(p.p, s);
         }
         rep.final_relative_residual = rel;
         const int k = rep.iterations;
@@ -400,7 +467,7 @@ struct GpuContext::Impl {
     }
 };
 
-GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
+GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpec* dist) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
@@ -408,7 +475,22 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
     BDDC_CUDA(cudaSetDevice(opt.device));
     impl_.reset(new Impl);
     Impl& I = *impl_;
-    I.pb = std::move(problem);
+    I.n_global = problem.decomposition.global_dofs;
+    if (dist && dist->world > 1) {
+        try {
+            sampled_symmetry_check(problem.global_matrix);
+        } catch (const std::invalid_argument& e) {
+            I.symmetry_error = e.what();
+        }
+        I.plan = std::make_unique<RankPlan>(make_rank_plan(
+            problem, dist->rank, dist->world, dist->sub_rank.empty() ? nullptr : dist->sub_rank.data()));
+        I.pb = std::move(I.plan->local);
+        I.plan->local = ProblemData{};
+        I.n_rows = I.plan->n_rows;
+        I.n_owned = I.plan->n_owned;
+    } else {
+        I.pb = std::move(problem);
+    }
     I.opt = opt;
     I.device = opt.device;
     BDDC_CUDA(cudaSetDevice(I.device));
@@ -420,7 +502,43 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
     FactorOptions fo;
     fo.leaf_size = opt.leaf_size;
     I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, I.pb.coords.empty() ? nullptr : I.pb.coords.data(),
-                         workers, fo);
+                         workers, fo, /*assemble=*/!I.plan);
+    if (I.plan) {
+        // A_c needs every subdomain's A_ci: gather the padded per-rank blocks over NCCL, then
+        // assemble in ascending global subdomain order exactly like one GPU would
+        const auto t0 = std::chrono::steady_clock::now();
+        const RankPlan& P = *I.plan;
+        I.comm = std::make_unique<Comm>(dist->nccl_id, dist->rank, dist->world);
+        const index_t nsub = static_cast<index_t>(P.sub_rank.size());
+        std::vector<std::int64_t> per_rank(dist->world, 0), off(nsub, 0);
+        for (index_t j = 0; j < nsub; ++j) {
+            const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
+            off[j] = per_rank[P.sub_rank[j]];
+            per_rank[P.sub_rank[j]] += np * np;
+        }
+        const std::int64_t pad = std::max<std::int64_t>(1, *std::max_element(per_rank.begin(), per_rank.end()));
+        std::vector<double> host(static_cast<std::size_t>(pad) * dist->world, 0.0);
+        for (std::size_t li = 0; li < P.subdomains.size(); ++li) {
+            const index_t j = P.subdomains[li];
+            const auto& a = I.setup.subs[li].aci;
+            std::copy(a.begin(), a.end(), host.begin() + dist->rank * pad + off[j]);
+        }
+        DBuf<double> buf;
+        buf.upload(host);
+        I.comm->allgather_inplace(buf.p, static_cast<std::size_t>(pad), nullptr);
+        BDDC_CUDA(cudaDeviceSynchronize());
+        BDDC_CUDA(cudaMemcpy(host.data(), buf.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost));
+        std::vector<std::vector<double>> aci(nsub);
+        std::vector<const std::vector<double>*> blocks(nsub);
+        for (index_t j = 0; j < nsub; ++j) {
+            const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
+            const auto b0 = host.begin() + P.sub_rank[j] * pad + off[j];
+            aci[j].assign(b0, b0 + np * np);
+            blocks[j] = &aci[j];
+        }
+        assemble_coarse(I.setup, blocks, P.primal_all, I.pb.constraints.n_coarse);
+        I.setup.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
     int nsm = 148;
     BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
     const int parts = opt.solve_parts > 0 ? opt.solve_parts : (d.n_subdomains <= nsm ? 2 : 1);
@@ -431,7 +549,8 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
     int unit = std::getenv("BDDC_UNIT_BYTES") ? std::atoi(std::getenv("BDDC_UNIT_BYTES")) : 4096;
     int spw = 0;
     for (;; unit /= 2) {
-        img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit);
+        img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit,
+                                 I.plan.get());
         const std::size_t fixed = interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit, 0);
         spw = 0;
         if (fixed < static_cast<std::size_t>(max_smem)) {
@@ -529,6 +648,20 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt) {
     I.vout.alloc(n);
     I.vtmp.alloc(n);
     I.vtmp2.alloc(n);
+    if (I.plan) {
+        const RankPlan& P = *I.plan;
+        I.halo_idx.upload(P.halo_send_idx);
+        I.iface_idx.upload(P.iface_send_slot);
+        I.halo_send.alloc(std::max<std::size_t>(P.halo_send_idx.size(), 1));
+        I.iface_send.alloc(std::max<std::size_t>(P.iface_send_slot.size(), 1));
+        I.halo_soff.assign(P.halo_send_off.begin(), P.halo_send_off.end());
+        I.halo_roff.assign(P.halo_recv_off.begin(), P.halo_recv_off.end());
+        I.iface_soff.assign(P.iface_send_off.begin(), P.iface_send_off.end());
+        I.iface_roff.assign(P.iface_recv_off.begin(), P.iface_recv_off.end());
+        BDDC_CUDA(cudaMemset(I.hbuf.p, 0, sizeof(double) * I.hbuf.n));
+        BDDC_CUDA(cudaMemset(I.cbuf.p, 0, sizeof(double) * I.cbuf.n));
+        BDDC_CUDA(cudaDeviceSynchronize());
+    }
     BDDC_CUDA(cudaDeviceSynchronize());
 }
 
@@ -540,7 +673,18 @@ GpuContext::~GpuContext() {
     }
 }
 
+void dist_nccl_id(char out[128]) { nccl_unique_id(out); }
+
 index_t GpuContext::n() const { return impl_->pb.decomposition.global_dofs; }
+index_t GpuContext::n_global() const { return impl_->n_global; }
+index_t GpuContext::n_owned() const { return impl_->dist() ? impl_->n_owned : n(); }
+index_t GpuContext::n_rows() const { return impl_->dist() ? impl_->n_rows : n(); }
+int GpuContext::rank() const { return impl_->dist() ? impl_->comm->rank() : 0; }
+int GpuContext::world() const { return impl_->dist() ? impl_->comm->world() : 1; }
+const std::vector<index_t>& GpuContext::local_to_global() const {
+    static const std::vector<index_t> none;
+    return impl_->plan ? impl_->plan->local_to_global : none;
+}
 
 void GpuContext::apply_device(const double* r, double* z, void* stream) {
     std::lock_guard<std::mutex> lk(impl_->mu);
@@ -554,8 +698,19 @@ void GpuContext::apply_host(const double* r, double* z) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
     const index_t n = I.pb.decomposition.global_dofs;
-    ensure_finite(r, n, "bddc apply");
+    ensure_finite(r, I.n_global, "bddc apply");
     BDDC_CUDA(cudaSetDevice(I.device));
+    if (I.dist()) {
+        std::vector<double> loc(n), out(I.n_rows);
+        for (index_t l = 0; l < n; ++l) loc[l] = r[I.plan->local_to_global[l]];
+        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, loc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+        I.apply(I.vin.p, I.vout.p, I.stream);
+        BDDC_CUDA(cudaMemcpyAsync(out.data(), I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
+        BDDC_CUDA(cudaStreamSynchronize(I.stream));
+        I.check_coarse(I.stream);
+        for (index_t l = 0; l < I.n_rows; ++l) z[I.plan->local_to_global[l]] = out[l];
+        return;
+    }
     BDDC_CUDA(cudaMemcpyAsync(I.vin.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
     I.apply(I.vin.p, I.vout.p, I.stream);
     I.check_coarse(I.stream);
@@ -567,8 +722,18 @@ SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
     const index_t n = I.pb.decomposition.global_dofs;
-    ensure_finite(b, n, "pcg rhs");
+    ensure_finite(b, I.n_global, "pcg rhs");
     BDDC_CUDA(cudaSetDevice(I.device));
+    if (I.dist()) {
+        std::vector<double> loc(n), out(I.n_rows);
+        for (index_t l = 0; l < n; ++l) loc[l] = b[I.plan->local_to_global[l]];
+        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, loc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+        SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);
+        BDDC_CUDA(cudaMemcpyAsync(out.data(), I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
+        BDDC_CUDA(cudaStreamSynchronize(I.stream));
+        for (index_t l = 0; l < I.n_rows; ++l) x[I.plan->local_to_global[l]] = out[l];
+        return rep;
+    }
     BDDC_CUDA(cudaMemcpyAsync(I.vin.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
     SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);
     BDDC_CUDA(cudaMemcpyAsync(x, I.vout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, I.stream));
@@ -587,6 +752,7 @@ void GpuContext::stage_host(Stage st, const double* in0, const double* in1, cons
     Impl& I = *impl_;
     const index_t n = I.pb.decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
+    if (I.dist()) throw std::invalid_argument("stage hooks are single-GPU parity hooks");
     cudaStream_t s = I.stream;
     const StageParams sp = I.stage_params();
     auto h2d = [&](double* dst, const double* src) {

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D
         double y = 0.0;
         for (int e = D.A_ptr[i]; e < D.A_ptr[i + 1]; ++e) y += D.A_val[e] * D.p[D.A_col[e]];
         D.q[i] = y;
-        acc = fma(D.p[i], y, acc);
+        if (i < D.n_dot) acc = fma(D.p[i], y, acc);
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D
 
 __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int it) {
     __shared__ double scratch[kVecThreads / 32];
-    const double pq = sum_partials(D.part_a, D.grid, scratch);
+    const double pq = sum_partials(D.red_a, D.red_a_n, scratch);
     if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
         if (blockIdx.x == 0 && threadIdx.x == 0) D.scal[3] = 1.0;
         return;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
         D.x[i] += alpha * D.p[i];
         const double ri = D.r[i] - alpha * D.q[i];
         D.r[i] = ri;
-        acc = fma(ri, ri, acc);
+        if (i < D.n_dot) acc = fma(ri, ri, acc);
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
 __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int it) {
     __shared__ double scratch[kVecThreads / 32];
     if (D.scal[3] != 0.0) return;
-    const double rr = sum_partials(D.part_b, D.grid, scratch);
+    const double rr = sum_partials(D.red_b, D.red_b_n, scratch);
     if (threadIdx.x == 0) {
         const double normb = D.scal[0];
         const double rel = sqrt(rr) / normb;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, i
 
 __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
-    const double rz = sum_partials(D.part_a, D.grid, scratch);
+    const double rz = sum_partials(D.red_a, D.red_a_n, scratch);
     if (blockIdx.x == 0 && threadIdx.x == 0) D.rho[0] = rz;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
         D.p[i] = D.z[i];
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D
 
 __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int it) {
     __shared__ double scratch[kVecThreads / 32];
-    const double rz = sum_partials(D.part_a, D.grid, scratch);
+    const double rz = sum_partials(D.red_a, D.red_a_n, scratch);
     const double beta = rz / D.rho[it - 1];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
         D.p[i] = D.z[i] + beta * D.p[i];
@@ -122,7 +122,7 @@ int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecTh
 }  // namespace
 
 void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s) {
-    dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D.n, a, b, part);
+    dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D.n_dot, a, b, part);
     BDDC_LAUNCHED();
 }
 void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s) {

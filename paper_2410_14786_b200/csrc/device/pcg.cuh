@@ -7,7 +7,8 @@ namespace bddc_b200 {
 // Device-resident CG state. Scalars live in device memory; kernels derive alpha/beta
 // from fixed-order partial sums, so results are deterministic run to run.
 struct PcgDevice {
-    int n;
+    int n;                    // rows updated (single GPU: all; distributed: the rank's dofs)
+    int n_dot;                // leading entries that enter dot products (distributed: owned dofs)
     int grid;                 // blocks of the vector kernels (fixed => fixed reduction order)
     const std::int32_t* A_ptr;
     const std::int32_t* A_col;
@@ -19,6 +20,12 @@ struct PcgDevice {
     double* q;
     double* part_a;   // grid partials
     double* part_b;
+    // what the consumers of p.q / r.z (red_a) and r.r (red_b) sum, in order: the grid
+    // partials on one GPU; the gathered per-rank totals (rank order) when distributed
+    const double* red_a;
+    int red_a_n;
+    const double* red_b;
+    int red_b_n;
     double* rho;      // [max_it + 1]
     double* alpha;    // [max_it]
     double* beta;     // [max_it]
@@ -32,7 +39,7 @@ constexpr int kVecThreads = 256;
 void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s);
 // scal[slot] = sqrt(sum part) (sqrt=true) or sum part
 void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s);
-void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s);           // q = A p ; part_a = p.q
+void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s);           // q = A p ; part_a = p.q (owned rows)
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s);     // x += a p ; r -= a q ; part_b = r.r
 void pcg_check(const PcgDevice& D, int it, cudaStream_t s);      // hist[it], converged flag
 void pcg_init_rho(const PcgDevice& D, cudaStream_t s);           // rho[0] = sum part_a ; p = z

@@ -226,9 +226,41 @@ void spd_inverse(std::vector<double>& a, index_t n, const char* what) {
         }
 }
 
+// assemble_coarse (preconditioner.cpp:68-98): triplets in ascending subdomain order, then
+// from_triplets (duplicates summed in input order); plus the dense inverse for the GEMV.
+void assemble_coarse(BddcSetup& out, const std::vector<const std::vector<double>*>& aci,
+                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse) {
+    std::vector<Triplet> entries;
+    const index_t nsub = static_cast<index_t>(aci.size());
+    for (index_t i = 0; i < nsub; ++i) {
+        const auto& blk = *aci[i];
+        const auto& map = primal_maps[i];
+        const index_t np = static_cast<index_t>(map.size());
+        if (static_cast<index_t>(blk.size()) != np * np)
+            throw std::invalid_argument("assemble_coarse: primal map size mismatch at subdomain " +
+                                        std::to_string(i));
+        for (index_t r = 0; r < np; ++r)
+            for (index_t c = 0; c < np; ++c) {
+                if (map[r] < 0 || map[r] >= n_coarse || map[c] < 0 || map[c] >= n_coarse)
+                    throw std::out_of_range("assemble_coarse: primal index out of range at subdomain " +
+                                            std::to_string(i));
+                const double v = blk[static_cast<std::size_t>(r) * np + c];
+                if (v != 0.0) entries.push_back({map[r], map[c], v});
+            }
+    }
+    out.coarse_matrix = CsrMatrix::from_triplets(n_coarse, n_coarse, std::move(entries));
+    const index_t nc = n_coarse;
+    out.coarse_inverse.assign(static_cast<std::size_t>(nc) * nc, 0.0);
+    for (index_t r = 0; r < nc; ++r)
+        for (index_t p = out.coarse_matrix.row_offsets[r]; p < out.coarse_matrix.row_offsets[r + 1]; ++p)
+            out.coarse_inverse[static_cast<std::size_t>(r) * nc + out.coarse_matrix.col_indices[p]] =
+                out.coarse_matrix.values[p];
+    spd_inverse(out.coarse_inverse, nc, "coarse matrix");
+}
+
 BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& d,
                      const ConstraintSet& cs, const index_t* coords, index_t workers,
-                     const FactorOptions& fopt) {
+                     const FactorOptions& fopt, bool assemble) {
     const auto t0 = std::chrono::steady_clock::now();
     const index_t nsub = d.n_subdomains;
     if (static_cast<index_t>(locals.size()) != nsub ||
@@ -280,32 +312,11 @@ BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& 
             out.subs[i].dedup_of = first_of[i];
         }
 
-    // assemble_coarse (preconditioner.cpp:68-98)
-    std::vector<Triplet> entries;
-    for (index_t i = 0; i < nsub; ++i) {
-        const auto& blk = out.subs[i].aci;
-        const auto& map = cs.primal_maps[i];
-        const index_t np = out.subs[i].n_primal;
-        if (static_cast<index_t>(map.size()) != np)
-            throw std::invalid_argument("assemble_coarse: primal map size mismatch at subdomain " +
-                                        std::to_string(i));
-        for (index_t r = 0; r < np; ++r)
-            for (index_t c = 0; c < np; ++c) {
-                if (map[r] < 0 || map[r] >= cs.n_coarse || map[c] < 0 || map[c] >= cs.n_coarse)
-                    throw std::out_of_range("assemble_coarse: primal index out of range at subdomain " +
-                                            std::to_string(i));
-                const double v = blk[static_cast<std::size_t>(r) * np + c];
-                if (v != 0.0) entries.push_back({map[r], map[c], v});
-            }
+    if (assemble) {
+        std::vector<const std::vector<double>*> blocks(nsub);
+        for (index_t i = 0; i < nsub; ++i) blocks[i] = &out.subs[i].aci;
+        assemble_coarse(out, blocks, cs.primal_maps, cs.n_coarse);
     }
-    out.coarse_matrix = CsrMatrix::from_triplets(cs.n_coarse, cs.n_coarse, std::move(entries));
-    const index_t nc = cs.n_coarse;
-    out.coarse_inverse.assign(static_cast<std::size_t>(nc) * nc, 0.0);
-    for (index_t r = 0; r < nc; ++r)
-        for (index_t p = out.coarse_matrix.row_offsets[r]; p < out.coarse_matrix.row_offsets[r + 1]; ++p)
-            out.coarse_inverse[static_cast<std::size_t>(r) * nc + out.coarse_matrix.col_indices[p]] =
-                out.coarse_matrix.values[p];
-    spd_inverse(out.coarse_inverse, nc, "coarse matrix");
     out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return out;
 }

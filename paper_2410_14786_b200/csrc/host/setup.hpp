@@ -39,9 +39,16 @@ struct BddcSetup {
 // coords: optional global (ix, iy) per dof (2*global_dofs); enables geometric ND.
 // Throws std::runtime_error("bddc setup: subdomain i: ...") like the reference ctor
 // (preconditioner.cpp:119-121).
+// assemble = false skips the coarse problem (multi-GPU: assembled after gathering every
+// rank's A_ci, see assemble_coarse).
 BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& d,
                      const ConstraintSet& cs, const index_t* coords, index_t workers,
-                     const FactorOptions& fopt = {});
+                     const FactorOptions& fopt = {}, bool assemble = true);
+
+// A_c = sum_i R_ci^T A_ci R_ci in ascending i (reference assemble_coarse,
+// preconditioner.cpp:68-98) and its dense inverse, into out.coarse_matrix / coarse_inverse.
+void assemble_coarse(BddcSetup& out, const std::vector<const std::vector<double>*>& aci,
+                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse);
 
 // Dense helpers (row-major).
 // In-place inverse via LU with partial pivoting; throws "singular" on a zero pivot.

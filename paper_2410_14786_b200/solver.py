@@ -59,8 +59,9 @@ def _csr(view: L.CsrView):
 class Problem:
     """A decomposed problem owned by the native library (bddc_problem*)."""
 
-    def __init__(self, handle: int):
+    def __init__(self, handle: int, owner=None):
         self._h = C.c_void_p(handle)
+        self._owner = owner  # borrowed handle (e.g. a RankPlan's local problem): never destroyed here
         self._view = L.ProblemView()
         L.check(L.lib().bddc_problem_get_view(self._h, C.byref(self._view)))
 
@@ -129,7 +130,7 @@ class Problem:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and getattr(self, "_owner", None) is None:
             L.lib().bddc_problem_destroy(h)
             self._h = C.c_void_p()
 
@@ -255,18 +256,95 @@ class HostSetup:
         return {k: getattr(s, k) for k, _ in L.Stats._fields_}
 
 
+def _i32(ptr, n) -> np.ndarray:
+    if n <= 0:
+        return np.zeros(0, dtype=np.int32)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).copy()
+
+
+class RankPlan:
+    """Host-only view of one rank's partition of a problem (bddc_rank_plan_*): the rank-local
+    vector layout, halo / interface exchange lists and the gathered coarse layout."""
+
+    def __init__(self, problem: Problem, rank: int, world: int, subdomain_rank=None):
+        self.problem = problem
+        h = C.c_void_p()
+        sr = None
+        if subdomain_rank is not None:
+            self._sr = np.ascontiguousarray(subdomain_rank, dtype=np.int32)
+            sr = self._sr.ctypes.data_as(C.POINTER(C.c_int32))
+        L.check(L.lib().bddc_rank_plan_create(problem.handle, rank, world, sr, C.byref(h)))
+        self._h = h
+        v = L.RankPlanView()
+        L.check(L.lib().bddc_rank_plan_get_view(h, C.byref(v)))
+        self.rank, self.world = v.rank, v.world
+        self.n_local, self.n_rows, self.n_owned = v.n_local, v.n_rows, v.n_owned
+        self.local_to_global = _i32(v.local_to_global, v.n_local)
+        self.subdomain_rank = _i32(v.subdomain_rank, v.n_subdomains_global)
+        self.subdomains = _i32(v.subdomains, v.n_local_subdomains)
+        self.halo_peers = _i32(v.halo_peers, v.n_halo_peers)
+        self.halo_send_off = _i32(v.halo_send_off, v.n_halo_peers + 1)
+        self.halo_send_idx = _i32(v.halo_send_idx, int(self.halo_send_off[-1]))
+        self.halo_recv_off = _i32(v.halo_recv_off, v.n_halo_peers + 1)
+        self.iface_peers = _i32(v.iface_peers, v.n_iface_peers)
+        self.iface_send_off = _i32(v.iface_send_off, v.n_iface_peers + 1)
+        self.iface_send_slot = _i32(v.iface_send_slot, int(self.iface_send_off[-1]))
+        self.iface_recv_off = _i32(v.iface_recv_off, v.n_iface_peers + 1)
+        self.n_local_slots, self.n_remote_slots = v.n_local_slots, v.n_remote_slots
+        self.remote_ptr = _i32(v.remote_ptr, v.n_rows + 1)
+        self.remote_subdomain = _i32(v.remote_subdomain, int(self.remote_ptr[-1]))
+        self.remote_slot = _i32(v.remote_slot, int(self.remote_ptr[-1]))
+        self.cbuf_pad = v.cbuf_pad
+        self.cbuf_offset = _i32(v.cbuf_offset, v.n_subdomains_global)
+        self.local_problem = Problem(v.local_problem, owner=self)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            L.lib().bddc_rank_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def dist_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = (C.c_uint8 * 128)()
+    L.check(L.lib().bddc_dist_unique_id(buf))
+    return bytes(buf)
+
+
 class Preconditioner:
-    """B200 BDDC preconditioner (reference bddc::Preconditioner semantics)."""
+    """B200 BDDC preconditioner (reference bddc::Preconditioner semantics).
+
+    dist=(rank, world, nccl_id[, subdomain_rank]) builds one rank of a multi-GPU
+    preconditioner from the GLOBAL problem (every rank passes the same problem); host-vector
+    calls then take global vectors and fill the entries of the rank's subdomains."""
 
     def __init__(self, problem: Problem, device: int = 0, workers: int = 0, coarse_mode: str = "direct",
                  coarse_options: SolverOptions | None = None, leaf_size: int = 16, local_blocks: int = 4,
-                 solve_parts: int = 0):
+                 solve_parts: int = 0, dist=None):
         self.problem = problem
         self.n = problem.global_dofs
         h = C.c_void_p()
         opts = gpu_options(device, workers, coarse_mode, coarse_options, leaf_size, local_blocks, solve_parts)
-        L.check(L.lib().bddc_gpu_create(problem.handle, C.byref(opts), C.byref(h)))
+        if dist is None:
+            L.check(L.lib().bddc_gpu_create(problem.handle, C.byref(opts), C.byref(h)))
+        else:
+            d = L.DistOptions()
+            d.rank, d.world = int(dist[0]), int(dist[1])
+            C.memmove(d.nccl_id, bytes(dist[2]), 128)
+            if len(dist) > 3 and dist[3] is not None:
+                self._sr = np.ascontiguousarray(dist[3], dtype=np.int32)
+                d.subdomain_rank = self._sr.ctypes.data_as(C.POINTER(C.c_int32))
+            L.check(L.lib().bddc_gpu_create_dist(problem.handle, C.byref(opts), C.byref(d), C.byref(h)))
         self._h = h
+
+    def layout(self):
+        """(n_local, n_rows, n_owned, local_to_global) of the device vectors."""
+        nl, nr, no = C.c_int32(), C.c_int32(), C.c_int32()
+        L.check(L.lib().bddc_gpu_layout(self._h, C.byref(nl), C.byref(nr), C.byref(no), None), self._h)
+        l2g = np.zeros(max(nl.value, 1), dtype=np.int32)
+        L.check(L.lib().bddc_gpu_layout(self._h, None, None, None, l2g.ctypes.data_as(C.POINTER(C.c_int32))),
+                self._h)
+        return nl.value, nr.value, no.value, l2g[:nl.value]
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -1,0 +1,108 @@
+"""Multi-GPU parity driver, run under torchrun (one rank per GPU) by tests/test_gpu_distributed.py.
+
+Every rank builds the same global problem, a distributed preconditioner (its block of
+subdomains) and, as the parity reference, a single-GPU preconditioner of the whole problem on
+its own device. Checks (BASELINE.json parity bar):
+  * the distributed apply equals the single-GPU apply BIT FOR BIT on the rank's dofs (same
+    factors, same owner-ordered interface sums, r_c summed over all subdomains in ascending order);
+  * distributed PCG: identical iteration count, residual history within 1e-10 and solution
+    within 1e-10 of the single-GPU solve and of the reference's golden fixtures (bundle route,
+    tests/golden/r4x2m8, r16x8m8);
+  * the C-ABI host entry points fill exactly the rank's rows.
+Prints one JSON line per config on rank 0 and exits non-zero on any failure.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    from conftest import golden, history_err
+    from paper_2410_14786_b200 import Preconditioner, Problem, SolverOptions
+    from paper_2410_14786_b200.distributed import fresh_nccl_id, init
+
+    rank, world, local_rank, nid = init()
+    opts = SolverOptions(1e-8, 0.0, 10000, True)
+    cfgs = [("r4x2m8", (32, 16, 4, 2)), ("k4m8", (32, 32, 4, 4)), ("r16x8m8", (128, 64, 16, 8)),
+            ("c2_16x8", (1600, 800, 16, 8))]
+    if world >= 4:
+        cfgs.append(("c2_16x16", (1600, 1600, 16, 16)))
+    failures = []
+    for name, (cx, cy, kx, ky) in cfgs:
+        if kx * ky < world:
+            continue
+        prob = Problem.poisson(cx, kx, cy, ky, rhs_seed=1)
+        b = prob.rhs()
+        single = Preconditioner(prob, device=local_rank)
+        pre = Preconditioner(prob, device=local_rank, dist=(rank, world, nid))
+        nid = fresh_nccl_id()  # the next communicator needs its own id
+        n_local, n_rows, n_owned, l2g = pre.layout()
+        rows = l2g[:n_rows]
+        res = {"config": name, "rank": rank, "world": world, "n_rows": n_rows, "n_owned": n_owned}
+        z1 = single.apply(b)
+        zd = np.full(prob.global_dofs, np.nan)
+        zd = _apply(pre, b, zd)
+        res["apply_bitwise"] = bool(np.array_equal(zd[rows], z1[rows]))
+        res["apply_untouched_elsewhere"] = bool(np.isnan(np.delete(zd, rows)).all())
+        x1, r1 = single.pcg(b, opts)
+        xd, rd = pre.pcg(b, opts)
+        res["iterations"] = [rd.iterations, r1.iterations]
+        res["history_err_vs_single"] = history_err(rd.residual_history, r1.residual_history)
+        res["x_err_vs_single"] = float(np.abs(xd[rows] - x1[rows]).max() / np.abs(x1).max())
+        try:
+            g = golden(name)
+            res["history_err_vs_reference"] = history_err(rd.residual_history, g["pcg_history"])
+            res["iterations_reference"] = int(g["pcg_report"][0])
+            if "pcg_x" in g:
+                res["x_err_vs_reference"] = float(np.abs(xd[rows] - g["pcg_x"][rows]).max() / np.abs(g["pcg_x"]).max())
+        except FileNotFoundError:
+            pass
+        # device entry point on the rank-local layout
+        dev = f"cuda:{local_rank}"
+        bl = torch.from_numpy(np.ascontiguousarray(b[l2g])).to(dev)
+        xl = torch.empty_like(bl)
+        rep = pre.pcg_device(bl.data_ptr(), xl.data_ptr(), opts)
+        res["device_matches_host"] = bool(np.array_equal(xl.cpu().numpy()[:n_rows], xd[rows])) and \
+            rep.iterations == rd.iterations
+        ok = (res["apply_bitwise"] and res["apply_untouched_elsewhere"] and rd.iterations == r1.iterations
+              and res["history_err_vs_single"] <= 1e-10 and res["x_err_vs_single"] <= 1e-10
+              and res["device_matches_host"] and rd.converged)
+        if "history_err_vs_reference" in res:
+            ok = ok and res["history_err_vs_reference"] <= 1e-10 and rd.iterations == res["iterations_reference"]
+        if "x_err_vs_reference" in res:
+            ok = ok and res["x_err_vs_reference"] <= 1e-10
+        res["ok"] = bool(ok)
+        allres = [None] * world
+        dist.all_gather_object(allres, res)
+        if rank == 0:
+            for rr in allres:
+                print(json.dumps(rr), flush=True)
+        failures += [rr for rr in allres if not rr["ok"]]
+        del pre, single
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(1 if failures else 0)
+
+
+def _apply(pre, b, out):
+    import ctypes as C
+
+    from paper_2410_14786_b200 import _lib as L
+
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    L.check(L.lib().bddc_gpu_apply(pre._h, bb.ctypes.data_as(C.POINTER(C.c_double)),
+                                   out.ctypes.data_as(C.POINTER(C.c_double))), pre._h)
+    return out
+
+
+if __name__ == "__main__":
+    main()
