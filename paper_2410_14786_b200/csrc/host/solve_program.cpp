@@ -154,11 +154,14 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         auto in_group = [&](index_t s) { return group[s] == part; };
 
         using Chunks = std::vector<Chunk>;
+        // output rows per chunk (= per warp job): 32 normally; levels with few chunks use 16
+        // or 8 so that their work spreads over more of the 16 warps (set by chunk_rows_for)
+        int kr = 32;
         auto diag_fwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size();
-            for (index_t r0 = 0; r0 < ns; r0 += 32) {
-                const int nr = static_cast<int>(std::min<index_t>(32, ns - r0));
+            for (index_t r0 = 0; r0 < ns; r0 += kr) {
+                const int nr = static_cast<int>(std::min<index_t>(kr, ns - r0));
                 out.push_back(make_chunk(unit_bytes,
                     nr, static_cast<int>(r0 + nr),
                     [&](int r, int j) { return j <= r0 + r ? S.Linv[static_cast<std::size_t>(r0 + r) * ns + j] : 0.0; },
@@ -168,8 +171,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         auto diag_bwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size();
-            for (index_t q0 = 0; q0 < ns; q0 += 32) {
-                const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
+            for (index_t q0 = 0; q0 < ns; q0 += kr) {
+                const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
                 out.push_back(make_chunk(unit_bytes,
                     nq, static_cast<int>(ns - q0),
                     [&](int r, int j) {
@@ -183,8 +186,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             const Supernode& S = sn[s];
             const index_t ns = S.size(), mI = S.n_interior_rows;
             if (mI == 0) return;
-            for (index_t q0 = 0; q0 < ns; q0 += 32) {
-                const int nq = static_cast<int>(std::min<index_t>(32, ns - q0));
+            for (index_t q0 = 0; q0 < ns; q0 += kr) {
+                const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
                 out.push_back(make_chunk(unit_bytes,
                     nq, static_cast<int>(mI),
                     [&](int r, int j) { return S.B[static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
@@ -199,7 +202,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         // t[R_d] -= L_{R_d,d} x_d restricted to the target rows accepted by `take`: rows in the
         // own group (or own top) go to own T, rows in the shared top from a group supernode
         // go to Q (partial).
-        auto push_fwd = [&](index_t d, Chunks& out, bool from_top, auto take) {
+        auto push_fwd = [&](index_t d, Chunks& out, bool from_top, auto take,
+                            std::vector<std::vector<index_t>>* tgt = nullptr) {
             const Supernode& D = sn[d];
             const index_t nd = D.size(), mI = D.n_interior_rows;
             for (int pass = 0; pass < 2; ++pass) {
@@ -213,12 +217,16 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     const bool is_top = !from_top && l >= n_group;
                     if (is_top == to_top) rows.push_back(a);
                 }
-                for (std::size_t c0 = 0; c0 < rows.size(); c0 += 32) {
-                    const int k = static_cast<int>(std::min<std::size_t>(32, rows.size() - c0));
+                for (std::size_t c0 = 0; c0 < rows.size(); c0 += static_cast<std::size_t>(kr)) {
+                    const int k = static_cast<int>(std::min<std::size_t>(kr, rows.size() - c0));
                     std::vector<std::int32_t> outidx(k);
                     for (int r = 0; r < k; ++r) {
                         const std::int32_t l = loc[D.rows[rows[c0 + r]]];
                         outidx[r] = to_top ? l - n_group : l;
+                    }
+                    if (tgt) {
+                        tgt->emplace_back();
+                        for (int r = 0; r < k; ++r) tgt->back().push_back(D.rows[rows[c0 + r]]);
                     }
                     out.push_back(make_chunk(unit_bytes,
                         k, static_cast<int>(nd),
@@ -229,6 +237,15 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             }
         };
         auto all_rows = [](index_t) { return true; };
+        // chunk rows for a level: the largest of 32/16/8 giving at least 2 chunks per warp
+        auto chunk_rows_for = [&](const std::vector<index_t>& rows_per_node) {
+            for (int k : {32, 16}) {
+                std::int64_t chunks = 0;
+                for (index_t r : rows_per_node) chunks += (r + k - 1) / k;
+                if (chunks >= 2 * kSolveWarps) return k;
+            }
+            return 8;
+        };
         auto singles = [](Chunks&& cs) {  // level-synchronous phase: every chunk is its own job
             Phase ph;
             for (Chunk& c : cs) {
@@ -330,25 +347,37 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         // (3) levels above the cut, level-synchronous
         for (index_t h : heights) {
             Chunks b;
-            std::vector<index_t> nodes;
+            std::vector<index_t> nodes, nrows, mrows;
             for (index_t s = 0; s < nsn; ++s)
                 if (in_group(s) && !local[s] && sn[s].height == h) {
-                    diag_fwd(s, b);
                     nodes.push_back(s);
+                    nrows.push_back(sn[s].size());
+                    mrows.push_back(sn[s].n_interior_rows);
                 }
+            kr = chunk_rows_for(nrows);
+            for (index_t s : nodes) diag_fwd(s, b);
             phases.push_back(singles(std::move(b)));
+            kr = chunk_rows_for(mrows);
+            // one job per 32-row output chunk: chunks of one supernode write disjoint rows and
+            // spread over the warps; chunks of different supernodes are coloured by target rows
             std::vector<std::vector<index_t>> targets;
             std::vector<Chunks> pushes;
             for (index_t d : nodes) {
-                targets.emplace_back(sn[d].rows.begin(), sn[d].rows.begin() + sn[d].n_interior_rows);
-                pushes.emplace_back();
-                push_fwd(d, pushes.back(), false, all_rows);
+                Chunks cs;
+                std::vector<std::vector<index_t>> tg;
+                push_fwd(d, cs, false, all_rows, &tg);
+                for (std::size_t c = 0; c < cs.size(); ++c) {
+                    targets.push_back(std::move(tg[c]));
+                    pushes.emplace_back();
+                    pushes.back().push_back(std::move(cs[c]));
+                }
             }
             for (const auto& cls : colour(targets)) {
                 Phase pp;
                 for (std::size_t j : cls) pp.jobs.push_back(std::move(pushes[j]));
                 phases.push_back(std::move(pp));
             }
+            kr = 32;
         }
         // ---------------- exchange the partial sums into the shared top (P = 2)
         if (P == 2) {
@@ -361,18 +390,21 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         // ---------------- forward sweep: shared top chain (identical in every part)
         for (index_t s : top) {
             Chunks b, ps;
+            kr = chunk_rows_for({sn[s].size()});
             diag_fwd(s, b);
+            kr = chunk_rows_for({sn[s].n_interior_rows});
             push_fwd(s, ps, true, all_rows);
+            kr = 32;
             phases.push_back(singles(std::move(b)));
-            Phase pp;
-            pp.jobs.push_back(std::move(ps));
-            phases.push_back(std::move(pp));
+            phases.push_back(singles(std::move(ps)));  // disjoint 32-row chunks: one warp each
         }
         // ---------------- backward sweep: top chain, levels above the cut, then subtrees
         for (auto it = top.rbegin(); it != top.rend(); ++it) {
             Chunks a, b;
+            kr = chunk_rows_for({sn[*it].size()});
             pull_bwd(*it, a);
             diag_bwd(*it, b);
+            kr = 32;
             Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
             pa.kind = pb2.kind = kPhaseBackward;
             phases.push_back(std::move(pa));
@@ -380,11 +412,16 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         for (auto hit = heights.rbegin(); hit != heights.rend(); ++hit) {
             Chunks a, b;
+            std::vector<index_t> nrows;
+            for (index_t s = 0; s < nsn; ++s)
+                if (in_group(s) && !local[s] && sn[s].height == *hit) nrows.push_back(sn[s].size());
+            kr = chunk_rows_for(nrows);
             for (index_t s = 0; s < nsn; ++s)
                 if (in_group(s) && !local[s] && sn[s].height == *hit) {
                     pull_bwd(s, a);
                     diag_bwd(s, b);
                 }
+            kr = 32;
             Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
             pa.kind = pb2.kind = kPhaseBackward;
             phases.push_back(std::move(pa));

@@ -42,8 +42,8 @@ def main():
             continue
         prob = Problem.poisson(cx, kx, cy, ky, rhs_seed=1)
         b = prob.rhs()
-        single = Preconditioner(prob, device=local_rank)
-        pre = Preconditioner(prob, device=local_rank, dist=(rank, world, nid))
+        single = Preconditioner(prob, device=local_rank, solve_parts=2)  # same program split as the ranks
+        pre = Preconditioner(prob, device=local_rank, dist=(rank, world, nid), solve_parts=2)
         nid = fresh_nccl_id()  # the next communicator needs its own id
         n_local, n_rows, n_owned, l2g = pre.layout()
         rows = l2g[:n_rows]

@@ -219,3 +219,19 @@ def test_device_pointer_entry_points(gpu):
     rep = pre.pcg_device(b.data_ptr(), x.data_ptr(), OPTS, stream=s.cuda_stream)
     xh, reph = pre.pcg(p.rhs(), OPTS)
     assert rep.iterations == reph.iterations and np.array_equal(x.cpu().numpy(), xh)
+
+
+@pytest.mark.parametrize("k,m", [(2, 8), (4, 16), (8, 32)])
+def test_reference_dropin(gpu, k, m):
+    # a program written against the reference API swaps in bddc_b200::Preconditioner / pcg on
+    # the SAME reference objects (oracle/dropin_check.cpp, include/bddc_b200.hpp)
+    import json
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_check")
+    assert os.path.exists(exe), "oracle/_ref/dropin_check not built (__graft_entry__.build())"
+    out = subprocess.run([exe, str(k), str(m)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    res = json.loads(out.stdout.strip().splitlines()[0])
+    assert res["ok"] and res["iterations"][0] == res["iterations"][1]
