@@ -170,6 +170,7 @@ struct GpuContext::Impl {
         P.max_top = max_top;
         P.max_iface = max_iface;
         P.debug = debug_solve;
+        P.stats = dbg_buf.p;
         return P;
     }
     std::int32_t max_loc = 0, max_top = 0;
@@ -591,7 +592,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.units.upload(img.solve.units);
     I.order.upload(img.solve.order);
     if (std::getenv("BDDC_SOLVE_STATS")) {
-        I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 4);
+        I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 8 + img.solve.max_phases);
         BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));
     }
     upload_pod(I.subs, img.subs);

@@ -68,7 +68,66 @@ struct RegTable {
     }
 };
 
-template <int MODE, int CLUSTER>
+// One tile GEMV (device_format.hpp): k <= 32 rows, G column groups (power of two), lane
+// = r * G + g owns row r and columns j = t * G + g; values are stored iteration-major,
+// value(r, t*G + g) at [t*k*G + r*G + g], so every iteration is one contiguous,
+// conflict-free shared-memory read per lane. The G partial sums of a row are reduced with
+// an xor butterfly inside the row's lane group; the row total then accumulates into `acc`
+// (all lanes of the group) and is flushed by the group's first lane on the chunk's last tile.
+__device__ __forceinline__ void tile_task(const TileTask& task, const unsigned char* tile, const double* in,
+                                          double* own, double* other, double* Q, double& acc, int lane) {
+    const int G = task.groups, k = task.nrows, kG = k * G;
+    const int iters = task.iters;
+    const int g = lane & (G - 1), r = lane >> (__ffs(G) - 1);
+    const bool indexed = task.flags & kTaskInIndexed;
+    const int vbytes = (iters * kG * 8 + 15) & ~15;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (lane < kG) {
+        const double* M = reinterpret_cast<const double*>(tile) + lane;
+        int t = 0;
+        if (indexed) {
+            const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
+            for (; t + 4 <= iters; t += 4) {
+                s0 = fma(M[t * kG], in[ix[t * G]], s0);
+                s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
+                s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
+                s3 = fma(M[(t + 3) * kG], in[ix[(t + 3) * G]], s3);
+            }
+            if (t < iters) s0 = fma(M[t * kG], in[ix[t * G]], s0);
+            if (t + 1 < iters) s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
+            if (t + 2 < iters) s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
+        } else {
+            const double* v = in + task.in_ref + g;
+            for (; t + 4 <= iters; t += 4) {
+                s0 = fma(M[t * kG], v[t * G], s0);
+                s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
+                s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
+                s3 = fma(M[(t + 3) * kG], v[(t + 3) * G], s3);
+            }
+            if (t < iters) s0 = fma(M[t * kG], v[t * G], s0);
+            if (t + 1 < iters) s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
+            if (t + 2 < iters) s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
+        }
+    }
+    double tot = (s0 + s1) + (s2 + s3);
+    for (int off = G >> 1; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+    acc += tot;
+    if ((task.flags & kTaskLast) && g == 0) {
+        if (task.flags & kTaskPush) {
+            if (r < k) {
+                const int ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
+                const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes)[r];
+                if (task.flags & kTaskPartial) Q[o] += acc;
+                else own[o] -= acc;
+            }
+        } else if (r < task.nvalid) {
+            if (task.flags & kTaskDiag) other[task.out_base + r] = acc;
+            else own[task.out_base + r] -= acc;
+        }
+    }
+}
+
+template <int MODE, int CLUSTER, bool STATS>
 __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const PartDesc& pdr = S.parts[blockIdx.x];
@@ -82,9 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     double* X = T + ldn;
     double* Q = X + ldn;
     double* ZG = Q + ((S.max_top + 1) & ~1);
-    unsigned char* glut = reinterpret_cast<unsigned char*>(ZG + ((S.max_iface + 1) & ~1));  // lane / k, k = 1..32
-    unsigned char* ring = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<std::uintptr_t>(glut + 33 * 32) + 127) & ~std::uintptr_t(127));
+    unsigned char* glut = reinterpret_cast<unsigned char*>(ZG + ((S.max_iface + 1) & ~1));  // spare 1 KB
+    // offset arithmetic on smem_raw (not through an integer cast) keeps the shared address
+    // space visible to the compiler: tile reads stay LDS instead of generic LD
+    unsigned char* ring = smem_raw + ((static_cast<std::size_t>(glut + 33 * 32 - smem_raw) + 127) & ~std::size_t(127));
     const int nsl = 1 << S.slot_shift;  // ring slots per warp
     const int slot_shift = S.slot_shift;
     unsigned char* my_ring = ring + static_cast<std::size_t>(warp) * nsl * unit;
@@ -128,12 +188,27 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     // ---- right-hand side (and, in MODE 1/2, the interface coupling)
     const std::int32_t* gmap = S.gmap + pdr.gmap;
     const int n_loc = pdr.n_loc, n_top = pdr.n_top;
-    for (int l = tid; l < ldn; l += kThreads) {
-        T[l] = l < n_loc ? S.in[gmap[l]] : 0.0;
-        X[l] = 0.0;  // padded columns of a tile read finite zeros
+    // rhs gather: four independent index/value loads in flight per thread
+    for (int l0 = tid; l0 < ldn; l0 += 4 * kThreads) {
+        int gi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int l = l0 + q * kThreads;
+            gi[q] = l < n_loc ? __ldg(gmap + l) : -1;
+        }
+        double gv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gv[q] = gi[q] >= 0 ? S.in[gi[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int l = l0 + q * kThreads;
+            if (l < ldn) {
+                T[l] = gv[q];
+                X[l] = 0.0;  // padded columns of a tile read finite zeros
+            }
+        }
     }
     for (int l = tid; l < n_top; l += kThreads) Q[l] = 0.0;
-    for (int i = tid; i < 33 * 32; i += kThreads) glut[i] = static_cast<unsigned char>(i >> 5 ? (i & 31) / (i >> 5) : 0);
     if (MODE != 0) {
         const SubdomainDesc& sd = S.subs[pdr.sub];
         const int ng = sd.n_iface;
@@ -162,6 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     }
     __syncthreads();
 
+    constexpr bool stats = STATS;
+    long long t_start = stats ? clock64() : 0, t_wait = 0, t_bar = 0, t_refill = 0, t_tiles = 0, n_tiles = 0;
     double acc = 0.0;
     int u = 0;  // next unit of this warp
     for (int ph = 0; ph < n_phases; ++ph) {
@@ -171,76 +248,50 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         double* other = (kind & kPhaseBackward) ? T : X;
         for (; u < u_end; ++u) {
             const int s = u & (nsl - 1);
-            mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+            if constexpr (stats) {
+                const long long t0 = clock64();
+                mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+                t_wait += clock64() - t0;
+            } else {
+                mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+            }
             const unsigned char* ubuf = my_ring + s * unit;
             std::uint32_t cur = 0;
-            while (cur != kNoTask) {
-                const unsigned char* hdr = ubuf + (cur << 4);
+            const long long t_tile0 = stats ? clock64() : 0;
+            int4 hdr4 = *reinterpret_cast<const int4*>(ubuf);
+            while (true) {
+                if (stats) ++n_tiles;
                 TileTask task;
-                *reinterpret_cast<int4*>(&task) = *reinterpret_cast<const int4*>(hdr);
+                *reinterpret_cast<int4*>(&task) = hdr4;
+                const unsigned char* tile = ubuf + (cur << 4) + 16;
                 cur = task.next;
-                const bool indexed = task.flags & kTaskInIndexed;
-                const int k = task.nrows, G = task.groups, kG = k * G;
-                const int iters = task.iters;
-                const int vbytes = (iters * kG * 8 + 15) & ~15;
-                const int ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
+                if (cur != kNoTask) hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));  // next header early
                 if (task.flags & kTaskFirst) acc = 0.0;
-                // flattened mapping: lane = g*k + r, columns j = t*G + g
-                const int g = glut[(k << 5) + lane];
-                const unsigned char* tile = hdr + 16;
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                if (lane < kG && S.debug != 1) {
-                    const double* M = reinterpret_cast<const double*>(tile) + lane;
-                    const double* in = (task.flags & kTaskDiag) ? own : other;
-                    int t = 0;
-                    if (indexed) {
-                        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
-                        for (; t + 4 <= iters; t += 4) {
-                            s0 = fma(M[t * kG], in[ix[t * G]], s0);
-                            s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
-                            s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
-                            s3 = fma(M[(t + 3) * kG], in[ix[(t + 3) * G]], s3);
-                        }
-                        for (; t < iters; ++t) s0 = fma(M[t * kG], in[ix[t * G]], s0);
-                    } else {
-                        const double* v = in + task.in_ref + g;
-                        for (; t + 4 <= iters; t += 4) {
-                            s0 = fma(M[t * kG], v[t * G], s0);
-                            s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
-                            s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
-                            s3 = fma(M[(t + 3) * kG], v[(t + 3) * G], s3);
-                        }
-                        for (; t < iters; ++t) s0 = fma(M[t * kG], v[t * G], s0);
-                    }
-                }
-                double tot = (s0 + s1) + (s2 + s3);
-                for (int off = 1; off < G; off <<= 1) {
-                    const double o = __shfl_down_sync(0xffffffffu, tot, off * k);
-                    if (g + off < G) tot += o;
-                }
-                acc += tot;  // meaningful in lanes r < k (g == 0)
-                if (task.flags & kTaskLast) {
-                    if (task.flags & kTaskPush) {
-                        if (lane < k) {
-                            const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes)[lane];
-                            if (task.flags & kTaskPartial) Q[o] += acc;
-                            else own[o] -= acc;
-                        }
-                    } else if (lane < task.nvalid) {
-                        if (task.flags & kTaskDiag) other[task.out_base + lane] = acc;
-                        else own[task.out_base + lane] -= acc;
-                    }
-                    __syncwarp();  // later tiles of this warp's job read what was just written
-                }
+                const double* in = (task.flags & kTaskDiag) ? own : other;
+                tile_task(task, tile, in, own, other, Q, acc, lane);
+                if ((task.flags & kTaskLast) && (kind & kPhaseChained))
+                    __syncwarp();  // a later tile of this warp's job reads what was just written
+                if (cur == kNoTask) break;
             }
             // slot consumed: refill it with the unit nsl ahead
+            const long long t_r0 = stats ? clock64() : 0;
+            if (stats) t_tiles += t_r0 - t_tile0;
             if (u + nsl < nunits) {
                 __syncwarp();
                 if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 fetch(u + nsl);
             }
+            if (stats) t_refill += clock64() - t_r0;
         }
-        __syncthreads();
+        if constexpr (stats) {
+            const long long t0 = clock64();
+            __syncthreads();
+            t_bar += clock64() - t0;
+            if (blockIdx.x == 0 && tid == 0)  // phase timeline of CTA 0
+                S.stats[static_cast<long long>(gridDim.x) * kSolveWarps * 8 + ph] = clock64() - t_start;
+        } else {
+            __syncthreads();
+        }
         if (CLUSTER > 1 && (kind & kPhaseCombine)) {
             cluster_sync_all();
             // t_top = (t - Q_rank0) - Q_rank1 : identical arithmetic in both CTAs
@@ -256,13 +307,33 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
     }
 
-    for (int l = tid; l < pdr.n_write; l += kThreads) S.out[gmap[l]] = T[l];
+    if (stats && lane == 0) {
+        long long* o = S.stats + (static_cast<long long>(blockIdx.x) * kSolveWarps + warp) * 8;
+        o[0] = clock64() - t_start;
+        o[1] = t_wait;
+        o[2] = t_bar;
+        o[3] = nunits;
+        o[4] = t_refill;
+        o[5] = t_tiles;
+        o[6] = n_tiles;
+    }
+    for (int l0 = tid; l0 < pdr.n_write; l0 += 4 * kThreads) {
+        int gi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int l = l0 + q * kThreads;
+            gi[q] = l < pdr.n_write ? __ldg(gmap + l) : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (gi[q] >= 0) S.out[gi[q]] = T[l0 + q * kThreads];
+    }
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
 }
 
 template <int MODE, int CLUSTER>
 void launch_one(const SolveParams& P, const SolveLaunch& L, cudaStream_t stream) {
-    auto kern = interior_solve_kernel<MODE, CLUSTER>;
+    auto kern = P.stats ? interior_solve_kernel<MODE, CLUSTER, true> : interior_solve_kernel<MODE, CLUSTER, false>;
     BDDC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(L.n_parts);

@@ -29,6 +29,8 @@ struct SolveParams {
     int max_top;
     int max_iface;
     int debug;     // timing experiments only: 1 = skip tile math
+    long long* stats;  // diagnostics (BDDC_SOLVE_STATS): per CTA, per warp {total, mbarrier wait,
+                       // CTA-barrier wait, units} cycles of the launch; null = off
 };
 
 struct SolveLaunch {

@@ -17,11 +17,11 @@
 //     CTA barriers).
 //
 // Every task is one warp-level tile GEMV with a flattened lane mapping: a tile has k
-// rows (k <= 32) and ncols columns; lane l < k*G (G = floor(32/k) column groups) owns
-// row r = l % k and columns j = t*G + l/k for t = 0, 1, ...; the tile values are stored
-// iteration-major, value(r, t*G + g) at [t*k*G + g*k + r], so each iteration is one
-// contiguous, conflict-free shared-memory read. Partial sums are reduced across the G
-// groups with shuffles; lane r then holds the row total. Accumulators persist across
+// rows (k <= 32) and ncols columns; lane l = r*G + g < k*G (G = the largest power of two
+// with k*G <= 32 column groups) owns row r and columns j = t*G + g for t = 0, 1, ...; the
+// tile values are stored iteration-major, value(r, t*G + g) at [t*k*G + r*G + g], so each
+// iteration is one contiguous, conflict-free shared-memory read. Partial sums are reduced
+// inside each row's group of G lanes with an xor butterfly. Accumulators persist across
 // consecutive tasks of the same output (FIRST/LAST flags).
 //
 // Task kinds (forward: own = T, other = X; backward: own = X, other = T):
@@ -50,7 +50,12 @@ enum TaskFlags : std::uint8_t {
     kTaskPartial = 32,   // with PUSH: Q[outidx[r]] += acc
 };
 
-enum PhaseKind : std::int32_t { kPhaseNormal = 0, kPhaseCombine = 1, kPhaseBackward = 2 };
+enum PhaseKind : std::int32_t {
+    kPhaseNormal = 0,
+    kPhaseCombine = 1,
+    kPhaseBackward = 2,
+    kPhaseChained = 4,  // a warp's later tiles read rows its earlier tiles wrote (subtree jobs)
+};
 
 // Each tile in a unit is preceded by its 16-byte header; `next` links the tiles of one
 // unit (offset in 16-byte units from the unit start), kNoTask ends the unit.
@@ -61,7 +66,7 @@ struct TileTask {
     std::uint16_t out_base; // output chunk start (DIAG / PULL)
     std::uint16_t iters;    // ceil(columns / groups): inner-loop trip count
     std::uint8_t nrows;     // k, <= 32
-    std::uint8_t groups;    // G = floor(32 / k)
+    std::uint8_t groups;    // G: largest power of two with k * G <= 32
     std::uint8_t flags;
     std::uint8_t nvalid;    // rows written on flush
 };

@@ -42,7 +42,8 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
                  int nvalid, std::uint8_t flags, const std::vector<std::int32_t>* outidx) {
     Chunk ch;
     if (k < 1 || k > 32 || ncols < 1) throw std::logic_error("solve program: bad tile shape");
-    const int G = 32 / k;
+    int G = 1;
+    while (k * G * 2 <= 32) G *= 2;
     // iterations per piece so that header + values + index list + output rows fit a unit
     const int room = unit_bytes - 16 - 128 - 32;
     const int per_iter = 8 * k * G + (indexed ? 4 * G : 0);
@@ -65,7 +66,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
                 const int j = t * G + g;
                 if (j >= jn) continue;
                 for (int r = 0; r < k; ++r)
-                    T.vals[static_cast<std::size_t>(t) * k * G + g * k + r] = val(r, j0 + j);
+                    T.vals[static_cast<std::size_t>(t) * k * G + r * G + g] = val(r, j0 + j);
             }
         if (indexed) {
             T.idx.resize(static_cast<std::size_t>(iters) * G);
@@ -318,6 +319,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         {
             // (1) warp-local subtrees: diag + pushes inside the subtree, postorder
             Phase ph;
+            ph.kind = kPhaseChained;
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 Chunks job;
                 for (index_t s : job_nodes[j]) {
@@ -429,7 +431,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         {
             Phase ph;
-            ph.kind = kPhaseBackward;
+            ph.kind = kPhaseBackward | kPhaseChained;
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 Chunks job;
                 for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it) {

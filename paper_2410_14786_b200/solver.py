@@ -409,11 +409,12 @@ class Preconditioner:
         return {k: getattr(t, k) for k, _ in L.KernelTimes._fields_}
 
     def solve_profile(self) -> np.ndarray:
-        """Per-CTA, per-warp cycle accounting of the last interior solve (diagnostics)."""
+        """Per-CTA, per-warp cycle accounting {total, mbarrier wait, barrier wait, units} of the last
+        interior solve, followed by the phase timeline of CTA 0 (diagnostics; BDDC_SOLVE_STATS=1)."""
         cap = 1 << 20
         out = np.zeros(cap, dtype=np.int64)
         n = L.lib().bddc_gpu_solve_profile(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), cap)
-        return out[:max(n, 0)].reshape(-1, 4)
+        return out[:max(n, 0)]
 
     def synchronize(self) -> None:
         L.check(L.lib().bddc_gpu_synchronize(self._h), self._h)

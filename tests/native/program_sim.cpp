@@ -58,7 +58,7 @@ void run_phase(const SolvePools& sp, PartState& st) {
                     for (int g = 0; g < G; ++g) {
                         const int j = it * G + g;
                         const double v = (task.flags & kTaskInIndexed) ? in.at(ix[j]) : in.at(task.in_ref + j);
-                        s += M[it * k * G + g * k + r] * v;
+                        s += M[it * k * G + r * G + g] * v;
                     }
                 acc[r] += s;
             }
