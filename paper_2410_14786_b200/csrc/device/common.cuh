@@ -30,6 +30,12 @@ extern std::atomic<std::int64_t> g_kernel_launches;
         ::bddc_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     } while (0)
 
+// Speculative launches of the pipelined PCG loop pass the solver's scalar block: a set
+// converged (scal[2]) or error (scal[3]) flag turns the kernel into a no-op.
+__device__ __forceinline__ bool skip_launch(const double* scal) {
+    return scal != nullptr && (scal[2] != 0.0 || scal[3] != 0.0);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

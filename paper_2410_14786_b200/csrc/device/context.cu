@@ -111,6 +111,8 @@ struct GpuContext::Impl {
     std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
+    const double* apply_skip = nullptr;  // set while the pipelined PCG enqueues speculative applies
+    Event check_ev;  // convergence read-back of the pipelined PCG loop
 
     // ---- multi-GPU (null / unused on one GPU)
     std::unique_ptr<RankPlan> plan;
@@ -149,6 +151,7 @@ struct GpuContext::Impl {
 
     SolveParams solve_params(const double* in, double* out) const {
         SolveParams P{};
+        P.skip = apply_skip;
         P.parts = parts.p;
         P.subs = subs.p;
         P.stream = sstream.p;
@@ -180,6 +183,7 @@ struct GpuContext::Impl {
 
     IfaceParams iface_params() const {
         IfaceParams P{};
+        P.skip = apply_skip;
         P.subs = subs.p;
         P.n_subdomains = pb.decomposition.n_subdomains;
         P.max_iface = max_iface;
@@ -422,6 +426,21 @@ struct GpuContext::Impl {
         pcg_init_rho(D, s);
         halo_exchange(p.p, s);
         double rel = 1.0;
+        // The convergence test of iteration `it` is read back while the GPU already runs the
+        // next iteration's apply / dot / xpay (speculatively: they only touch z, p, rho, beta,
+        // which are unused once the loop stops), so the host round trip leaves no bubble.
+        // The reference-faithful coarse CG (check_coarse reads its status after every apply)
+        // keeps the synchronous order.
+        const bool pipelined = opt.coarse_mode == 0 || !precondition;
+        auto next_direction = [&](int it) {
+            apply_skip = scal.p;  // no-op once iteration `it` has converged or failed
+            if (precondition) apply(rd, zd, s);
+            apply_skip = nullptr;
+            pcg_dot(D, rd, zd, part_a.p, s);
+            gather_partial(part_a.p, D.grid, gath_a.p, s);
+            pcg_xpay(D, it, s);
+            halo_exchange(p.p, s);
+        };
         for (int it = 1; it <= o.max_iterations; ++it) {
             pcg_spmv_dot(D, s);
             gather_partial(part_a.p, D.grid, gath_a.p, s);
@@ -429,9 +448,16 @@ struct GpuContext::Impl {
             gather_partial(part_b.p, D.grid, gath_b.p, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
-            BDDC_CUDA(cudaStreamSynchronize(s));
-            if (pinned[3] == 1.0) throw std::runtime_error("matrix not SPD");
+            BDDC_CUDA(cudaEventRecord(check_ev.e, s));
+            const bool spec = pipelined && it < o.max_iterations;
+            if (spec) next_direction(it);
+            BDDC_CUDA(cudaEventSynchronize(check_ev.e));
+            if (pinned[3] == 1.0) {
+                BDDC_CUDA(cudaStreamSynchronize(s));
+                throw std::runtime_error("matrix not SPD");
+            }
             if (pinned[3] == 2.0) {
+                BDDC_CUDA(cudaStreamSynchronize(s));
                 DBuf<int> bad;
                 bad.alloc(1);
                 device_first_nonfinite(n, rd, bad.p, s);
@@ -444,14 +470,16 @@ struct GpuContext::Impl {
             rep.iterations = it;
             if (pinned[2] != 0.0) { rep.converged = true; break; }
             if (it == o.max_iterations) break;
-            if (precondition) {
-                apply(rd, zd, s);
-                check_coarse(s);
+            if (!spec) {
+                if (precondition) {
+                    apply(rd, zd, s);
+                    check_coarse(s);
+                }
+                pcg_dot(D, rd, zd, part_a.p, s);
+                gather_partial(part_a.p, D.grid, gath_a.p, s);
+                pcg_xpay(D, it, s);
+                halo_exchange(p.p, s);
             }
-            pcg_dot(D, rd, zd, part_a.p, s);
-            gather_partial(part_a.p, D.grid, gath_a.p, s);
-            pcg_xpay(D, it, s);
-            halo_exchange(p.p, s);
         }
         rep.final_relative_residual = rel;
         const int k = rep.iterations;

@@ -19,6 +19,7 @@ constexpr int kRestrictThreads = 256;
 
 __global__ void __launch_bounds__(kRestrictThreads)
 iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const double* __restrict__ u0) {
+    if (skip_launch(P.skip)) return;
     extern __shared__ double sg[];
     const SubdomainDesc& sd = P.subs[blockIdx.x];
     const int ng = sd.n_iface, np = sd.n_primal;
@@ -47,6 +48,7 @@ constexpr int kCoarseRows = 16;
 
 __global__ void __launch_bounds__(kCoarseThreads)
 coarse_direct_kernel(const IfaceParams P) {
+    if (skip_launch(P.skip)) return;
     extern __shared__ double rc[];
     const int nc = P.n_coarse;
     for (int q = threadIdx.x; q < nc; q += blockDim.x) {
@@ -67,9 +69,13 @@ coarse_direct_kernel(const IfaceParams P) {
 }
 
 constexpr int kLocalThreads = 256;
+constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads per lane)
 
+// h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each warp streams
+// kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight.
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
+    if (skip_launch(P.skip)) return;
     extern __shared__ double sm[];
     const int sub = blockIdx.x / blocks_per_sub, part = blockIdx.x % blocks_per_sub;
     const SubdomainDesc& sd = P.subs[sub];
@@ -85,22 +91,41 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* K = P.kmat + sd.kmat;
     const double* phig = P.phig + sd.phig;
-    for (int row = r0 + warp; row < r1; row += kLocalThreads / 32) {
-        const double* krow = K + static_cast<std::size_t>(row) * ng;
-        double a0 = 0.0, a1 = 0.0;
+    constexpr int kWarps = kLocalThreads / 32;
+    for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += kWarps * kLocalRows) {
+        const double* kr[kLocalRows];
+        bool live[kLocalRows];
+#pragma unroll
+        for (int q = 0; q < kLocalRows; ++q) {
+            live[q] = row0 + q < r1;
+            kr[q] = K + static_cast<std::size_t>(live[q] ? row0 + q : row0) * ng;
+        }
+        double a[kLocalRows][2] = {};
         int k = lane;
         for (; k + 32 < ng; k += 64) {
-            a0 = fma(ld_stream(krow + k), g[k], a0);
-            a1 = fma(ld_stream(krow + k + 32), g[k + 32], a1);
+            const double g0 = g[k], g1 = g[k + 32];
+#pragma unroll
+            for (int q = 0; q < kLocalRows; ++q)
+                if (live[q]) {
+                    a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
+                    a[q][1] = fma(ld_stream(kr[q] + k + 32), g1, a[q][1]);
+                }
         }
-        if (k < ng) a0 = fma(ld_stream(krow + k), g[k], a0);
-        double acc = warp_sum(a0 + a1);
-        if (lane == 0) {
+        if (k < ng) {
+            const double g0 = g[k];
+#pragma unroll
+            for (int q = 0; q < kLocalRows; ++q)
+                if (live[q]) a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
+        }
+#pragma unroll
+        for (int q = 0; q < kLocalRows; ++q) {
+            if (!live[q]) continue;  // warp-uniform
+            const int row = row0 + q;
+            const double acc = warp_sum(a[q][0] + a[q][1]);
             if (with_coarse) {
-                double coarse = 0.0;
-                for (int j = 0; j < np; ++j) coarse = fma(phig[row * np + j], xl[j], coarse);
-                P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (coarse + acc);
-            } else {
+                const double c = warp_sum(lane < np ? phig[row * np + lane] * xl[lane] : 0.0);
+                if (lane == 0) P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + acc);
+            } else if (lane == 0) {
                 P.hbuf[sd.hbuf + row] = acc;
             }
         }

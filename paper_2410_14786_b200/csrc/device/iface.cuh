@@ -5,6 +5,7 @@
 namespace bddc_b200 {
 
 struct IfaceParams {
+    const double* skip;  // pipelined PCG: skip when scal[2] / scal[3] is set (null: never)
     const SubdomainDesc* subs;
     int n_subdomains;
     int max_iface;

@@ -130,6 +130,7 @@ __device__ __forceinline__ void tile_task(const TileTask& task, const unsigned c
 template <int MODE, int CLUSTER, bool STATS>
 __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    if (skip_launch(S.skip)) return;  // uniform over the cluster: every CTA reads the same flag
     const PartDesc& pdr = S.parts[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int unit = S.unit_bytes;

@@ -5,6 +5,7 @@
 namespace bddc_b200 {
 
 struct SolveParams {
+    const double* skip;  // pipelined PCG: skip when scal[2] / scal[3] is set (null: never)
     const PartDesc* parts;
     const SubdomainDesc* subs;
     const double* stream;
