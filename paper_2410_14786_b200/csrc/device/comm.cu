@@ -109,6 +109,136 @@ void Comm::exchange(const std::vector<int>& peers, const double* sendbuf, const 
     check(api.GroupEnd(), "ncclGroupEnd");
 }
 
+namespace {
+
+__device__ __forceinline__ void st_release_sys(std::uint64_t* p, std::uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) {
+    std::uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr int kExThreads = 256;
+
+__device__ __forceinline__ std::uint64_t next_seq(const ExchangeDesc* D, std::uint64_t* seq_s) {
+    if (threadIdx.x == 0) {
+        *seq_s = *D->seq + 1;  // every rank runs the same exchanges in the same order
+        *D->seq = *seq_s;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ void put_all(const ExchangeDesc* D, const double* src) {
+    const int n = D->n_items;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) D->item_dst[i][0] = src[D->item_src[i]];
+}
+
+__device__ __forceinline__ void wait_all(const ExchangeDesc* D, std::uint64_t seq, int lane_base) {
+    const int w = static_cast<int>(threadIdx.x) - lane_base;
+    if (w >= 0 && w < D->n_wait) {
+        const std::uint64_t* f = D->wait[w];
+        std::uint64_t t0 = 0, t = 0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire_sys(f) < seq) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 20000000000ull) __trap();  // no peer progress for 20 s: fail loudly, never hang
+        }
+    }
+}
+
+// desc2 may be null. The flags are released by thread 0 after the CTA barrier: bar.sync
+// orders every thread's peer stores before thread 0's st.release.sys (cumulativity).
+__global__ void __launch_bounds__(kExThreads) exchange_kernel(const ExchangeDesc* __restrict__ D1, double* src1,
+                                                              const ExchangeDesc* __restrict__ D2, double* src2,
+                                                              const double* part, int grid, int slot) {
+    __shared__ double scratch[kExThreads / 32];
+    __shared__ std::uint64_t seq_s[2];
+    std::uint64_t t_start = 0, t_wait = 0, t_end = 0;
+    if (D1->stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    next_seq(D1, &seq_s[0]);
+    if (D2) next_seq(D2, &seq_s[1]);
+    if (part) {  // scalar gather: this rank's total first (fixed order)
+        double v = 0.0;
+        for (int i = threadIdx.x; i < grid; i += blockDim.x) v += part[i];
+        v = block_sum<kExThreads>(v, scratch);
+        if (threadIdx.x == 0) (D2 ? src2 : src1)[slot] = v;
+    }
+    __syncthreads();
+    put_all(D1, src1);
+    if (D2) put_all(D2, src2);
+    __syncthreads();
+    // bar.sync above orders every thread's peer stores before the flag stores; each flag is
+    // published by its own thread with a system-scope release (PTX release cumulativity)
+    if (threadIdx.x < D1->n_put) st_release_sys(D1->put[threadIdx.x].flag, seq_s[0]);
+    if (D2 && threadIdx.x >= kMaxPeers && threadIdx.x - kMaxPeers < D2->n_put)
+        st_release_sys(D2->put[threadIdx.x - kMaxPeers].flag, seq_s[1]);
+    if (D1->stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_wait));
+    wait_all(D1, seq_s[0], 0);
+    if (D2) wait_all(D2, seq_s[1], kMaxPeers);
+    __syncthreads();
+    if (D1->stats && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        D1->stats[0] += 1;
+        D1->stats[1] += t_end - t_start;
+        D1->stats[2] += t_end - t_wait;
+    }
+}
+
+}  // namespace
+
+PeerLinks::PeerLinks(Comm& comm, const std::vector<void*>& exports)
+    : nbuf_(static_cast<int>(exports.size())), rank_(comm.rank()), world_(comm.world()) {
+    const std::size_t hb = sizeof(cudaIpcMemHandle_t);
+    const std::size_t per = (hb * exports.size() + 7) / 8;  // doubles per rank
+    std::vector<double> host(per * world_, 0.0);
+    for (std::size_t b = 0; b < exports.size(); ++b) {
+        cudaIpcMemHandle_t h;
+        BDDC_CUDA(cudaIpcGetMemHandle(&h, exports[b]));
+        std::memcpy(reinterpret_cast<char*>(host.data() + per * rank_) + b * hb, &h, hb);
+    }
+    double* dev = nullptr;
+    BDDC_CUDA(cudaMalloc(&dev, sizeof(double) * host.size()));
+    BDDC_CUDA(cudaMemcpy(dev, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+    comm.allgather_inplace(dev, per, nullptr);
+    BDDC_CUDA(cudaDeviceSynchronize());
+    BDDC_CUDA(cudaMemcpy(host.data(), dev, sizeof(double) * host.size(), cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    ptrs_.assign(static_cast<std::size_t>(world_) * nbuf_, nullptr);
+    for (int q = 0; q < world_; ++q)
+        for (int b = 0; b < nbuf_; ++b) {
+            if (q == rank_) {
+                ptrs_[static_cast<std::size_t>(q) * nbuf_ + b] = exports[b];
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, reinterpret_cast<const char*>(host.data() + per * q) + b * hb, hb);
+            void* p = nullptr;
+            BDDC_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            ptrs_[static_cast<std::size_t>(q) * nbuf_ + b] = p;
+        }
+}
+
+PeerLinks::~PeerLinks() {
+    for (int q = 0; q < world_; ++q)
+        if (q != rank_)
+            for (int b = 0; b < nbuf_; ++b)
+                if (void* p = ptrs_[static_cast<std::size_t>(q) * nbuf_ + b]) cudaIpcCloseMemHandle(p);
+}
+
+void launch_exchange(const ExchangeDesc* desc, double* src, const double* part, int grid, int slot,
+                     cudaStream_t s) {
+    exchange_kernel<<<1, kExThreads, 0, s>>>(desc, src, nullptr, nullptr, part, grid, slot);
+    BDDC_LAUNCHED();
+}
+
+void launch_exchange2(const ExchangeDesc* desc1, double* src1, const ExchangeDesc* desc2, double* src2,
+                      const double* part, int grid, int slot, cudaStream_t s) {
+    exchange_kernel<<<1, kExThreads, 0, s>>>(desc1, src1, desc2, src2, part, grid, slot);
+    BDDC_LAUNCHED();
+}
+
 void launch_pack(int n, const std::int32_t* idx, const double* src, double* dst, cudaStream_t s) {
     if (n <= 0) return;
     pack_kernel<<<std::min(148 * 4, (n + 255) / 256), 256, 0, s>>>(n, idx, src, dst);

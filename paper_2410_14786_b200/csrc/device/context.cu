@@ -48,6 +48,10 @@ struct Event {
     ~Event() { if (e) cudaEventDestroy(e); }
 };
 
+struct ApplyEvents {  // interior solve | interface steps | interior solve of one apply
+    Event e[4];
+};
+
 void ensure_finite(const double* x, index_t n, const char* context) {
     for (index_t i = 0; i < n; ++i)
         if (!std::isfinite(x[i]))
@@ -103,6 +107,7 @@ struct GpuContext::Impl {
     DBuf<double> U, gbuf, hbuf, cbuf, xc, lbuf, vin, vout, vtmp, vtmp2;
     // pcg
     DBuf<double> x, r, z, p, q, part_a, part_b, rho, alpha, beta, hist, scal;
+    DBuf<int> iter_ctr;
     double* pinned = nullptr;
     int max_it_alloc = 0;
 
@@ -112,13 +117,73 @@ struct GpuContext::Impl {
 
     KernelTimes times;
     const double* apply_skip = nullptr;  // set while the pipelined PCG enqueues speculative applies
+
+    // CUDA graphs of the PCG iteration (BDDC_GRAPH=0 disables): A = spmv/update/check and the
+    // convergence read-back, B = the speculative apply, r.z and the new direction. The device
+    // iteration counter and exchange sequence counters make one capture valid for every
+    // iteration; with profiling on, B's four event-record nodes are rebound to fresh pool
+    // events before each launch so the per-kernel timing stays live.
+    struct IterGraphs {
+        cudaGraphExec_t a = nullptr, b = nullptr;
+        cudaGraph_t b_graph = nullptr;  // kept alive: its event-record nodes are rebound per launch
+        std::int64_t a_kernels = 0, b_kernels = 0;
+        cudaGraphNode_t ev_nodes[4] = {};
+        PcgDevice key{};
+        bool precondition = false, profile = false, valid = false;
+        void reset() {
+            if (a) cudaGraphExecDestroy(a);
+            if (b) cudaGraphExecDestroy(b);
+            if (b_graph) cudaGraphDestroy(b_graph);
+            a = b = nullptr;
+            b_graph = nullptr;
+            valid = false;
+        }
+        ~IterGraphs() { reset(); }
+    } graphs;
+    ApplyEvents* capture_events = nullptr;
+    std::unique_ptr<ApplyEvents> graph_events;
+    bool use_graphs = !(std::getenv("BDDC_GRAPH") && std::atoi(std::getenv("BDDC_GRAPH")) == 0);
+
+    template <typename Body>
+    cudaGraphExec_t capture(cudaStream_t s, Body&& body, std::int64_t* kernels, cudaGraph_t* keep = nullptr) {
+        cudaGraph_t g = nullptr;
+        const std::int64_t l0 = g_kernel_launches.load();
+        BDDC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        try {
+            body();
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        BDDC_CUDA(cudaStreamEndCapture(s, &g));
+        // captured launches run at every graph launch: count them there, not here
+        *kernels = g_kernel_launches.load() - l0;
+        g_kernel_launches.fetch_sub(*kernels);
+        cudaGraphExec_t e = nullptr;
+        BDDC_CUDA(cudaGraphInstantiate(&e, g, 0));
+        if (keep) *keep = g;
+        else cudaGraphDestroy(g);
+        return e;
+    }
     Event check_ev;  // convergence read-back of the pipelined PCG loop
 
     // ---- multi-GPU (null / unused on one GPU)
     std::unique_ptr<RankPlan> plan;
     std::unique_ptr<Comm> comm;
     DBuf<std::int32_t> halo_idx, iface_idx;
-    DBuf<double> halo_send, iface_send, gath_a, gath_b;
+    DBuf<double> halo_send, iface_send, gath_a, gath_b, gath_c, gath_d;  // p.q, r.r, r.z, b.b per rank
+    // peer-memory exchanges (default): IPC mappings, one descriptor + sequence per type
+    enum ExType { kExU = 0, kExP = 1, kExH = 2, kExC = 3, kExPQ = 4, kExRR = 5, kExRZ = 6, kExNB = 7, kExZ = 8 };
+    std::unique_ptr<PeerLinks> links;
+    DBuf<ExchangeDesc> ex_desc;
+    DBuf<std::uint64_t> ex_flags, ex_seq;  // flags [type][src]; per-type sequence counters
+    DBuf<unsigned long long> ex_stats;
+    DBuf<double*> ex_item_dst;
+    DBuf<std::int32_t> ex_item_src;
+    bool p2p() const { return static_cast<bool>(links); }
+    // timing experiments only (wrong results): BDDC_NO_EXCHANGE=1 skips every exchange
+    bool no_exchange = std::getenv("BDDC_NO_EXCHANGE") && std::atoi(std::getenv("BDDC_NO_EXCHANGE")) == 1;
     std::vector<std::int32_t> halo_soff, halo_roff, iface_soff, iface_roff;
     index_t n_global = 0, n_rows = 0, n_owned = 0;
     std::string symmetry_error;  // distributed: global symmetry check done once at creation
@@ -128,23 +193,46 @@ struct GpuContext::Impl {
 
     // u0 / p halo: owners send their entries, the halo region [n_rows, n) is overwritten
     void halo_exchange(double* v, cudaStream_t s) {
-        if (!dist()) return;
+        if (!dist() || no_exchange) return;
+        if (p2p()) {
+            const int t = v == U.p ? kExU : kExP;
+            launch_exchange(ex_desc.p + t, v, nullptr, 0, 0, s);
+            return;
+        }
         launch_pack(static_cast<int>(plan->halo_send_idx.size()), halo_idx.p, v, halo_send.p, s);
         comm->exchange(plan->halo_peers, halo_send.p, halo_soff, v + n_rows, halo_roff, s);
     }
     // h_i of interface dofs shared with other ranks -> remote hbuf slots
     void iface_exchange(cudaStream_t s) {
-        if (!dist()) return;
+        if (!dist() || no_exchange) return;
+        if (p2p()) {
+            launch_exchange(ex_desc.p + kExH, hbuf.p, nullptr, 0, 0, s);
+            return;
+        }
         launch_pack(static_cast<int>(plan->iface_send_slot.size()), iface_idx.p, hbuf.p, iface_send.p, s);
         comm->exchange(plan->iface_peers, iface_send.p, iface_soff, hbuf.p + plan->n_local_slots, iface_roff, s);
     }
     // every rank's c_i (padded blocks, rank order) for the ordered r_c sum
     void gather_cbuf(cudaStream_t s) {
-        if (dist()) comm->allgather_inplace(cbuf.p, static_cast<std::size_t>(plan->cbuf_pad), s);
+        if (!dist() || no_exchange) return;
+        if (p2p()) launch_exchange(ex_desc.p + kExC, cbuf.p, nullptr, 0, 0, s);
+        else comm->allgather_inplace(cbuf.p, static_cast<std::size_t>(plan->cbuf_pad), s);
     }
+    // r.z gather fused with the halo of z (peer-memory mode, preconditioned): the new direction
+    // p = z + beta p is then formed on the halo locally, bit-identical to its owner's values
+    void gather_rz_with_z_halo(const double* part, int grid, cudaStream_t s) {
+        if (no_exchange) return;
+        launch_exchange2(ex_desc.p + kExZ, z.p, ex_desc.p + kExRZ, gath_c.p, part, grid, comm->rank(), s);
+    }
+
     // part[0..grid) -> gath[rank], then gathered over ranks (consumers sum in rank order)
     void gather_partial(const double* part, int grid, double* gath, cudaStream_t s) {
-        if (!dist()) return;
+        if (!dist() || no_exchange) return;
+        if (p2p()) {
+            const int t = gath == gath_a.p ? kExPQ : gath == gath_b.p ? kExRR : gath == gath_c.p ? kExRZ : kExNB;
+            launch_exchange(ex_desc.p + t, gath, part, grid, comm->rank(), s);
+            return;
+        }
         launch_reduce_to(part, grid, gath + comm->rank(), false, s);
         comm->allgather_inplace(gath, 1, s);
     }
@@ -272,9 +360,6 @@ struct GpuContext::Impl {
     // Profiling: CUDA events recorded on the launching stream around the two interior
     // solves and the interface steps of every apply, without synchronising; they are
     // resolved lazily (kernel_times()), so profiling does not perturb the timed region.
-    struct ApplyEvents {
-        Event e[4];
-    };
     std::vector<std::unique_ptr<ApplyEvents>> ev_pool;
     std::size_t ev_used = 0;
 
@@ -296,16 +381,22 @@ struct GpuContext::Impl {
         ev_used = 0;
     }
 
+    // inside a graph capture an event record must be an explicit (external) node
+    void record(cudaEvent_t e, cudaStream_t s) {
+        if (capture_events) BDDC_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+        else BDDC_CUDA(cudaEventRecord(e, s));
+    }
+
     void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
-        ApplyEvents* E = nullptr;
-        if (opt.profile) {
+        ApplyEvents* E = capture_events;  // graph capture: fixed events, rebound per launch
+        if (opt.profile && !E) {
             if (ev_used == 4096) resolve_events();
             if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
             E = ev_pool[ev_used++].get();
         }
-        if (E) BDDC_CUDA(cudaEventRecord(E->e[0].e, s));
+        if (E) record(E->e[0].e, s);
         launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
-        if (E) BDDC_CUDA(cudaEventRecord(E->e[1].e, s));
+        if (E) record(E->e[1].e, s);
         halo_exchange(U.p, s);
         const IfaceParams ip = iface_params();
         launch_iface_restrict(ip, r_dev, U.p, s);
@@ -313,9 +404,9 @@ struct GpuContext::Impl {
         coarse_solve(s);
         launch_iface_local(ip, opt.local_blocks, s, true);
         iface_exchange(s);
-        if (E) BDDC_CUDA(cudaEventRecord(E->e[2].e, s));
+        if (E) record(E->e[2].e, s);
         launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
-        if (E) BDDC_CUDA(cudaEventRecord(E->e[3].e, s));
+        if (E) record(E->e[3].e, s);
     }
 
     void ensure_pcg(int max_it) {
@@ -325,9 +416,12 @@ struct GpuContext::Impl {
             const int g = pcg_grid_for(dist() ? n_rows : n);
             part_a.alloc(g);
             part_b.alloc(g);
-            gath_a.alloc(dist() ? comm->world() : 1);
-            gath_b.alloc(dist() ? comm->world() : 1);
+            for (DBuf<double>* gb : {&gath_a, &gath_b, &gath_c, &gath_d}) {
+                gb->alloc(dist() ? comm->world() : 1);
+                BDDC_CUDA(cudaMemset(gb->p, 0, sizeof(double) * gb->n));
+            }
             scal.alloc(8);
+            iter_ctr.alloc(1);
             BDDC_CUDA(cudaMallocHost(&pinned, sizeof(double) * 8));
         }
         if (max_it > max_it_alloc) {
@@ -343,6 +437,7 @@ struct GpuContext::Impl {
         PcgDevice D{};
         D.n = dist() ? n_rows : pb.decomposition.global_dofs;
         D.n_dot = dist() ? n_owned : D.n;
+        D.n_dir = D.n;  // pcg() widens it to the halo when z's halo arrives with r.z
         D.grid = pcg_grid_for(D.n);
         D.A_ptr = A_ptr.p;
         D.A_col = A_col.p;
@@ -358,14 +453,116 @@ struct GpuContext::Impl {
         D.red_a_n = dist() ? comm->world() : D.grid;
         D.red_b = dist() ? gath_b.p : part_b.p;
         D.red_b_n = dist() ? comm->world() : D.grid;
+        D.red_c = dist() ? gath_c.p : part_a.p;
+        D.red_c_n = dist() ? comm->world() : D.grid;
         D.rho = rho.p;
         D.alpha = alpha.p;
         D.beta = beta.p;
         D.hist = hist.p;
         D.scal = scal.p;
+        D.iter = iter_ctr.p;
         D.rtol = o.rel_tolerance;
         D.atol = o.abs_tolerance;
         return D;
+    }
+
+    // Peer-memory exchange descriptors (see device/comm.cuh). Buffers exported, in order:
+    // U, p, hbuf, cbuf, gath_a, gath_b, gath_c, gath_d, flags, z.
+    void setup_peer_links() {
+        const RankPlan& P = *plan;
+        const int me = comm->rank(), world = comm->world();
+        ex_flags.alloc(static_cast<std::size_t>(kFlagTypes) * kMaxPeers);
+        BDDC_CUDA(cudaMemset(ex_flags.p, 0, sizeof(std::uint64_t) * ex_flags.n));
+        ex_seq.alloc(kFlagTypes);
+        BDDC_CUDA(cudaMemset(ex_seq.p, 0, sizeof(std::uint64_t) * ex_seq.n));
+        // where each peer receives this rank's halo / interface values: rank r publishes
+        // (n_rows + halo_recv_off, n_local_slots + iface_recv_off) for every source q
+        std::vector<double> tbl(static_cast<std::size_t>(world) * world * 2, -1.0);
+        for (std::size_t k = 0; k < P.halo_peers.size(); ++k)
+            tbl[(static_cast<std::size_t>(me) * world + P.halo_peers[k]) * 2] = P.n_rows + P.halo_recv_off[k];
+        for (std::size_t k = 0; k < P.iface_peers.size(); ++k)
+            tbl[(static_cast<std::size_t>(me) * world + P.iface_peers[k]) * 2 + 1] = P.n_local_slots + P.iface_recv_off[k];
+        {
+            DBuf<double> d;
+            d.upload(tbl);
+            comm->allgather_inplace(d.p, static_cast<std::size_t>(world) * 2, nullptr);
+            BDDC_CUDA(cudaDeviceSynchronize());
+            BDDC_CUDA(cudaMemcpy(tbl.data(), d.p, sizeof(double) * tbl.size(), cudaMemcpyDeviceToHost));
+        }
+        links = std::make_unique<PeerLinks>(*comm, std::vector<void*>{U.p, p.p, hbuf.p, cbuf.p, gath_a.p, gath_b.p,
+                                                                      gath_c.p, gath_d.p, ex_flags.p, z.p});
+        std::vector<ExchangeDesc> desc(kFlagTypes);
+        auto flag_of = [&](int q, int type) {
+            return static_cast<std::uint64_t*>(links->peer(q, 8)) + type * kMaxPeers + me;
+        };
+        auto neighbour = [&](ExchangeDesc& D, int type, int buffer, const std::vector<int>& peers,
+                             const std::vector<index_t>& soff, const std::int32_t* idx, int col) {
+            D.idx = idx;
+            for (std::size_t k = 0; k < peers.size(); ++k) {
+                const int q = peers[k];
+                const double at = tbl[(static_cast<std::size_t>(q) * world + me) * 2 + col];
+                if (at < 0) throw std::logic_error("rank plan: peer does not expect this rank's values");
+                PeerPut& pp = D.put[D.n_put++];
+                pp.dst = static_cast<double*>(links->peer(q, buffer)) + static_cast<std::int64_t>(at);
+                pp.flag = flag_of(q, type);
+                pp.off = soff[k];
+                pp.cnt = soff[k + 1] - soff[k];
+                D.wait[D.n_wait++] = ex_flags.p + type * kMaxPeers + q;
+            }
+        };
+        neighbour(desc[kExU], kExU, 0, P.halo_peers, P.halo_send_off, halo_idx.p, 0);
+        neighbour(desc[kExP], kExP, 1, P.halo_peers, P.halo_send_off, halo_idx.p, 0);
+        neighbour(desc[kExH], kExH, 2, P.iface_peers, P.iface_send_off, iface_idx.p, 1);
+        neighbour(desc[kExZ], kExZ, 9, P.halo_peers, P.halo_send_off, halo_idx.p, 0);
+        auto all_to_all = [&](ExchangeDesc& D, int type, int buffer, std::int32_t off, std::int32_t cnt) {
+            for (int q = 0; q < world; ++q) {
+                if (q == me) continue;
+                PeerPut& pp = D.put[D.n_put++];
+                pp.dst = static_cast<double*>(links->peer(q, buffer)) + off;
+                pp.flag = flag_of(q, type);
+                pp.off = off;
+                pp.cnt = cnt;
+                D.wait[D.n_wait++] = ex_flags.p + type * kMaxPeers + q;
+            }
+        };
+        all_to_all(desc[kExC], kExC, 3, me * P.cbuf_pad, P.cbuf_pad);
+        all_to_all(desc[kExPQ], kExPQ, 4, me, 1);
+        all_to_all(desc[kExRR], kExRR, 5, me, 1);
+        all_to_all(desc[kExRZ], kExRZ, 6, me, 1);
+        all_to_all(desc[kExNB], kExNB, 7, me, 1);
+        for (int t = 0; t < kFlagTypes; ++t) desc[t].seq = ex_seq.p + t;
+        if (std::getenv("BDDC_EXCH_STATS")) {  // diagnostics: per-type {count, total ns, wait ns}
+            ex_stats.alloc(3 * kFlagTypes);
+            BDDC_CUDA(cudaMemset(ex_stats.p, 0, sizeof(unsigned long long) * ex_stats.n));
+            for (int t = 0; t < kFlagTypes; ++t) desc[t].stats = ex_stats.p + 3 * t;
+        }
+        // flatten every descriptor's puts over its peers (one parallel loop in the kernel)
+        std::vector<double*> dst_all;
+        std::vector<std::int32_t> src_all;
+        std::vector<std::size_t> first(desc.size() + 1, 0);
+        for (std::size_t t = 0; t < desc.size(); ++t) {
+            const ExchangeDesc& D = desc[t];
+            const std::vector<index_t>* ids = D.idx == halo_idx.p ? &P.halo_send_idx
+                                              : D.idx == iface_idx.p ? &P.iface_send_slot : nullptr;
+            for (int k = 0; k < D.n_put; ++k)
+                for (int i = 0; i < D.put[k].cnt; ++i) {
+                    dst_all.push_back(D.put[k].dst + i);
+                    src_all.push_back(ids ? (*ids)[D.put[k].off + i] : D.put[k].off + i);
+                }
+            first[t + 1] = dst_all.size();
+        }
+        ex_item_dst.alloc(std::max<std::size_t>(dst_all.size(), 1));
+        if (!dst_all.empty())
+            BDDC_CUDA(cudaMemcpy(ex_item_dst.p, dst_all.data(), sizeof(double*) * dst_all.size(), cudaMemcpyHostToDevice));
+        ex_item_src.upload(src_all);
+        for (std::size_t t = 0; t < desc.size(); ++t) {
+            desc[t].n_items = static_cast<std::int32_t>(first[t + 1] - first[t]);
+            desc[t].item_dst = ex_item_dst.p + first[t];
+            desc[t].item_src = ex_item_src.p + first[t];
+        }
+        ex_desc.alloc(desc.size());
+        BDDC_CUDA(cudaMemcpy(ex_desc.p, desc.data(), sizeof(ExchangeDesc) * desc.size(), cudaMemcpyHostToDevice));
+        BDDC_CUDA(cudaDeviceSynchronize());
     }
 
     index_t global_index(int local) const {
@@ -390,13 +587,16 @@ struct GpuContext::Impl {
         double* rd = r.p;
         double* zd = precondition ? z.p : r.p;
         PcgDevice D = pcg_device(o, xd, rd, zd);
+        const bool fused_dir = dist() && p2p() && precondition;  // z halo arrives with r.z
+        if (fused_dir) D.n_dir = static_cast<int>(n);
         BDDC_CUDA(cudaMemsetAsync(xd, 0, sizeof(double) * n, s));
         BDDC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(double) * 8, s));
+        BDDC_CUDA(cudaMemsetAsync(iter_ctr.p, 0, sizeof(int), s));
         BDDC_CUDA(cudaMemcpyAsync(rd, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         pcg_dot(D, b, b, part_b.p, s);
         if (dist()) {
-            gather_partial(part_b.p, D.grid, gath_b.p, s);
-            launch_reduce_to(gath_b.p, comm->world(), scal.p, true, s);
+            gather_partial(part_b.p, D.grid, gath_d.p, s);
+            launch_reduce_to(gath_d.p, comm->world(), scal.p, true, s);
         } else {
             pcg_finalize(D, part_b.p, 0, true, s);
         }
@@ -422,9 +622,14 @@ struct GpuContext::Impl {
             check_coarse(s);
         }
         pcg_dot(D, rd, zd, part_a.p, s);
-        gather_partial(part_a.p, D.grid, gath_a.p, s);
-        pcg_init_rho(D, s);
-        halo_exchange(p.p, s);
+        if (fused_dir) {
+            gather_rz_with_z_halo(part_a.p, D.grid, s);
+            pcg_init_rho(D, s);
+        } else {
+            gather_partial(part_a.p, D.grid, gath_c.p, s);
+            pcg_init_rho(D, s);
+            halo_exchange(p.p, s);
+        }
         double rel = 1.0;
         // The convergence test of iteration `it` is read back while the GPU already runs the
         // next iteration's apply / dot / xpay (speculatively: they only touch z, p, rho, beta,
@@ -432,25 +637,96 @@ struct GpuContext::Impl {
         // The reference-faithful coarse CG (check_coarse reads its status after every apply)
         // keeps the synchronous order.
         const bool pipelined = opt.coarse_mode == 0 || !precondition;
+        // graphs: pipelined loop, peer-memory (or no) exchanges, not under an outer capture
+        cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+        BDDC_CUDA(cudaStreamIsCapturing(s, &cap_status));
+        const bool graphed = use_graphs && pipelined && (!dist() || p2p()) && cap_status == cudaStreamCaptureStatusNone;
         auto next_direction = [&](int it) {
             apply_skip = scal.p;  // no-op once iteration `it` has converged or failed
             if (precondition) apply(rd, zd, s);
             apply_skip = nullptr;
             pcg_dot(D, rd, zd, part_a.p, s);
-            gather_partial(part_a.p, D.grid, gath_a.p, s);
-            pcg_xpay(D, it, s);
-            halo_exchange(p.p, s);
+            if (fused_dir) {
+                gather_rz_with_z_halo(part_a.p, D.grid, s);
+                pcg_xpay(D, it, s);
+            } else {
+                gather_partial(part_a.p, D.grid, gath_c.p, s);
+                pcg_xpay(D, it, s);
+                halo_exchange(p.p, s);
+            }
         };
-        for (int it = 1; it <= o.max_iterations; ++it) {
+        auto check_part = [&](int it) {
             pcg_spmv_dot(D, s);
             gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_update(D, it, s);
             gather_partial(part_b.p, D.grid, gath_b.p, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+        };
+        if (graphed) {
+            const bool prof = opt.profile;
+            if (!graphs.valid || std::memcmp(&graphs.key, &D, sizeof D) != 0 || graphs.precondition != precondition ||
+                graphs.profile != prof) {
+                graphs.reset();
+                graphs.a = capture(s, [&] { check_part(0); }, &graphs.a_kernels);
+                cudaGraph_t gb = nullptr;
+                if (prof) {
+                    if (!graph_events) graph_events = std::make_unique<ApplyEvents>();
+                    capture_events = graph_events.get();
+                }
+                try {
+                    graphs.b = capture(s, [&] { next_direction(0); }, &graphs.b_kernels, &gb);
+                } catch (...) {
+                    capture_events = nullptr;
+                    throw;
+                }
+                capture_events = nullptr;
+                if (prof && precondition) {  // locate the event-record nodes of the apply
+                    std::size_t nn = 0;
+                    BDDC_CUDA(cudaGraphGetNodes(gb, nullptr, &nn));
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    BDDC_CUDA(cudaGraphGetNodes(gb, nodes.data(), &nn));
+                    for (cudaGraphNode_t nd : nodes) {
+                        cudaGraphNodeType ty;
+                        BDDC_CUDA(cudaGraphNodeGetType(nd, &ty));
+                        if (ty != cudaGraphNodeTypeEventRecord) continue;
+                        cudaEvent_t ev = nullptr;
+                        BDDC_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+                        for (int k = 0; k < 4; ++k)
+                            if (ev == graph_events->e[k].e) graphs.ev_nodes[k] = nd;
+                    }
+                }
+                graphs.b_graph = gb;
+                graphs.key = D;
+                graphs.precondition = precondition;
+                graphs.profile = prof;
+                graphs.valid = true;
+            }
+        }
+        auto launch_b = [&]() {
+            if (graphs.profile && precondition) {  // bind this launch's timing events
+                if (ev_used == 4096) resolve_events();
+                if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
+                ApplyEvents* E = ev_pool[ev_used++].get();
+                for (int k = 0; k < 4; ++k)
+                    BDDC_CUDA(cudaGraphExecEventRecordNodeSetEvent(graphs.b, graphs.ev_nodes[k], E->e[k].e));
+            }
+            BDDC_CUDA(cudaGraphLaunch(graphs.b, s));
+            g_kernel_launches.fetch_add(graphs.b_kernels);
+        };
+        for (int it = 1; it <= o.max_iterations; ++it) {
+            if (graphed) {
+                BDDC_CUDA(cudaGraphLaunch(graphs.a, s));
+                g_kernel_launches.fetch_add(graphs.a_kernels);
+            } else {
+                check_part(it);
+            }
             BDDC_CUDA(cudaEventRecord(check_ev.e, s));
             const bool spec = pipelined && it < o.max_iterations;
-            if (spec) next_direction(it);
+            if (spec) {
+                if (graphed) launch_b();
+                else next_direction(it);
+            }
             BDDC_CUDA(cudaEventSynchronize(check_ev.e));
             if (pinned[3] == 1.0) {
                 BDDC_CUDA(cudaStreamSynchronize(s));
@@ -476,7 +752,7 @@ struct GpuContext::Impl {
                     check_coarse(s);
                 }
                 pcg_dot(D, rd, zd, part_a.p, s);
-                gather_partial(part_a.p, D.grid, gath_a.p, s);
+                gather_partial(part_a.p, D.grid, gath_c.p, s);
                 pcg_xpay(D, it, s);
                 halo_exchange(p.p, s);
             }
@@ -689,7 +965,10 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         I.iface_roff.assign(P.iface_recv_off.begin(), P.iface_recv_off.end());
         BDDC_CUDA(cudaMemset(I.hbuf.p, 0, sizeof(double) * I.hbuf.n));
         BDDC_CUDA(cudaMemset(I.cbuf.p, 0, sizeof(double) * I.cbuf.n));
+        I.ensure_pcg(1);
         BDDC_CUDA(cudaDeviceSynchronize());
+        const char* p2p_env = std::getenv("BDDC_P2P");
+        if (!(p2p_env && std::atoi(p2p_env) == 0)) I.setup_peer_links();
     }
     BDDC_CUDA(cudaDeviceSynchronize());
 }
@@ -859,6 +1138,12 @@ int GpuContext::device() const { return impl_->device; }
 void GpuContext::synchronize() { BDDC_CUDA(cudaStreamSynchronize(impl_->stream)); }
 std::int64_t GpuContext::solve_profile(std::int64_t* out, std::int64_t cap) {
     Impl& I = *impl_;
+    if (I.ex_stats.p) {  // exchange diagnostics take precedence (BDDC_EXCH_STATS)
+        const std::int64_t n = std::min<std::int64_t>(cap, static_cast<std::int64_t>(I.ex_stats.n));
+        BDDC_CUDA(cudaDeviceSynchronize());
+        BDDC_CUDA(cudaMemcpy(out, I.ex_stats.p, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+        return n;
+    }
     if (!I.dbg_buf.p) return 0;
     const std::int64_t n = std::min<std::int64_t>(cap, static_cast<std::int64_t>(I.dbg_buf.n));
     BDDC_CUDA(cudaDeviceSynchronize());

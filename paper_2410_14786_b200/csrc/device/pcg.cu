@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(kVecThreads) finalize_kernel(const double* par
 
 __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *D.iter += 1;  // read by the later kernels of this iteration
     double acc = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
         double y = 0.0;
@@ -41,8 +42,9 @@ __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D
     if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
 }
 
-__global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int it) {
+__global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
+    const int it = *D.iter;
     const double pq = sum_partials(D.red_a, D.red_a_n, scratch);
     if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
         if (blockIdx.x == 0 && threadIdx.x == 0) D.scal[3] = 1.0;
@@ -61,8 +63,9 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
 }
 
-__global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int it) {
+__global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
+    const int it = *D.iter;
     if (D.scal[3] != 0.0) return;
     const double rr = sum_partials(D.red_b, D.red_b_n, scratch);
     if (threadIdx.x == 0) {
@@ -77,17 +80,18 @@ __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, i
 
 __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
-    const double rz = sum_partials(D.red_a, D.red_a_n, scratch);
+    const double rz = sum_partials(D.red_c, D.red_c_n, scratch);
     if (blockIdx.x == 0 && threadIdx.x == 0) D.rho[0] = rz;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x)
         D.p[i] = D.z[i];
 }
 
-__global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int it) {
+__global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
-    const double rz = sum_partials(D.red_a, D.red_a_n, scratch);
+    const int it = *D.iter;
+    const double rz = sum_partials(D.red_c, D.red_c_n, scratch);
     const double beta = rz / D.rho[it - 1];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x)
         D.p[i] = D.z[i] + beta * D.p[i];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         D.beta[it - 1] = beta;

@@ -9,6 +9,8 @@ namespace bddc_b200 {
 struct PcgDevice {
     int n;                    // rows updated (single GPU: all; distributed: the rank's dofs)
     int n_dot;                // leading entries that enter dot products (distributed: owned dofs)
+    int n_dir;                // entries p = z (+ beta p) updates (distributed peer-memory mode: rows +
+                              // halo, the halo of z arriving with the r.z exchange)
     int grid;                 // blocks of the vector kernels (fixed => fixed reduction order)
     const std::int32_t* A_ptr;
     const std::int32_t* A_col;
@@ -22,15 +24,19 @@ struct PcgDevice {
     double* part_b;
     // what the consumers of p.q / r.z (red_a) and r.r (red_b) sum, in order: the grid
     // partials on one GPU; the gathered per-rank totals (rank order) when distributed
-    const double* red_a;
+    const double* red_a;      // p.q   (update)
     int red_a_n;
-    const double* red_b;
+    const double* red_b;      // r.r   (check)
     int red_b_n;
+    const double* red_c;      // r.z   (init_rho, xpay)
+    int red_c_n;
     double* rho;      // [max_it + 1]
     double* alpha;    // [max_it]
     double* beta;     // [max_it]
     double* hist;     // [max_it + 1]
     double* scal;     // [0]=||b||, [1]=rel, [2]=converged flag, [3]=error code
+    int* iter;        // device iteration counter: spmv_dot advances it, update/check/xpay read it
+                      // (so one captured graph serves every iteration)
     double rtol, atol;
 };
 
