@@ -1,5 +1,6 @@
 // GpuContext: uploads the device image and orchestrates the apply / PCG on one B200.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -187,7 +188,28 @@ struct GpuContext::Impl {
     std::vector<std::int32_t> halo_soff, halo_roff, iface_soff, iface_roff;
     index_t n_global = 0, n_rows = 0, n_owned = 0;
     std::string symmetry_error;  // distributed: global symmetry check done once at creation
-    DBuf<double> hx_in, hx_out;  // host-entry staging (rank-local layout)
+    // host entry points: the rank-local layout as runs {local, global, length} of consecutive
+    // indices (split at n_rows), copied through a pinned staging buffer
+    std::vector<std::array<index_t, 3>> runs;
+    double* stage = nullptr;
+    void build_runs() {
+        const auto& l2g = plan->local_to_global;
+        const index_t n = static_cast<index_t>(l2g.size());
+        for (index_t l = 0; l < n;) {
+            index_t e = l + 1;
+            while (e < n && e != n_rows && l2g[e] == l2g[e - 1] + 1) ++e;
+            runs.push_back({l, l2g[l], e - l});
+            l = e;
+        }
+        BDDC_CUDA(cudaMallocHost(&stage, sizeof(double) * std::max<index_t>(n, 1)));
+    }
+    void gather_host(const double* g) const {  // global -> stage (all local entries)
+        for (const auto& r : runs) std::memcpy(stage + r[0], g + r[1], sizeof(double) * r[2]);
+    }
+    void scatter_host(double* g) const {  // stage rows -> global
+        for (const auto& r : runs)
+            if (r[0] < n_rows) std::memcpy(g + r[1], stage + r[0], sizeof(double) * r[2]);
+    }
 
     bool dist() const { return static_cast<bool>(comm); }
 
@@ -955,6 +977,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.vtmp2.alloc(n);
     if (I.plan) {
         const RankPlan& P = *I.plan;
+        I.build_runs();
         I.halo_idx.upload(P.halo_send_idx);
         I.iface_idx.upload(P.iface_send_slot);
         I.halo_send.alloc(std::max<std::size_t>(P.halo_send_idx.size(), 1));
@@ -977,6 +1000,7 @@ GpuContext::~GpuContext() {
     if (impl_) {
         cudaSetDevice(impl_->device);
         if (impl_->pinned) cudaFreeHost(impl_->pinned);
+        if (impl_->stage) cudaFreeHost(impl_->stage);
         if (impl_->stream) cudaStreamDestroy(impl_->stream);
     }
 }
@@ -1009,14 +1033,13 @@ void GpuContext::apply_host(const double* r, double* z) {
     ensure_finite(r, I.n_global, "bddc apply");
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {
-        std::vector<double> loc(n), out(I.n_rows);
-        for (index_t l = 0; l < n; ++l) loc[l] = r[I.plan->local_to_global[l]];
-        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, loc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+        I.gather_host(r);
+        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, I.stage, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
         I.apply(I.vin.p, I.vout.p, I.stream);
-        BDDC_CUDA(cudaMemcpyAsync(out.data(), I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
+        BDDC_CUDA(cudaMemcpyAsync(I.stage, I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
         BDDC_CUDA(cudaStreamSynchronize(I.stream));
         I.check_coarse(I.stream);
-        for (index_t l = 0; l < I.n_rows; ++l) z[I.plan->local_to_global[l]] = out[l];
+        I.scatter_host(z);
         return;
     }
     BDDC_CUDA(cudaMemcpyAsync(I.vin.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
@@ -1033,13 +1056,12 @@ SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x
     ensure_finite(b, I.n_global, "pcg rhs");
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {
-        std::vector<double> loc(n), out(I.n_rows);
-        for (index_t l = 0; l < n; ++l) loc[l] = b[I.plan->local_to_global[l]];
-        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, loc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
+        I.gather_host(b);
+        BDDC_CUDA(cudaMemcpyAsync(I.vin.p, I.stage, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
         SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);
-        BDDC_CUDA(cudaMemcpyAsync(out.data(), I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
+        BDDC_CUDA(cudaMemcpyAsync(I.stage, I.vout.p, sizeof(double) * I.n_rows, cudaMemcpyDeviceToHost, I.stream));
         BDDC_CUDA(cudaStreamSynchronize(I.stream));
-        for (index_t l = 0; l < I.n_rows; ++l) x[I.plan->local_to_global[l]] = out[l];
+        I.scatter_host(x);
         return rep;
     }
     BDDC_CUDA(cudaMemcpyAsync(I.vin.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));

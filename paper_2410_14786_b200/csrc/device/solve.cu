@@ -68,61 +68,65 @@ struct RegTable {
     }
 };
 
-// One tile GEMV (device_format.hpp): k <= 32 rows, G column groups (power of two), lane
-// = r * G + g owns row r and columns j = t * G + g; values are stored iteration-major,
-// value(r, t*G + g) at [t*k*G + r*G + g], so every iteration is one contiguous,
-// conflict-free shared-memory read per lane. The G partial sums of a row are reduced with
-// an xor butterfly inside the row's lane group; the row total then accumulates into `acc`
-// (all lanes of the group) and is flushed by the group's first lane on the chunk's last tile.
-__device__ __forceinline__ void tile_task(const TileTask& task, const unsigned char* tile, const double* in,
-                                          double* own, double* other, double* Q, double& acc, int lane) {
-    const int G = task.groups, k = task.nrows, kG = k * G;
-    const int iters = task.iters;
-    const int g = lane & (G - 1), r = lane >> (__ffs(G) - 1);
-    const bool indexed = task.flags & kTaskInIndexed;
+// One tile GEMV (device_format.hpp): k <= 32 rows, G = 2^lg column groups, lane = r*G + g
+// owns row r and columns j = t*G + g; values are stored iteration-major, value(r, t*G + g)
+// at [t*k*G + r*G + g], so every iteration is one contiguous, conflict-free shared-memory
+// read per lane. Written for a short issue path (most tiles hold ~5 values per lane): no
+// divergent guard around the loop (lanes beyond k*G read in-bounds slack and are masked
+// before the reduction), a 4-way body with predicated tails, pointer increments only. The
+// G partial sums of a row are reduced with an xor butterfly inside the row's lane group; the
+// row total accumulates into `acc` and is flushed by the group's first lane.
+__device__ __forceinline__ void tile_task(const int4 h, const unsigned char* tile, double* own, double* other,
+                                          double* Q, double& acc, int lane) {
+    const int k = h.w & 0xff, lg = (h.w >> 8) & 0xff, flags = (h.w >> 16) & 0xff;
+    const int iters = static_cast<unsigned>(h.z) >> 16;
+    const int G = 1 << lg, kG = k << lg;
+    const int g = lane & (G - 1), r = lane >> lg;
+    const double* in = (flags & kTaskDiag) ? own : other;
+    const double* M = reinterpret_cast<const double*>(tile) + lane;
     const int vbytes = (iters * kG * 8 + 15) & ~15;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    if (lane < kG) {
-        const double* M = reinterpret_cast<const double*>(tile) + lane;
-        int t = 0;
-        if (indexed) {
-            const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
-            for (; t + 4 <= iters; t += 4) {
-                s0 = fma(M[t * kG], in[ix[t * G]], s0);
-                s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
-                s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
-                s3 = fma(M[(t + 3) * kG], in[ix[(t + 3) * G]], s3);
-            }
-            if (t < iters) s0 = fma(M[t * kG], in[ix[t * G]], s0);
-            if (t + 1 < iters) s1 = fma(M[(t + 1) * kG], in[ix[(t + 1) * G]], s1);
-            if (t + 2 < iters) s2 = fma(M[(t + 2) * kG], in[ix[(t + 2) * G]], s2);
-        } else {
-            const double* v = in + task.in_ref + g;
-            for (; t + 4 <= iters; t += 4) {
-                s0 = fma(M[t * kG], v[t * G], s0);
-                s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
-                s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
-                s3 = fma(M[(t + 3) * kG], v[(t + 3) * G], s3);
-            }
-            if (t < iters) s0 = fma(M[t * kG], v[t * G], s0);
-            if (t + 1 < iters) s1 = fma(M[(t + 1) * kG], v[(t + 1) * G], s1);
-            if (t + 2 < iters) s2 = fma(M[(t + 2) * kG], v[(t + 2) * G], s2);
+    if (flags & kTaskInIndexed) {
+        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
+#pragma unroll 1
+        for (int t = 0; t < iters; t += 4) {
+            s0 = fma(M[0], in[ix[0]], s0);
+            if (t + 1 < iters) s1 = fma(M[kG], in[ix[G]], s1);
+            if (t + 2 < iters) s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
+            if (t + 3 < iters) s3 = fma(M[3 * kG], in[ix[3 * G]], s3);
+            M += 4 * kG;
+            ix += 4 * G;
+        }
+    } else {
+        const double* v = in + h.y + g;
+#pragma unroll 1
+        for (int t = 0; t < iters; t += 4) {
+            s0 = fma(M[0], v[0], s0);
+            if (t + 1 < iters) s1 = fma(M[kG], v[G], s1);
+            if (t + 2 < iters) s2 = fma(M[2 * kG], v[2 * G], s2);
+            if (t + 3 < iters) s3 = fma(M[3 * kG], v[3 * G], s3);
+            M += 4 * kG;
+            v += 4 * G;
         }
     }
-    double tot = (s0 + s1) + (s2 + s3);
-    for (int off = G >> 1; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-    acc += tot;
-    if ((task.flags & kTaskLast) && g == 0) {
-        if (task.flags & kTaskPush) {
+    double tot = lane < kG ? (s0 + s1) + (s2 + s3) : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+        if (off < G) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+    acc = ((flags & kTaskFirst) ? 0.0 : acc) + tot;
+    if ((flags & kTaskLast) && g == 0) {
+        const int nvalid = static_cast<unsigned>(h.w) >> 24;
+        if (flags & kTaskPush) {
             if (r < k) {
-                const int ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
+                const int ibytes = (flags & kTaskInIndexed) ? ((iters * G * 4 + 15) & ~15) : 0;
                 const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes)[r];
-                if (task.flags & kTaskPartial) Q[o] += acc;
+                if (flags & kTaskPartial) Q[o] += acc;
                 else own[o] -= acc;
             }
-        } else if (r < task.nvalid) {
-            if (task.flags & kTaskDiag) other[task.out_base + r] = acc;
-            else own[task.out_base + r] -= acc;
+        } else if (r < nvalid) {
+            const int out = (h.z & 0xffff) + r;
+            if (flags & kTaskDiag) other[out] = acc;
+            else own[out] -= acc;
         }
     }
 }
@@ -262,15 +266,12 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             int4 hdr4 = *reinterpret_cast<const int4*>(ubuf);
             while (true) {
                 if (stats) ++n_tiles;
-                TileTask task;
-                *reinterpret_cast<int4*>(&task) = hdr4;
+                const int4 h = hdr4;
                 const unsigned char* tile = ubuf + (cur << 4) + 16;
-                cur = task.next;
+                cur = static_cast<std::uint32_t>(h.x);
                 if (cur != kNoTask) hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));  // next header early
-                if (task.flags & kTaskFirst) acc = 0.0;
-                const double* in = (task.flags & kTaskDiag) ? own : other;
-                tile_task(task, tile, in, own, other, Q, acc, lane);
-                if ((task.flags & kTaskLast) && (kind & kPhaseChained))
+                tile_task(h, tile, own, other, Q, acc, lane);
+                if ((kind & kPhaseChained) && ((h.w >> 16) & kTaskLast))
                     __syncwarp();  // a later tile of this warp's job reads what was just written
                 if (cur == kNoTask) break;
             }
@@ -357,7 +358,8 @@ std::size_t interior_solve_smem(int max_loc, int max_top, int max_iface, int uni
     return static_cast<std::size_t>(kSolveWarps) * kMaxWarpSlots * 8 +
            8 * (2 * static_cast<std::size_t>((max_loc + 64 + 1) & ~1) + ((max_top + 1) & ~1) +
                 ((max_iface + 1) & ~1)) +
-           33 * 32 + 128 + static_cast<std::size_t>(kSolveWarps) * slots_per_warp * unit_bytes;
+           33 * 32 + 128 + static_cast<std::size_t>(kSolveWarps) * slots_per_warp * unit_bytes +
+           512;  // slack: lanes beyond a tile's k*G read (and discard) up to 32 values past it
 }
 
 int max_solve_smem(int device) {

@@ -66,7 +66,7 @@ struct TileTask {
     std::uint16_t out_base; // output chunk start (DIAG / PULL)
     std::uint16_t iters;    // ceil(columns / groups): inner-loop trip count
     std::uint8_t nrows;     // k, <= 32
-    std::uint8_t groups;    // G: largest power of two with k * G <= 32
+    std::uint8_t groups;    // log2 G; G: the largest power of two with k * G <= 32
     std::uint8_t flags;
     std::uint8_t nvalid;    // rows written on flush
 };

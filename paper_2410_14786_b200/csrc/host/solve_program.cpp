@@ -56,7 +56,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         T.t.out_base = static_cast<std::uint16_t>(out_base);
         T.t.iters = static_cast<std::uint16_t>(iters);
         T.t.nrows = static_cast<std::uint8_t>(k);
-        T.t.groups = static_cast<std::uint8_t>(G);
+        T.t.groups = static_cast<std::uint8_t>(__builtin_ctz(static_cast<unsigned>(G)));  // log2 G
         T.t.nvalid = static_cast<std::uint8_t>(nvalid);
         T.t.flags = flags | (indexed ? kTaskInIndexed : 0) | (j0 == 0 ? kTaskFirst : 0) |
                     (j0 + jn >= ncols ? kTaskLast : 0);

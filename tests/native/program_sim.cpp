@@ -44,7 +44,7 @@ void run_phase(const SolvePools& sp, PartState& st) {
             std::memcpy(&task, ubase + std::int64_t(cur) * 16, 16);
             const char* tb = ubase + std::int64_t(cur) * 16 + 16;
             cur = task.next;
-            const int k = task.nrows, G = task.groups, iters = task.iters;
+            const int k = task.nrows, G = 1 << task.groups, iters = task.iters;
             const double* M = reinterpret_cast<const double*>(tb);
             const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + pad16i(iters * k * G * 8));
             const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(
@@ -113,10 +113,10 @@ extern "C" int bddc_sim_program_stats(int cells, int k, int parts, int leaf_size
             wl += tk.iters + 12;
             const int kind = (bwd ? 2 : 0) + ((tk.flags & kTaskDiag) ? 1 : 0);
             cnt[kind]++;
-            elems[kind] += tk.nrows * tk.groups * tk.iters;
+            elems[kind] += tk.nrows * (1 << tk.groups) * tk.iters;
             iters[kind] += tk.iters;
             const int g = 32 / tk.nrows;
-            flat[kind] += tk.nrows * tk.groups * tk.iters; (void)g;
+            flat[kind] += tk.nrows * (1 << tk.groups) * tk.iters; (void)g;
             rows_hist[tk.nrows]++;
           }
           crit = std::max(crit, wl);
