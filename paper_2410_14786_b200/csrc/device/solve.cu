@@ -86,33 +86,39 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
     const double* M = reinterpret_cast<const double*>(tile) + lane;
     const int vbytes = (iters * kG * 8 + 15) & ~15;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int full = iters & ~3, rem = iters & 3;
     if (flags & kTaskInIndexed) {
         const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
 #pragma unroll 1
-        for (int t = 0; t < iters; t += 4) {
+        for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], in[ix[0]], s0);
-            if (t + 1 < iters) s1 = fma(M[kG], in[ix[G]], s1);
-            if (t + 2 < iters) s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
-            if (t + 3 < iters) s3 = fma(M[3 * kG], in[ix[3 * G]], s3);
+            s1 = fma(M[kG], in[ix[G]], s1);
+            s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
+            s3 = fma(M[3 * kG], in[ix[3 * G]], s3);
             M += 4 * kG;
             ix += 4 * G;
         }
+        if (rem > 0) s0 = fma(M[0], in[ix[0]], s0);
+        if (rem > 1) s1 = fma(M[kG], in[ix[G]], s1);
+        if (rem > 2) s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
     } else {
         const double* v = in + h.y + g;
 #pragma unroll 1
-        for (int t = 0; t < iters; t += 4) {
+        for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], v[0], s0);
-            if (t + 1 < iters) s1 = fma(M[kG], v[G], s1);
-            if (t + 2 < iters) s2 = fma(M[2 * kG], v[2 * G], s2);
-            if (t + 3 < iters) s3 = fma(M[3 * kG], v[3 * G], s3);
+            s1 = fma(M[kG], v[G], s1);
+            s2 = fma(M[2 * kG], v[2 * G], s2);
+            s3 = fma(M[3 * kG], v[3 * G], s3);
             M += 4 * kG;
             v += 4 * G;
         }
+        if (rem > 0) s0 = fma(M[0], v[0], s0);
+        if (rem > 1) s1 = fma(M[kG], v[G], s1);
+        if (rem > 2) s2 = fma(M[2 * kG], v[2 * G], s2);
     }
     double tot = lane < kG ? (s0 + s1) + (s2 + s3) : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-        if (off < G) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+#pragma unroll 1
+    for (int off = G >> 1; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
     acc = ((flags & kTaskFirst) ? 0.0 : acc) + tot;
     if ((flags & kTaskLast) && g == 0) {
         const int nvalid = static_cast<unsigned>(h.w) >> 24;
