@@ -195,7 +195,7 @@ void bddc_default_gpu_options(bddc_gpu_options* o) {
     o->coarse_rel_tolerance = 1e-12;
     o->coarse_abs_tolerance = 0.0;
     o->coarse_max_iterations = 500;
-    o->leaf_size = 16;
+    o->leaf_size = 24;
     o->local_blocks = 4;
     o->solve_parts = 0;
 }

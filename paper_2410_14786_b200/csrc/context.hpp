@@ -25,7 +25,7 @@ struct GpuOptions {
     double coarse_rtol = 1e-12;   // reference preconditioner.hpp:42
     double coarse_atol = 0.0;
     int coarse_max_iterations = 500;
-    int leaf_size = 16;
+    int leaf_size = 24;           // measured best on B200 (tools/leaf_sweep.sh)
     int local_blocks = 4;         // CTAs per subdomain for the K_i GEMV
     int solve_parts = 0;          // CTAs per subdomain in the interior solve (0 = auto)
     bool profile = false;         // record per-kernel CUDA events in apply()

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 
 k, m = int(os.environ.get("K", 8)), int(os.environ.get("M", 100))
 p = Problem.poisson(k * m, k)
-pre = Preconditioner(p, leaf_size=int(os.environ.get("LEAF", 16)), solve_parts=int(os.environ.get("PARTS", 0)))
+pre = Preconditioner(p, leaf_size=int(os.environ.get("LEAF", 24)), solve_parts=int(os.environ.get("PARTS", 0)))
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
 r = torch.tensor(p.rhs(), device="cuda")

@@ -70,7 +70,7 @@ def run(name, k, m, reps=20, leaf=16):
 
 
 if __name__ == "__main__":
-    leaf = int(os.environ.get("LEAF", "16"))
+    leaf = int(os.environ.get("LEAF", "24"))
     cfgs = {"k4m8": (4, 8), "c1": (4, 64), "c2": (8, 100)}
     names = sys.argv[1:] or list(cfgs)
     for nm in names:

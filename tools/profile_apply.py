@@ -17,7 +17,7 @@ def main():
     import torch
 
     p = Problem.poisson(k * m, k, rhs_seed=1)
-    pre = Preconditioner(p, leaf_size=int(os.environ.get("LEAF", "16")),
+    pre = Preconditioner(p, leaf_size=int(os.environ.get("LEAF", "24")),
                          solve_parts=int(os.environ.get("PARTS", "0")))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
