@@ -107,12 +107,12 @@ def run_distributed_bench(args, workload: dict, layout, cells: int) -> None:
 
     # e2e: host global b -> each rank's block -> host x (C-ABI bddc_gpu_pcg)
     b_pin = torch.from_numpy(b_host).pin_memory().numpy()
-    xh = np.zeros(prob.global_dofs)
-    xh, rh = pre.pcg(b_pin, opts)
+    x_pin = torch.zeros(prob.global_dofs, dtype=torch.float64).pin_memory().numpy()
+    xh, rh = pre.pcg(b_pin, opts, out=x_pin)
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        xh, rh = pre.pcg(b_pin, opts)
+        xh, rh = pre.pcg(b_pin, opts, out=x_pin)
     dist.barrier()
     e2e_local = (time.perf_counter() - t0) / args.steps
     it = rh.iterations

@@ -419,11 +419,17 @@ class Preconditioner:
     def synchronize(self) -> None:
         L.check(L.lib().bddc_gpu_synchronize(self._h), self._h)
 
-    def pcg(self, b, options: SolverOptions | None = None, precondition: bool = True):
-        """Device-resident PCG with M = self.apply (reference pcg + study.cpp:113-119)."""
+    def pcg(self, b, options: SolverOptions | None = None, precondition: bool = True, out=None):
+        """Device-resident PCG with M = self.apply (reference pcg + study.cpp:113-119).
+        `out` (optional, float64, length n; e.g. pinned) receives the solution."""
         options = options or SolverOptions()
         b = self._vec(b)
-        x = np.empty(self.n)
+        if out is None:
+            x = np.empty(self.n)
+        else:
+            x = out
+            if x.dtype != np.float64 or x.size != self.n or not x.flags.c_contiguous:
+                raise L.InvalidArgument(L.ERR_INVALID_ARGUMENT, "pcg: out must be a contiguous float64 vector of size n")
         rep = L.SolveReport()
         cap = options.max_iterations + 1
         hist = np.zeros(cap)
