@@ -238,7 +238,7 @@ def run_ours(args) -> None:
 
     # ---- roofline of the dominant kernel: the batched interior solve
     launch_ms = kt["interior_ms"] / max(1, kt["interior_launches"])
-    alg_bytes = 8 * (2 * st["factor_values"] + 2 * st["interior_dofs"])
+    alg_bytes = st["interior_apply_bytes"] / 2  # mean over the apply's two interior-solve launches
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}

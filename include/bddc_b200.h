@@ -126,6 +126,7 @@ typedef struct {
     int32_t max_interior;
     int32_t max_interface;
     int64_t interior_dofs;        /* sum of n_I over subdomains */
+    int64_t interior_apply_bytes; /* algorithmic FP64 bytes of the two interior solves of one apply */
 } bddc_stats;
 
 typedef struct {

@@ -81,7 +81,8 @@ class SolveReport(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("setup_seconds", f64), ("factor_values", i64), ("interior_solve_bytes", i64),
                 ("apply_bytes", i64), ("n_subdomains", i32), ("global_dofs", i32), ("n_coarse", i32),
-                ("unique_subdomains", i32), ("max_interior", i32), ("max_interface", i32), ("interior_dofs", i64)]
+                ("unique_subdomains", i32), ("max_interior", i32), ("max_interface", i32), ("interior_dofs", i64),
+                ("interior_apply_bytes", i64)]
 
 
 class KernelTimes(C.Structure):

@@ -553,6 +553,7 @@ int bddc_gpu_get_stats(const bddc_gpu_ctx* c, bddc_stats* st) {
         st->factor_values = g.factor_values();
         st->interior_solve_bytes = g.interior_pass_bytes();
         st->apply_bytes = g.apply_bytes();
+        st->interior_apply_bytes = g.interior_apply_bytes();
         st->n_subdomains = g.problem().decomposition.n_subdomains;
         st->global_dofs = g.problem().decomposition.global_dofs;
         st->n_coarse = g.problem().constraints.n_coarse;

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -29,6 +30,9 @@ struct GpuOptions {
     int local_blocks = 4;         // CTAs per subdomain for the K_i GEMV
     int solve_parts = 0;          // CTAs per subdomain in the interior solve (0 = auto)
     bool profile = false;         // record per-kernel CUDA events in apply()
+    // second interior solve of the apply as the harmonic extension u0 - A_II^{-1} A_IG z_G with a
+    // pruned forward sweep (BDDC_HARMONIC=0 selects the full solve of r_I - A_IG z_G)
+    bool harmonic = !(std::getenv("BDDC_HARMONIC") && std::string(std::getenv("BDDC_HARMONIC")) == "0");
 };
 
 struct SolverOpts {
@@ -105,6 +109,7 @@ public:
     const ProblemData& problem() const;
     double setup_seconds() const;
     std::int64_t apply_bytes() const;       // algorithmic FP64 bytes per apply
+    std::int64_t interior_apply_bytes() const;  // algorithmic bytes of the two interior solves of an apply
     std::int64_t interior_pass_bytes() const;  // stream bytes of one batched interior solve
     int solve_parts() const;
     std::int64_t factor_values() const;

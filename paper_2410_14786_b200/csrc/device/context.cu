@@ -86,12 +86,31 @@ struct GpuContext::Impl {
     cudaStream_t stream = nullptr;
     std::mutex mu;  // the reference apply() is callable concurrently; serialise here
 
-    // interior-solve program
-    DBuf<PartDesc> parts;
-    DBuf<double> sstream;
-    DBuf<std::int32_t> units, order;
-    DBuf<std::int32_t> phases, gmap, couple_ptr, couple_gamma;
-    DBuf<double> couple_val;
+    // interior-solve programs: the full solve, and the harmonic extension A_II^{-1} A_IG z_G of
+    // the second solve of the apply (pruned forward sweep; BDDC_HARMONIC=0 disables)
+    struct SolveProgram {
+        DBuf<PartDesc> parts;
+        DBuf<double> stream;
+        DBuf<std::int32_t> units, phases, gmap, couple_ptr, couple_gamma;
+        DBuf<double> couple_val;
+        std::int64_t stream_bytes = 0;
+        bool valid = false;
+        void upload(const SolvePools& sp) {
+            parts.alloc(std::max<std::size_t>(sp.parts.size(), 1));
+            if (!sp.parts.empty())
+                BDDC_CUDA(cudaMemcpy(parts.p, sp.parts.data(), sizeof(PartDesc) * sp.parts.size(), cudaMemcpyHostToDevice));
+            stream.upload(sp.stream);
+            units.upload(sp.units);
+            phases.upload(sp.phases);
+            gmap.upload(sp.gmap);
+            couple_ptr.upload(sp.couple_ptr);
+            couple_gamma.upload(sp.couple_gamma);
+            couple_val.upload(sp.couple_val);
+            for (const PartDesc& pd : sp.parts) stream_bytes += pd.stream_bytes;
+            valid = !sp.parts.empty();
+        }
+    };
+    SolveProgram prog, harm;
     SolveLaunch launch;
     // interface data
     DBuf<SubdomainDesc> subs;
@@ -113,7 +132,7 @@ struct GpuContext::Impl {
     int max_it_alloc = 0;
 
     std::int32_t max_iface = 0, max_primal = 0, n_coarse = 0, n_gi = 0;
-    std::int64_t solve_stream_bytes = 0, factor_vals = 0;
+    std::int64_t solve_stream_bytes = 0, harm_stream_bytes = 0, factor_vals = 0, harm_fwd_values = 0;
     std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
@@ -259,18 +278,20 @@ struct GpuContext::Impl {
         comm->allgather_inplace(gath, 1, s);
     }
 
-    SolveParams solve_params(const double* in, double* out) const {
+    SolveParams solve_params(const double* in, double* out, const SolveProgram* pg = nullptr) const {
+        const SolveProgram& G = pg ? *pg : prog;
         SolveParams P{};
         P.skip = apply_skip;
-        P.parts = parts.p;
+        P.parts = G.parts.p;
         P.subs = subs.p;
-        P.stream = sstream.p;
-        P.units = units.p;
-        P.phases = phases.p;
-        P.gmap = gmap.p;
-        P.couple_ptr = couple_ptr.p;
-        P.couple_gamma = couple_gamma.p;
-        P.couple_val = couple_val.p;
+        P.stream = G.stream.p;
+        P.units = G.units.p;
+        P.phases = G.phases.p;
+        P.gmap = G.gmap.p;
+        P.couple_ptr = G.couple_ptr.p;
+        P.couple_gamma = G.couple_gamma.p;
+        P.couple_val = G.couple_val.p;
+        P.u0 = U.p;
         P.iface_gid = iface_gid.p;
         P.iface_dof = iface_dof.p;
         P.iface_writer = iface_writer.p;
@@ -427,7 +448,8 @@ struct GpuContext::Impl {
         launch_iface_local(ip, opt.local_blocks, s, true);
         iface_exchange(s);
         if (E) record(E->e[2].e, s);
-        launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
+        if (harm.valid) launch_interior_solve(solve_params(r_dev, z_dev, &harm), launch, 3, s);  // z_I = u0 - A_II^-1 A_IG z_G
+        else launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
         if (E) record(E->e[3].e, s);
     }
 
@@ -877,7 +899,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     int spw = 0;
     for (;; unit /= 2) {
         img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit,
-                                 I.plan.get());
+                                 I.plan.get(), I.opt.harmonic);
         const std::size_t fixed = interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit, 0);
         spw = 0;
         if (fixed < static_cast<std::size_t>(max_smem)) {
@@ -897,6 +919,8 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.max_top = img.solve.max_top;
     I.factor_vals = img.factor_values;
     for (const PartDesc& pd : img.solve.parts) I.solve_stream_bytes += pd.stream_bytes;
+    for (const PartDesc& pd : img.harm.parts) I.harm_stream_bytes += pd.stream_bytes;
+    I.harm_fwd_values = img.harm.parts.empty() ? I.factor_vals : img.harm.fwd_factor_values;
     I.k_values = static_cast<std::int64_t>(img.kmat.size());
     I.phig_values = static_cast<std::int64_t>(img.phig.size());
     I.ginnz = static_cast<std::int64_t>(img.gi_row_val.size());
@@ -914,20 +938,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         buf.alloc(std::max<std::size_t>(vec.size(), 1));
         if (!vec.empty()) BDDC_CUDA(cudaMemcpy(buf.p, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice));
     };
-    upload_pod(I.parts, img.solve.parts);
-    I.units.upload(img.solve.units);
-    I.order.upload(img.solve.order);
+    I.prog.upload(img.solve);
+    I.harm.upload(img.harm);
     if (std::getenv("BDDC_SOLVE_STATS")) {
         I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 8 + img.solve.max_phases);
         BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));
     }
     upload_pod(I.subs, img.subs);
-    I.sstream.upload(img.solve.stream);
-    I.phases.upload(img.solve.phases);
-    I.gmap.upload(img.solve.gmap);
-    I.couple_ptr.upload(img.solve.couple_ptr);
-    I.couple_gamma.upload(img.solve.couple_gamma);
-    I.couple_val.upload(img.solve.couple_val);
     I.iface_dof.upload(img.iface_dof);
     I.iface_w.upload(img.iface_w);
     I.iface_gid.upload(img.iface_gid);
@@ -1138,11 +1155,21 @@ int GpuContext::solve_parts() const { return impl_->launch.cluster; }
 std::int64_t GpuContext::apply_bytes() const {
     const Impl& I = *impl_;
     const std::int64_t n = I.pb.decomposition.global_dofs;
-    // algorithmic FP64 bytes: two interior solves (forward + backward over every factor
-    // value), K_i, Phi_G (restrict + prolong), the coarse inverse, interface rows and
-    // coupling, plus vector traffic (r read twice, u0 written/read, z written)
-    return 8 * (4 * I.factor_vals + I.k_values + 2 * I.phig_values +
-                static_cast<std::int64_t>(I.n_coarse) * I.n_coarse + I.ginnz + I.couple_nnz + 5 * n);
+    // algorithmic FP64 bytes: the two interior solves (forward + backward over every factor
+    // value; the harmonic extension's forward sweep only over its active supernodes), K_i,
+    // Phi_G (restrict + prolong), the coarse inverse, interface rows and coupling, plus vector
+    // traffic (r read twice, u0 written/read, z written)
+    return interior_apply_bytes() +
+           8 * (I.k_values + 2 * I.phig_values + static_cast<std::int64_t>(I.n_coarse) * I.n_coarse + I.ginnz +
+                I.couple_nnz + 5 * n);
+}
+std::int64_t GpuContext::interior_apply_bytes() const {
+    const Impl& I = *impl_;
+    std::int64_t ni = 0;
+    for (const auto& sub : I.setup.subs) ni += sub.n_interior;
+    // solve 1: 2F values + rhs gather + solution write; solve 2: F + F_fwd(active) values + u0 read
+    // + z write (its rhs comes from the interface coupling, counted in couple_nnz)
+    return 8 * (2 * I.factor_vals + 2 * ni) + 8 * (I.factor_vals + I.harm_fwd_values + 2 * ni);
 }
 KernelTimes GpuContext::kernel_times() {
     std::lock_guard<std::mutex> lk(impl_->mu);

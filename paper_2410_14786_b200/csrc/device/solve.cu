@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
         double gv[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) gv[q] = gi[q] >= 0 ? S.in[gi[q]] : 0.0;
+        for (int q = 0; q < 4; ++q) gv[q] = (MODE != 3 && gi[q] >= 0) ? S.in[gi[q]] : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int l = l0 + q * kThreads;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         const int ng = sd.n_iface;
         for (int g = tid; g < ng; g += kThreads) {
             double z;
-            if (MODE == 1) {
+            if (MODE == 1 || MODE == 3) {
                 // z_G = sum over the subdomains sharing the dof of their h, ascending
                 // subdomain (reference prolong_add order, preconditioner.cpp:168-169,189-190)
                 const int gid = S.iface_gid[sd.iface + g];
@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             double acc = 0.0;
             for (int e = cp[l]; e < cp[l + 1]; ++e)
                 acc += S.couple_val[pdr.couple_ent + e] * ZG[S.couple_gamma[pdr.couple_ent + e]];
-            T[l] -= acc;
+            if (MODE == 3) T[l] = acc;  // harmonic extension: rhs A_IG z_G
+            else T[l] -= acc;
         }
     }
     __syncthreads();
@@ -334,7 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (gi[q] >= 0) S.out[gi[q]] = T[l0 + q * kThreads];
+            if (gi[q] >= 0) {
+                if (MODE == 3) S.out[gi[q]] = S.u0[gi[q]] - T[l0 + q * kThreads];  // z_I = u0 - extension
+                else S.out[gi[q]] = T[l0 + q * kThreads];
+            }
     }
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
 }
@@ -381,11 +385,13 @@ void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaSt
     if (L.cluster == 2) {
         if (mode == 0) launch_one<0, 2>(P, L, stream);
         else if (mode == 1) launch_one<1, 2>(P, L, stream);
-        else launch_one<2, 2>(P, L, stream);
+        else if (mode == 2) launch_one<2, 2>(P, L, stream);
+        else launch_one<3, 2>(P, L, stream);
     } else {
         if (mode == 0) launch_one<0, 1>(P, L, stream);
         else if (mode == 1) launch_one<1, 1>(P, L, stream);
-        else launch_one<2, 1>(P, L, stream);
+        else if (mode == 2) launch_one<2, 1>(P, L, stream);
+        else launch_one<3, 1>(P, L, stream);
     }
     BDDC_LAUNCHED();
 }

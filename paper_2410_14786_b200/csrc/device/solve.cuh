@@ -24,6 +24,7 @@ struct SolveParams {
     const double* hbuf;
     const double* in;
     double* out;
+    const double* u0;  // MODE 3: the first interior solve's result (z_I = u0 - harmonic extension)
     int unit_bytes;  // set by the launcher
     int slot_shift;  // log2(ring slots per warp)
     int max_loc;
@@ -47,6 +48,7 @@ int max_solve_smem(int device);
 // mode 0: out[I] = A_II^{-1} in[I]
 // mode 1: z_G = sum of h over owners (written to out), out[I] = A_II^{-1}(in_I - A_IG z_G)
 // mode 2: out[I] = A_II^{-1}(in_I - A_IG h_own)   (local saddle solve, stage hook)
+// mode 3: z_G as mode 1, out[I] = u0_I - A_II^{-1} A_IG z_G  (harmonic-extension program)
 void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaStream_t stream);
 
 }  // namespace bddc_b200

@@ -11,7 +11,8 @@ namespace bddc_b200 {
 
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
-                               const BddcSetup& setup, int parts, int unit_bytes, const RankPlan* plan) {
+                               const BddcSetup& setup, int parts, int unit_bytes, const RankPlan* plan,
+                               bool harmonic) {
     DeviceImage img;
     const index_t nsub = d.n_subdomains;
     img.parts = parts;
@@ -108,6 +109,7 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
 
         // interior-solve program (local dof -> vector index = the subdomain map)
         build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.solve);
+        if (harmonic) build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.harm, true);
     }
 
     if (plan) {

@@ -20,6 +20,7 @@ struct RankPlan;
 struct DeviceImage {
     std::vector<SubdomainDesc> subs;
     SolvePools solve;  // interior-solve parts
+    SolvePools harm;   // harmonic-extension parts (pruned forward sweep; empty when disabled)
     int parts = 1;     // CTAs per subdomain in the interior solve
     std::vector<std::int32_t> iface_dof;     // per (subdomain, gamma): vector index
     std::vector<double> iface_w;             // weight
@@ -49,6 +50,6 @@ struct DeviceImage {
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
                                const BddcSetup& setup, int parts, int unit_bytes = 4096,
-                               const RankPlan* plan = nullptr);
+                               const RankPlan* plan = nullptr, bool harmonic = false);
 
 }  // namespace bddc_b200

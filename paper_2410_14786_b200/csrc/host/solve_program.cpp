@@ -82,10 +82,31 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
 }  // namespace
 
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std::vector<index_t>& l2v, int sub,
-                         int P, int unit_bytes, SolvePools& pools) {
+                         int P, int unit_bytes, SolvePools& pools, bool prune_forward) {
     const auto& sn = F.snodes;
     const index_t nsn = static_cast<index_t>(sn.size());
     const index_t nI = F.n_interior;
+    // Harmonic-extension program: the forward sweep of A_II^{-1} (A_IG z_G) only reaches the
+    // supernodes whose subtree holds an interior dof coupled to the interface (the rhs is zero
+    // elsewhere, and so is the forward solution); the backward sweep stays complete.
+    std::vector<char> fwd(nsn, 1);
+    if (prune_forward) {
+        std::fill(fwd.begin(), fwd.end(), 0);
+        for (index_t sidx = 0; sidx < nsn; ++sidx) {
+            for (index_t c = sn[sidx].col_begin; c < sn[sidx].col_end && !fwd[sidx]; ++c) {
+                const index_t v = F.perm[c];
+                for (index_t q = A.row_offsets[v]; q < A.row_offsets[v + 1]; ++q)
+                    if (A.col_indices[q] >= nI) { fwd[sidx] = 1; break; }
+            }
+        }
+        for (index_t sidx = 0; sidx < nsn; ++sidx)  // postorder: children before parents
+            if (fwd[sidx] && sn[sidx].parent >= 0) fwd[sn[sidx].parent] = 1;
+    }
+    for (index_t sidx = 0; sidx < nsn; ++sidx)
+        if (fwd[sidx]) {
+            const std::int64_t ns = sn[sidx].size();
+            pools.fwd_factor_values += ns * (ns + 1) / 2 + static_cast<std::int64_t>(sn[sidx].n_interior_rows) * ns;
+        }
     if (P < 1 || P > 2) throw std::invalid_argument("solve program: parts must be 1 or 2");
 
     // ---- tree and group assignment (P = 2: halves below the top separator chain)
@@ -239,8 +260,11 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         };
         auto all_rows = [](index_t) { return true; };
         // chunk rows for a level: the largest of 32/16/8 giving at least 2 chunks per warp
+        static const int min_kr = std::getenv("BDDC_MIN_CHUNK_ROWS") ? std::atoi(std::getenv("BDDC_MIN_CHUNK_ROWS")) : 8;
         auto chunk_rows_for = [&](const std::vector<index_t>& rows_per_node) {
+            if (min_kr >= 32) return 32;
             for (int k : {32, 16}) {
+                if (k == 16 && min_kr >= 16) return 16;
                 std::int64_t chunks = 0;
                 for (index_t r : rows_per_node) chunks += (r + k - 1) / k;
                 if (chunks >= 2 * kSolveWarps) return k;
@@ -323,6 +347,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 Chunks job;
                 for (index_t s : job_nodes[j]) {
+                    if (!fwd[s]) continue;
                     diag_fwd(s, job);
                     push_fwd(s, job, false, [&](index_t r) { return local[owner[r]] && job_of[owner[r]] == (index_t)j; });
                 }
@@ -335,6 +360,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 auto outside = [&](index_t r) { return !(local[owner[r]] && job_of[owner[r]] == (index_t)j); };
                 for (index_t s : job_nodes[j]) {
+                    if (!fwd[s]) continue;
                     push_fwd(s, ext[j], false, outside);
                     for (index_t a = 0; a < sn[s].n_interior_rows; ++a)
                         if (outside(sn[s].rows[a])) targets[j].push_back(sn[s].rows[a]);
@@ -351,7 +377,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             Chunks b;
             std::vector<index_t> nodes, nrows, mrows;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == h) {
+                if (in_group(s) && !local[s] && sn[s].height == h && fwd[s]) {
                     nodes.push_back(s);
                     nrows.push_back(sn[s].size());
                     mrows.push_back(sn[s].n_interior_rows);
@@ -391,6 +417,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         // ---------------- forward sweep: shared top chain (identical in every part)
         for (index_t s : top) {
+            if (!fwd[s]) continue;
             Chunks b, ps;
             kr = chunk_rows_for({sn[s].size()});
             diag_fwd(s, b);

@@ -20,6 +20,7 @@ struct SolvePools {
     std::vector<double> couple_val;
     std::vector<PartDesc> parts;
     std::int64_t tile_values = 0;   // FP64 values in all tiles (incl. explicit zeros of diag tiles)
+    std::int64_t fwd_factor_values = 0;  // factor values the forward sweep reads (all, unless pruned)
     std::int64_t n_tiles = 0;
     std::int32_t max_loc = 0, max_top = 0, max_phases = 0, max_units = 0;
 };
@@ -27,8 +28,10 @@ struct SolvePools {
 // local_to_vec: local dof index (interior first) -> device vector index.
 // parts: 1 (one CTA per subdomain) or 2 (CTA pair in a cluster); unit_bytes: size of the
 // per-warp TMA units (and of each ring slot).
+// prune_forward: the harmonic-extension program (rhs supported on the interior dofs coupled
+// to the interface): forward tasks only for supernodes whose subtree holds such a dof.
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A_local,
                          const std::vector<index_t>& local_to_vec, int sub, int parts, int unit_bytes,
-                         SolvePools& pools);
+                         SolvePools& pools, bool prune_forward = false);
 
 }  // namespace bddc_b200

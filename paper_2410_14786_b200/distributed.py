@@ -129,7 +129,7 @@ def run_distributed_bench(args, workload: dict, layout, cells: int) -> None:
         raise SystemExit("a rank's timed solves disagree or did not converge")
     n = prob.global_dofs
     launch_ms = kt["interior_ms"] / max(1, kt["interior_launches"])
-    alg_bytes = 8 * (2 * st["factor_values"] + 2 * st["interior_dofs"])
+    alg_bytes = st["interior_apply_bytes"] / 2  # mean over the apply's two interior-solve launches
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     import json as _json
 

@@ -137,8 +137,8 @@ extern "C" int bddc_sim_program_stats(int cells, int k, int parts, int leaf_size
     return 0;
 }
 
-extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
-                                       int use_coords, const double* in, double* out, char* err, int errlen) {
+static int sim_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size, int use_coords,
+                     int harm, const double* in, double* out, char* err, int errlen) {
     try {
         PoissonProblem pp = assemble_poisson(cells_x, cells_y, kx, ky);
         ProblemData pb;
@@ -152,8 +152,8 @@ extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky,
         const BddcSetup setup = bddc_setup(pb.local_matrices, pb.decomposition, pb.constraints,
                                            pb.coords.empty() ? nullptr : pb.coords.data(), 4, fo);
         const DeviceImage img = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
-                                                   pb.global_matrix, setup, parts);
-        const SolvePools& sp = img.solve;
+                                                   pb.global_matrix, setup, parts, 4096, nullptr, harm != 0);
+        const SolvePools& sp = harm ? img.harm : img.solve;
         for (std::size_t i0 = 0; i0 < sp.parts.size(); i0 += parts) {
             std::vector<PartState> st(parts);
             for (int c = 0; c < parts; ++c) {
@@ -204,4 +204,16 @@ extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky,
         std::snprintf(err, errlen, "%s", e.what());
         return 1;
     }
+}
+
+extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
+                                       int use_coords, const double* in, double* out, char* err, int errlen) {
+    return sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 0, in, out, err, errlen);
+}
+
+// The harmonic-extension program (pruned forward sweep) on an rhs supported on the interior
+// dofs coupled to the interface.
+extern "C" int bddc_sim_harmonic_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
+                                       int use_coords, const double* in, double* out, char* err, int errlen) {
+    return sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 1, in, out, err, errlen);
 }

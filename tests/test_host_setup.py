@@ -132,3 +132,26 @@ def test_device_program_reproduces_interior_solve(sim, k, m, parts, leaf, coords
                                      out.ctypes.data_as(dp), err, 512)
     assert rc == 0, err.value
     assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("k,m,parts,leaf,coords", [(3, 6, 2, 16, 1), (4, 16, 2, 8, 0), (3, 32, 2, 24, 1),
+                                                   (3, 32, 1, 24, 1)])
+def test_harmonic_program_matches_full_solve(sim, k, m, parts, leaf, coords):
+    # second interior solve of the apply: A_II^{-1} (A_IG z_G) with a pruned forward sweep must
+    # equal the full solve of the same (interface-coupled) right-hand side
+    prob, cs, _ = o.poisson_setup(k, m)
+    A = prob.global_matrix.scipy()
+    kinds = prob.decomposition.kind == o.INTERIOR
+    rng = np.random.default_rng(5)
+    n = A.shape[0]
+    v = np.where(~kinds, rng.standard_normal(n), 0.0)   # values on interface dofs
+    c = np.where(kinds, A @ v, 0.0)                     # A_IG v on interior dofs
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    ref = P.interior_correction(c)
+    out = np.zeros_like(c)
+    err = C.create_string_buffer(512)
+    dp = C.POINTER(C.c_double)
+    rc = sim.bddc_sim_harmonic_solve(k * m, k * m, k, k, parts, leaf, coords, c.ctypes.data_as(dp),
+                                     out.ctypes.data_as(dp), err, 512)
+    assert rc == 0, err.value
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
