@@ -122,23 +122,24 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
 
 constexpr int kExThreads = 256;
 
-__device__ __forceinline__ std::uint64_t next_seq(const ExchangeDesc* D, std::uint64_t* seq_s) {
-    if (threadIdx.x == 0) {
-        *seq_s = *D->seq + 1;  // every rank runs the same exchanges in the same order
-        *D->seq = *seq_s;
-    }
-    return 0;
+// The descriptors travel as __grid_constant__ kernel parameters (constant bank: no dependent
+// global loads before the first put).
+struct ExchangeArgs {
+    ExchangeDesc d[2];
+    double* src[2];
+    const double* part;
+    int grid, slot, nd;
+};
+
+__device__ __forceinline__ void put_all(const ExchangeDesc& D, const double* src) {
+    const int n = D.n_items;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) D.item_dst[i][0] = src[D.item_src[i]];
 }
 
-__device__ __forceinline__ void put_all(const ExchangeDesc* D, const double* src) {
-    const int n = D->n_items;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) D->item_dst[i][0] = src[D->item_src[i]];
-}
-
-__device__ __forceinline__ void wait_all(const ExchangeDesc* D, std::uint64_t seq, int lane_base) {
+__device__ __forceinline__ void wait_all(const ExchangeDesc& D, std::uint64_t seq, int lane_base) {
     const int w = static_cast<int>(threadIdx.x) - lane_base;
-    if (w >= 0 && w < D->n_wait) {
-        const std::uint64_t* f = D->wait[w];
+    if (w >= 0 && w < D.n_wait) {
+        const std::uint64_t* f = D.wait[w];
         std::uint64_t t0 = 0, t = 0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         while (ld_acquire_sys(f) < seq) {
@@ -148,41 +149,48 @@ __device__ __forceinline__ void wait_all(const ExchangeDesc* D, std::uint64_t se
     }
 }
 
-// desc2 may be null. The flags are released by thread 0 after the CTA barrier: bar.sync
-// orders every thread's peer stores before thread 0's st.release.sys (cumulativity).
-__global__ void __launch_bounds__(kExThreads) exchange_kernel(const ExchangeDesc* __restrict__ D1, double* src1,
-                                                              const ExchangeDesc* __restrict__ D2, double* src2,
-                                                              const double* part, int grid, int slot) {
+// The flags are released after the CTA barrier: bar.sync orders every thread's peer stores
+// before the flag stores, each flag published by its own thread with a system-scope release
+// (PTX release cumulativity).
+__global__ void __launch_bounds__(kExThreads) exchange_kernel(const __grid_constant__ ExchangeArgs A) {
     __shared__ double scratch[kExThreads / 32];
     __shared__ std::uint64_t seq_s[2];
+    const ExchangeDesc& D1 = A.d[0];
+    const ExchangeDesc& D2 = A.d[1];
+    const bool two = A.nd > 1;
     std::uint64_t t_start = 0, t_wait = 0, t_end = 0;
-    if (D1->stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    next_seq(D1, &seq_s[0]);
-    if (D2) next_seq(D2, &seq_s[1]);
-    if (part) {  // scalar gather: this rank's total first (fixed order)
+    if (D1.stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (threadIdx.x == 0) {  // every rank runs the same exchanges in the same order
+        seq_s[0] = *D1.seq + 1;
+        *D1.seq = seq_s[0];
+        if (two) {
+            seq_s[1] = *D2.seq + 1;
+            *D2.seq = seq_s[1];
+        }
+    }
+    double* const dst_scalar = two ? A.src[1] : A.src[0];
+    if (A.part) {  // scalar gather: this rank's total first (fixed order)
         double v = 0.0;
-        for (int i = threadIdx.x; i < grid; i += blockDim.x) v += part[i];
+        for (int i = threadIdx.x; i < A.grid; i += blockDim.x) v += A.part[i];
         v = block_sum<kExThreads>(v, scratch);
-        if (threadIdx.x == 0) (D2 ? src2 : src1)[slot] = v;
+        if (threadIdx.x == 0) dst_scalar[A.slot] = v;
     }
     __syncthreads();
-    put_all(D1, src1);
-    if (D2) put_all(D2, src2);
+    put_all(D1, A.src[0]);
+    if (two) put_all(D2, A.src[1]);
     __syncthreads();
-    // bar.sync above orders every thread's peer stores before the flag stores; each flag is
-    // published by its own thread with a system-scope release (PTX release cumulativity)
-    if (threadIdx.x < D1->n_put) st_release_sys(D1->put[threadIdx.x].flag, seq_s[0]);
-    if (D2 && threadIdx.x >= kMaxPeers && threadIdx.x - kMaxPeers < D2->n_put)
-        st_release_sys(D2->put[threadIdx.x - kMaxPeers].flag, seq_s[1]);
-    if (D1->stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_wait));
+    if (static_cast<int>(threadIdx.x) < D1.n_put) st_release_sys(D1.put[threadIdx.x].flag, seq_s[0]);
+    if (two && threadIdx.x >= kMaxPeers && static_cast<int>(threadIdx.x) - kMaxPeers < D2.n_put)
+        st_release_sys(D2.put[threadIdx.x - kMaxPeers].flag, seq_s[1]);
+    if (D1.stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_wait));
     wait_all(D1, seq_s[0], 0);
-    if (D2) wait_all(D2, seq_s[1], kMaxPeers);
+    if (two) wait_all(D2, seq_s[1], kMaxPeers);
     __syncthreads();
-    if (D1->stats && threadIdx.x == 0) {
+    if (D1.stats && threadIdx.x == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        D1->stats[0] += 1;
-        D1->stats[1] += t_end - t_start;
-        D1->stats[2] += t_end - t_wait;
+        D1.stats[0] += 1;
+        D1.stats[1] += t_end - t_start;
+        D1.stats[2] += t_end - t_wait;
     }
 }
 
@@ -227,15 +235,31 @@ PeerLinks::~PeerLinks() {
                 if (void* p = ptrs_[static_cast<std::size_t>(q) * nbuf_ + b]) cudaIpcCloseMemHandle(p);
 }
 
-void launch_exchange(const ExchangeDesc* desc, double* src, const double* part, int grid, int slot,
+void launch_exchange(const ExchangeDesc& desc, double* src, const double* part, int grid, int slot,
                      cudaStream_t s) {
-    exchange_kernel<<<1, kExThreads, 0, s>>>(desc, src, nullptr, nullptr, part, grid, slot);
+    ExchangeArgs A{};
+    A.d[0] = desc;
+    A.src[0] = src;
+    A.part = part;
+    A.grid = grid;
+    A.slot = slot;
+    A.nd = 1;
+    exchange_kernel<<<1, kExThreads, 0, s>>>(A);
     BDDC_LAUNCHED();
 }
 
-void launch_exchange2(const ExchangeDesc* desc1, double* src1, const ExchangeDesc* desc2, double* src2,
+void launch_exchange2(const ExchangeDesc& desc1, double* src1, const ExchangeDesc& desc2, double* src2,
                       const double* part, int grid, int slot, cudaStream_t s) {
-    exchange_kernel<<<1, kExThreads, 0, s>>>(desc1, src1, desc2, src2, part, grid, slot);
+    ExchangeArgs A{};
+    A.d[0] = desc1;
+    A.d[1] = desc2;
+    A.src[0] = src1;
+    A.src[1] = src2;
+    A.part = part;
+    A.grid = grid;
+    A.slot = slot;
+    A.nd = 2;
+    exchange_kernel<<<1, kExThreads, 0, s>>>(A);
     BDDC_LAUNCHED();
 }
 

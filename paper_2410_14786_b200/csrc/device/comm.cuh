@@ -90,11 +90,11 @@ private:
 // One exchange: seq = ++*desc->seq, puts per desc, system fence, flags = seq, then wait for
 // the incoming flags. part != null: first reduces part[0..grid) (fixed order) into src[slot]
 // (scalar gathers).
-void launch_exchange(const ExchangeDesc* desc, double* src, const double* part, int grid, int slot,
+void launch_exchange(const ExchangeDesc& desc, double* src, const double* part, int grid, int slot,
                      cudaStream_t s);
 // Two exchanges fused in one launch (e.g. the halo of z together with the r.z gather): the
 // scalar reduction (if any) feeds desc2's src2.
-void launch_exchange2(const ExchangeDesc* desc1, double* src1, const ExchangeDesc* desc2, double* src2,
+void launch_exchange2(const ExchangeDesc& desc1, double* src1, const ExchangeDesc& desc2, double* src2,
                       const double* part, int grid, int slot, cudaStream_t s);
 
 // dst[k] = src[idx[k]], k < n

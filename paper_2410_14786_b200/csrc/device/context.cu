@@ -196,7 +196,7 @@ struct GpuContext::Impl {
     // peer-memory exchanges (default): IPC mappings, one descriptor + sequence per type
     enum ExType { kExU = 0, kExP = 1, kExH = 2, kExC = 3, kExPQ = 4, kExRR = 5, kExRZ = 6, kExNB = 7, kExZ = 8 };
     std::unique_ptr<PeerLinks> links;
-    DBuf<ExchangeDesc> ex_desc;
+    std::vector<ExchangeDesc> ex_host;  // passed by value (kernel parameters)
     DBuf<std::uint64_t> ex_flags, ex_seq;  // flags [type][src]; per-type sequence counters
     DBuf<unsigned long long> ex_stats;
     DBuf<double*> ex_item_dst;
@@ -237,7 +237,7 @@ struct GpuContext::Impl {
         if (!dist() || no_exchange) return;
         if (p2p()) {
             const int t = v == U.p ? kExU : kExP;
-            launch_exchange(ex_desc.p + t, v, nullptr, 0, 0, s);
+            launch_exchange(ex_host[t], v, nullptr, 0, 0, s);
             return;
         }
         launch_pack(static_cast<int>(plan->halo_send_idx.size()), halo_idx.p, v, halo_send.p, s);
@@ -247,7 +247,7 @@ struct GpuContext::Impl {
     void iface_exchange(cudaStream_t s) {
         if (!dist() || no_exchange) return;
         if (p2p()) {
-            launch_exchange(ex_desc.p + kExH, hbuf.p, nullptr, 0, 0, s);
+            launch_exchange(ex_host[kExH], hbuf.p, nullptr, 0, 0, s);
             return;
         }
         launch_pack(static_cast<int>(plan->iface_send_slot.size()), iface_idx.p, hbuf.p, iface_send.p, s);
@@ -256,14 +256,14 @@ struct GpuContext::Impl {
     // every rank's c_i (padded blocks, rank order) for the ordered r_c sum
     void gather_cbuf(cudaStream_t s) {
         if (!dist() || no_exchange) return;
-        if (p2p()) launch_exchange(ex_desc.p + kExC, cbuf.p, nullptr, 0, 0, s);
+        if (p2p()) launch_exchange(ex_host[kExC], cbuf.p, nullptr, 0, 0, s);
         else comm->allgather_inplace(cbuf.p, static_cast<std::size_t>(plan->cbuf_pad), s);
     }
     // r.z gather fused with the halo of z (peer-memory mode, preconditioned): the new direction
     // p = z + beta p is then formed on the halo locally, bit-identical to its owner's values
     void gather_rz_with_z_halo(const double* part, int grid, cudaStream_t s) {
         if (no_exchange) return;
-        launch_exchange2(ex_desc.p + kExZ, z.p, ex_desc.p + kExRZ, gath_c.p, part, grid, comm->rank(), s);
+        launch_exchange2(ex_host[kExZ], z.p, ex_host[kExRZ], gath_c.p, part, grid, comm->rank(), s);
     }
 
     // part[0..grid) -> gath[rank], then gathered over ranks (consumers sum in rank order)
@@ -271,7 +271,7 @@ struct GpuContext::Impl {
         if (!dist() || no_exchange) return;
         if (p2p()) {
             const int t = gath == gath_a.p ? kExPQ : gath == gath_b.p ? kExRR : gath == gath_c.p ? kExRZ : kExNB;
-            launch_exchange(ex_desc.p + t, gath, part, grid, comm->rank(), s);
+            launch_exchange(ex_host[t], gath, part, grid, comm->rank(), s);
             return;
         }
         launch_reduce_to(part, grid, gath + comm->rank(), false, s);
@@ -604,8 +604,7 @@ struct GpuContext::Impl {
             desc[t].item_dst = ex_item_dst.p + first[t];
             desc[t].item_src = ex_item_src.p + first[t];
         }
-        ex_desc.alloc(desc.size());
-        BDDC_CUDA(cudaMemcpy(ex_desc.p, desc.data(), sizeof(ExchangeDesc) * desc.size(), cudaMemcpyHostToDevice));
+        ex_host = desc;
         BDDC_CUDA(cudaDeviceSynchronize());
     }
 
