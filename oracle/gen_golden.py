@@ -41,6 +41,8 @@ CONFIGS = {
     "k8m32": (8, 32, 1, "history", ["--plain"]),
     "c1": (4, 64, 1, "solve", ["--plain"]),
     "c2": (8, 100, 1, "history", ["--no-stages"]),
+    "c2g4": (16, 100, 1, "history", ["--no-stages"]),   # C2 weak-scaling layout at 4 GPUs
+    "c3": (24, 105, 1, "history", ["--no-stages"]),     # C3 strong scaling, 6,345,361 dofs
 }
 
 # Problems the reference cannot assemble itself (rectangular layouts, heterogeneous
@@ -52,6 +54,7 @@ BUNDLES = {
     "h4m8": (32, 32, 4, 4, 2.0, 0x5EED, 1, "full"),
     "r16x8m8": (128, 64, 16, 8, 0.0, 0, 1, "solve"),
     "c5": (352, 352, 8, 8, 2.0, 0x5EED, 1, "history"),
+    "c2g2": (1600, 800, 16, 8, 0.0, 0, 1, "history"),  # C2 weak-scaling layout at 2 GPUs
 }
 
 MAP_ARRAYS = ("subdomain_dofs", "subdomain_dofs_off", "interior_counts", "class_kind",

@@ -889,7 +889,10 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     }
     int nsm = 148;
     BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
-    const int parts = opt.solve_parts > 0 ? opt.solve_parts : (d.n_subdomains <= nsm ? 2 : 1);
+    // CTA pairs always: with more subdomains than SMs they run in waves, and halving the shared-
+    // memory vectors keeps 4 KB TMA units (a one-CTA subdomain at C3 would fall back to 1 KB)
+    const int parts = opt.solve_parts > 0 ? opt.solve_parts : 2;
+    (void)nsm;
     // TMA unit size: the largest for which every warp gets at least two ring slots next to
     // the vectors (BDDC_UNIT_BYTES overrides, for experiments)
     const int max_smem = max_solve_smem(I.device);

@@ -32,15 +32,21 @@ def main():
 
     rank, world, local_rank, nid = init()
     opts = SolverOptions(1e-8, 0.0, 10000, True)
+    # (golden fixture, (cells_x, cells_y, kx, ky[, kappa_decades, kappa_seed]))
     cfgs = [("r4x2m8", (32, 16, 4, 2)), ("k4m8", (32, 32, 4, 4)), ("r16x8m8", (128, 64, 16, 8)),
-            ("c2_16x8", (1600, 800, 16, 8))]
+            ("h4m8", (32, 32, 4, 4, 2.0, 0x5EED)), ("c5", (352, 352, 8, 8, 2.0, 0x5EED)),
+            ("c2g2", (1600, 800, 16, 8))]
     if world >= 4:
-        cfgs.append(("c2_16x16", (1600, 1600, 16, 16)))
+        cfgs.append(("c2g4", (1600, 1600, 16, 16)))
+    if os.environ.get("DIST_CHECK_C3"):
+        cfgs.append(("c3", (2520, 2520, 24, 24)))
     failures = []
-    for name, (cx, cy, kx, ky) in cfgs:
+    for name, cfg in cfgs:
+        cx, cy, kx, ky = cfg[:4]
+        kappa = cfg[4:] if len(cfg) > 4 else (0.0, 0x5EED)
         if kx * ky < world:
             continue
-        prob = Problem.poisson(cx, kx, cy, ky, rhs_seed=1)
+        prob = Problem.poisson(cx, kx, cy, ky, kappa_decades=kappa[0], kappa_seed=kappa[1], rhs_seed=1)
         b = prob.rhs()
         single = Preconditioner(prob, device=local_rank, solve_parts=2)  # same program split as the ranks
         pre = Preconditioner(prob, device=local_rank, dist=(rank, world, nid), solve_parts=2)
@@ -64,6 +70,11 @@ def main():
             res["iterations_reference"] = int(g["pcg_report"][0])
             if "pcg_x" in g:
                 res["x_err_vs_reference"] = float(np.abs(xd[rows] - g["pcg_x"][rows]).max() / np.abs(g["pcg_x"]).max())
+            elif "pcg_x_sample" in g:  # large problems: every stride-th entry of the reference solution
+                stride = int(g["pcg_x_sample_stride"][0])
+                idx = np.intersect1d(rows, np.arange(0, prob.global_dofs, stride))
+                xs = g["pcg_x_sample"]
+                res["x_err_vs_reference"] = float(np.abs(xd[idx] - xs[idx // stride]).max() / np.abs(xs).max())
         except FileNotFoundError:
             pass
         # device entry point on the rank-local layout
@@ -77,7 +88,10 @@ def main():
               and res["history_err_vs_single"] <= 1e-10 and res["x_err_vs_single"] <= 1e-10
               and res["device_matches_host"] and rd.converged)
         if "history_err_vs_reference" in res:
-            ok = ok and res["history_err_vs_reference"] <= 1e-10 and rd.iterations == res["iterations_reference"]
+            # heterogeneous coefficients: the reference itself is only 1e-8-stable (test_gpu_parity)
+            htol = 1e-7 if kappa[0] else 1e-10
+            ok = ok and res["history_err_vs_reference"] <= htol and abs(rd.iterations - res["iterations_reference"]) <= (
+                1 if kappa[0] else 0)
         if "x_err_vs_reference" in res:
             ok = ok and res["x_err_vs_reference"] <= 1e-10
         res["ok"] = bool(ok)

@@ -235,3 +235,17 @@ def test_reference_dropin(gpu, k, m):
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[0])
     assert res["ok"] and res["iterations"][0] == res["iterations"][1]
+
+
+def test_c3_strong_scaling_point_vs_reference(gpu):
+    # C3: 2520x2520 cells, 24x24 subdomains, 6,345,361 dofs on one B200 against
+    # the unmodified reference's history and sampled solution (oracle/gen_golden.py c3)
+    g = golden("c3")
+    p = Problem.poisson(2520, 24)
+    assert p.global_dofs == 6345361
+    pre = Preconditioner(p)
+    x, rep = pre.pcg(p.rhs(), OPTS)
+    assert rep.converged and rep.iterations == int(g["pcg_report"][0])
+    assert history_err(rep.residual_history, g["pcg_history"]) <= 1e-10
+    stride = int(g["pcg_x_sample_stride"][0])
+    assert np.abs(x[::stride] - g["pcg_x_sample"]).max() <= 1e-10 * np.abs(g["pcg_x_sample"]).max()
