@@ -82,7 +82,7 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
     const int iters = static_cast<unsigned>(h.z) >> 16;
     const int G = 1 << lg, kG = k << lg;
     const int g = lane & (G - 1), r = lane >> lg;
-    const double* in = (flags & kTaskDiag) ? own : other;
+    const double* in = (flags & kTaskInOwn) ? own : other;
     const double* M = reinterpret_cast<const double*>(tile) + lane;
     const int vbytes = (iters * kG * 8 + 15) & ~15;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;

@@ -48,6 +48,7 @@ enum TaskFlags : std::uint8_t {
     kTaskDiag = 8,       // other[out_base + r] = acc
     kTaskPush = 16,      // own[outidx[r]] -= acc (outidx after the values / index list)
     kTaskPartial = 32,   // with PUSH: Q[outidx[r]] += acc
+    kTaskInOwn = 64,     // inputs from own (else from other)
 };
 
 enum PhaseKind : std::int32_t {

@@ -159,6 +159,22 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
     std::vector<index_t> owner(nI, -1);
     for (index_t s = 0; s < nsn; ++s)
         for (index_t c = sn[s].col_begin; c < sn[s].col_end; ++c) owner[c] = s;
+    // BL_s = L_{R_s,s} L_ss^{-1} (interior rows of R_s): the forward push t[R] -= L_{R,s} x_s
+    // becomes t[R] -= BL_s t_s, so it reads the same t_s as the diagonal solve and shares its
+    // phase; the backward sweep x_s = L_ss^{-T} y_s - BL_s^T x_R is one chunk with two pieces.
+    std::vector<std::vector<double>> BL(nsn);
+    for (index_t sidx = 0; sidx < nsn; ++sidx) {
+        const Supernode& S = sn[sidx];
+        const index_t ns = S.size(), mI = S.n_interior_rows;
+        BL[sidx].assign(static_cast<std::size_t>(mI) * ns, 0.0);
+        for (index_t a = 0; a < mI; ++a)
+            for (index_t j = 0; j < ns; ++j) {
+                double acc = 0.0;
+                for (index_t k = j; k < ns; ++k)
+                    acc += S.B[static_cast<std::size_t>(a) * ns + k] * S.Linv[static_cast<std::size_t>(k) * ns + j];
+                BL[sidx][static_cast<std::size_t>(a) * ns + j] = acc;
+            }
+    }
 
     for (int part = 0; part < P; ++part) {
         // local index space: group positions ascending, then top positions ascending
@@ -187,38 +203,40 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 out.push_back(make_chunk(unit_bytes,
                     nr, static_cast<int>(r0 + nr),
                     [&](int r, int j) { return j <= r0 + r ? S.Linv[static_cast<std::size_t>(r0 + r) * ns + j] : 0.0; },
-                    false, [](int) { return 0; }, loc[S.col_begin], loc[S.col_begin + r0], nr, kTaskDiag, nullptr));
+                    false, [](int) { return 0; }, loc[S.col_begin], loc[S.col_begin + r0], nr,
+                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr));
             }
         };
-        auto diag_bwd = [&](index_t s, Chunks& out) {
+        // backward chunk of rows q0.. of supernode s: piece A = L_ss^{-T} y_s (own = X,
+        // contiguous), piece B = -BL_s^T x_R (other = T, indexed); flush T[s rows] = acc
+        auto bwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
-            const index_t ns = S.size();
+            const index_t ns = S.size(), mI = S.n_interior_rows;
             for (index_t q0 = 0; q0 < ns; q0 += kr) {
                 const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
-                out.push_back(make_chunk(unit_bytes,
+                Chunk a = make_chunk(unit_bytes,
                     nq, static_cast<int>(ns - q0),
                     [&](int r, int j) {
                         return j >= r ? S.Linv[static_cast<std::size_t>(q0 + j) * ns + q0 + r] : 0.0;
                     },
-                    false, [](int) { return 0; }, loc[S.col_begin + q0], loc[S.col_begin + q0], nq, kTaskDiag,
-                    nullptr));
-            }
-        };
-        auto pull_bwd = [&](index_t s, Chunks& out) {
-            const Supernode& S = sn[s];
-            const index_t ns = S.size(), mI = S.n_interior_rows;
-            if (mI == 0) return;
-            for (index_t q0 = 0; q0 < ns; q0 += kr) {
-                const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
-                out.push_back(make_chunk(unit_bytes,
-                    nq, static_cast<int>(mI),
-                    [&](int r, int j) { return S.B[static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
-                    [&](int j) {
-                        const std::int32_t l = loc[S.rows[j]];
-                        if (l < 0) throw std::logic_error("solve program: ancestor row not local");
-                        return l;
-                    },
-                    0, loc[S.col_begin + q0], nq, 0, nullptr));
+                    false, [](int) { return 0; }, loc[S.col_begin + q0], loc[S.col_begin + q0], nq,
+                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr);
+                if (mI > 0) {
+                    Chunk b = make_chunk(unit_bytes,
+                        nq, static_cast<int>(mI),
+                        [&](int r, int j) { return -BL[s][static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
+                        [&](int j) {
+                            const std::int32_t l = loc[S.rows[j]];
+                            if (l < 0) throw std::logic_error("solve program: ancestor row not local");
+                            return l;
+                        },
+                        0, loc[S.col_begin + q0], nq, kTaskDiag, nullptr);
+                    a.tiles.back().t.flags &= static_cast<std::uint8_t>(~kTaskLast);   // accumulation continues
+                    b.tiles.front().t.flags &= static_cast<std::uint8_t>(~kTaskFirst);
+                    for (Tile& t : b.tiles) a.tiles.push_back(std::move(t));
+                    a.cost += b.cost;
+                }
+                out.push_back(std::move(a));
             }
         };
         // t[R_d] -= L_{R_d,d} x_d restricted to the target rows accepted by `take`: rows in the
@@ -252,9 +270,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     }
                     out.push_back(make_chunk(unit_bytes,
                         k, static_cast<int>(nd),
-                        [&](int r, int j) { return D.B[static_cast<std::size_t>(rows[c0 + r]) * nd + j]; }, false,
+                        [&](int r, int j) { return BL[d][static_cast<std::size_t>(rows[c0 + r]) * nd + j]; }, false,
                         [](int) { return 0; }, loc[D.col_begin], 0, k,
-                        static_cast<std::uint8_t>(kTaskPush | (to_top ? kTaskPartial : 0)), &outidx));
+                        static_cast<std::uint8_t>(kTaskPush | kTaskInOwn | (to_top ? kTaskPartial : 0)), &outidx));
                 }
             }
         };
@@ -384,7 +402,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 }
             kr = chunk_rows_for(nrows);
             for (index_t s : nodes) diag_fwd(s, b);
-            phases.push_back(singles(std::move(b)));
+            Phase diag_phase = singles(std::move(b));
             kr = chunk_rows_for(mrows);
             // one job per 32-row output chunk: chunks of one supernode write disjoint rows and
             // spread over the warps; chunks of different supernodes are coloured by target rows
@@ -400,11 +418,17 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     pushes.back().push_back(std::move(cs[c]));
                 }
             }
+            // the diagonal solves read the same final t_s as the pushes (and write X): they
+            // share the first colour class's phase
+            bool first = true;
             for (const auto& cls : colour(targets)) {
                 Phase pp;
+                if (first) pp = std::move(diag_phase);
                 for (std::size_t j : cls) pp.jobs.push_back(std::move(pushes[j]));
                 phases.push_back(std::move(pp));
+                first = false;
             }
+            if (first) phases.push_back(std::move(diag_phase));
             kr = 32;
         }
         // ---------------- exchange the partial sums into the shared top (P = 2)
@@ -424,19 +448,17 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             kr = chunk_rows_for({sn[s].n_interior_rows});
             push_fwd(s, ps, true, all_rows);
             kr = 32;
+            for (Chunk& c : ps) b.push_back(std::move(c));  // diag and pushes read t_s: one phase
             phases.push_back(singles(std::move(b)));
-            phases.push_back(singles(std::move(ps)));  // disjoint 32-row chunks: one warp each
         }
         // ---------------- backward sweep: top chain, levels above the cut, then subtrees
         for (auto it = top.rbegin(); it != top.rend(); ++it) {
-            Chunks a, b;
+            Chunks b;
             kr = chunk_rows_for({sn[*it].size()});
-            pull_bwd(*it, a);
-            diag_bwd(*it, b);
+            bwd(*it, b);
             kr = 32;
-            Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
-            pa.kind = pb2.kind = kPhaseBackward;
-            phases.push_back(std::move(pa));
+            Phase pb2 = singles(std::move(b));
+            pb2.kind = kPhaseBackward;
             phases.push_back(std::move(pb2));
         }
         for (auto hit = heights.rbegin(); hit != heights.rend(); ++hit) {
@@ -446,14 +468,11 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 if (in_group(s) && !local[s] && sn[s].height == *hit) nrows.push_back(sn[s].size());
             kr = chunk_rows_for(nrows);
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == *hit) {
-                    pull_bwd(s, a);
-                    diag_bwd(s, b);
-                }
+                if (in_group(s) && !local[s] && sn[s].height == *hit) bwd(s, b);
             kr = 32;
-            Phase pa = singles(std::move(a)), pb2 = singles(std::move(b));
-            pa.kind = pb2.kind = kPhaseBackward;
-            phases.push_back(std::move(pa));
+            (void)a;
+            Phase pb2 = singles(std::move(b));
+            pb2.kind = kPhaseBackward;
             phases.push_back(std::move(pb2));
         }
         {
@@ -461,10 +480,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             ph.kind = kPhaseBackward | kPhaseChained;
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 Chunks job;
-                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it) {
-                    pull_bwd(*it, job);
-                    diag_bwd(*it, job);
-                }
+                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it) bwd(*it, job);
                 ph.jobs.push_back(std::move(job));
             }
             phases.push_back(std::move(ph));

@@ -51,7 +51,7 @@ void run_phase(const SolvePools& sp, PartState& st) {
                 tb + pad16i(iters * k * G * 8) + ((task.flags & kTaskInIndexed) ? pad16i(iters * G * 4) : 0));
             if (task.flags & kTaskFirst)
                 for (double& a : acc) a = 0.0;
-            const std::vector<double>& in = (task.flags & kTaskDiag) ? own : other;
+            const std::vector<double>& in = (task.flags & kTaskInOwn) ? own : other;
             for (int r = 0; r < k; ++r) {
                 double s = 0.0;
                 for (int it = 0; it < iters; ++it)
