@@ -137,6 +137,10 @@ struct GpuContext::Impl {
 
     KernelTimes times;
     const double* apply_skip = nullptr;  // set while the pipelined PCG enqueues speculative applies
+    // set by pcg(): the harmonic-extension launch also forms the per-CTA partials of r.z
+    const double* apply_dot_r = nullptr;
+    int apply_dot_n = 0;
+    DBuf<double> part_rz;
 
     // CUDA graphs of the PCG iteration (BDDC_GRAPH=0 disables): A = spmv/update/check and the
     // convergence read-back, B = the speculative apply, r.z and the new direction. The device
@@ -448,7 +452,15 @@ struct GpuContext::Impl {
         launch_iface_local(ip, opt.local_blocks, s, true);
         iface_exchange(s);
         if (E) record(E->e[2].e, s);
-        if (harm.valid) launch_interior_solve(solve_params(r_dev, z_dev, &harm), launch, 3, s);  // z_I = u0 - A_II^-1 A_IG z_G
+        if (harm.valid) {  // z_I = u0 - A_II^-1 A_IG z_G
+            SolveParams hp = solve_params(r_dev, z_dev, &harm);
+            if (apply_dot_r) {
+                hp.dot_r = apply_dot_r;
+                hp.dot_part = part_rz.p;
+                hp.n_dot = apply_dot_n;
+            }
+            launch_interior_solve(hp, launch, 3, s);
+        }
         else launch_interior_solve(solve_params(r_dev, z_dev), launch, 1, s);
         if (E) record(E->e[3].e, s);
     }
@@ -632,6 +644,25 @@ struct GpuContext::Impl {
         PcgDevice D = pcg_device(o, xd, rd, zd);
         const bool fused_dir = dist() && p2p() && precondition;  // z halo arrives with r.z
         if (fused_dir) D.n_dir = static_cast<int>(n);
+        // r.z formed inside the harmonic-extension launch (per-CTA partials) instead of a dot pass
+        const bool fused_dot = precondition && harm.valid;
+        if (fused_dot) {
+            if (part_rz.n < static_cast<std::size_t>(launch.n_parts)) part_rz.alloc(launch.n_parts);
+            if (!dist()) {
+                D.red_c = part_rz.p;
+                D.red_c_n = launch.n_parts;
+            }
+        }
+        auto apply_rz = [&]() {  // apply + the r.z partials for the following reduction
+            if (fused_dot) {
+                apply_dot_r = rd;
+                apply_dot_n = D.n_dot;
+            }
+            apply(rd, zd, s);
+            apply_dot_r = nullptr;
+        };
+        const double* rz_part = fused_dot ? part_rz.p : part_a.p;
+        const int rz_grid = fused_dot ? launch.n_parts : D.grid;
         BDDC_CUDA(cudaMemsetAsync(xd, 0, sizeof(double) * n, s));
         BDDC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(double) * 8, s));
         BDDC_CUDA(cudaMemsetAsync(iter_ctr.p, 0, sizeof(int), s));
@@ -661,15 +692,15 @@ struct GpuContext::Impl {
             return rep;
         }
         if (precondition) {
-            apply(rd, zd, s);
+            apply_rz();
             check_coarse(s);
         }
-        pcg_dot(D, rd, zd, part_a.p, s);
+        if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
         if (fused_dir) {
-            gather_rz_with_z_halo(part_a.p, D.grid, s);
+            gather_rz_with_z_halo(rz_part, rz_grid, s);
             pcg_init_rho(D, s);
         } else {
-            gather_partial(part_a.p, D.grid, gath_c.p, s);
+            gather_partial(rz_part, rz_grid, gath_c.p, s);
             pcg_init_rho(D, s);
             halo_exchange(p.p, s);
         }
@@ -686,14 +717,14 @@ struct GpuContext::Impl {
         const bool graphed = use_graphs && pipelined && (!dist() || p2p()) && cap_status == cudaStreamCaptureStatusNone;
         auto next_direction = [&](int it) {
             apply_skip = scal.p;  // no-op once iteration `it` has converged or failed
-            if (precondition) apply(rd, zd, s);
+            if (precondition) apply_rz();
             apply_skip = nullptr;
-            pcg_dot(D, rd, zd, part_a.p, s);
+            if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
             if (fused_dir) {
-                gather_rz_with_z_halo(part_a.p, D.grid, s);
+                gather_rz_with_z_halo(rz_part, rz_grid, s);
                 pcg_xpay(D, it, s);
             } else {
-                gather_partial(part_a.p, D.grid, gath_c.p, s);
+                gather_partial(rz_part, rz_grid, gath_c.p, s);
                 pcg_xpay(D, it, s);
                 halo_exchange(p.p, s);
             }
@@ -791,11 +822,11 @@ struct GpuContext::Impl {
             if (it == o.max_iterations) break;
             if (!spec) {
                 if (precondition) {
-                    apply(rd, zd, s);
+                    apply_rz();
                     check_coarse(s);
                 }
-                pcg_dot(D, rd, zd, part_a.p, s);
-                gather_partial(part_a.p, D.grid, gath_c.p, s);
+                if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
+                gather_partial(rz_part, rz_grid, gath_c.p, s);
                 pcg_xpay(D, it, s);
                 halo_exchange(p.p, s);
             }

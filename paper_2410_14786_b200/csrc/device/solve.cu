@@ -141,6 +141,7 @@ template <int MODE, int CLUSTER, bool STATS>
 __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     if (skip_launch(S.skip)) return;  // uniform over the cluster: every CTA reads the same flag
+    double rz = 0.0;  // MODE 3 with dot_part: this thread's share of r.z
     const PartDesc& pdr = S.parts[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int unit = S.unit_bytes;
@@ -231,7 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 const int gid = S.iface_gid[sd.iface + g];
                 z = 0.0;
                 for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) z += S.hbuf[S.gi_own_ref[o]];
-                if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) S.out[S.iface_dof[sd.iface + g]] = z;
+                if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) {
+                    const int dof = S.iface_dof[sd.iface + g];
+                    S.out[dof] = z;
+                    if (MODE == 3 && S.dot_part && dof < S.n_dot) rz += S.dot_r[dof] * z;
+                }
             } else {
                 z = S.hbuf[sd.hbuf + g];
             }
@@ -336,9 +341,19 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             if (gi[q] >= 0) {
-                if (MODE == 3) S.out[gi[q]] = S.u0[gi[q]] - T[l0 + q * kThreads];  // z_I = u0 - extension
-                else S.out[gi[q]] = T[l0 + q * kThreads];
+                if (MODE == 3) {
+                    const double z = S.u0[gi[q]] - T[l0 + q * kThreads];  // z_I = u0 - extension
+                    S.out[gi[q]] = z;
+                    if (S.dot_part && gi[q] < S.n_dot) rz += S.dot_r[gi[q]] * z;
+                } else {
+                    S.out[gi[q]] = T[l0 + q * kThreads];
+                }
             }
+    }
+    if (MODE == 3 && S.dot_part) {  // r.z of the entries this CTA wrote (fused PCG dot product)
+        __shared__ double red[kSolveWarps];
+        rz = block_sum<kThreads>(rz, red);
+        if (tid == 0) S.dot_part[blockIdx.x] = rz;
     }
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
 }

@@ -25,6 +25,11 @@ struct SolveParams {
     const double* in;
     double* out;
     const double* u0;  // MODE 3: the first interior solve's result (z_I = u0 - harmonic extension)
+    // MODE 3, fused PCG dot product: per CTA, sum of dot_r[i] * z[i] over the z entries it writes
+    // with i < n_dot, into dot_part[blockIdx.x] (null: off)
+    const double* dot_r;
+    double* dot_part;
+    int n_dot;
     int unit_bytes;  // set by the launcher
     int slot_shift;  // log2(ring slots per warp)
     int max_loc;
