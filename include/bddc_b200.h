@@ -92,7 +92,7 @@ typedef struct {
     double coarse_abs_tolerance;   /* 0 */
     int32_t coarse_max_iterations; /* 500 */
     int32_t leaf_size;             /* nested-dissection leaf size (default 24) */
-    int32_t local_blocks;          /* CTAs per subdomain for the K_i GEMV (default 4) */
+    int32_t local_blocks;          /* CTAs per subdomain for the K_i GEMV (default 8) */
     int32_t solve_parts;           /* CTAs (cluster size) per subdomain in the interior solve: 0 auto, 1, 2 */
 } bddc_gpu_options;
 

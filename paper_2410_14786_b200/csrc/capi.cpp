@@ -196,7 +196,7 @@ void bddc_default_gpu_options(bddc_gpu_options* o) {
     o->coarse_abs_tolerance = 0.0;
     o->coarse_max_iterations = 500;
     o->leaf_size = 24;
-    o->local_blocks = 4;
+    o->local_blocks = 8;
     o->solve_parts = 0;
 }
 

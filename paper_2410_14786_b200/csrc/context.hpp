@@ -27,7 +27,7 @@ struct GpuOptions {
     double coarse_atol = 0.0;
     int coarse_max_iterations = 500;
     int leaf_size = 24;           // measured best on B200 (tools/leaf_sweep.sh)
-    int local_blocks = 4;         // CTAs per subdomain for the K_i GEMV
+    int local_blocks = 8;         // CTAs per subdomain for the K_i GEMV (measured: 8 > 4, = 16)
     int solve_parts = 0;          // CTAs per subdomain in the interior solve (0 = auto)
     bool profile = false;         // record per-kernel CUDA events in apply()
     // second interior solve of the apply as the harmonic extension u0 - A_II^{-1} A_IG z_G with a

@@ -448,8 +448,12 @@ struct GpuContext::Impl {
         const IfaceParams ip = iface_params();
         launch_iface_restrict(ip, r_dev, U.p, s);
         gather_cbuf(s);
-        coarse_solve(s);
-        launch_iface_local(ip, opt.local_blocks, s, true);
+        if (opt.coarse_mode == 0) {
+            launch_iface_local(ip, opt.local_blocks, s, 2);  // coarse GEMV rows fused in
+        } else {
+            coarse_solve(s);
+            launch_iface_local(ip, opt.local_blocks, s, 1);
+        }
         iface_exchange(s);
         if (E) record(E->e[2].e, s);
         if (harm.valid) {  // z_I = u0 - A_II^-1 A_IG z_G
@@ -1157,7 +1161,7 @@ void GpuContext::stage_host(Stage st, const double* in0, const double* in1, cons
             BDDC_CUDA(cudaMemsetAsync(I.vtmp.p, 0, sizeof(double) * n, s));
             launch_interior_solve(I.solve_params(I.vin.p, I.vtmp.p), I.launch, 0, s);  // y = A_II^-1 f_I
             launch_stage_local_g(sp, I.vin.p, I.vtmp.p, s);                             // g = f_G - A_GI y
-            launch_iface_local(I.iface_params(), I.opt.local_blocks, s, false);         // z_G = K g
+            launch_iface_local(I.iface_params(), I.opt.local_blocks, s, 0);             // z_G = K g
             BDDC_CUDA(cudaMemsetAsync(I.vout.p, 0, sizeof(double) * n, s));
             launch_interior_solve(I.solve_params(I.vin.p, I.vout.p), I.launch, 2, s);  // z_I
             launch_stage_iface_gather(sp, I.hbuf.p, I.vout.p, s);                       // sum_i w z_G

@@ -82,9 +82,29 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     const int ng = sd.n_iface, np = sd.n_primal;
     double* g = sm;
     double* xl = sm + ((ng + 1) & ~1);
+    double* rc = xl + ((P.max_primal + 1) & ~1);
     for (int k = threadIdx.x; k < ng; k += blockDim.x) g[k] = P.gbuf[sd.hbuf + k];
-    if (with_coarse)
+    if (with_coarse == 1) {
         for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
+    } else if (with_coarse == 2) {
+        // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
+        // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
+        const int nc = P.n_coarse;
+        for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+            double acc = 0.0;
+            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) acc += P.cbuf[P.c_own_ref[o]];
+            rc[q] = acc;
+        }
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int j = warp; j < np; j += kLocalThreads / 32) {
+            const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
+            double acc = 0.0;
+            for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) xl[j] = acc;
+        }
+    }
     __syncthreads();
     const int rows_per = (ng + blocks_per_sub - 1) / blocks_per_sub;
     const int r0 = part * rows_per, r1 = min(ng, r0 + rows_per);
@@ -317,13 +337,13 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
     BDDC_LAUNCHED();
 }
 
-void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, bool with_coarse) {
-    const std::size_t smem = sizeof(double) * (P.max_iface + P.max_primal + 4);
+void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse) {
+    const std::size_t smem =
+        sizeof(double) * (P.max_iface + P.max_primal + 4 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0));
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub,
-                                                                                 with_coarse ? 1 : 0);
+    iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub, coarse);
     BDDC_LAUNCHED();
 }
 

@@ -89,6 +89,8 @@ void launch_iface_restrict(const IfaceParams& P, const double* r, const double* 
 void launch_coarse_direct(const IfaceParams& P, cudaStream_t s);
 // K5: h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i); rows split over blocks_per_sub CTAs.
 // with_coarse = false: h_i = K_i g_i (unweighted; local_correction stage)
-void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, bool with_coarse = true);
+// coarse: 0 = h_i = K_i g_i; 1 = W_i(Phi x_c[map] + K g) with x_c from the coarse kernel;
+// 2 = the same with the rows of x_c = A_c^{-1} r_c formed in the kernel (dense direct mode)
+void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse);
 
 }  // namespace bddc_b200

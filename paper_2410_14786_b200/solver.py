@@ -202,7 +202,7 @@ class Problem:
 
 
 def gpu_options(device=0, workers=0, coarse_mode="direct", coarse_options: SolverOptions | None = None,
-                leaf_size=24, local_blocks=4, solve_parts=0) -> L.GpuOptions:
+                leaf_size=24, local_blocks=8, solve_parts=0) -> L.GpuOptions:
     o = L.GpuOptions()
     L.lib().bddc_default_gpu_options(C.byref(o))
     o.device, o.workers = device, workers
@@ -319,7 +319,7 @@ class Preconditioner:
     calls then take global vectors and fill the entries of the rank's subdomains."""
 
     def __init__(self, problem: Problem, device: int = 0, workers: int = 0, coarse_mode: str = "direct",
-                 coarse_options: SolverOptions | None = None, leaf_size: int = 24, local_blocks: int = 4,
+                 coarse_options: SolverOptions | None = None, leaf_size: int = 24, local_blocks: int = 8,
                  solve_parts: int = 0, dist=None):
         self.problem = problem
         self.n = problem.global_dofs
