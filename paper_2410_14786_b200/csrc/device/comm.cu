@@ -120,7 +120,31 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
     return v;
 }
 
-constexpr int kExThreads = 256;
+constexpr int kExThreads = 512;
+
+// value i of D goes from src[item_src[i]] to item_dst[i] (peer memory). Four items per thread
+// in flight: the index, pointer and value loads of a round issue back to back instead of one
+// dependent chain per item (the put loop of a single CTA is latency-bound otherwise).
+template <int THREADS>
+__device__ __forceinline__ void put_items(const ExchangeDesc& D, const double* src) {
+    const int n = D.n_items;
+    for (int i0 = static_cast<int>(threadIdx.x); i0 < n; i0 += 4 * THREADS) {
+        int si[4];
+        double* di[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * THREADS;
+            si[q] = i < n ? __ldg(D.item_src + i) : 0;
+            di[q] = i < n ? D.item_dst[i] : nullptr;
+        }
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = di[q] ? __ldcg(src + si[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (di[q]) *di[q] = v[q];
+    }
+}
 
 // The descriptors travel as __grid_constant__ kernel parameters (constant bank: no dependent
 // global loads before the first put).
@@ -131,10 +155,6 @@ struct ExchangeArgs {
     int grid, slot, nd;
 };
 
-__device__ __forceinline__ void put_all(const ExchangeDesc& D, const double* src) {
-    const int n = D.n_items;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) D.item_dst[i][0] = src[D.item_src[i]];
-}
 
 __device__ __forceinline__ void wait_all(const ExchangeDesc& D, std::uint64_t seq, int lane_base) {
     const int w = static_cast<int>(threadIdx.x) - lane_base;
@@ -176,8 +196,8 @@ __global__ void __launch_bounds__(kExThreads) exchange_kernel(const __grid_const
         if (threadIdx.x == 0) dst_scalar[A.slot] = v;
     }
     __syncthreads();
-    put_all(D1, A.src[0]);
-    if (two) put_all(D2, A.src[1]);
+    put_items<kExThreads>(D1, A.src[0]);
+    if (two) put_items<kExThreads>(D2, A.src[1]);
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < D1.n_put) st_release_sys(D1.put[threadIdx.x].flag, seq_s[0]);
     if (two && threadIdx.x >= kMaxPeers && static_cast<int>(threadIdx.x) - kMaxPeers < D2.n_put)

@@ -205,7 +205,50 @@ struct GpuContext::Impl {
     DBuf<unsigned long long> ex_stats;
     DBuf<double*> ex_item_dst;
     DBuf<std::int32_t> ex_item_src;
+    // fused LL exchanges (device/fused_comm.cuh): a per-rank LL receive buffer (exported to the
+    // peers), the sent items bucketed by producing CTA, one grid ticket per type. BDDC_FUSED_EX
+    // bit mask (default 7): 1 = the p.q / r.r scalars, 2 = the apply's u0 halo / c_i / h_i,
+    // 4 = z's halo with r.z; 0 keeps the separate exchange launches
+    DBuf<ll_word> ll_buf;
+    std::int64_t ll_off[5] = {};  // my regions (words): u0 halo, z halo, h_i, c_i, scalars
+    DBuf<std::int32_t> ll_src, ll_cta;
+    DBuf<ll_word*> ll_dst, ll_sc_dst;  // item destinations; scalar destinations [row][peer != me]
+    std::int64_t ll_cta_off[kFlagTypes] = {};
+    bool ll_has[kFlagTypes] = {};
+    DBuf<unsigned int> ex_ticket;
+    int fused_ex = std::getenv("BDDC_FUSED_EX") ? std::atoi(std::getenv("BDDC_FUSED_EX")) : 7;
+    bool pub_rz = false;  // set by pcg(): the harmonic-extension launch publishes z's halo + r.z
     bool p2p() const { return static_cast<bool>(links); }
+    // the apply's exchanges ride on its kernels (u0 halo, c_i gather, h_i) when peer-memory
+    bool fused_apply() const {
+        return dist() && p2p() && (fused_ex & 2) && !no_exchange && harm.valid && opt.coarse_mode == 0;
+    }
+    bool fused_pcg() const { return dist() && p2p() && (fused_ex & 1) && !no_exchange; }
+    DBuf<unsigned long long> fused_trace;  // diagnostics: BDDC_FUSED_TRACE=1 (event ring)
+    // kernel ids of the trace: 0 solve0, 1 restrict, 2 K_i, 3 harmonic solve, 5 spmv_dot, 6 update
+    Publish ll_publish(int t, int kid, const double* src) const {
+        Publish P;
+        P.seq = ex_seq.p + t;
+        P.ticket = ex_ticket.p + t;
+        P.trace = fused_trace.p;
+        P.kid = kid;
+        if (ll_has[t]) {
+            P.cta_ptr = ll_cta.p + ll_cta_off[t];
+            P.item_src = ll_src.p;
+            P.item_dst = ll_dst.p;
+            P.src = src;
+        }
+        return P;
+    }
+    // scalar row (0 p.q, 1 r.r, 2 r.z): part[0..grid) -> red[rank] -> every peer's row slot
+    void ll_scalar(Publish& P, int row, const double* part, int grid, double* red) const {
+        P.part = part;
+        P.red = red;
+        P.grid = grid;
+        P.slot = comm->rank();
+        P.sc_dst = ll_sc_dst.p + static_cast<std::int64_t>(row) * (comm->world() - 1);
+        P.n_sc = comm->world() - 1;
+    }
     // timing experiments only (wrong results): BDDC_NO_EXCHANGE=1 skips every exchange
     bool no_exchange = std::getenv("BDDC_NO_EXCHANGE") && std::atoi(std::getenv("BDDC_NO_EXCHANGE")) == 1;
     std::vector<std::int32_t> halo_soff, halo_roff, iface_soff, iface_roff;
@@ -441,20 +484,35 @@ struct GpuContext::Impl {
             if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
             E = ev_pool[ev_used++].get();
         }
+        const bool fused = fused_apply();
         if (E) record(E->e[0].e, s);
-        launch_interior_solve(solve_params(r_dev, U.p), launch, 0, s);
+        SolveParams sp = solve_params(r_dev, U.p);
+        if (fused) sp.pub = ll_publish(kExU, 0, U.p);
+        launch_interior_solve(sp, launch, 0, s);
         if (E) record(E->e[1].e, s);
-        halo_exchange(U.p, s);
-        const IfaceParams ip = iface_params();
+        IfaceParams ip = iface_params();
+        if (fused) {
+            ip.ll_u = ll_buf.p + ll_off[0];
+            ip.seq_u = ex_seq.p + kExU;
+            ip.ll_u_base = static_cast<int>(n_rows);
+            ip.pub_c = ll_publish(kExC, 1, cbuf.p);
+            ip.ll_c = ll_buf.p + ll_off[3];
+            ip.seq_c = ex_seq.p + kExC;
+            ip.c_own_lo = comm->rank() * plan->cbuf_pad;
+            ip.c_own_hi = ip.c_own_lo + plan->cbuf_pad;
+            ip.pub_h = ll_publish(kExH, 2, hbuf.p);
+        } else {
+            halo_exchange(U.p, s);
+        }
         launch_iface_restrict(ip, r_dev, U.p, s);
-        gather_cbuf(s);
+        if (!fused) gather_cbuf(s);
         if (opt.coarse_mode == 0) {
             launch_iface_local(ip, opt.local_blocks, s, 2);  // coarse GEMV rows fused in
         } else {
             coarse_solve(s);
             launch_iface_local(ip, opt.local_blocks, s, 1);
         }
-        iface_exchange(s);
+        if (!fused) iface_exchange(s);
         if (E) record(E->e[2].e, s);
         if (harm.valid) {  // z_I = u0 - A_II^-1 A_IG z_G
             SolveParams hp = solve_params(r_dev, z_dev, &harm);
@@ -462,6 +520,15 @@ struct GpuContext::Impl {
                 hp.dot_r = apply_dot_r;
                 hp.dot_part = part_rz.p;
                 hp.n_dot = apply_dot_n;
+            }
+            if (fused) {
+                hp.ll_h = ll_buf.p + ll_off[2];
+                hp.seq_h = ex_seq.p + kExH;
+                hp.ll_h_base = static_cast<int>(plan->n_local_slots);
+                if (pub_rz) {  // z's halo + this rank's r.z, as gather_rz_with_z_halo
+                    hp.pub = ll_publish(kExZ, 3, z_dev);
+                    ll_scalar(hp.pub, 2, part_rz.p, launch.n_parts, gath_c.p);
+                }
             }
             launch_interior_solve(hp, launch, 3, s);
         }
@@ -528,7 +595,7 @@ struct GpuContext::Impl {
 
     // Peer-memory exchange descriptors (see device/comm.cuh). Buffers exported, in order:
     // U, p, hbuf, cbuf, gath_a, gath_b, gath_c, gath_d, flags, z.
-    void setup_peer_links() {
+    void setup_peer_links(const DeviceImage& img) {
         const RankPlan& P = *plan;
         const int me = comm->rank(), world = comm->world();
         ex_flags.alloc(static_cast<std::size_t>(kFlagTypes) * kMaxPeers);
@@ -537,20 +604,37 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaMemset(ex_seq.p, 0, sizeof(std::uint64_t) * ex_seq.n));
         // where each peer receives this rank's halo / interface values: rank r publishes
         // (n_rows + halo_recv_off, n_local_slots + iface_recv_off) for every source q
-        std::vector<double> tbl(static_cast<std::size_t>(world) * world * 2, -1.0);
-        for (std::size_t k = 0; k < P.halo_peers.size(); ++k)
-            tbl[(static_cast<std::size_t>(me) * world + P.halo_peers[k]) * 2] = P.n_rows + P.halo_recv_off[k];
-        for (std::size_t k = 0; k < P.iface_peers.size(); ++k)
-            tbl[(static_cast<std::size_t>(me) * world + P.iface_peers[k]) * 2 + 1] = P.n_local_slots + P.iface_recv_off[k];
+        // (+ the same offsets relative to the receive regions, and the LL region offsets)
+        constexpr int kCols = 4, kLLRegions = 5;
+        const std::int64_t n_halo = static_cast<std::int64_t>(U.n) - n_rows;
+        const std::int64_t n_hrecv = img.hbuf_total - P.n_local_slots;
+        ll_off[0] = 0;
+        ll_off[1] = 2 * n_halo;
+        ll_off[2] = 4 * n_halo;
+        ll_off[3] = ll_off[2] + 2 * n_hrecv;
+        ll_off[4] = ll_off[3] + 2 * static_cast<std::int64_t>(world) * P.cbuf_pad;
+        ll_buf.alloc(ll_off[4] + 2 * 3 * static_cast<std::int64_t>(world));
+        BDDC_CUDA(cudaMemset(ll_buf.p, 0, sizeof(ll_word) * ll_buf.n));
+        const std::size_t row = static_cast<std::size_t>(world) * kCols + kLLRegions;
+        std::vector<double> tbl(row * world, -1.0);
+        for (std::size_t k = 0; k < P.halo_peers.size(); ++k) {
+            tbl[me * row + P.halo_peers[k] * kCols] = P.n_rows + P.halo_recv_off[k];
+            tbl[me * row + P.halo_peers[k] * kCols + 2] = P.halo_recv_off[k];
+        }
+        for (std::size_t k = 0; k < P.iface_peers.size(); ++k) {
+            tbl[me * row + P.iface_peers[k] * kCols + 1] = P.n_local_slots + P.iface_recv_off[k];
+            tbl[me * row + P.iface_peers[k] * kCols + 3] = P.iface_recv_off[k];
+        }
+        for (int r = 0; r < kLLRegions; ++r) tbl[me * row + world * kCols + r] = static_cast<double>(ll_off[r]);
         {
             DBuf<double> d;
             d.upload(tbl);
-            comm->allgather_inplace(d.p, static_cast<std::size_t>(world) * 2, nullptr);
+            comm->allgather_inplace(d.p, row, nullptr);
             BDDC_CUDA(cudaDeviceSynchronize());
             BDDC_CUDA(cudaMemcpy(tbl.data(), d.p, sizeof(double) * tbl.size(), cudaMemcpyDeviceToHost));
         }
         links = std::make_unique<PeerLinks>(*comm, std::vector<void*>{U.p, p.p, hbuf.p, cbuf.p, gath_a.p, gath_b.p,
-                                                                      gath_c.p, gath_d.p, ex_flags.p, z.p});
+                                                                      gath_c.p, gath_d.p, ex_flags.p, z.p, ll_buf.p});
         std::vector<ExchangeDesc> desc(kFlagTypes);
         auto flag_of = [&](int q, int type) {
             return static_cast<std::uint64_t*>(links->peer(q, 8)) + type * kMaxPeers + me;
@@ -560,7 +644,7 @@ struct GpuContext::Impl {
             D.idx = idx;
             for (std::size_t k = 0; k < peers.size(); ++k) {
                 const int q = peers[k];
-                const double at = tbl[(static_cast<std::size_t>(q) * world + me) * 2 + col];
+                const double at = tbl[q * row + me * kCols + col];
                 if (at < 0) throw std::logic_error("rank plan: peer does not expect this rank's values");
                 PeerPut& pp = D.put[D.n_put++];
                 pp.dst = static_cast<double*>(links->peer(q, buffer)) + static_cast<std::int64_t>(at);
@@ -592,9 +676,9 @@ struct GpuContext::Impl {
         all_to_all(desc[kExNB], kExNB, 7, me, 1);
         for (int t = 0; t < kFlagTypes; ++t) desc[t].seq = ex_seq.p + t;
         if (std::getenv("BDDC_EXCH_STATS")) {  // diagnostics: per-type {count, total ns, wait ns}
-            ex_stats.alloc(3 * kFlagTypes);
+            ex_stats.alloc(8 * kFlagTypes);
             BDDC_CUDA(cudaMemset(ex_stats.p, 0, sizeof(unsigned long long) * ex_stats.n));
-            for (int t = 0; t < kFlagTypes; ++t) desc[t].stats = ex_stats.p + 3 * t;
+            for (int t = 0; t < kFlagTypes; ++t) desc[t].stats = ex_stats.p + 8 * t;
         }
         // flatten every descriptor's puts over its peers (one parallel loop in the kernel)
         std::vector<double*> dst_all;
@@ -611,6 +695,124 @@ struct GpuContext::Impl {
                 }
             first[t + 1] = dst_all.size();
         }
+        // fused LL exchanges: every sent value's destination word pair in the peer's LL buffer,
+        // bucketed by the CTA of the producing kernel that writes its source value
+        {
+            auto peer_ll = [&](int q, int region, std::int64_t word) {
+                return static_cast<ll_word*>(links->peer(q, 10)) +
+                       static_cast<std::int64_t>(tbl[q * row + world * kCols + region]) + word;
+            };
+            std::vector<std::int32_t> all_src, all_cta;
+            std::vector<ll_word*> all_dst;
+            auto add_type = [&](int t, const std::vector<std::int32_t>& src, const std::vector<ll_word*>& dst,
+                                const std::vector<std::int32_t>& writer, int grid, bool need_writer) {
+                std::vector<std::int32_t> cta(src.size());
+                for (std::size_t i = 0; i < src.size(); ++i) {
+                    std::int32_t w = src[i] >= 0 && src[i] < static_cast<std::int32_t>(writer.size()) ? writer[src[i]] : -1;
+                    if (w < 0) {
+                        if (need_writer) throw std::logic_error("fused exchange: a sent value has no producing CTA");
+                        w = 0;  // never written (constant): any CTA may send it
+                    }
+                    cta[i] = w;
+                }
+                std::vector<std::size_t> ord(src.size());
+                for (std::size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+                std::stable_sort(ord.begin(), ord.end(), [&](std::size_t x, std::size_t y) { return cta[x] < cta[y]; });
+                const std::int32_t base = static_cast<std::int32_t>(all_src.size());
+                std::vector<std::int32_t> ptr(grid + 1, 0);
+                for (std::size_t i : ord) {
+                    all_src.push_back(src[i]);
+                    all_dst.push_back(dst[i]);
+                    ++ptr[cta[i] + 1];
+                }
+                ptr[0] = base;
+                for (int b = 0; b < grid; ++b) ptr[b + 1] += ptr[b];
+                ll_cta_off[t] = static_cast<std::int64_t>(all_cta.size());
+                all_cta.insert(all_cta.end(), ptr.begin(), ptr.end());
+                ll_has[t] = true;
+            };
+            auto neighbour_items = [&](int region, const std::vector<int>& peers, const std::vector<index_t>& soff,
+                                       const std::vector<index_t>& ids, int col, std::vector<std::int32_t>& src,
+                                       std::vector<ll_word*>& dst) {
+                for (std::size_t k = 0; k < peers.size(); ++k) {
+                    const int q = peers[k];
+                    const double rel = tbl[q * row + me * kCols + col];
+                    if (rel < 0) throw std::logic_error("rank plan: peer does not expect this rank's values");
+                    for (index_t i = soff[k]; i < soff[k + 1]; ++i) {
+                        src.push_back(static_cast<std::int32_t>(ids[i]));
+                        dst.push_back(peer_ll(q, region, 2 * (static_cast<std::int64_t>(rel) + i - soff[k])));
+                    }
+                }
+            };
+            // writers: solve0 CTAs (u0), harmonic-solve CTAs (z, incl. the interface values
+            // written by the lowest owner's first CTA), restrict CTAs (c_i), K_i CTAs (h_i)
+            const std::size_t nvec = U.n;
+            std::vector<std::int32_t> wu(nvec, -1), wz(nvec, -1);
+            for (std::size_t q = 0; q < img.solve.parts.size(); ++q) {
+                const PartDesc& pd = img.solve.parts[q];
+                for (int l = 0; l < pd.n_write; ++l) wu[img.solve.gmap[pd.gmap + l]] = static_cast<std::int32_t>(q);
+            }
+            for (std::size_t q = 0; q < img.harm.parts.size(); ++q) {
+                const PartDesc& pd = img.harm.parts[q];
+                for (int l = 0; l < pd.n_write; ++l) wz[img.harm.gmap[pd.gmap + l]] = static_cast<std::int32_t>(q);
+                if (pd.rank != 0) continue;
+                const SubdomainDesc& sd = img.subs[pd.sub];
+                for (int g = 0; g < sd.n_iface; ++g)
+                    if (img.iface_writer[sd.iface + g]) wz[img.iface_dof[sd.iface + g]] = static_cast<std::int32_t>(q);
+            }
+            std::vector<std::int32_t> wc(std::max<std::int64_t>(img.cbuf_total, 1), -1);
+            std::vector<std::int32_t> wh(std::max<std::int64_t>(img.hbuf_total, 1), -1);
+            const int bps = opt.local_blocks;
+            for (std::size_t b = 0; b < img.subs.size(); ++b) {
+                const SubdomainDesc& sd = img.subs[b];
+                for (int j = 0; j < sd.n_primal; ++j) wc[sd.cbuf + j] = static_cast<std::int32_t>(b);
+                const int rows_per = (sd.n_iface + bps - 1) / bps;
+                for (int g = 0; g < sd.n_iface; ++g) wh[sd.hbuf + g] = static_cast<std::int32_t>(b * bps + g / rows_per);
+            }
+            const int nsub = static_cast<int>(img.subs.size());
+            {
+                std::vector<std::int32_t> src;
+                std::vector<ll_word*> dst;
+                neighbour_items(0, P.halo_peers, P.halo_send_off, P.halo_send_idx, 2, src, dst);
+                add_type(kExU, src, dst, wu, static_cast<int>(img.solve.parts.size()), false);
+            }
+            if (!img.harm.parts.empty()) {
+                std::vector<std::int32_t> src;
+                std::vector<ll_word*> dst;
+                neighbour_items(1, P.halo_peers, P.halo_send_off, P.halo_send_idx, 2, src, dst);
+                add_type(kExZ, src, dst, wz, static_cast<int>(img.harm.parts.size()), true);
+            }
+            {
+                std::vector<std::int32_t> src;
+                std::vector<ll_word*> dst;
+                neighbour_items(2, P.iface_peers, P.iface_send_off, P.iface_send_slot, 3, src, dst);
+                add_type(kExH, src, dst, wh, nsub * bps, true);
+            }
+            {
+                std::vector<std::int32_t> src;
+                std::vector<ll_word*> dst;
+                for (int q = 0; q < world; ++q) {
+                    if (q == me) continue;
+                    for (std::int32_t i = 0; i < P.cbuf_pad; ++i) {
+                        src.push_back(me * P.cbuf_pad + i);
+                        dst.push_back(peer_ll(q, 3, 2 * (static_cast<std::int64_t>(me) * P.cbuf_pad + i)));
+                    }
+                }
+                add_type(kExC, src, dst, wc, nsub, false);
+            }
+            std::vector<ll_word*> sc;
+            for (int r = 0; r < 3; ++r)
+                for (int q = 0; q < world; ++q)
+                    if (q != me) sc.push_back(peer_ll(q, 4, 2 * (static_cast<std::int64_t>(r) * world + me)));
+            ll_src.upload(all_src);
+            ll_cta.upload(all_cta);
+            ll_dst.alloc(std::max<std::size_t>(all_dst.size(), 1));
+            if (!all_dst.empty())
+                BDDC_CUDA(cudaMemcpy(ll_dst.p, all_dst.data(), sizeof(ll_word*) * all_dst.size(), cudaMemcpyHostToDevice));
+            ll_sc_dst.alloc(std::max<std::size_t>(sc.size(), 1));
+            if (!sc.empty())
+                BDDC_CUDA(cudaMemcpy(ll_sc_dst.p, sc.data(), sizeof(ll_word*) * sc.size(), cudaMemcpyHostToDevice));
+        }
         ex_item_dst.alloc(std::max<std::size_t>(dst_all.size(), 1));
         if (!dst_all.empty())
             BDDC_CUDA(cudaMemcpy(ex_item_dst.p, dst_all.data(), sizeof(double*) * dst_all.size(), cudaMemcpyHostToDevice));
@@ -621,6 +823,12 @@ struct GpuContext::Impl {
             desc[t].item_src = ex_item_src.p + first[t];
         }
         ex_host = desc;
+        if (std::getenv("BDDC_FUSED_TRACE")) {
+            fused_trace.alloc(1 + 2 * (std::size_t(1) << 20));
+            BDDC_CUDA(cudaMemset(fused_trace.p, 0, sizeof(unsigned long long) * fused_trace.n));
+        }
+        ex_ticket.alloc(kFlagTypes);
+        BDDC_CUDA(cudaMemset(ex_ticket.p, 0, sizeof(unsigned int) * ex_ticket.n));
         BDDC_CUDA(cudaDeviceSynchronize());
     }
 
@@ -665,6 +873,30 @@ struct GpuContext::Impl {
             apply(rd, zd, s);
             apply_dot_r = nullptr;
         };
+        // exchanges riding on the producing / consuming kernels (device/fused_comm.cuh)
+        const bool fpcg = fused_pcg();
+        const bool frz = fused_dir && fused_dot && fused_apply() && (fused_ex & 4);
+        if (fpcg || frz) {
+            D.ll_sc = ll_buf.p + ll_off[4];
+            D.me = comm->rank();
+        }
+        if (fpcg) {
+            D.pub_pq = ll_publish(kExPQ, 5, nullptr);
+            ll_scalar(D.pub_pq, 0, part_a.p, D.grid, gath_a.p);
+            D.seq_pq = ex_seq.p + kExPQ;
+            D.pub_rr = ll_publish(kExRR, 6, nullptr);
+            ll_scalar(D.pub_rr, 1, part_b.p, D.grid, gath_b.p);
+            D.seq_rr = ex_seq.p + kExRR;
+        }
+        if (frz) {
+            D.seq_rz = ex_seq.p + kExZ;  // r.z travels with z's halo, under its tag
+            D.ll_z = ll_buf.p + ll_off[1];
+        }
+        pub_rz = frz;
+        struct ResetPub {
+            bool& f;
+            ~ResetPub() { f = false; }
+        } reset_pub{pub_rz};
         const double* rz_part = fused_dot ? part_rz.p : part_a.p;
         const int rz_grid = fused_dot ? launch.n_parts : D.grid;
         BDDC_CUDA(cudaMemsetAsync(xd, 0, sizeof(double) * n, s));
@@ -701,7 +933,7 @@ struct GpuContext::Impl {
         }
         if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
         if (fused_dir) {
-            gather_rz_with_z_halo(rz_part, rz_grid, s);
+            if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
             pcg_init_rho(D, s);
         } else {
             gather_partial(rz_part, rz_grid, gath_c.p, s);
@@ -725,7 +957,7 @@ struct GpuContext::Impl {
             apply_skip = nullptr;
             if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
             if (fused_dir) {
-                gather_rz_with_z_halo(rz_part, rz_grid, s);
+                if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
                 pcg_xpay(D, it, s);
             } else {
                 gather_partial(rz_part, rz_grid, gath_c.p, s);
@@ -735,9 +967,9 @@ struct GpuContext::Impl {
         };
         auto check_part = [&](int it) {
             pcg_spmv_dot(D, s);
-            gather_partial(part_a.p, D.grid, gath_a.p, s);
+            if (!fpcg) gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_update(D, it, s);
-            gather_partial(part_b.p, D.grid, gath_b.p, s);
+            if (!fpcg) gather_partial(part_b.p, D.grid, gath_b.p, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
         };
@@ -930,7 +1162,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     (void)nsm;
     // TMA unit size: the largest for which every warp gets at least two ring slots next to
     // the vectors (BDDC_UNIT_BYTES overrides, for experiments)
-    const int max_smem = max_solve_smem(I.device);
+    const int max_smem = max_solve_smem(I.device) - kSolveStaticSmemReserve;
     DeviceImage img;
     int unit = std::getenv("BDDC_UNIT_BYTES") ? std::atoi(std::getenv("BDDC_UNIT_BYTES")) : 4096;
     int spw = 0;
@@ -1045,7 +1277,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         I.ensure_pcg(1);
         BDDC_CUDA(cudaDeviceSynchronize());
         const char* p2p_env = std::getenv("BDDC_P2P");
-        if (!(p2p_env && std::atoi(p2p_env) == 0)) I.setup_peer_links();
+        if (!(p2p_env && std::atoi(p2p_env) == 0)) I.setup_peer_links(img);
     }
     BDDC_CUDA(cudaDeviceSynchronize());
 }
@@ -1224,6 +1456,12 @@ int GpuContext::device() const { return impl_->device; }
 void GpuContext::synchronize() { BDDC_CUDA(cudaStreamSynchronize(impl_->stream)); }
 std::int64_t GpuContext::solve_profile(std::int64_t* out, std::int64_t cap) {
     Impl& I = *impl_;
+    if (I.fused_trace.p) {  // fused-exchange event ring (BDDC_FUSED_TRACE)
+        const std::int64_t n = std::min<std::int64_t>(cap, static_cast<std::int64_t>(I.fused_trace.n));
+        BDDC_CUDA(cudaDeviceSynchronize());
+        BDDC_CUDA(cudaMemcpy(out, I.fused_trace.p, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+        return n;
+    }
     if (I.ex_stats.p) {  // exchange diagnostics take precedence (BDDC_EXCH_STATS)
         const std::int64_t n = std::min<std::int64_t>(cap, static_cast<std::int64_t>(I.ex_stats.n));
         BDDC_CUDA(cudaDeviceSynchronize());

@@ -20,14 +20,19 @@ constexpr int kRestrictThreads = 256;
 __global__ void __launch_bounds__(kRestrictThreads)
 iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const double* __restrict__ u0) {
     if (skip_launch(P.skip)) return;
+    const std::uint32_t tag_u = P.ll_u ? ll_tag(P.seq_u) : 0u;
     extern __shared__ double sg[];
     const SubdomainDesc& sd = P.subs[blockIdx.x];
     const int ng = sd.n_iface, np = sd.n_primal;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
         const int gid = P.iface_gid[sd.iface + g];
         double acc = 0.0;
-        for (int e = P.gi_row_ptr[gid]; e < P.gi_row_ptr[gid + 1]; ++e)
-            acc += P.gi_row_val[e] * u0[P.gi_row_col[e]];
+        for (int e = P.gi_row_ptr[gid]; e < P.gi_row_ptr[gid + 1]; ++e) {
+            const int col = P.gi_row_col[e];
+            const double u = (P.ll_u && col >= P.ll_u_base) ? ll_get(P.ll_u + 2 * static_cast<std::int64_t>(col - P.ll_u_base), tag_u)
+                                                           : u0[col];
+            acc += P.gi_row_val[e] * u;
+        }
         const double v = P.iface_w[sd.iface + g] * (r[P.iface_dof[sd.iface + g]] - acc);
         sg[g] = v;
         P.gbuf[sd.hbuf + g] = v;
@@ -41,6 +46,7 @@ iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const d
         acc = warp_sum(acc);
         if (lane == 0) P.cbuf[sd.cbuf + j] = acc;
     }
+    publish<kRestrictThreads>(P.pub_c);
 }
 
 constexpr int kCoarseThreads = 512;
@@ -90,9 +96,14 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
         // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
         // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
         const int nc = P.n_coarse;
+        const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
         for (int q = threadIdx.x; q < nc; q += blockDim.x) {
             double acc = 0.0;
-            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) acc += P.cbuf[P.c_own_ref[o]];
+            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) {
+                const int ref = P.c_own_ref[o];
+                acc += (P.ll_c && (ref < P.c_own_lo || ref >= P.c_own_hi)) ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref), tag_c)
+                                                                           : P.cbuf[ref];
+            }
             rc[q] = acc;
         }
         __syncthreads();
@@ -150,6 +161,7 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
             }
         }
     }
+    publish<kLocalThreads>(P.pub_h);
 }
 
 

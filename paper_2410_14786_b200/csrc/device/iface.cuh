@@ -1,11 +1,21 @@
 #pragma once
 
-#include "common.cuh"
+#include "fused_comm.cuh"
 
 namespace bddc_b200 {
 
 struct IfaceParams {
     const double* skip;  // pipelined PCG: skip when scal[2] / scal[3] is set (null: never)
+    // multi-GPU fused LL exchanges (null on one GPU): restrict reads the u0 halo (vector index
+    // >= ll_u_base) from its LL buffer and publishes the c_i; the K_i kernel reads the other
+    // ranks' c_i (outside [c_own_lo, c_own_hi)) from theirs and publishes the shared h_i
+    const ll_word* ll_u;
+    const std::uint64_t* seq_u;
+    int ll_u_base;
+    const ll_word* ll_c;
+    const std::uint64_t* seq_c;
+    int c_own_lo, c_own_hi;
+    Publish pub_c, pub_h;
     const SubdomainDesc* subs;
     int n_subdomains;
     int max_iface;

@@ -11,6 +11,18 @@ __device__ __forceinline__ double sum_partials(const double* part, int n, double
     return block_sum<kVecThreads>(v, scratch);
 }
 
+// Sum over ranks in rank order (same arithmetic as sum_partials over the gathered buffer): my
+// own value from red[me], the peers' from the LL scalar row (seq null: gathered buffer).
+__device__ __forceinline__ double sum_ranks(const PcgDevice& D, const double* red, int n, int row,
+                                            const std::uint64_t* seq, double* scratch) {
+    if (!seq) return sum_partials(red, n, scratch);
+    const std::uint32_t tag = ll_tag(seq);
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        v += i == D.me ? red[i] : ll_get(D.ll_sc + 2 * (static_cast<std::int64_t>(row) * n + i), tag);
+    return block_sum<kVecThreads>(v, scratch);
+}
+
 __global__ void __launch_bounds__(kVecThreads) dot_kernel(int n, const double* __restrict__ a,
                                                           const double* __restrict__ b, double* part) {
     __shared__ double scratch[kVecThreads / 32];
@@ -40,12 +52,13 @@ __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
+    publish<kVecThreads>(D.pub_pq);
 }
 
 __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
-    const double pq = sum_partials(D.red_a, D.red_a_n, scratch);
+    const double pq = sum_ranks(D, D.red_a, D.red_a_n, 0, D.seq_pq, scratch);
     if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
         if (blockIdx.x == 0 && threadIdx.x == 0) D.scal[3] = 1.0;
         return;
@@ -61,13 +74,14 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
+    publish<kVecThreads>(D.pub_rr);
 }
 
 __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
     if (D.scal[3] != 0.0) return;
-    const double rr = sum_partials(D.red_b, D.red_b_n, scratch);
+    const double rr = sum_ranks(D, D.red_b, D.red_b_n, 1, D.seq_rr, scratch);
     if (threadIdx.x == 0) {
         const double normb = D.scal[0];
         const double rel = sqrt(rr) / normb;
@@ -80,19 +94,23 @@ __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, i
 
 __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
-    const double rz = sum_partials(D.red_c, D.red_c_n, scratch);
+    const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     if (blockIdx.x == 0 && threadIdx.x == 0) D.rho[0] = rz;
+    const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x)
-        D.p[i] = D.z[i];
+        D.p[i] = (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : D.z[i];
 }
 
 __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
-    const double rz = sum_partials(D.red_c, D.red_c_n, scratch);
+    const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     const double beta = rz / D.rho[it - 1];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x)
-        D.p[i] = D.z[i] + beta * D.p[i];
+    const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x) {
+        const double zi = (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : D.z[i];
+        D.p[i] = zi + beta * D.p[i];
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         D.beta[it - 1] = beta;
         D.rho[it] = rz;

@@ -1,6 +1,6 @@
 #pragma once
 
-#include "common.cuh"
+#include "fused_comm.cuh"
 
 namespace bddc_b200 {
 
@@ -37,6 +37,17 @@ struct PcgDevice {
     double* scal;     // [0]=||b||, [1]=rel, [2]=converged flag, [3]=error code
     int* iter;        // device iteration counter: spmv_dot advances it, update/check/xpay read it
                       // (so one captured graph serves every iteration)
+    // multi-GPU, fused LL exchanges (null on one GPU): p.q published by spmv_dot and read by
+    // update, r.r published by update and read by check, r.z (+ the halo of z, entries >= n)
+    // published by the harmonic-extension solve and read by init_rho / xpay. ll_sc: scalar
+    // rows [p.q | r.r | r.z][rank] (word pairs); seq_*: the tags (null: gathered buffers)
+    Publish pub_pq, pub_rr;
+    const ll_word* ll_sc;
+    const ll_word* ll_z;
+    const std::uint64_t* seq_pq;
+    const std::uint64_t* seq_rr;
+    const std::uint64_t* seq_rz;
+    int me;
     double rtol, atol;
 };
 

@@ -231,7 +231,16 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 // subdomain (reference prolong_add order, preconditioner.cpp:168-169,189-190)
                 const int gid = S.iface_gid[sd.iface + g];
                 z = 0.0;
-                for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) z += S.hbuf[S.gi_own_ref[o]];
+                if (MODE == 3 && S.ll_h) {  // peers' h_i from the LL buffer (multi-GPU, fused)
+                    const std::uint32_t tag = ll_tag(S.seq_h);
+                    for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) {
+                        const int ref = S.gi_own_ref[o];
+                        z += ref >= S.ll_h_base ? ll_get(S.ll_h + 2 * static_cast<std::int64_t>(ref - S.ll_h_base), tag)
+                                                : S.hbuf[ref];
+                    }
+                } else {
+                    for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) z += S.hbuf[S.gi_own_ref[o]];
+                }
                 if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) {
                     const int dof = S.iface_dof[sd.iface + g];
                     S.out[dof] = z;
@@ -356,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         if (tid == 0) S.dot_part[blockIdx.x] = rz;
     }
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
+    if (MODE == 0 || MODE == 3) publish<kThreads>(S.pub);  // after the cluster barrier: non-last CTAs return
 }
 
 template <int MODE, int CLUSTER>

@@ -1,8 +1,14 @@
 #pragma once
 
+#include "fused_comm.cuh"
+
 #include "common.cuh"
 
 namespace bddc_b200 {
+
+// static shared memory of the solve kernel (reductions, fused-exchange bookkeeping), kept out
+// of the dynamic carve-up
+constexpr int kSolveStaticSmemReserve = 1024;
 
 struct SolveParams {
     const double* skip;  // pipelined PCG: skip when scal[2] / scal[3] is set (null: never)
@@ -38,6 +44,13 @@ struct SolveParams {
     int debug;     // timing experiments only: 1 = skip tile math
     long long* stats;  // diagnostics (BDDC_SOLVE_STATS): per CTA, per warp {total, mbarrier wait,
                        // CTA-barrier wait, units} cycles of the launch; null = off
+    // multi-GPU fused LL exchanges (null on one GPU): MODE 0 publishes the halo of u0; MODE 3
+    // reads the peers' h_i (hbuf slots >= ll_h_base) from its LL buffer and publishes the halo
+    // of z with r.z
+    Publish pub;
+    const ll_word* ll_h;
+    const std::uint64_t* seq_h;
+    int ll_h_base;
 };
 
 struct SolveLaunch {
