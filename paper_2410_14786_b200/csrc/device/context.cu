@@ -129,6 +129,9 @@ struct GpuContext::Impl {
     DBuf<double> x, r, z, p, q, part_a, part_b, rho, alpha, beta, hist, scal;
     DBuf<int> iter_ctr;
     double* pinned = nullptr;
+    double* pinned_dev = nullptr;  // the same buffer, mapped (update's fused check writes it)
+    DBuf<std::uint64_t> solo_seq;  // one GPU: the grid ticket of update's fused check
+    DBuf<unsigned int> solo_ticket;
     int max_it_alloc = 0;
 
     std::int32_t max_iface = 0, max_primal = 0, n_coarse = 0, n_gi = 0;
@@ -550,6 +553,11 @@ struct GpuContext::Impl {
             scal.alloc(8);
             iter_ctr.alloc(1);
             BDDC_CUDA(cudaMallocHost(&pinned, sizeof(double) * 8));
+            BDDC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pinned_dev), pinned, 0));
+            solo_seq.alloc(1);
+            BDDC_CUDA(cudaMemset(solo_seq.p, 0, sizeof(std::uint64_t)));
+            solo_ticket.alloc(1);
+            BDDC_CUDA(cudaMemset(solo_ticket.p, 0, sizeof(unsigned int)));
         }
         if (max_it > max_it_alloc) {
             rho.alloc(max_it + 1);
@@ -892,6 +900,20 @@ struct GpuContext::Impl {
             D.seq_rz = ex_seq.p + kExZ;  // r.z travels with z's halo, under its tag
             D.ll_z = ll_buf.p + ll_off[1];
         }
+        // convergence check in update's last CTA, flags straight to pinned host memory
+        const bool fcheck = !dist() || fpcg;
+        if (fcheck) {
+            D.fuse_check = 1;
+            D.host_scal = pinned_dev;
+            if (!dist()) {  // grid ticket + the r.r reduction only (no peers)
+                D.pub_rr.seq = solo_seq.p;
+                D.pub_rr.ticket = solo_ticket.p;
+                D.pub_rr.part = part_b.p;
+                D.pub_rr.red = gath_b.p;
+                D.pub_rr.grid = D.grid;
+                D.pub_rr.slot = 0;
+            }
+        }
         pub_rz = frz;
         struct ResetPub {
             bool& f;
@@ -969,6 +991,7 @@ struct GpuContext::Impl {
             pcg_spmv_dot(D, s);
             if (!fpcg) gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_update(D, it, s);
+            if (fcheck) return;
             if (!fpcg) gather_partial(part_b.p, D.grid, gath_b.p, s);
             pcg_check(D, it, s);
             BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
@@ -985,7 +1008,16 @@ struct GpuContext::Impl {
                     capture_events = graph_events.get();
                 }
                 try {
-                    graphs.b = capture(s, [&] { next_direction(0); }, &graphs.b_kernels, &gb);
+                    // one graph per pipelined iteration: check part, the read-back event (a
+                    // record node), then the speculative next direction
+                    graphs.b = capture(
+                        s,
+                        [&] {
+                            check_part(0);
+                            BDDC_CUDA(cudaEventRecordWithFlags(check_ev.e, s, cudaEventRecordExternal));
+                            next_direction(0);
+                        },
+                        &graphs.b_kernels, &gb);
                 } catch (...) {
                     capture_events = nullptr;
                     throw;
@@ -1025,17 +1057,18 @@ struct GpuContext::Impl {
             g_kernel_launches.fetch_add(graphs.b_kernels);
         };
         for (int it = 1; it <= o.max_iterations; ++it) {
-            if (graphed) {
-                BDDC_CUDA(cudaGraphLaunch(graphs.a, s));
-                g_kernel_launches.fetch_add(graphs.a_kernels);
-            } else {
-                check_part(it);
-            }
-            BDDC_CUDA(cudaEventRecord(check_ev.e, s));
             const bool spec = pipelined && it < o.max_iterations;
-            if (spec) {
-                if (graphed) launch_b();
-                else next_direction(it);
+            if (graphed && spec) {
+                launch_b();  // check part + read-back event + speculative next direction
+            } else {
+                if (graphed) {
+                    BDDC_CUDA(cudaGraphLaunch(graphs.a, s));
+                    g_kernel_launches.fetch_add(graphs.a_kernels);
+                } else {
+                    check_part(it);
+                }
+                BDDC_CUDA(cudaEventRecord(check_ev.e, s));
+                if (spec) next_direction(it);
             }
             BDDC_CUDA(cudaEventSynchronize(check_ev.e));
             if (pinned[3] == 1.0) {

@@ -85,9 +85,10 @@ __device__ __forceinline__ std::uint32_t ll_tag(const std::uint64_t* seq) {
 }
 
 // Call from EVERY thread of every CTA of the producer grid, after its last global writes.
+// Returns true in the grid's last CTA (after its tail: red[slot] holds the reduced scalar).
 template <int THREADS>
-__device__ __forceinline__ void publish(const Publish& P) {
-    if (P.seq == nullptr) return;
+__device__ __forceinline__ bool publish(const Publish& P) {
+    if (P.seq == nullptr) return false;
     __shared__ int last_s;
     __shared__ double red_s[THREADS / 32];
     const std::uint64_t t_in = P.trace ? gtimer() : 0;
@@ -104,7 +105,7 @@ __device__ __forceinline__ void publish(const Publish& P) {
         for (int i = __ldg(P.cta_ptr + b) + static_cast<int>(threadIdx.x); i < i1; i += THREADS)
             ll_store(P.item_dst[i], __ldcg(P.src + __ldg(P.item_src + i)), tag);
     }
-    if (!last_s) return;
+    if (!last_s) return false;
     if (threadIdx.x == 0) {
         *P.seq = tag;  // every CTA has read the old value (before its ticket)
         *P.ticket = 0u;
@@ -119,6 +120,8 @@ __device__ __forceinline__ void publish(const Publish& P) {
         if (static_cast<int>(threadIdx.x) < P.n_sc) ll_store(P.sc_dst[threadIdx.x], v, tag);
     }
     if (P.trace && threadIdx.x == 0) trace_event(P.trace, P.kid * 4 + 3, gtimer());
+    __syncthreads();
+    return true;
 }
 
 }  // namespace bddc_b200

@@ -78,7 +78,9 @@ constexpr int kLocalThreads = 256;
 constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads per lane)
 
 // h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each warp streams
-// kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight.
+// kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight. The K_i g_i
+// rows stream first (into shared memory): the coarse prologue (r_c, the x_c rows) is latency-
+// bound and then overlaps the other CTAs' streaming instead of delaying every CTA's first load.
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     if (skip_launch(P.skip)) return;
@@ -86,42 +88,17 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     const int sub = blockIdx.x / blocks_per_sub, part = blockIdx.x % blocks_per_sub;
     const SubdomainDesc& sd = P.subs[sub];
     const int ng = sd.n_iface, np = sd.n_primal;
+    const int nc = P.n_coarse;
     double* g = sm;
     double* xl = sm + ((ng + 1) & ~1);
     double* rc = xl + ((P.max_primal + 1) & ~1);
+    double* kg = rc + (with_coarse == 2 ? ((nc + 1) & ~1) : 0);  // this CTA's rows of K_i g_i
     for (int k = threadIdx.x; k < ng; k += blockDim.x) g[k] = P.gbuf[sd.hbuf + k];
-    if (with_coarse == 1) {
-        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
-    } else if (with_coarse == 2) {
-        // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
-        // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
-        const int nc = P.n_coarse;
-        const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
-        for (int q = threadIdx.x; q < nc; q += blockDim.x) {
-            double acc = 0.0;
-            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) {
-                const int ref = P.c_own_ref[o];
-                acc += (P.ll_c && (ref < P.c_own_lo || ref >= P.c_own_hi)) ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref), tag_c)
-                                                                           : P.cbuf[ref];
-            }
-            rc[q] = acc;
-        }
-        __syncthreads();
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int j = warp; j < np; j += kLocalThreads / 32) {
-            const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
-            double acc = 0.0;
-            for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
-            acc = warp_sum(acc);
-            if (lane == 0) xl[j] = acc;
-        }
-    }
     __syncthreads();
     const int rows_per = (ng + blocks_per_sub - 1) / blocks_per_sub;
     const int r0 = part * rows_per, r1 = min(ng, r0 + rows_per);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* K = P.kmat + sd.kmat;
-    const double* phig = P.phig + sd.phig;
     constexpr int kWarps = kLocalThreads / 32;
     for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += kWarps * kLocalRows) {
         const double* kr[kLocalRows];
@@ -151,14 +128,43 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
 #pragma unroll
         for (int q = 0; q < kLocalRows; ++q) {
             if (!live[q]) continue;  // warp-uniform
-            const int row = row0 + q;
             const double acc = warp_sum(a[q][0] + a[q][1]);
-            if (with_coarse) {
-                const double c = warp_sum(lane < np ? phig[row * np + lane] * xl[lane] : 0.0);
-                if (lane == 0) P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + acc);
-            } else if (lane == 0) {
-                P.hbuf[sd.hbuf + row] = acc;
+            if (lane == 0) {
+                if (with_coarse) kg[row0 + q - r0] = acc;
+                else P.hbuf[sd.hbuf + row0 + q] = acc;
             }
+        }
+    }
+    if (with_coarse == 1) {
+        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
+    } else if (with_coarse == 2) {
+        // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
+        // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
+        const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
+        for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+            double acc = 0.0;
+            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) {
+                const int ref = P.c_own_ref[o];
+                acc += (P.ll_c && (ref < P.c_own_lo || ref >= P.c_own_hi)) ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref), tag_c)
+                                                                           : P.cbuf[ref];
+            }
+            rc[q] = acc;
+        }
+        __syncthreads();
+        for (int j = warp; j < np; j += kWarps) {
+            const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
+            double acc = 0.0;
+            for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) xl[j] = acc;
+        }
+    }
+    if (with_coarse) {
+        __syncthreads();
+        const double* phig = P.phig + sd.phig;
+        for (int row = r0 + warp; row < r1; row += kWarps) {
+            const double c = warp_sum(lane < np ? phig[row * np + lane] * xl[lane] : 0.0);
+            if (lane == 0) P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + kg[row - r0]);
         }
     }
     publish<kLocalThreads>(P.pub_h);
@@ -351,7 +357,8 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
 
 void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse) {
     const std::size_t smem =
-        sizeof(double) * (P.max_iface + P.max_primal + 4 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0));
+        sizeof(double) * (P.max_iface + P.max_primal + 6 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0) +
+                          (P.max_iface + blocks_per_sub - 1) / blocks_per_sub);
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));

@@ -55,12 +55,31 @@ __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D
     publish<kVecThreads>(D.pub_pq);
 }
 
+// pcg.cpp:94-100: relative residual, history, convergence / failure flags (one thread)
+__device__ __forceinline__ void check_scalar(const PcgDevice& D, int it, double rr) {
+    if (D.scal[3] == 0.0) {
+        const double normb = D.scal[0];
+        const double rel = sqrt(rr) / normb;
+        D.hist[it] = rel;
+        D.scal[1] = rel;
+        if (!isfinite(rel)) D.scal[3] = 2.0;
+        if (rel <= D.rtol || (D.atol > 0.0 && rel * normb <= D.atol)) D.scal[2] = 1.0;
+    }
+    if (D.host_scal) {
+        volatile double* h = D.host_scal;
+        for (int k = 0; k < 4; ++k) h[k] = D.scal[k];
+    }
+}
+
 __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
     const double pq = sum_ranks(D, D.red_a, D.red_a_n, 0, D.seq_pq, scratch);
     if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
-        if (blockIdx.x == 0 && threadIdx.x == 0) D.scal[3] = 1.0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            D.scal[3] = 1.0;
+            if (D.host_scal) reinterpret_cast<volatile double*>(D.host_scal)[3] = 1.0;
+        }
         return;
     }
     const double alpha = D.rho[it - 1] / pq;
@@ -74,22 +93,20 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
-    publish<kVecThreads>(D.pub_rr);
+    const bool last = publish<kVecThreads>(D.pub_rr);
+    if (D.fuse_check && last) {  // check_kernel's work, in the grid's last CTA
+        const double rr = D.seq_rr ? sum_ranks(D, D.red_b, D.red_b_n, 1, D.seq_rr, scratch) : D.pub_rr.red[0];
+        if (threadIdx.x == 0) check_scalar(D, it, rr);
+    }
 }
 
 __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int) {
+    // (fuse_check: done by update_kernel's last CTA)
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
     if (D.scal[3] != 0.0) return;
     const double rr = sum_ranks(D, D.red_b, D.red_b_n, 1, D.seq_rr, scratch);
-    if (threadIdx.x == 0) {
-        const double normb = D.scal[0];
-        const double rel = sqrt(rr) / normb;
-        D.hist[it] = rel;
-        D.scal[1] = rel;
-        if (!isfinite(rel)) D.scal[3] = 2.0;
-        if (rel <= D.rtol || (D.atol > 0.0 && rel * normb <= D.atol)) D.scal[2] = 1.0;
-    }
+    if (threadIdx.x == 0) check_scalar(D, it, rr);
 }
 
 __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {

@@ -48,6 +48,10 @@ struct PcgDevice {
     const std::uint64_t* seq_rr;
     const std::uint64_t* seq_rz;
     int me;
+    // convergence check fused into update's last CTA (r.r reduced there; peers' r.r from the LL
+    // row), scal[0..3] written straight to mapped pinned host memory (null: check kernel + copy)
+    double* host_scal;
+    int fuse_check;
     double rtol, atol;
 };
 
