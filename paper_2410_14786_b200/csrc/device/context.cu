@@ -130,8 +130,12 @@ struct GpuContext::Impl {
     DBuf<int> iter_ctr;
     double* pinned = nullptr;
     double* pinned_dev = nullptr;  // the same buffer, mapped (update's fused check writes it)
-    DBuf<std::uint64_t> solo_seq;  // one GPU: the grid ticket of update's fused check
+    DBuf<std::uint64_t> solo_seq;  // one GPU: grid tickets of update's fused check and dir_spmv
     DBuf<unsigned int> solo_ticket;
+    DBuf<double> p_alt;            // second direction buffer (pcg_dir_spmv)
+    // BDDC_DIR_SPMV=1: fuse p = z + beta p into the SpMV. Off by default: measured on B200 the
+    // on-the-fly p entries (two extra gathers per nonzero) cost more than the xpay pass saves
+    bool use_dir_spmv = std::getenv("BDDC_DIR_SPMV") && std::atoi(std::getenv("BDDC_DIR_SPMV")) == 1;
     int max_it_alloc = 0;
 
     std::int32_t max_iface = 0, max_primal = 0, n_coarse = 0, n_gi = 0;
@@ -542,7 +546,7 @@ struct GpuContext::Impl {
     void ensure_pcg(int max_it) {
         const index_t n = pb.decomposition.global_dofs;
         if (!x.p) {
-            for (DBuf<double>* b : {&x, &r, &z, &p, &q}) b->alloc(n);
+            for (DBuf<double>* b : {&x, &r, &z, &p, &q, &p_alt}) b->alloc(n);
             const int g = pcg_grid_for(dist() ? n_rows : n);
             part_a.alloc(g);
             part_b.alloc(g);
@@ -554,10 +558,10 @@ struct GpuContext::Impl {
             iter_ctr.alloc(1);
             BDDC_CUDA(cudaMallocHost(&pinned, sizeof(double) * 8));
             BDDC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pinned_dev), pinned, 0));
-            solo_seq.alloc(1);
-            BDDC_CUDA(cudaMemset(solo_seq.p, 0, sizeof(std::uint64_t)));
-            solo_ticket.alloc(1);
-            BDDC_CUDA(cudaMemset(solo_ticket.p, 0, sizeof(unsigned int)));
+            solo_seq.alloc(2);
+            BDDC_CUDA(cudaMemset(solo_seq.p, 0, sizeof(std::uint64_t) * 2));
+            solo_ticket.alloc(2);
+            BDDC_CUDA(cudaMemset(solo_ticket.p, 0, sizeof(unsigned int) * 2));
         }
         if (max_it > max_it_alloc) {
             rho.alloc(max_it + 1);
@@ -914,6 +918,16 @@ struct GpuContext::Impl {
                 D.pub_rr.slot = 0;
             }
         }
+        // p = z + beta p fused into the next iteration's SpMV (no xpay pass, no init_rho)
+        const bool dirspmv = use_dir_spmv && precondition && fused_dot && (!dist() || frz);
+        if (dirspmv) {
+            D.fuse_dir = 1;
+            D.p_alt = p_alt.p;
+            if (!D.pub_pq.seq) {  // grid ticket only: the last CTA advances the iteration counter
+                D.pub_pq.seq = solo_seq.p + 1;
+                D.pub_pq.ticket = solo_ticket.p + 1;
+            }
+        }
         pub_rz = frz;
         struct ResetPub {
             bool& f;
@@ -954,7 +968,9 @@ struct GpuContext::Impl {
             check_coarse(s);
         }
         if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-        if (fused_dir) {
+        if (dirspmv) {
+            // rho[0] and p_1 = z are formed by the first dir_spmv
+        } else if (fused_dir) {
             if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
             pcg_init_rho(D, s);
         } else {
@@ -978,7 +994,9 @@ struct GpuContext::Impl {
             if (precondition) apply_rz();
             apply_skip = nullptr;
             if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-            if (fused_dir) {
+            if (dirspmv) {
+                // p = z + beta p happens inside the next dir_spmv
+            } else if (fused_dir) {
                 if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
                 pcg_xpay(D, it, s);
             } else {
@@ -988,7 +1006,8 @@ struct GpuContext::Impl {
             }
         };
         auto check_part = [&](int it) {
-            pcg_spmv_dot(D, s);
+            if (dirspmv) pcg_dir_spmv(D, s);
+            else pcg_spmv_dot(D, s);
             if (!fpcg) gather_partial(part_a.p, D.grid, gath_a.p, s);
             pcg_update(D, it, s);
             if (fcheck) return;
@@ -1095,9 +1114,11 @@ struct GpuContext::Impl {
                     check_coarse(s);
                 }
                 if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-                gather_partial(rz_part, rz_grid, gath_c.p, s);
-                pcg_xpay(D, it, s);
-                halo_exchange(p.p, s);
+                if (!dirspmv) {
+                    gather_partial(rz_part, rz_grid, gath_c.p, s);
+                    pcg_xpay(D, it, s);
+                    halo_exchange(p.p, s);
+                }
             }
         }
         rep.final_relative_residual = rel;

@@ -15,7 +15,7 @@
 namespace bddc_b200 {
 namespace {
 
-constexpr int kRestrictThreads = 256;
+constexpr int kRestrictThreads = 512;  // one interface dof per thread at C2 (n_G <= 400)
 
 __global__ void __launch_bounds__(kRestrictThreads)
 iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const double* __restrict__ u0) {
@@ -27,11 +27,26 @@ iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const d
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
         const int gid = P.iface_gid[sd.iface + g];
         double acc = 0.0;
-        for (int e = P.gi_row_ptr[gid]; e < P.gi_row_ptr[gid + 1]; ++e) {
-            const int col = P.gi_row_col[e];
-            const double u = (P.ll_u && col >= P.ll_u_base) ? ll_get(P.ll_u + 2 * static_cast<std::int64_t>(col - P.ll_u_base), tag_u)
-                                                           : u0[col];
-            acc += P.gi_row_val[e] * u;
+        // four entries per round: their column / value / u0 loads issue back to back; the sum
+        // stays sequential in CSR order
+        const int e0 = P.gi_row_ptr[gid], e1 = P.gi_row_ptr[gid + 1];
+        for (int e = e0; e < e1; e += 4) {
+            int col[4];
+            double val[4], u[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                col[q] = e + q < e1 ? P.gi_row_col[e + q] : -1;
+                val[q] = e + q < e1 ? P.gi_row_val[e + q] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                u[q] = col[q] < 0 ? 0.0
+                       : (P.ll_u && col[q] >= P.ll_u_base)
+                           ? ll_get(P.ll_u + 2 * static_cast<std::int64_t>(col[q] - P.ll_u_base), tag_u)
+                           : u0[col[q]];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (col[q] >= 0) acc += val[q] * u[q];
         }
         const double v = P.iface_w[sd.iface + g] * (r[P.iface_dof[sd.iface + g]] - acc);
         sg[g] = v;

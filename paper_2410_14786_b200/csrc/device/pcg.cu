@@ -71,6 +71,45 @@ __device__ __forceinline__ void check_scalar(const PcgDevice& D, int it, double 
     }
 }
 
+// pcg.cpp:101-104 + 74: beta = rz / rho, p_k = z + beta p_{k-1} (p_1 = z), q = A p_k, p.q.
+// Every row forms the p entries of its columns from z and p_{k-1} (the same expression as
+// xpay_kernel, so the iterates are bitwise those of the unfused loop); the distributed halo of
+// z comes from the LL buffer. The iteration counter is advanced by the grid's last CTA, after
+// every CTA has read it.
+__global__ void __launch_bounds__(kVecThreads) dir_spmv_kernel(const PcgDevice D) {
+    __shared__ double scratch[kVecThreads / 32];
+    const int km1 = *D.iter;  // k - 1
+    const int k = km1 + 1;
+    double* pn = (k & 1) ? D.p_alt : D.p;
+    const double* po = (k & 1) ? D.p : D.p_alt;
+    double beta = 0.0;
+    const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
+    if (km1 > 0) beta = rz / D.rho[km1 - 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        D.rho[km1] = rz;
+        if (km1 > 0) D.beta[km1 - 1] = beta;
+    }
+    const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
+    auto p_at = [&](int j) {
+        const double zj = (D.ll_z && j >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(j - D.n), tag) : D.z[j];
+        return km1 > 0 ? zj + beta * po[j] : zj;
+    };
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+        double y = 0.0;
+        for (int e = D.A_ptr[i]; e < D.A_ptr[i + 1]; ++e) y += D.A_val[e] * p_at(D.A_col[e]);
+        const double pi = p_at(i);
+        pn[i] = pi;
+        D.q[i] = y;
+        if (i < D.n_dot) acc = fma(pi, y, acc);
+    }
+    for (int i = D.n + blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x)
+        pn[i] = p_at(i);  // the halo of p_k (read as p_{k-1} next iteration)
+    acc = block_sum<kVecThreads>(acc, scratch);
+    if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
+    if (publish<kVecThreads>(D.pub_pq) && threadIdx.x == 0) *D.iter = k;
+}
+
 __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
     const int it = *D.iter;
@@ -84,9 +123,10 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     }
     const double alpha = D.rho[it - 1] / pq;
     if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[it - 1] = alpha;
+    const double* p = (D.fuse_dir && (it & 1)) ? D.p_alt : D.p;
     double acc = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
-        D.x[i] += alpha * D.p[i];
+        D.x[i] += alpha * p[i];
         const double ri = D.r[i] - alpha * D.q[i];
         D.r[i] = ri;
         if (i < D.n_dot) acc = fma(ri, ri, acc);
@@ -170,6 +210,10 @@ void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sq
 }
 void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
     spmv_dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    BDDC_LAUNCHED();
+}
+void pcg_dir_spmv(const PcgDevice& D, cudaStream_t s) {
+    dir_spmv_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
     BDDC_LAUNCHED();
 }
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s) {

@@ -52,6 +52,11 @@ struct PcgDevice {
     // row), scal[0..3] written straight to mapped pinned host memory (null: check kernel + copy)
     double* host_scal;
     int fuse_check;
+    // p = z + beta p fused into the next SpMV (pcg_dir_spmv; no xpay pass): p_k lives in p (k
+    // even) / p_alt (k odd), each row forms the p entries it reads on the fly from z and
+    // p_{k-1}; the grid's last CTA advances the iteration counter
+    double* p_alt;
+    int fuse_dir;
     double rtol, atol;
 };
 
@@ -61,6 +66,7 @@ void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part,
 // scal[slot] = sqrt(sum part) (sqrt=true) or sum part
 void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sqrt, cudaStream_t s);
 void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s);           // q = A p ; part_a = p.q (owned rows)
+void pcg_dir_spmv(const PcgDevice& D, cudaStream_t s);           // p = z + beta p ; q = A p ; part_a = p.q
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s);     // x += a p ; r -= a q ; part_b = r.r
 void pcg_check(const PcgDevice& D, int it, cudaStream_t s);      // hist[it], converged flag
 void pcg_init_rho(const PcgDevice& D, cudaStream_t s);           // rho[0] = sum part_a ; p = z
