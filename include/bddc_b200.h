@@ -191,6 +191,10 @@ int bddc_problem_poisson(int32_t cells_x, int32_t cells_y, int32_t kx, int32_t k
 int bddc_problem_from_view(const bddc_problem_view* view, bddc_problem** out);
 int bddc_problem_get_view(const bddc_problem* p, bddc_problem_view* view);
 int bddc_problem_export_bundle(const bddc_problem* p, const char* directory);
+/* Reads a reference bundle (manifest + Matrix Market locals + maps + classes + rhs) into a
+ * problem: replaces bddc::ingest_bundle (include/bddc/bundle.hpp, src/bundle.cpp:113-290) with
+ * the same validation messages; no coordinates (the factorisation orders by graph). */
+int bddc_problem_ingest_bundle(const char* manifest_path, bddc_problem** out);
 void bddc_problem_destroy(bddc_problem* p);
 
 /* ---- host setup only (no GPU; used by CPU tests and tooling) ---- */

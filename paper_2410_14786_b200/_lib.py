@@ -101,6 +101,7 @@ SIGNATURES = {
     "bddc_problem_from_view": (C.c_int, [P(ProblemView), P(vp)]),
     "bddc_problem_get_view": (C.c_int, [vp, P(ProblemView)]),
     "bddc_problem_export_bundle": (C.c_int, [vp, C.c_char_p]),
+    "bddc_problem_ingest_bundle": (C.c_int, [C.c_char_p, P(vp)]),
     "bddc_problem_destroy": (None, [vp]),
     "bddc_host_setup_create": (C.c_int, [vp, P(GpuOptions), P(vp)]),
     "bddc_host_setup_blocks": (C.c_int, [vp, i32, pd, pd, pd]),

@@ -308,6 +308,21 @@ int bddc_problem_export_bundle(const bddc_problem* p, const char* directory) {
     });
 }
 
+int bddc_problem_ingest_bundle(const char* manifest_path, bddc_problem** out) {
+    return guarded([&] {
+        if (!manifest_path || !out) throw std::invalid_argument("bddc_problem_ingest_bundle: null argument");
+        IngestedProblem ing = ingest_bundle(manifest_path);
+        auto p = std::make_unique<bddc_problem>();
+        p->data.decomposition = std::move(ing.decomposition);
+        p->data.local_matrices = std::move(ing.local_matrices);
+        p->data.constraints = std::move(ing.constraints);
+        p->data.global_matrix = std::move(ing.global_matrix);
+        p->rhs = std::move(ing.rhs);
+        p->flatten();
+        *out = p.release();
+    });
+}
+
 void bddc_problem_destroy(bddc_problem* p) { delete p; }
 
 int bddc_host_setup_create(const bddc_problem* p, const bddc_gpu_options* opt, bddc_host_setup** out) {

@@ -84,4 +84,21 @@ std::vector<double> study_rhs(index_t n, std::uint64_t seed);
 std::string export_bundle(const Decomposition& d, const std::vector<CsrMatrix>& locals,
                           const std::vector<double>& rhs, const std::string& directory);
 
+// Matrix Market "coordinate real general|symmetric" (reference src/matrix_market.cpp:23-71):
+// 1-based entries, symmetric files mirrored, duplicates summed in file order (from_triplets).
+CsrMatrix read_matrix_market_file(const std::string& path);
+
+// Bundle ingestion (reference src/bundle.cpp:113-290): manifest keys, rhs / classes / maps /
+// Matrix Market locals, multiplicity validation with the reference's messages, stable
+// interior-first reorder of every map (and its matrix), weights 1/multiplicity, constraints and
+// the global matrix rebuilt from the locals.
+struct IngestedProblem {
+    Decomposition decomposition;
+    std::vector<CsrMatrix> local_matrices;
+    ConstraintSet constraints;
+    CsrMatrix global_matrix;
+    std::vector<double> rhs;
+};
+IngestedProblem ingest_bundle(const std::string& manifest_path);
+
 }  // namespace bddc_b200

@@ -74,6 +74,14 @@ class Problem:
         return cls(h.value)
 
     @classmethod
+    def from_bundle(cls, manifest_path: str) -> "Problem":
+        """Reference bundle ingestion (src/bundle.cpp:113-290, `ingest_bundle`): the local
+        matrices, maps, classes and rhs of an external (e.g. openCARP-exported) problem."""
+        h = C.c_void_p()
+        L.check(L.lib().bddc_problem_ingest_bundle(manifest_path.encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
     def from_arrays(cls, global_matrix, local_matrices, subdomain_dofs, interior_counts, weights,
                     constraint_matrices, primal_maps, n_coarse, class_kind=None, class_entity=None,
                     multiplicity=None, rhs=None, coords=None) -> "Problem":

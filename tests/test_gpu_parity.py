@@ -147,6 +147,26 @@ def test_rectangular_and_heterogeneous_vs_reference(gpu, name):
         assert np.abs(pre.apply(p.rhs()) - g["apply_rhs"]).max() <= 1e-11 * np.abs(g["apply_rhs"]).max()
 
 
+@pytest.mark.parametrize("name", ["h4m8", "c5"])
+def test_ingested_bundle_vs_reference(gpu, name, tmp_path):
+    # the reference's bundle route end to end on the GPU — export, ingest
+    # with our reader (no coordinates: graph ordering for the factorisation), solve, compare
+    # with the reference run on the same bundle
+    g = golden(name)
+    cx, cy, kx, ky, dm, ks, seed = (int(v) for v in g["config"])
+    src = Problem.poisson(cx, kx, cy, ky, kappa_decades=dm / 1000.0, kappa_seed=ks, rhs_seed=seed)
+    p = Problem.from_bundle(src.export_bundle(str(tmp_path)))
+    assert p.coords() is None
+    x, rep = Preconditioner(p).pcg(p.rhs(), OPTS)
+    assert abs(rep.iterations - int(g["pcg_report"][0])) <= 1
+    assert history_err(rep.residual_history, g["pcg_history"]) <= (1e-7 if dm else 1e-10)
+    if "pcg_x" in g:
+        assert np.abs(x - g["pcg_x"]).max() <= 1e-10 * np.abs(g["pcg_x"]).max()
+    else:
+        stride = int(g["pcg_x_sample_stride"][0])
+        assert np.abs(x[::stride] - g["pcg_x_sample"]).max() <= 1e-10 * np.abs(g["pcg_x_sample"]).max()
+
+
 def test_c2_weak_point_vs_reference(gpu):
     g = golden("c2")
     p = Problem.poisson(800, 8)
