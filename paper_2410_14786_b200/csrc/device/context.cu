@@ -110,7 +110,12 @@ struct GpuContext::Impl {
             valid = !sp.parts.empty();
         }
     };
-    SolveProgram prog, harm;
+    SolveProgram prog, harm, head;
+    // split apply (head + harmonic programs, device/solve.cuh y_out / y_in): y0 = L^-1 r_I per
+    // part in local order; BDDC_SPLIT=0 keeps u0 from a full solve
+    DBuf<double> ybuf;
+    bool use_split = !(std::getenv("BDDC_SPLIT") && std::atoi(std::getenv("BDDC_SPLIT")) == 0);
+    bool split() const { return use_split && harm.valid && head.valid; }
     SolveLaunch launch;
     // interface data
     DBuf<SubdomainDesc> subs;
@@ -139,7 +144,8 @@ struct GpuContext::Impl {
     int max_it_alloc = 0;
 
     std::int32_t max_iface = 0, max_primal = 0, n_coarse = 0, n_gi = 0;
-    std::int64_t solve_stream_bytes = 0, harm_stream_bytes = 0, factor_vals = 0, harm_fwd_values = 0;
+    std::int64_t solve_stream_bytes = 0, harm_stream_bytes = 0, factor_vals = 0, harm_fwd_values = 0,
+                 head_bwd_values = 0;
     std::int64_t k_values = 0, phig_values = 0, ginnz = 0, couple_nnz = 0;
 
     KernelTimes times;
@@ -493,7 +499,9 @@ struct GpuContext::Impl {
         }
         const bool fused = fused_apply();
         if (E) record(E->e[0].e, s);
-        SolveParams sp = solve_params(r_dev, U.p);
+        const bool spl = split();
+        SolveParams sp = solve_params(r_dev, U.p, spl ? &head : nullptr);
+        if (spl) sp.y_out = ybuf.p;  // u0 only where A_GI reads it (pruned backward sweep)
         if (fused) sp.pub = ll_publish(kExU, 0, U.p);
         launch_interior_solve(sp, launch, 0, s);
         if (E) record(E->e[1].e, s);
@@ -523,6 +531,7 @@ struct GpuContext::Impl {
         if (E) record(E->e[2].e, s);
         if (harm.valid) {  // z_I = u0 - A_II^-1 A_IG z_G
             SolveParams hp = solve_params(r_dev, z_dev, &harm);
+            if (spl) hp.y_in = ybuf.p;  // z_I = L^-T (y0 - L^-1 A_IG z_G)
             if (apply_dot_r) {
                 hp.dot_r = apply_dot_r;
                 hp.dot_part = part_rz.p;
@@ -1263,6 +1272,16 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     };
     I.prog.upload(img.solve);
     I.harm.upload(img.harm);
+    I.head.upload(img.head);
+    if (I.head.valid) {
+        if (img.head.parts.size() != img.harm.parts.size()) throw std::logic_error("head/harmonic programs differ in parts");
+        for (std::size_t q = 0; q < img.head.parts.size(); ++q)
+            if (img.head.parts[q].gmap != img.harm.parts[q].gmap || img.head.parts[q].n_loc != img.harm.parts[q].n_loc)
+                throw std::logic_error("head/harmonic programs differ in local layout");
+        I.ybuf.alloc(std::max<std::size_t>(img.head.gmap.size(), 1));
+        BDDC_CUDA(cudaMemset(I.ybuf.p, 0, sizeof(double) * I.ybuf.n));
+        I.head_bwd_values = img.head.bwd_factor_values;
+    }
     if (std::getenv("BDDC_SOLVE_STATS")) {
         I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 8 + img.solve.max_phases);
         BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));
@@ -1491,7 +1510,11 @@ std::int64_t GpuContext::interior_apply_bytes() const {
     std::int64_t ni = 0;
     for (const auto& sub : I.setup.subs) ni += sub.n_interior;
     // solve 1: 2F values + rhs gather + solution write; solve 2: F + F_fwd(active) values + u0 read
-    // + z write (its rhs comes from the interface coupling, counted in couple_nnz)
+    // + z write (its rhs comes from the interface coupling, counted in couple_nnz). Split apply:
+    // solve 1 = F + F_bwd(active) + rhs gather + u0 write + y0 write, solve 2 = F_fwd + F + y0
+    // read + z write.
+    if (I.use_split && I.harm.valid && I.head.valid)
+        return 8 * (I.factor_vals + I.head_bwd_values + 3 * ni) + 8 * (I.harm_fwd_values + I.factor_vals + 2 * ni);
     return 8 * (2 * I.factor_vals + 2 * ni) + 8 * (I.factor_vals + I.harm_fwd_values + 2 * ni);
 }
 KernelTimes GpuContext::kernel_times() {

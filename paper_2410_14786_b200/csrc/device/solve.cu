@@ -267,9 +267,19 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     long long t_start = stats ? clock64() : 0, t_wait = 0, t_bar = 0, t_refill = 0, t_tiles = 0, n_tiles = 0;
     double acc = 0.0;
     int u = 0;  // next unit of this warp
+    bool split_done = !(MODE == 0 ? S.y_out : (MODE == 3 ? S.y_in : nullptr));
     for (int ph = 0; ph < n_phases; ++ph) {
         const int kind = pkind.get(ph, gtable + 2 * kSolveWarps, kPhaseStride);
         const int u_end = uend.get(ph, gtable + kSolveWarps + warp, kPhaseStride);
+        if (!split_done && (kind & kPhaseBackward)) {  // forward sweep complete: X = y (block-uniform)
+            split_done = true;
+            if (MODE == 0) {
+                for (int l = tid; l < n_loc; l += kThreads) S.y_out[pdr.gmap + l] = X[l];
+            } else {
+                for (int l = tid; l < n_loc; l += kThreads) X[l] = __ldg(S.y_in + pdr.gmap + l) - X[l];
+                __syncthreads();
+            }
+        }
         double* own = (kind & kPhaseBackward) ? X : T;
         double* other = (kind & kPhaseBackward) ? T : X;
         for (; u < u_end; ++u) {
@@ -351,7 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         for (int q = 0; q < 4; ++q)
             if (gi[q] >= 0) {
                 if (MODE == 3) {
-                    const double z = S.u0[gi[q]] - T[l0 + q * kThreads];  // z_I = u0 - extension
+                    // z_I = u0 - extension, or (split apply) the backward sweep's result itself
+                    const double z = S.y_in ? T[l0 + q * kThreads] : S.u0[gi[q]] - T[l0 + q * kThreads];
                     S.out[gi[q]] = z;
                     if (S.dot_part && gi[q] < S.n_dot) rz += S.dot_r[gi[q]] * z;
                 } else {

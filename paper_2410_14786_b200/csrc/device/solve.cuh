@@ -31,6 +31,12 @@ struct SolveParams {
     const double* in;
     double* out;
     const double* u0;  // MODE 3: the first interior solve's result (z_I = u0 - harmonic extension)
+    // Split apply (head program + harmonic program): MODE 0 stores its forward result y0 =
+    // L^-1 r_I (part-local order, at part.gmap) into y_out before the (pruned) backward sweep;
+    // MODE 3 with y_in forms y0 - L^-1 A_IG z_G before its backward sweep, whose result is z_I
+    // itself (one full backward sweep per apply instead of two). Null: off.
+    double* y_out;
+    const double* y_in;
     // MODE 3, fused PCG dot product: per CTA, sum of dot_r[i] * z[i] over the z entries it writes
     // with i < n_dot, into dot_part[blockIdx.x] (null: off)
     const double* dot_r;

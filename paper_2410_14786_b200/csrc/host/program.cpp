@@ -109,7 +109,10 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
 
         // interior-solve program (local dof -> vector index = the subdomain map)
         build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.solve);
-        if (harmonic) build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.harm, true);
+        if (harmonic) {
+            build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.harm, true);
+            build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.head, false, true);
+        }
     }
 
     if (plan) {

@@ -21,6 +21,7 @@ struct DeviceImage {
     std::vector<SubdomainDesc> subs;
     SolvePools solve;  // interior-solve parts
     SolvePools harm;   // harmonic-extension parts (pruned forward sweep; empty when disabled)
+    SolvePools head;   // the apply's first solve: full forward, pruned backward (with harm)
     int parts = 1;     // CTAs per subdomain in the interior solve
     std::vector<std::int32_t> iface_dof;     // per (subdomain, gamma): vector index
     std::vector<double> iface_w;             // weight

@@ -82,7 +82,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
 }  // namespace
 
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std::vector<index_t>& l2v, int sub,
-                         int P, int unit_bytes, SolvePools& pools, bool prune_forward) {
+                         int P, int unit_bytes, SolvePools& pools, bool prune_forward, bool prune_backward) {
     const auto& sn = F.snodes;
     const index_t nsn = static_cast<index_t>(sn.size());
     const index_t nI = F.n_interior;
@@ -90,7 +90,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
     // supernodes whose subtree holds an interior dof coupled to the interface (the rhs is zero
     // elsewhere, and so is the forward solution); the backward sweep stays complete.
     std::vector<char> fwd(nsn, 1);
-    if (prune_forward) {
+    if (prune_forward || prune_backward) {
         std::fill(fwd.begin(), fwd.end(), 0);
         for (index_t sidx = 0; sidx < nsn; ++sidx) {
             for (index_t c = sn[sidx].col_begin; c < sn[sidx].col_end && !fwd[sidx]; ++c) {
@@ -102,11 +102,17 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         for (index_t sidx = 0; sidx < nsn; ++sidx)  // postorder: children before parents
             if (fwd[sidx] && sn[sidx].parent >= 0) fwd[sn[sidx].parent] = 1;
     }
-    for (index_t sidx = 0; sidx < nsn; ++sidx)
-        if (fwd[sidx]) {
-            const std::int64_t ns = sn[sidx].size();
-            pools.fwd_factor_values += ns * (ns + 1) / 2 + static_cast<std::int64_t>(sn[sidx].n_interior_rows) * ns;
-        }
+    // active = coupled to the interface or an ancestor of such a supernode
+    const std::vector<char> active = fwd;
+    std::vector<char> bwdm(nsn, 1);
+    if (prune_backward) bwdm = active;
+    if (!prune_forward) std::fill(fwd.begin(), fwd.end(), 1);
+    for (index_t sidx = 0; sidx < nsn; ++sidx) {
+        const std::int64_t ns = sn[sidx].size();
+        const std::int64_t v = ns * (ns + 1) / 2 + static_cast<std::int64_t>(sn[sidx].n_interior_rows) * ns;
+        if (fwd[sidx]) pools.fwd_factor_values += v;
+        if (bwdm[sidx]) pools.bwd_factor_values += v;
+    }
     if (P < 1 || P > 2) throw std::invalid_argument("solve program: parts must be 1 or 2");
 
     // ---- tree and group assignment (P = 2: halves below the top separator chain)
@@ -453,6 +459,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         // ---------------- backward sweep: top chain, levels above the cut, then subtrees
         for (auto it = top.rbegin(); it != top.rend(); ++it) {
+            if (!bwdm[*it]) continue;
             Chunks b;
             kr = chunk_rows_for({sn[*it].size()});
             bwd(*it, b);
@@ -465,10 +472,10 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             Chunks a, b;
             std::vector<index_t> nrows;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == *hit) nrows.push_back(sn[s].size());
+                if (in_group(s) && !local[s] && sn[s].height == *hit && bwdm[s]) nrows.push_back(sn[s].size());
             kr = chunk_rows_for(nrows);
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == *hit) bwd(s, b);
+                if (in_group(s) && !local[s] && sn[s].height == *hit && bwdm[s]) bwd(s, b);
             kr = 32;
             (void)a;
             Phase pb2 = singles(std::move(b));
@@ -480,7 +487,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             ph.kind = kPhaseBackward | kPhaseChained;
             for (std::size_t j = 0; j < job_nodes.size(); ++j) {
                 Chunks job;
-                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it) bwd(*it, job);
+                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it)
+                    if (bwdm[*it]) bwd(*it, job);
                 ph.jobs.push_back(std::move(job));
             }
             phases.push_back(std::move(ph));

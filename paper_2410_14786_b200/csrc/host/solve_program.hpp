@@ -21,6 +21,7 @@ struct SolvePools {
     std::vector<PartDesc> parts;
     std::int64_t tile_values = 0;   // FP64 values in all tiles (incl. explicit zeros of diag tiles)
     std::int64_t fwd_factor_values = 0;  // factor values the forward sweep reads (all, unless pruned)
+    std::int64_t bwd_factor_values = 0;  // factor values the backward sweep reads (all, unless pruned)
     std::int64_t n_tiles = 0;
     std::int32_t max_loc = 0, max_top = 0, max_phases = 0, max_units = 0;
 };
@@ -30,8 +31,11 @@ struct SolvePools {
 // per-warp TMA units (and of each ring slot).
 // prune_forward: the harmonic-extension program (rhs supported on the interior dofs coupled
 // to the interface): forward tasks only for supernodes whose subtree holds such a dof.
+// prune_backward: the apply's first solve (full forward, y0 kept): the backward sweep only for
+// the supernodes that hold an interface-coupled dof or are ancestors of one — the same set —
+// so u0 is exact on the dofs A_GI reads and unspecified elsewhere.
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A_local,
                          const std::vector<index_t>& local_to_vec, int sub, int parts, int unit_bytes,
-                         SolvePools& pools, bool prune_forward = false);
+                         SolvePools& pools, bool prune_forward = false, bool prune_backward = false);
 
 }  // namespace bddc_b200

@@ -23,6 +23,7 @@ struct PartState {
     const PartDesc* pd;
     std::vector<double> T, X, Q;
     int ph = 0;
+    bool split_done = false;
 };
 
 void run_phase(const SolvePools& sp, PartState& st) {
@@ -137,8 +138,11 @@ extern "C" int bddc_sim_program_stats(int cells, int k, int parts, int leaf_size
     return 0;
 }
 
+// harm: 0 full program, 1 harmonic program, 2 head program (y0 -> ybuf, u0 -> out),
+// 3 harmonic program with y_in = ybuf (out = L^-T (y0 - L^-1 in)); the split hooks follow
+// device/solve.cu (applied at the first backward phase, X = forward result).
 static int sim_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size, int use_coords,
-                     int harm, const double* in, double* out, char* err, int errlen) {
+                     int harm, const double* in, double* out, char* err, int errlen, double* ybuf = nullptr) {
     try {
         PoissonProblem pp = assemble_poisson(cells_x, cells_y, kx, ky);
         ProblemData pb;
@@ -153,7 +157,7 @@ static int sim_solve(int cells_x, int cells_y, int kx, int ky, int parts, int le
                                            pb.coords.empty() ? nullptr : pb.coords.data(), 4, fo);
         const DeviceImage img = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
                                                    pb.global_matrix, setup, parts, 4096, nullptr, harm != 0);
-        const SolvePools& sp = harm ? img.harm : img.solve;
+        const SolvePools& sp = harm == 2 ? img.head : (harm ? img.harm : img.solve);
         for (std::size_t i0 = 0; i0 < sp.parts.size(); i0 += parts) {
             std::vector<PartState> st(parts);
             for (int c = 0; c < parts; ++c) {
@@ -174,6 +178,13 @@ static int sim_solve(int cells_x, int cells_y, int kx, int ky, int parts, int le
                     PartState& s = st[c];
                     while (s.ph < s.pd->n_phases) {
                         const std::int32_t* row = &sp.phases[s.pd->phases + s.ph * kPhaseStride];
+                        if ((harm == 2 || harm == 3) && !s.split_done && (row[2 * kSolveWarps] & kPhaseBackward)) {
+                            s.split_done = true;
+                            for (int l = 0; l < s.pd->n_loc; ++l) {
+                                if (harm == 2) ybuf[s.pd->gmap + l] = s.X[l];
+                                else s.X[l] = ybuf[s.pd->gmap + l] - s.X[l];
+                            }
+                        }
                         run_phase(sp, s);
                         ++s.ph;
                         progress = true;
@@ -209,6 +220,16 @@ static int sim_solve(int cells_x, int cells_y, int kx, int ky, int parts, int le
 extern "C" int bddc_sim_interior_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
                                        int use_coords, const double* in, double* out, char* err, int errlen) {
     return sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 0, in, out, err, errlen);
+}
+
+// Split apply: head program on r (u0 exact where the interface couples, y0 kept), then the
+// harmonic program on c with y_in: z = A_II^-1 (r - c).
+extern "C" int bddc_sim_split_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
+                                    int use_coords, const double* r, const double* c, double* u0, double* z,
+                                    char* err, int errlen) {
+    std::vector<double> y(static_cast<std::size_t>(cells_x + 1) * (cells_y + 1) * 2, 0.0);
+    if (sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 2, r, u0, err, errlen, y.data())) return 1;
+    return sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 3, c, z, err, errlen, y.data());
 }
 
 // The harmonic-extension program (pruned forward sweep) on an rhs supported on the interior

@@ -155,3 +155,32 @@ def test_harmonic_program_matches_full_solve(sim, k, m, parts, leaf, coords):
                                      out.ctypes.data_as(dp), err, 512)
     assert rc == 0, err.value
     assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("k,m,parts,leaf,coords", [(3, 6, 2, 16, 1), (4, 16, 2, 8, 0), (3, 32, 2, 24, 1),
+                                                   (3, 32, 1, 24, 1)])
+def test_split_apply_programs(sim, k, m, parts, leaf, coords):
+    # split apply: the head program (full forward, pruned backward) gives u0 = A_II^-1 r exactly
+    # on the interior dofs coupled to the interface and keeps y0 = L^-1 r; the harmonic program
+    # with y_in then returns z_I = A_II^-1 (r - A_IG v) from one backward sweep
+    prob, cs, _ = o.poisson_setup(k, m)
+    A = prob.global_matrix.scipy()
+    kinds = prob.decomposition.kind == o.INTERIOR
+    rng = np.random.default_rng(11)
+    n = A.shape[0]
+    r = np.where(kinds, rng.standard_normal(n), 0.0)
+    v = np.where(~kinds, rng.standard_normal(n), 0.0)
+    c = np.where(kinds, A @ v, 0.0)
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    ref_u0 = P.interior_correction(r)
+    ref_z = P.interior_correction(r - c)
+    coupled = kinds & (np.abs(A[:, np.flatnonzero(~kinds)]).sum(axis=1).A1 > 0)
+    u0, z = np.zeros(n), np.zeros(n)
+    err = C.create_string_buffer(512)
+    dp = C.POINTER(C.c_double)
+    rc = sim.bddc_sim_split_solve(k * m, k * m, k, k, parts, leaf, coords, r.ctypes.data_as(dp),
+                                  c.ctypes.data_as(dp), u0.ctypes.data_as(dp), z.ctypes.data_as(dp), err, 512)
+    assert rc == 0, err.value
+    assert coupled.sum() > 0
+    assert np.abs(u0[coupled] - ref_u0[coupled]).max() <= 1e-12 * np.abs(ref_u0).max()
+    assert np.abs(z[kinds] - ref_z[kinds]).max() <= 1e-12 * np.abs(ref_z).max()
