@@ -30,6 +30,31 @@ extern std::atomic<std::int64_t> g_kernel_launches;
         ::bddc_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     } while (0)
 
+// Programmatic dependent launch (PDL): the PCG loop's kernels are launched with programmatic
+// stream serialisation (launch_pdl), so a kernel's CTAs become resident while its predecessor
+// drains instead of after it. Each such kernel lets its own dependents launch at entry
+// (pdl_trigger) and waits for its predecessor (pdl_wait: that grid complete, its memory
+// visible; transitively every earlier grid) before it reads or writes anything a
+// predecessor touches. Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();  // BDDC_PDL=1 turns the attribute on
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    BDDC_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 // Speculative launches of the pipelined PCG loop pass the solver's scalar block: a set
 // converged (scal[2]) or error (scal[3]) flag turns the kernel into a no-op.
 __device__ __forceinline__ bool skip_launch(const double* scal) {

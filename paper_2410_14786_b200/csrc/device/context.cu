@@ -21,6 +21,12 @@
 namespace bddc_b200 {
 
 std::atomic<std::int64_t> g_kernel_launches{0};
+// BDDC_PDL=1: programmatic dependent launch for the PCG loop's kernels. Off by default:
+// measured on B200 inside the per-iteration CUDA graph it changed nothing (within noise).
+bool pdl_enabled() {
+    static const bool on = std::getenv("BDDC_PDL") && std::atoi(std::getenv("BDDC_PDL")) == 1;
+    return on;
+}
 
 namespace {
 

@@ -19,6 +19,8 @@ constexpr int kRestrictThreads = 512;  // one interface dof per thread at C2 (n_
 
 __global__ void __launch_bounds__(kRestrictThreads)
 iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const double* __restrict__ u0) {
+    pdl_trigger();
+    pdl_wait();
     if (skip_launch(P.skip)) return;
     const std::uint32_t tag_u = P.ll_u ? ll_tag(P.seq_u) : 0u;
     extern __shared__ double sg[];
@@ -98,6 +100,8 @@ constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads p
 // bound and then overlaps the other CTAs' streaming instead of delaying every CTA's first load.
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
+    pdl_trigger();
+    pdl_wait();
     if (skip_launch(P.skip)) return;
     extern __shared__ double sm[];
     const int sub = blockIdx.x / blocks_per_sub, part = blockIdx.x % blocks_per_sub;
@@ -356,7 +360,7 @@ void launch_iface_restrict(const IfaceParams& P, const double* r, const double* 
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    iface_restrict_kernel<<<P.n_subdomains, kRestrictThreads, smem, s>>>(P, r, u0);
+    launch_pdl(iface_restrict_kernel, P.n_subdomains, kRestrictThreads, smem, s, P, r, u0);
     BDDC_LAUNCHED();
 }
 
@@ -377,7 +381,7 @@ void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    iface_local_kernel<<<P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s>>>(P, blocks_per_sub, coarse);
+    launch_pdl(iface_local_kernel, P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s, P, blocks_per_sub, coarse);
     BDDC_LAUNCHED();
 }
 

@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(kVecThreads) finalize_kernel(const double* par
 
 __global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *D.iter += 1;  // read by the later kernels of this iteration
     double acc = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
@@ -78,6 +80,8 @@ __device__ __forceinline__ void check_scalar(const PcgDevice& D, int it, double 
 // every CTA has read it.
 __global__ void __launch_bounds__(kVecThreads) dir_spmv_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     const int km1 = *D.iter;  // k - 1
     const int k = km1 + 1;
     double* pn = (k & 1) ? D.p_alt : D.p;
@@ -112,6 +116,8 @@ __global__ void __launch_bounds__(kVecThreads) dir_spmv_kernel(const PcgDevice D
 
 __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     const int it = *D.iter;
     const double pq = sum_ranks(D, D.red_a, D.red_a_n, 0, D.seq_pq, scratch);
     if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
@@ -143,6 +149,8 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
 __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, int) {
     // (fuse_check: done by update_kernel's last CTA)
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     const int it = *D.iter;
     if (D.scal[3] != 0.0) return;
     const double rr = sum_ranks(D, D.red_b, D.red_b_n, 1, D.seq_rr, scratch);
@@ -151,6 +159,8 @@ __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, i
 
 __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     if (blockIdx.x == 0 && threadIdx.x == 0) D.rho[0] = rz;
     const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
@@ -160,6 +170,8 @@ __global__ void __launch_bounds__(kVecThreads) init_rho_kernel(const PcgDevice D
 
 __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, int) {
     __shared__ double scratch[kVecThreads / 32];
+    pdl_trigger();
+    pdl_wait();
     const int it = *D.iter;
     const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     const double beta = rz / D.rho[it - 1];
@@ -209,27 +221,27 @@ void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sq
     BDDC_LAUNCHED();
 }
 void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
-    spmv_dot_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    launch_pdl(spmv_dot_kernel, D.grid, kVecThreads, 0, s, D);
     BDDC_LAUNCHED();
 }
 void pcg_dir_spmv(const PcgDevice& D, cudaStream_t s) {
-    dir_spmv_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    launch_pdl(dir_spmv_kernel, D.grid, kVecThreads, 0, s, D);
     BDDC_LAUNCHED();
 }
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s) {
-    update_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
+    launch_pdl(update_kernel, D.grid, kVecThreads, 0, s, D, it);
     BDDC_LAUNCHED();
 }
 void pcg_check(const PcgDevice& D, int it, cudaStream_t s) {
-    check_kernel<<<1, kVecThreads, 0, s>>>(D, it);
+    launch_pdl(check_kernel, 1, kVecThreads, 0, s, D, it);
     BDDC_LAUNCHED();
 }
 void pcg_init_rho(const PcgDevice& D, cudaStream_t s) {
-    init_rho_kernel<<<D.grid, kVecThreads, 0, s>>>(D);
+    launch_pdl(init_rho_kernel, D.grid, kVecThreads, 0, s, D);
     BDDC_LAUNCHED();
 }
 void pcg_xpay(const PcgDevice& D, int it, cudaStream_t s) {
-    xpay_kernel<<<D.grid, kVecThreads, 0, s>>>(D, it);
+    launch_pdl(xpay_kernel, D.grid, kVecThreads, 0, s, D, it);
     BDDC_LAUNCHED();
 }
 void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,

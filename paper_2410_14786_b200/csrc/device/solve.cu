@@ -140,7 +140,7 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
 template <int MODE, int CLUSTER, bool STATS>
 __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    if (skip_launch(S.skip)) return;  // uniform over the cluster: every CTA reads the same flag
+    pdl_trigger();
     double rz = 0.0;  // MODE 3 with dot_part: this thread's share of r.z
     const PartDesc& pdr = S.parts[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -196,6 +196,13 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
     };
     for (int u = 0; u < nsl && u < nunits; ++u) fetch(u);
+    // everything above reads only the program (immutable): it overlaps the predecessor's tail
+    // under programmatic dependent launch; from here on the inputs are the predecessors'
+    pdl_wait();
+    if (skip_launch(S.skip)) {  // uniform over the cluster: every CTA reads the same flag
+        for (int u = 0; u < nsl && u < nunits; ++u) mbar_wait(&my_bars[u], 0);  // drain the prefetch
+        return;
+    }
 
     // ---- right-hand side (and, in MODE 1/2, the interface coupling)
     const std::int32_t* gmap = S.gmap + pdr.gmap;
@@ -388,13 +395,15 @@ void launch_one(const SolveParams& P, const SolveLaunch& L, cudaStream_t stream)
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = L.smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CLUSTER;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     BDDC_CUDA(cudaLaunchKernelEx(&cfg, kern, P));
 }
 
