@@ -63,6 +63,7 @@ __global__ void pack_kernel(int n, const std::int32_t* __restrict__ idx, const d
 __global__ void reduce_to_kernel(const double* part, int n, double* out, int take_sqrt) {
     __shared__ double scratch[8];
     double v = 0.0;
+#pragma unroll 8  // independent loads in flight; the sum order is unchanged
     for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
     v = block_sum<256>(v, scratch);
     if (threadIdx.x == 0) *out = take_sqrt ? sqrt(v) : v;

@@ -114,6 +114,7 @@ __device__ __forceinline__ bool publish(const Publish& P) {
     if (P.part) {
         __threadfence();  // every other CTA's partial is visible to the last one
         double v = 0.0;
+#pragma unroll 8  // independent loads in flight; the sum order is unchanged
         for (int i = threadIdx.x; i < P.grid; i += THREADS) v += __ldcg(P.part + i);
         v = block_sum<THREADS>(v, red_s);
         if (threadIdx.x == 0) P.red[P.slot] = v;

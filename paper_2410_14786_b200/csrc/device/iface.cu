@@ -94,10 +94,15 @@ coarse_direct_kernel(const IfaceParams P) {
 constexpr int kLocalThreads = 256;
 constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads per lane)
 
-// h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each warp streams
-// kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight. The K_i g_i
-// rows stream first (into shared memory): the coarse prologue (r_c, the x_c rows) is latency-
-// bound and then overlaps the other CTAs' streaming instead of delaying every CTA's first load.
+// h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each streaming warp
+// handles kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight;
+// the K_i g_i rows go to shared memory. With the fused coarse solve (with_coarse == 2) the last
+// one or two warps form r_c and this subdomain's x_c rows meanwhile (latency-bound gathers and
+// short GEMVs, hidden behind the stream), then every warp finishes its rows with Phi_G x_c.
+__device__ __forceinline__ void coarse_bar(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     pdl_trigger();
@@ -119,58 +124,71 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* K = P.kmat + sd.kmat;
     constexpr int kWarps = kLocalThreads / 32;
-    for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += kWarps * kLocalRows) {
-        const double* kr[kLocalRows];
-        bool live[kLocalRows];
+    const int cw = with_coarse == 2 ? (nc > 640 ? 2 : 1) : 0;  // coarse warps
+    const int sw = kWarps - cw;                                  // streaming warps
+    if (warp < sw) {
+        for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += sw * kLocalRows) {
+            const double* kr[kLocalRows];
+            bool live[kLocalRows];
 #pragma unroll
-        for (int q = 0; q < kLocalRows; ++q) {
-            live[q] = row0 + q < r1;
-            kr[q] = K + static_cast<std::size_t>(live[q] ? row0 + q : row0) * ng;
-        }
-        double a[kLocalRows][2] = {};
-        int k = lane;
-        for (; k + 32 < ng; k += 64) {
-            const double g0 = g[k], g1 = g[k + 32];
+            for (int q = 0; q < kLocalRows; ++q) {
+                live[q] = row0 + q < r1;
+                kr[q] = K + static_cast<std::size_t>(live[q] ? row0 + q : row0) * ng;
+            }
+            double a[kLocalRows][2] = {};
+            int k = lane;
+            for (; k + 32 < ng; k += 64) {
+                const double g0 = g[k], g1 = g[k + 32];
 #pragma unroll
-            for (int q = 0; q < kLocalRows; ++q)
-                if (live[q]) {
-                    a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
-                    a[q][1] = fma(ld_stream(kr[q] + k + 32), g1, a[q][1]);
+                for (int q = 0; q < kLocalRows; ++q)
+                    if (live[q]) {
+                        a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
+                        a[q][1] = fma(ld_stream(kr[q] + k + 32), g1, a[q][1]);
+                    }
+            }
+            if (k < ng) {
+                const double g0 = g[k];
+#pragma unroll
+                for (int q = 0; q < kLocalRows; ++q)
+                    if (live[q]) a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
+            }
+#pragma unroll
+            for (int q = 0; q < kLocalRows; ++q) {
+                if (!live[q]) continue;  // warp-uniform
+                const double acc = warp_sum(a[q][0] + a[q][1]);
+                if (lane == 0) {
+                    if (with_coarse) kg[row0 + q - r0] = acc;
+                    else P.hbuf[sd.hbuf + row0 + q] = acc;
                 }
-        }
-        if (k < ng) {
-            const double g0 = g[k];
-#pragma unroll
-            for (int q = 0; q < kLocalRows; ++q)
-                if (live[q]) a[q][0] = fma(ld_stream(kr[q] + k), g0, a[q][0]);
-        }
-#pragma unroll
-        for (int q = 0; q < kLocalRows; ++q) {
-            if (!live[q]) continue;  // warp-uniform
-            const double acc = warp_sum(a[q][0] + a[q][1]);
-            if (lane == 0) {
-                if (with_coarse) kg[row0 + q - r0] = acc;
-                else P.hbuf[sd.hbuf + row0 + q] = acc;
             }
         }
-    }
-    if (with_coarse == 1) {
-        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
-    } else if (with_coarse == 2) {
+    } else {
         // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
         // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
+        const int ct = threadIdx.x - sw * 32, nct = cw * 32;
         const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
-        for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+        for (int q = ct; q < nc; q += nct) {
             double acc = 0.0;
-            for (int o = P.c_own_ptr[q]; o < P.c_own_ptr[q + 1]; ++o) {
-                const int ref = P.c_own_ref[o];
-                acc += (P.ll_c && (ref < P.c_own_lo || ref >= P.c_own_hi)) ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref), tag_c)
-                                                                           : P.cbuf[ref];
+            const int o0 = P.c_own_ptr[q], o1 = P.c_own_ptr[q + 1];
+            for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
+                int ref[4];
+                double c[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) ref[t] = o + t < o1 ? P.c_own_ref[o + t] : -1;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    c[t] = ref[t] < 0 ? 0.0
+                           : (P.ll_c && (ref[t] < P.c_own_lo || ref[t] >= P.c_own_hi))
+                               ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref[t]), tag_c)
+                               : P.cbuf[ref[t]];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (ref[t] >= 0) acc += c[t];
             }
             rc[q] = acc;
         }
-        __syncthreads();
-        for (int j = warp; j < np; j += kWarps) {
+        coarse_bar(nct);
+        for (int j = warp - sw; j < np; j += cw) {
             const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
             double acc = 0.0;
             for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
@@ -178,12 +196,27 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
             if (lane == 0) xl[j] = acc;
         }
     }
+    if (with_coarse == 1)
+        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
     if (with_coarse) {
         __syncthreads();
         const double* phig = P.phig + sd.phig;
-        for (int row = r0 + warp; row < r1; row += kWarps) {
-            const double c = warp_sum(lane < np ? phig[row * np + lane] * xl[lane] : 0.0);
-            if (lane == 0) P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + kg[row - r0]);
+        constexpr int kB = 8;  // rows per batch: their Phi_G / weight loads issue together
+        for (int rb = r0 + warp; rb < r1; rb += kB * kWarps) {
+            double ph[kB], w[kB];
+#pragma unroll
+            for (int q = 0; q < kB; ++q) {
+                const int row = rb + q * kWarps;
+                ph[q] = row < r1 && lane < np ? phig[row * np + lane] : 0.0;
+                w[q] = row < r1 ? P.iface_w[sd.iface + row] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kB; ++q) {
+                const int row = rb + q * kWarps;
+                if (row >= r1) break;  // warp-uniform
+                const double c = warp_sum(lane < np ? ph[q] * xl[lane] : 0.0);
+                if (lane == 0) P.hbuf[sd.hbuf + row] = w[q] * (c + kg[row - r0]);
+            }
         }
     }
     publish<kLocalThreads>(P.pub_h);

@@ -7,6 +7,7 @@ namespace {
 
 __device__ __forceinline__ double sum_partials(const double* part, int n, double* scratch) {
     double v = 0.0;
+#pragma unroll 8  // independent loads in flight; the sum order is unchanged
     for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
     return block_sum<kVecThreads>(v, scratch);
 }
