@@ -166,6 +166,7 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     from paper_2410_14786_b200 import Preconditioner, Problem, SolverOptions, lib
+    from paper_2410_14786_b200.distributed import survey_8d
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -271,7 +272,8 @@ def run_ours(args) -> None:
         "iterations": rep.iterations, "final_relative_residual": rep.final_relative_residual,
         "setup_seconds": setup_s,
         "apply": {"ms": apply_ms, "bytes": st["apply_bytes"], "GBps": st["apply_bytes"] / (apply_ms * 1e-3) / 1e9,
-                  "frac": st["apply_bytes"] / (apply_ms * 1e-3) / 1e9 / peak},
+                  "frac": st["apply_bytes"] / (apply_ms * 1e-3) / 1e9 / peak,
+                  "vs_survey_8d": survey_8d(apply_ms, peak)},
         "roofline": {"kernel": "interior_solve_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_ms,
