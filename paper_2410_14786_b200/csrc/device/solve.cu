@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
     }
     for (int l = tid; l < n_top; l += kThreads) Q[l] = 0.0;
+    if (MODE == 3 && S.y_in)  // y0 is read at the forward/backward switch: bring it into L2 now
+        for (int l = tid * 16; l < n_loc; l += kThreads * 16)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(S.y_in + pdr.gmap + l));
     if (MODE != 0) {
         const SubdomainDesc& sd = S.subs[pdr.sub];
         const int ng = sd.n_iface;
@@ -259,13 +262,15 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             ZG[g] = z;
         }
         __syncthreads();
-        const std::int32_t* cp = S.couple_ptr + pdr.couple_ptr;
-        for (int l = tid; l < n_loc; l += kThreads) {
+        // coupled rows only ({row, end} pairs); the other rows keep T (MODE 3: zero)
+        const int2* cp = reinterpret_cast<const int2*>(S.couple_ptr + pdr.couple_ptr);
+        for (int i = tid; i < pdr.n_coupled; i += kThreads) {
+            const int2 re = __ldg(cp + i);
             double acc = 0.0;
-            for (int e = cp[l]; e < cp[l + 1]; ++e)
+            for (int e = i ? __ldg(&cp[i - 1].y) : 0; e < re.y; ++e)
                 acc += S.couple_val[pdr.couple_ent + e] * ZG[S.couple_gamma[pdr.couple_ent + e]];
-            if (MODE == 3) T[l] = acc;  // harmonic extension: rhs A_IG z_G
-            else T[l] -= acc;
+            if (MODE == 3) T[re.x] = acc;  // harmonic extension: rhs A_IG z_G
+            else T[re.x] -= acc;
         }
     }
     __syncthreads();

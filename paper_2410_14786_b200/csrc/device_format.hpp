@@ -97,7 +97,7 @@ struct PartDesc {
     std::int64_t order;         // offset (int4 entries) of the producer's unit order
     std::int32_t n_units;
     std::int64_t gmap;          // local index -> vector index
-    std::int64_t couple_ptr;    // coupling rows per local index (n_loc + 1)
+    std::int64_t couple_ptr;    // coupled rows only: {local row, end of its entries} int2 pairs
     std::int64_t couple_ent;    // coupling entries (gamma, value)
     std::int32_t phases;        // offset (int32) into the phase pool
     std::int32_t n_phases;
@@ -107,6 +107,7 @@ struct PartDesc {
     std::int32_t n_write;       // locals written on output (rank 0 also writes the top)
     std::int32_t sub;           // subdomain
     std::int32_t rank;          // 0 .. P-1 within the cluster
+    std::int32_t n_coupled;     // local rows with interface coupling (A_IG entries)
 };
 
 // Per-subdomain descriptor for the interface steps and stage hooks.

@@ -73,7 +73,9 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
             for (int j = 0; j < iters * G; ++j) T.idx[j] = in_idx(j0 + std::min(j, jn - 1));
         }
         if (outidx && (T.t.flags & kTaskLast)) T.outidx = *outidx;
-        ch.cost += iters + 16;  // ~16 iterations' worth of per-tile overhead
+        // per-tile overhead in iterations (LPT cost model; BDDC_TILE_COST overrides, experiments)
+        static const int tile_cost = std::getenv("BDDC_TILE_COST") ? std::atoi(std::getenv("BDDC_TILE_COST")) : 16;
+        ch.cost += iters + tile_cost + (indexed ? iters / 2 : 0);
         ch.tiles.push_back(std::move(T));
     }
     return ch;
@@ -617,19 +619,27 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
 
         pd.gmap = static_cast<std::int64_t>(pools.gmap.size());
         for (index_t l = 0; l < n_loc; ++l) pools.gmap.push_back(l2v[F.perm[locpos[l]]]);
+        // interface coupling A_IG, only for the rows that have any (the boundary-adjacent
+        // interior dofs): {row, end} pairs so the kernel's threads visit coupled rows only
+        if (pools.couple_ptr.size() & 1) pools.couple_ptr.push_back(0);  // int2 alignment
         pd.couple_ptr = static_cast<std::int64_t>(pools.couple_ptr.size());
         pd.couple_ent = static_cast<std::int64_t>(pools.couple_gamma.size());
+        pd.n_coupled = 0;
         std::int32_t cnt = 0;
-        pools.couple_ptr.push_back(0);
         for (index_t l = 0; l < n_loc; ++l) {
             const index_t v = F.perm[locpos[l]];
+            const std::int32_t c0 = cnt;
             for (index_t q = A.row_offsets[v]; q < A.row_offsets[v + 1]; ++q)
                 if (A.col_indices[q] >= nI) {
                     pools.couple_gamma.push_back(A.col_indices[q] - nI);
                     pools.couple_val.push_back(A.values[q]);
                     ++cnt;
                 }
-            pools.couple_ptr.push_back(cnt);
+            if (cnt > c0) {
+                pools.couple_ptr.push_back(static_cast<std::int32_t>(l));
+                pools.couple_ptr.push_back(cnt);
+                ++pd.n_coupled;
+            }
         }
         pools.max_loc = std::max(pools.max_loc, n_loc);
         pools.max_top = std::max(pools.max_top, n_top);
