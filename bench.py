@@ -55,7 +55,9 @@ def workload(n_gpus: int) -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region. start()
+    returns once the first sample arrived, so the sampler's start-up (process launch, NVML init)
+    never overlaps the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -77,6 +79,10 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        t0 = time.perf_counter()
+        while not self.lines and time.perf_counter() - t0 < 5.0:
+            time.sleep(0.01)
+        time.sleep(0.1)
 
     def _read(self):
         for line in self.proc.stdout:

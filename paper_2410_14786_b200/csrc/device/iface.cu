@@ -97,12 +97,10 @@ constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads p
 // h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each streaming warp
 // handles kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight;
 // the K_i g_i rows go to shared memory. With the fused coarse solve (with_coarse == 2) the last
-// one or two warps form r_c and this subdomain's x_c rows meanwhile (latency-bound gathers and
-// short GEMVs, hidden behind the stream), then every warp finishes its rows with Phi_G x_c.
-__device__ __forceinline__ void coarse_bar(int nthreads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
+// warp starts forming r_c right away (latency-bound owner gathers, hidden behind the stream)
+// and the streaming warps join it when their rows are done (entries handed out by a shared
+// counter, each summed in its fixed owner order); then this subdomain's x_c rows, then every
+// warp finishes its rows with Phi_G x_c.
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     pdl_trigger();
@@ -124,8 +122,11 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* K = P.kmat + sd.kmat;
     constexpr int kWarps = kLocalThreads / 32;
-    const int cw = with_coarse == 2 ? (nc > 640 ? 2 : 1) : 0;  // coarse warps
-    const int sw = kWarps - cw;                                  // streaming warps
+    const int cw = with_coarse == 2 ? 1 : 0;  // coarse warps
+    const int sw = kWarps - cw;               // streaming warps
+    __shared__ int next_q;
+    if (threadIdx.x == 0) next_q = 0;
+    __syncthreads();
     if (warp < sw) {
         for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += sw * kLocalRows) {
             const double* kr[kLocalRows];
@@ -162,12 +163,12 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
                 }
             }
         }
-    } else {
+    }
+    if (with_coarse == 2) {
         // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
         // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
-        const int ct = threadIdx.x - sw * 32, nct = cw * 32;
         const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
-        for (int q = ct; q < nc; q += nct) {
+        for (int q = atomicAdd(&next_q, 1); q < nc; q = atomicAdd(&next_q, 1)) {
             double acc = 0.0;
             const int o0 = P.c_own_ptr[q], o1 = P.c_own_ptr[q + 1];
             for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
@@ -187,8 +188,8 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
             }
             rc[q] = acc;
         }
-        coarse_bar(nct);
-        for (int j = warp - sw; j < np; j += cw) {
+        __syncthreads();
+        for (int j = warp; j < np; j += kWarps) {
             const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
             double acc = 0.0;
             for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
