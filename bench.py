@@ -19,6 +19,7 @@ solves. `cpu_baseline` is the unmodified reference (oracle/_ref/ref_driver, comp
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -211,12 +212,14 @@ def run_ours(args) -> None:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     l0 = lib().bddc_kernel_launches()
+    gc.disable()  # the PCG loop is host-driven: no interpreter GC pause inside the timed region
     e0.record(stream)
     reps = []
     for _ in range(args.steps):
         reps.append(pre.pcg_device(b.data_ptr(), x.data_ptr(), opts, stream=stream.cuda_stream))
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     launches = lib().bddc_kernel_launches() - l0
     clk = clocks.stop()
     pre.set_profile(False)

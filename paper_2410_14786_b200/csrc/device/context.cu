@@ -117,6 +117,11 @@ struct GpuContext::Impl {
         }
     };
     SolveProgram prog, harm, head;
+    // fused coarse solve: r_c formed once per GPU inside the cooperative K_i grid (large n_c),
+    // else (or when the grid cannot be co-resident) every CTA forms r_c itself
+    DBuf<double> rc_g;
+    DBuf<unsigned long long> coarse_ctr;
+    bool coop_coarse = false;
     // split apply (head + harmonic programs, device/solve.cuh y_out / y_in): y0 = L^-1 r_I per
     // part in local order; BDDC_SPLIT=0 keeps u0 from a full solve
     DBuf<double> ybuf;
@@ -168,6 +173,7 @@ struct GpuContext::Impl {
     // events before each launch so the per-kernel timing stays live.
     struct IterGraphs {
         cudaGraphExec_t a = nullptr, b = nullptr;
+        cudaGraphExec_t b_plain = nullptr;  // profiling on: the same iteration without event nodes
         cudaGraph_t b_graph = nullptr;  // kept alive: its event-record nodes are rebound per launch
         std::int64_t a_kernels = 0, b_kernels = 0;
         cudaGraphNode_t ev_nodes[4] = {};
@@ -176,6 +182,8 @@ struct GpuContext::Impl {
         void reset() {
             if (a) cudaGraphExecDestroy(a);
             if (b) cudaGraphExecDestroy(b);
+            if (b_plain) cudaGraphExecDestroy(b_plain);
+            b_plain = nullptr;
             if (b_graph) cudaGraphDestroy(b_graph);
             a = b = nullptr;
             b_graph = nullptr;
@@ -184,6 +192,10 @@ struct GpuContext::Impl {
         ~IterGraphs() { reset(); }
     } graphs;
     ApplyEvents* capture_events = nullptr;
+    bool suppress_profile = false;  // capturing the unprofiled iteration graph
+    // profiling samples one pipelined iteration in BDDC_PROFILE_STRIDE (default 4): rebinding the
+    // event nodes costs host time inside the host-driven loop (~6% of the solve if every iteration)
+    int profile_stride = std::getenv("BDDC_PROFILE_STRIDE") ? std::max(1, std::atoi(std::getenv("BDDC_PROFILE_STRIDE"))) : 4;
     std::unique_ptr<ApplyEvents> graph_events;
     bool use_graphs = !(std::getenv("BDDC_GRAPH") && std::atoi(std::getenv("BDDC_GRAPH")) == 0);
 
@@ -398,6 +410,10 @@ struct GpuContext::Impl {
         P.c_own_ptr = c_own_ptr.p;
         P.c_own_ref = c_own_ref.p;
         P.coarse_inv = coarse_inv.p;
+        if (coop_coarse) {
+            P.rc_g = rc_g.p;
+            P.coarse_ctr = coarse_ctr.p;
+        }
         P.gbuf = gbuf.p;
         P.hbuf = hbuf.p;
         P.cbuf = cbuf.p;
@@ -498,7 +514,7 @@ struct GpuContext::Impl {
 
     void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
         ApplyEvents* E = capture_events;  // graph capture: fixed events, rebound per launch
-        if (opt.profile && !E) {
+        if (opt.profile && !E && !suppress_profile) {
             if (ev_used == 4096) resolve_events();
             if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
             E = ev_pool[ev_used++].get();
@@ -979,7 +995,17 @@ struct GpuContext::Impl {
             return rep;
         }
         if (precondition) {
-            apply_rz();
+            // graphed loop + profiling: only the sampled graph iterations are timed (steady
+            // state); the eager pre-loop apply is not
+            const bool graph_loop = use_graphs && (opt.coarse_mode == 0) && (!dist() || p2p());
+            suppress_profile = graph_loop && opt.profile;
+            try {
+                apply_rz();
+            } catch (...) {
+                suppress_profile = false;
+                throw;
+            }
+            suppress_profile = false;
             check_coarse(s);
         }
         if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
@@ -1057,6 +1083,24 @@ struct GpuContext::Impl {
                     throw;
                 }
                 capture_events = nullptr;
+                if (prof) {  // the same iteration without the apply's event nodes
+                    suppress_profile = true;
+                    std::int64_t plain_kernels = 0;
+                    try {
+                        graphs.b_plain = capture(
+                            s,
+                            [&] {
+                                check_part(0);
+                                BDDC_CUDA(cudaEventRecordWithFlags(check_ev.e, s, cudaEventRecordExternal));
+                                next_direction(0);
+                            },
+                            &plain_kernels);
+                    } catch (...) {
+                        suppress_profile = false;
+                        throw;
+                    }
+                    suppress_profile = false;
+                }
                 if (prof && precondition) {  // locate the event-record nodes of the apply
                     std::size_t nn = 0;
                     BDDC_CUDA(cudaGraphGetNodes(gb, nullptr, &nn));
@@ -1079,21 +1123,26 @@ struct GpuContext::Impl {
                 graphs.valid = true;
             }
         }
-        auto launch_b = [&]() {
-            if (graphs.profile && precondition) {  // bind this launch's timing events
-                if (ev_used == 4096) resolve_events();
-                if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
-                ApplyEvents* E = ev_pool[ev_used++].get();
-                for (int k = 0; k < 4; ++k)
-                    BDDC_CUDA(cudaGraphExecEventRecordNodeSetEvent(graphs.b, graphs.ev_nodes[k], E->e[k].e));
+        auto launch_b = [&](int it) {
+            cudaGraphExec_t g = graphs.b;
+            if (graphs.profile && precondition) {
+                if (graphs.b_plain && (it - 1) % profile_stride != 0) {
+                    g = graphs.b_plain;  // unsampled iteration
+                } else {  // bind this launch's timing events
+                    if (ev_used == 4096) resolve_events();
+                    if (ev_used == ev_pool.size()) ev_pool.emplace_back(new ApplyEvents);
+                    ApplyEvents* E = ev_pool[ev_used++].get();
+                    for (int k = 0; k < 4; ++k)
+                        BDDC_CUDA(cudaGraphExecEventRecordNodeSetEvent(graphs.b, graphs.ev_nodes[k], E->e[k].e));
+                }
             }
-            BDDC_CUDA(cudaGraphLaunch(graphs.b, s));
+            BDDC_CUDA(cudaGraphLaunch(g, s));
             g_kernel_launches.fetch_add(graphs.b_kernels);
         };
         for (int it = 1; it <= o.max_iterations; ++it) {
             const bool spec = pipelined && it < o.max_iterations;
             if (graphed && spec) {
-                launch_b();  // check part + read-back event + speculative next direction
+                launch_b(it);  // check part + read-back event + speculative next direction
             } else {
                 if (graphed) {
                     BDDC_CUDA(cudaGraphLaunch(graphs.a, s));
@@ -1316,6 +1365,9 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.c_own_ptr.upload(img.c_own_ptr);
     I.c_own_ref.upload(img.c_own_ref);
     I.coarse_inv.upload(img.coarse_inv);
+    I.rc_g.alloc(std::max(img.n_coarse, 1));
+    I.coarse_ctr.alloc(1);
+    BDDC_CUDA(cudaMemset(I.coarse_ctr.p, 0, sizeof(unsigned long long)));
     {
         std::vector<double> wl;
         for (const auto& w : d.weights) wl.insert(wl.end(), w.begin(), w.end());
@@ -1336,6 +1388,14 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.cbuf.alloc(std::max<std::int64_t>(img.cbuf_total, 1));
     I.lbuf.alloc(std::max<std::int64_t>(img.local_total, 1));
     I.xc.alloc(std::max(img.n_coarse, 1));
+    {
+        // measured on B200: at n_c = 161 / 337 the grid barrier costs more than the redundant
+        // per-CTA r_c (3-4 us per apply), at 705 they tie; it pays from ~1,000 coarse dofs (C2 at
+        // N=8: 1,441). BDDC_COOP_COARSE=0/1 forces it.
+        const char* e = std::getenv("BDDC_COOP_COARSE");
+        const bool want = e ? std::atoi(e) == 1 : img.n_coarse >= 1024;
+        if (want) I.coop_coarse = iface_local_cooperative_fits(I.iface_params(), I.opt.local_blocks, I.device);
+    }
     I.vin.alloc(n);
     I.vout.alloc(n);
     I.vtmp.alloc(n);

@@ -96,11 +96,32 @@ constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads p
 
 // h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each streaming warp
 // handles kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight;
-// the K_i g_i rows go to shared memory. With the fused coarse solve (with_coarse == 2) the last
-// warp starts forming r_c right away (latency-bound owner gathers, hidden behind the stream)
-// and the streaming warps join it when their rows are done (entries handed out by a shared
-// counter, each summed in its fixed owner order); then this subdomain's x_c rows, then every
-// warp finishes its rows with Phi_G x_c.
+// the K_i g_i rows go to shared memory. With the fused coarse solve (with_coarse == 2, a
+// cooperative launch) r_c is formed once per GPU: the last warp of every CTA sums its share of
+// the coarse entries (latency-bound owner gathers, each entry in its fixed owner order) while
+// the other warps stream K_i; after a grid barrier every CTA reads the whole r_c, forms this
+// subdomain's x_c rows, and every warp finishes its rows with Phi_G x_c.
+__device__ __forceinline__ double coarse_entry(const IfaceParams& P, int q, std::uint32_t tag_c) {
+    double acc = 0.0;
+    const int o0 = P.c_own_ptr[q], o1 = P.c_own_ptr[q + 1];
+    for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
+        int ref[4];
+        double c[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ref[t] = o + t < o1 ? P.c_own_ref[o + t] : -1;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            c[t] = ref[t] < 0 ? 0.0
+                   : (P.ll_c && (ref[t] < P.c_own_lo || ref[t] >= P.c_own_hi))
+                       ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref[t]), tag_c)
+                       : P.cbuf[ref[t]];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (ref[t] >= 0) acc += c[t];
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     pdl_trigger();
@@ -115,18 +136,18 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     double* xl = sm + ((ng + 1) & ~1);
     double* rc = xl + ((P.max_primal + 1) & ~1);
     double* kg = rc + (with_coarse == 2 ? ((nc + 1) & ~1) : 0);  // this CTA's rows of K_i g_i
+    __shared__ int next_q;  // local r_c (grid not co-resident): next entry to form
     for (int k = threadIdx.x; k < ng; k += blockDim.x) g[k] = P.gbuf[sd.hbuf + k];
+    if (threadIdx.x == 0) next_q = 0;
     __syncthreads();
     const int rows_per = (ng + blocks_per_sub - 1) / blocks_per_sub;
     const int r0 = part * rows_per, r1 = min(ng, r0 + rows_per);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* K = P.kmat + sd.kmat;
     constexpr int kWarps = kLocalThreads / 32;
+    const std::uint32_t tag_c = with_coarse == 2 && P.ll_c ? ll_tag(P.seq_c) : 0u;
     const int cw = with_coarse == 2 ? 1 : 0;  // coarse warps
     const int sw = kWarps - cw;               // streaming warps
-    __shared__ int next_q;
-    if (threadIdx.x == 0) next_q = 0;
-    __syncthreads();
     if (warp < sw) {
         for (int row0 = r0 + warp * kLocalRows; row0 < r1; row0 += sw * kLocalRows) {
             const double* kr[kLocalRows];
@@ -163,32 +184,41 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
                 }
             }
         }
+    } else if (P.coarse_ctr) {
+        // this CTA's share of r_c (every owner's c_i, ascending subdomain), to rc_g, then arrive
+        const int q0 = static_cast<int>(static_cast<long long>(nc) * blockIdx.x / gridDim.x);
+        const int q1 = static_cast<int>(static_cast<long long>(nc) * (blockIdx.x + 1) / gridDim.x);
+        for (int q = q0 + lane; q < q1; q += 32) P.rc_g[q] = coarse_entry(P, q, tag_c);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(P.coarse_ctr, 1ull);
+        }
+    } else {
+        for (int q = atomicAdd(&next_q, 1); q < nc; q = atomicAdd(&next_q, 1)) rc[q] = coarse_entry(P, q, tag_c);
     }
-    if (with_coarse == 2) {
-        // fused dense coarse solve: r_c (every owner's c_i, ascending subdomain), then only the
-        // rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
-        const std::uint32_t tag_c = P.ll_c ? ll_tag(P.seq_c) : 0u;
-        for (int q = atomicAdd(&next_q, 1); q < nc; q = atomicAdd(&next_q, 1)) {
-            double acc = 0.0;
-            const int o0 = P.c_own_ptr[q], o1 = P.c_own_ptr[q + 1];
-            for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
-                int ref[4];
-                double c[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) ref[t] = o + t < o1 ? P.c_own_ref[o + t] : -1;
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    c[t] = ref[t] < 0 ? 0.0
-                           : (P.ll_c && (ref[t] < P.c_own_lo || ref[t] >= P.c_own_hi))
-                               ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref[t]), tag_c)
-                               : P.cbuf[ref[t]];
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (ref[t] >= 0) acc += c[t];
+    if (with_coarse == 2 && !P.coarse_ctr) {
+        // grid too large to be co-resident: every CTA forms the whole r_c itself (the coarse
+        // warp started during the stream, the streaming warps join it through the counter)
+        for (int q = atomicAdd(&next_q, 1); q < nc; q = atomicAdd(&next_q, 1)) rc[q] = coarse_entry(P, q, tag_c);
+        __syncthreads();
+    } else if (with_coarse == 2) {
+        __syncthreads();
+        if (threadIdx.x == 0) {  // grid barrier: every CTA's share of r_c is in rc_g
+            // the counter only grows (gridDim.x per launch): the target is the end of this launch's
+            // block of arrivals, which this CTA's own arrival falls into
+            const unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr);
+            const unsigned long long target = (seen + gridDim.x - 1) / gridDim.x * gridDim.x;
+            while (*reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr) < target) {
             }
-            rc[q] = acc;
+            __threadfence();
         }
         __syncthreads();
+        for (int q = threadIdx.x; q < nc; q += blockDim.x) rc[q] = __ldcg(P.rc_g + q);
+        __syncthreads();
+    }
+    if (with_coarse == 2) {
+        // only the rows of x_c = A_c^{-1} r_c this subdomain needs, in coarse_direct_kernel's order
         for (int j = warp; j < np; j += kWarps) {
             const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
             double acc = 0.0;
@@ -408,6 +438,19 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
     BDDC_LAUNCHED();
 }
 
+bool iface_local_cooperative_fits(const IfaceParams& P, int blocks_per_sub, int device) {
+    const std::size_t smem =
+        sizeof(double) * (P.max_iface + P.max_primal + 6 + static_cast<std::size_t>(P.n_coarse) +
+                          (P.max_iface + blocks_per_sub - 1) / blocks_per_sub);
+    if (smem > 48 * 1024)
+        BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, nsm = 0, coop = 0;
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iface_local_kernel, kLocalThreads, smem));
+    BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    BDDC_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    return coop && static_cast<long long>(per_sm) * nsm >= static_cast<long long>(P.n_subdomains) * blocks_per_sub;
+}
+
 void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse) {
     const std::size_t smem =
         sizeof(double) * (P.max_iface + P.max_primal + 6 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0) +
@@ -415,7 +458,21 @@ void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s
     if (smem > 48 * 1024)
         BDDC_CUDA(cudaFuncSetAttribute(iface_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    launch_pdl(iface_local_kernel, P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s, P, blocks_per_sub, coarse);
+    if (coarse == 2 && P.coarse_ctr) {  // grid barrier inside: all CTAs co-resident (cooperative launch)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P.n_subdomains * blocks_per_sub);
+        cfg.blockDim = dim3(kLocalThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        BDDC_CUDA(cudaLaunchKernelEx(&cfg, iface_local_kernel, P, blocks_per_sub, coarse));
+    } else {
+        launch_pdl(iface_local_kernel, P.n_subdomains * blocks_per_sub, kLocalThreads, smem, s, P, blocks_per_sub, coarse);
+    }
     BDDC_LAUNCHED();
 }
 

@@ -41,6 +41,10 @@ struct IfaceParams {
     double* hbuf;   // w * (Phi_G x_c + K g) per (subdomain, gamma)
     double* cbuf;   // Phi_G^T g per (subdomain, primal)
     double* xc;     // coarse solution
+    // fused coarse solve (K_i kernel, cooperative launch): r_c formed once per GPU, each CTA
+    // its share, exchanged through rc_g and a grid barrier on the monotonic coarse_ctr
+    double* rc_g;
+    unsigned long long* coarse_ctr;
 };
 
 struct StageParams {
@@ -102,5 +106,8 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s);
 // coarse: 0 = h_i = K_i g_i; 1 = W_i(Phi x_c[map] + K g) with x_c from the coarse kernel;
 // 2 = the same with the rows of x_c = A_c^{-1} r_c formed in the kernel (dense direct mode)
 void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse);
+// Whether the fused-coarse K_i grid (n_subdomains * blocks_per_sub CTAs) can be co-resident on
+// `device` (cooperative launch, one r_c per GPU); otherwise every CTA forms r_c itself.
+bool iface_local_cooperative_fits(const IfaceParams& P, int blocks_per_sub, int device);
 
 }  // namespace bddc_b200

@@ -9,6 +9,7 @@ subdomain worker pool (include/bddc/parallel.hpp:19-45). SURVEY.md §8e is the d
 """
 from __future__ import annotations
 
+import gc
 import os
 import time
 
@@ -102,12 +103,14 @@ def run_distributed_bench(args, workload: dict, layout, cells: int) -> None:
     dist.barrier()
     torch.cuda.synchronize()
     l0 = lib().bddc_kernel_launches()
+    gc.disable()  # the PCG loop is host-driven: no interpreter GC pause inside the timed region
     e0.record(stream)
     reps = []
     for _ in range(args.steps):
         reps.append(pre.pcg_device(b.data_ptr(), x.data_ptr(), opts, stream=stream.cuda_stream))
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     launches = lib().bddc_kernel_launches() - l0
     dist.barrier()
     clk = clocks.stop()
