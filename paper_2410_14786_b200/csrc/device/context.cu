@@ -193,9 +193,9 @@ struct GpuContext::Impl {
     } graphs;
     ApplyEvents* capture_events = nullptr;
     bool suppress_profile = false;  // capturing the unprofiled iteration graph
-    // profiling samples one pipelined iteration in BDDC_PROFILE_STRIDE (default 4): rebinding the
+    // profiling samples one pipelined iteration in BDDC_PROFILE_STRIDE (default 8): rebinding the
     // event nodes costs host time inside the host-driven loop (~6% of the solve if every iteration)
-    int profile_stride = std::getenv("BDDC_PROFILE_STRIDE") ? std::max(1, std::atoi(std::getenv("BDDC_PROFILE_STRIDE"))) : 4;
+    int profile_stride = std::getenv("BDDC_PROFILE_STRIDE") ? std::max(1, std::atoi(std::getenv("BDDC_PROFILE_STRIDE"))) : 8;
     std::unique_ptr<ApplyEvents> graph_events;
     bool use_graphs = !(std::getenv("BDDC_GRAPH") && std::atoi(std::getenv("BDDC_GRAPH")) == 0);
 
@@ -1123,6 +1123,7 @@ struct GpuContext::Impl {
                 graphs.valid = true;
             }
         }
+        int profiled_it = -1;  // iteration whose graph launch carries the apply's timing events
         auto launch_b = [&](int it) {
             cudaGraphExec_t g = graphs.b;
             if (graphs.profile && precondition) {
@@ -1134,6 +1135,7 @@ struct GpuContext::Impl {
                     ApplyEvents* E = ev_pool[ev_used++].get();
                     for (int k = 0; k < 4; ++k)
                         BDDC_CUDA(cudaGraphExecEventRecordNodeSetEvent(graphs.b, graphs.ev_nodes[k], E->e[k].e));
+                    profiled_it = it;
                 }
             }
             BDDC_CUDA(cudaGraphLaunch(g, s));
@@ -1170,7 +1172,16 @@ struct GpuContext::Impl {
             }
             rel = pinned[1];
             rep.iterations = it;
-            if (pinned[2] != 0.0) { rep.converged = true; break; }
+            if (pinned[2] != 0.0) {
+                rep.converged = true;
+                // the speculative apply launched with this iteration is skipped on the device:
+                // not an apply sample
+                if (profiled_it == it && ev_used > 0) {
+                    BDDC_CUDA(cudaStreamSynchronize(s));
+                    --ev_used;
+                }
+                break;
+            }
             if (it == o.max_iterations) break;
             if (!spec) {
                 if (precondition) {
