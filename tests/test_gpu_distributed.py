@@ -17,12 +17,16 @@ def _gpus():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_matches_single_gpu_and_reference(gpu, world):
+@pytest.mark.parametrize("world,env", [(2, {}), (4, {}),
+                                       (2, {"BDDC_FUSED_EX": "0"}),  # separate flag-based exchange kernels
+                                       (2, {"BDDC_P2P": "0"})],      # NCCL exchanges
+                         ids=["w2", "w4", "w2-exchange-kernels", "w2-nccl"])
+def test_distributed_matches_single_gpu_and_reference(gpu, world, env):
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs (have {_gpus()})")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world), os.path.join(ROOT, "tests", "dist_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + 10 * len(env)),
+           os.path.join(ROOT, "tests", "dist_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env={**os.environ, **env})
     print(out.stdout[-4000:], out.stderr[-4000:])
     assert out.returncode == 0
