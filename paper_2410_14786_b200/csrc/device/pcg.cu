@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kVecThreads) nonfinite_kernel(int n, const dou
         if (!isfinite(x[i])) atomicMin(res, i);
 }
 
-int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecThreads, 148 * 8)); }
+int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecThreads, 148 * 4)); }
 
 }  // namespace
 

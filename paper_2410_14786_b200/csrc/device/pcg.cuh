@@ -60,7 +60,7 @@ struct PcgDevice {
     double rtol, atol;
 };
 
-constexpr int kVecThreads = 256;
+constexpr int kVecThreads = 512;  // 4 CTAs per SM (vec_grid): 592 grid partials per reduction
 
 void pcg_dot(const PcgDevice& D, const double* a, const double* b, double* part, cudaStream_t s);
 // scal[slot] = sqrt(sum part) (sqrt=true) or sum part
