@@ -41,17 +41,22 @@ __global__ void __launch_bounds__(kVecThreads) finalize_kernel(const double* par
     if (threadIdx.x == 0) *out = take_sqrt ? sqrt(v) : v;
 }
 
-__global__ void __launch_bounds__(kVecThreads) spmv_dot_kernel(const PcgDevice D) {
+__global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
     pdl_trigger();
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *D.iter += 1;  // read by the later kernels of this iteration
+    const std::int32_t* __restrict__ ap = D.A_ptr;
+    const std::int32_t* __restrict__ ac = D.A_col;
+    const double* __restrict__ av = D.A_val;
+    const double* __restrict__ p = D.p;
+    double* __restrict__ q = D.q;
     double acc = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
         double y = 0.0;
-        for (int e = D.A_ptr[i]; e < D.A_ptr[i + 1]; ++e) y += D.A_val[e] * D.p[D.A_col[e]];
-        D.q[i] = y;
-        if (i < D.n_dot) acc = fma(D.p[i], y, acc);
+        for (int e = ap[i]; e < ap[i + 1]; ++e) y += av[e] * p[ac[e]];
+        q[i] = y;
+        if (i < D.n_dot) acc = fma(p[i], y, acc);
     }
     acc = block_sum<kVecThreads>(acc, scratch);
     if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
@@ -130,12 +135,16 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     }
     const double alpha = D.rho[it - 1] / pq;
     if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[it - 1] = alpha;
-    const double* p = (D.fuse_dir && (it & 1)) ? D.p_alt : D.p;
+    const double* __restrict__ p = (D.fuse_dir && (it & 1)) ? D.p_alt : D.p;
+    const double* __restrict__ q = D.q;
+    double* __restrict__ x = D.x;
+    double* __restrict__ r = D.r;
     double acc = 0.0;
+#pragma unroll 2
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
-        D.x[i] += alpha * p[i];
-        const double ri = D.r[i] - alpha * D.q[i];
-        D.r[i] = ri;
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
         if (i < D.n_dot) acc = fma(ri, ri, acc);
     }
     acc = block_sum<kVecThreads>(acc, scratch);
@@ -177,9 +186,12 @@ __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, in
     const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     const double beta = rz / D.rho[it - 1];
     const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
+    const double* __restrict__ z = D.z;
+    double* __restrict__ p = D.p;
+#pragma unroll 2
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x) {
-        const double zi = (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : D.z[i];
-        D.p[i] = zi + beta * D.p[i];
+        const double zi = (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : z[i];
+        p[i] = zi + beta * p[i];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         D.beta[it - 1] = beta;
