@@ -116,11 +116,13 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
         if (rem > 1) s1 = fma(M[kG], v[G], s1);
         if (rem > 2) s2 = fma(M[2 * kG], v[2 * G], s2);
     }
-    double tot = lane < kG ? (s0 + s1) + (s2 + s3) : 0.0;
+    // per-lane partial sums accumulate over the pieces of a chunk (same k, hence same G and
+    // lane -> row map); the row's lane group is reduced once, at its last piece
+    acc = ((flags & kTaskFirst) ? 0.0 : acc) + (lane < kG ? (s0 + s1) + (s2 + s3) : 0.0);
+    if (!(flags & kTaskLast)) return;
 #pragma unroll 1
-    for (int off = G >> 1; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-    acc = ((flags & kTaskFirst) ? 0.0 : acc) + tot;
-    if ((flags & kTaskLast) && g == 0) {
+    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (g == 0) {
         const int nvalid = static_cast<unsigned>(h.w) >> 24;
         if (flags & kTaskPush) {
             if (r < k) {
