@@ -92,7 +92,8 @@ __device__ __forceinline__ bool publish(const Publish& P) {
     __shared__ int last_s;
     __shared__ double red_s[THREADS / 32];
     const std::uint64_t t_in = P.trace ? gtimer() : 0;
-    const std::uint32_t tag = ll_tag(P.seq) + 1u;
+    const std::uint32_t last = ll_tag(P.seq);
+    const std::uint32_t tag = last == 0xffffffffu ? 1u : last + 1u;  // never 0 (the buffers start zeroed)
     __syncthreads();  // this CTA's outputs are written
     if (threadIdx.x == 0) {
         __threadfence();  // local writes only (the peer stores follow: no wait for NVLink acks)
