@@ -1005,15 +1005,27 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
         BDDC_CUDA(cudaStreamSynchronize(s));
         const double normb = pinned[0];
-        if (!std::isfinite(normb)) {
+        if (!std::isfinite(normb)) {  // every rank sees the same ||b||: the decision is collective
             DBuf<int> bad;
             bad.alloc(1);
-            device_first_nonfinite(n, b, bad.p, s);
+            device_first_nonfinite(dist() ? static_cast<int>(n_owned) : static_cast<int>(n), b, bad.p, s);
             int idx = 0;
             BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             BDDC_CUDA(cudaStreamSynchronize(s));
-            if (idx != 0x7fffffff)  // else: finite entries whose squares overflow (the reference carries on)
-                throw std::invalid_argument("pcg rhs: non-finite entry at index " + std::to_string(global_index(idx)));
+            double first = idx != 0x7fffffff ? static_cast<double>(global_index(idx)) : 1e300;
+            if (dist()) {  // smallest global index over the ranks (each owns its rows)
+                DBuf<double> all;
+                all.alloc(comm->world());
+                BDDC_CUDA(cudaMemcpy(all.p + comm->rank(), &first, sizeof(double), cudaMemcpyHostToDevice));
+                comm->allgather_inplace(all.p, 1, s);
+                std::vector<double> h(comm->world());
+                BDDC_CUDA(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+                BDDC_CUDA(cudaStreamSynchronize(s));
+                first = *std::min_element(h.begin(), h.end());
+            }
+            if (first < 1e300)  // else: finite entries whose squares overflow (the reference carries on)
+                throw std::invalid_argument("pcg rhs: non-finite entry at index " +
+                                            std::to_string(static_cast<long long>(first)));
         }
         if (o.record_history) rep.history.push_back(1.0);
         if (normb == 0.0) {
@@ -1516,9 +1528,7 @@ SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x
     Impl& I = *impl_;
     const index_t n = I.pb.decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
-    if (I.dist()) {
-        // every rank scans the whole rhs, so all ranks reject it together before any exchange
-        ensure_finite(b, I.n_global, "pcg rhs");
+    if (I.dist()) {  // non-finite rhs entries: found on the devices, agreed over the ranks (pcg)
         I.gather_host(b);
         BDDC_CUDA(cudaMemcpyAsync(I.vin.p, I.stage, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
         SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);

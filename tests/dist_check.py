@@ -84,12 +84,24 @@ def main():
         rep = pre.pcg_device(bl.data_ptr(), xl.data_ptr(), opts)
         res["device_matches_host"] = bool(np.array_equal(xl.cpu().numpy()[:n_rows], xd[rows])) and \
             rep.iterations == rd.iterations
+        if name == "k4m8":  # a non-finite rhs: every rank rejects it with the smallest global index
+            from paper_2410_14786_b200 import InvalidArgument
+            bad = b.copy()
+            j = prob.global_dofs // 2 + 3
+            bad[j], bad[prob.global_dofs - 1] = np.nan, np.inf
+            try:
+                pre.pcg(bad, opts)
+                res["nonfinite_rejected"] = False
+            except InvalidArgument as e:
+                res["nonfinite_rejected"] = f"non-finite entry at index {j}" in str(e)
+            res["usable_after_error"] = pre.pcg(b, opts)[1].iterations == rd.iterations
         # heterogeneous coefficients amplify the reordered dot products of the distributed PCG
         # (and the reference itself is only 1e-8-stable there, test_gpu_parity): 1e-7 on histories
         htol = 1e-7 if kappa[0] else 1e-10
         ok = (res["apply_bitwise"] and res["apply_untouched_elsewhere"] and rd.iterations == r1.iterations
               and res["history_err_vs_single"] <= htol and res["x_err_vs_single"] <= 1e-10
-              and res["device_matches_host"] and rd.converged)
+              and res["device_matches_host"] and rd.converged and res.get("nonfinite_rejected", True)
+              and res.get("usable_after_error", True))
         if "history_err_vs_reference" in res:
             ok = ok and res["history_err_vs_reference"] <= htol and abs(rd.iterations - res["iterations_reference"]) <= (
                 1 if kappa[0] else 0)
