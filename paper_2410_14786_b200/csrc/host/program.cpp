@@ -1,6 +1,10 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <utility>
 
 #include "distribute.hpp"
@@ -107,11 +111,60 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
             img.lrow_ptr.push_back(static_cast<std::int32_t>(img.lrow_col.size()));
         }
 
-        // interior-solve program (local dof -> vector index = the subdomain map)
-        build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.solve);
-        if (harmonic) {
-            build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.harm, true);
-            build_solve_program(S.factor, A, dofs, i, parts, unit_bytes, img.head, false, true);
+    }
+
+    // interior-solve programs (local dof -> vector index = the subdomain map), built per
+    // subdomain on host threads and appended in subdomain order (deterministic image)
+    {
+        const int nprog = harmonic ? 3 : 1;
+        std::vector<SolvePools> built(static_cast<std::size_t>(nsub) * nprog);
+        std::atomic<index_t> next{0};
+        std::exception_ptr err;
+        std::mutex err_mu;
+        auto work = [&] {
+            for (index_t i = next++; i < nsub; i = next++) {
+                try {
+                    const SubdomainSetup& S = setup.subs[i];
+                    const auto& dofs = d.subdomain_dofs[i];
+                    build_solve_program(S.factor, locals[i], dofs, i, parts, unit_bytes, built[i * nprog]);
+                    if (harmonic) {
+                        build_solve_program(S.factor, locals[i], dofs, i, parts, unit_bytes, built[i * nprog + 1], true);
+                        build_solve_program(S.factor, locals[i], dofs, i, parts, unit_bytes, built[i * nprog + 2], false,
+                                            true);
+                    }
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(err_mu);
+                    if (!err) err = std::current_exception();
+                }
+            }
+        };
+        const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), nsub));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto& t : th) t.join();
+        if (err) std::rethrow_exception(err);
+        for (int k = 0; k < nprog; ++k) {  // one allocation per pool
+            SolvePools& dst = k == 0 ? img.solve : (k == 1 ? img.harm : img.head);
+            std::size_t ns = 0, nu = 0, no = 0, ng = 0;
+            for (index_t i = 0; i < nsub; ++i) {
+                const SolvePools& b = built[i * nprog + k];
+                ns += b.stream.size();
+                nu += b.units.size();
+                no += b.order.size();
+                ng += b.gmap.size();
+            }
+            dst.stream.reserve(ns);
+            dst.units.reserve(nu);
+            dst.order.reserve(no);
+            dst.gmap.reserve(ng);
+        }
+        for (index_t i = 0; i < nsub; ++i) {
+            append_pools(img.solve, std::move(built[i * nprog]));
+            if (harmonic) {
+                append_pools(img.harm, std::move(built[i * nprog + 1]));
+                append_pools(img.head, std::move(built[i * nprog + 2]));
+            }
         }
     }
 

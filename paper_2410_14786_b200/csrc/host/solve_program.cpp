@@ -648,4 +648,46 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
     }
 }
 
+void append_pools(SolvePools& dst, SolvePools&& src) {
+    if (dst.couple_ptr.size() & 1) dst.couple_ptr.push_back(0);  // int2 alignment of the parts' pairs
+    const std::int64_t stream = static_cast<std::int64_t>(dst.stream.size());
+    const std::int64_t units = static_cast<std::int64_t>(dst.units.size() / 2);
+    const std::int64_t order = static_cast<std::int64_t>(dst.order.size() / 4);
+    const std::int32_t phases = static_cast<std::int32_t>(dst.phases.size());
+    const std::int64_t gmap = static_cast<std::int64_t>(dst.gmap.size());
+    const std::int64_t cptr = static_cast<std::int64_t>(dst.couple_ptr.size());
+    const std::int64_t cent = static_cast<std::int64_t>(dst.couple_gamma.size());
+    for (PartDesc pd : src.parts) {
+        pd.stream += stream;
+        pd.units += units;
+        pd.order += order;
+        pd.phases += phases;
+        pd.gmap += gmap;
+        pd.couple_ptr += cptr;
+        pd.couple_ent += cent;
+        dst.parts.push_back(pd);
+    }
+    auto cat = [](auto& a, auto& b) {
+        a.insert(a.end(), b.begin(), b.end());
+        b.clear();
+        b.shrink_to_fit();
+    };
+    cat(dst.stream, src.stream);
+    cat(dst.units, src.units);
+    cat(dst.order, src.order);
+    cat(dst.phases, src.phases);
+    cat(dst.gmap, src.gmap);
+    cat(dst.couple_ptr, src.couple_ptr);
+    cat(dst.couple_gamma, src.couple_gamma);
+    cat(dst.couple_val, src.couple_val);
+    dst.tile_values += src.tile_values;
+    dst.fwd_factor_values += src.fwd_factor_values;
+    dst.bwd_factor_values += src.bwd_factor_values;
+    dst.n_tiles += src.n_tiles;
+    dst.max_loc = std::max(dst.max_loc, src.max_loc);
+    dst.max_top = std::max(dst.max_top, src.max_top);
+    dst.max_phases = std::max(dst.max_phases, src.max_phases);
+    dst.max_units = std::max(dst.max_units, src.max_units);
+}
+
 }  // namespace bddc_b200

@@ -26,6 +26,9 @@ struct SolvePools {
     std::int32_t max_loc = 0, max_top = 0, max_phases = 0, max_units = 0;
 };
 
+// Appends `src` (built from empty pools) to `dst`, rebasing the parts' offsets.
+void append_pools(SolvePools& dst, SolvePools&& src);
+
 // local_to_vec: local dof index (interior first) -> device vector index.
 // parts: 1 (one CTA per subdomain) or 2 (CTA pair in a cluster); unit_bytes: size of the
 // per-warp TMA units (and of each ring slot).
