@@ -8,7 +8,7 @@ import torch  # noqa: E402
 from paper_2410_14786_b200 import Preconditioner, Problem  # noqa: E402
 
 p = Problem.poisson(800, 8)
-for lb in (4, 8, 16):
+for lb in (4, 6, 8, 12, 16):
     pre = Preconditioner(p, local_blocks=lb)
     st = torch.cuda.Stream()
     r = torch.tensor(p.rhs(), device="cuda")
