@@ -406,14 +406,11 @@ struct GpuContext::Impl {
         P.max_loc = max_loc;
         P.max_top = max_top;
         P.max_iface = max_iface;
-        P.debug = debug_solve;
         P.stats = dbg_buf.p;
         return P;
     }
     std::int32_t max_loc = 0, max_top = 0;
-    int debug_solve = std::getenv("BDDC_DEBUG_SOLVE") ? std::atoi(std::getenv("BDDC_DEBUG_SOLVE")) : 0;
     DBuf<long long> dbg_buf;
-    int l2_ahead = std::getenv("BDDC_L2_AHEAD") ? std::atoi(std::getenv("BDDC_L2_AHEAD")) : 6;
 
     IfaceParams iface_params() const {
         IfaceParams P{};

@@ -47,7 +47,6 @@ struct SolveParams {
     int max_loc;
     int max_top;
     int max_iface;
-    int debug;     // timing experiments only: 1 = skip tile math
     long long* stats;  // diagnostics (BDDC_SOLVE_STATS): per CTA, per warp {total, mbarrier wait,
                        // CTA-barrier wait, units} cycles of the launch; null = off
     // multi-GPU fused LL exchanges (null on one GPU): MODE 0 publishes the halo of u0; MODE 3
