@@ -243,15 +243,23 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 // subdomain (reference prolong_add order, preconditioner.cpp:168-169,189-190)
                 const int gid = S.iface_gid[sd.iface + g];
                 z = 0.0;
-                if (MODE == 3 && S.ll_h) {  // peers' h_i from the LL buffer (multi-GPU, fused)
-                    const std::uint32_t tag = ll_tag(S.seq_h);
-                    for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) {
-                        const int ref = S.gi_own_ref[o];
-                        z += ref >= S.ll_h_base ? ll_get(S.ll_h + 2 * static_cast<std::int64_t>(ref - S.ll_h_base), tag)
-                                                : S.hbuf[ref];
-                    }
-                } else {
-                    for (int o = S.gi_own_ptr[gid]; o < S.gi_own_ptr[gid + 1]; ++o) z += S.hbuf[S.gi_own_ref[o]];
+                const bool ll = MODE == 3 && S.ll_h;  // peers' h_i from the LL buffer (multi-GPU, fused)
+                const std::uint32_t tag = ll ? ll_tag(S.seq_h) : 0u;
+                const int o0 = S.gi_own_ptr[gid], o1 = S.gi_own_ptr[gid + 1];
+                for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
+                    int ref[4];
+                    double h[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) ref[t] = o + t < o1 ? S.gi_own_ref[o + t] : -1;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        h[t] = ref[t] < 0 ? 0.0
+                               : (ll && ref[t] >= S.ll_h_base)
+                                   ? ll_get(S.ll_h + 2 * static_cast<std::int64_t>(ref[t] - S.ll_h_base), tag)
+                                   : S.hbuf[ref[t]];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (ref[t] >= 0) z += h[t];
                 }
                 if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) {
                     const int dof = S.iface_dof[sd.iface + g];
