@@ -243,6 +243,7 @@ struct GpuContext::Impl {
         return e;
     }
     Event check_ev;  // convergence read-back of the pipelined PCG loop
+    Event norm_ev;   // ||b|| read-back
 
     // ---- multi-GPU (null / unused on one GPU)
     std::unique_ptr<RankPlan> plan;
@@ -1000,7 +1001,44 @@ struct GpuContext::Impl {
             pcg_finalize(D, part_b.p, 0, true, s);
         }
         BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
-        BDDC_CUDA(cudaStreamSynchronize(s));
+        // z_0 = M r_0 and rho_0 are queued before the host looks at ||b|| (pipelined mode): the
+        // checks below can only discard them (a zero rhs converges at once, a non-finite one
+        // throws on every rank alike), so the device never waits for that round trip
+        auto first_direction = [&]() {
+            if (precondition) {
+                // graphed loop + profiling: only the sampled graph iterations are timed (steady
+                // state); the eager pre-loop apply is not
+                const bool graph_loop = use_graphs && (opt.coarse_mode == 0) && (!dist() || p2p());
+                suppress_profile = graph_loop && opt.profile;
+                try {
+                    apply_rz();
+                } catch (...) {
+                    suppress_profile = false;
+                    throw;
+                }
+                suppress_profile = false;
+                check_coarse(s);
+            }
+            if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
+            if (dirspmv) {
+                // rho[0] and p_1 = z are formed by the first dir_spmv
+            } else if (fused_dir) {
+                if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
+                pcg_init_rho(D, s);
+            } else {
+                gather_partial(rz_part, rz_grid, gath_c.p, s);
+                pcg_init_rho(D, s);
+                halo_exchange(p.p, s);
+            }
+        };
+        const bool early = precondition && opt.coarse_mode == 0;
+        if (early) {
+            BDDC_CUDA(cudaEventRecord(norm_ev.e, s));
+            first_direction();
+            BDDC_CUDA(cudaEventSynchronize(norm_ev.e));
+        } else {
+            BDDC_CUDA(cudaStreamSynchronize(s));
+        }
         const double normb = pinned[0];
         if (!std::isfinite(normb)) {  // every rank sees the same ||b||: the decision is collective
             DBuf<int> bad;
@@ -1029,31 +1067,7 @@ struct GpuContext::Impl {
             rep.converged = true;
             return rep;
         }
-        if (precondition) {
-            // graphed loop + profiling: only the sampled graph iterations are timed (steady
-            // state); the eager pre-loop apply is not
-            const bool graph_loop = use_graphs && (opt.coarse_mode == 0) && (!dist() || p2p());
-            suppress_profile = graph_loop && opt.profile;
-            try {
-                apply_rz();
-            } catch (...) {
-                suppress_profile = false;
-                throw;
-            }
-            suppress_profile = false;
-            check_coarse(s);
-        }
-        if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-        if (dirspmv) {
-            // rho[0] and p_1 = z are formed by the first dir_spmv
-        } else if (fused_dir) {
-            if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
-            pcg_init_rho(D, s);
-        } else {
-            gather_partial(rz_part, rz_grid, gath_c.p, s);
-            pcg_init_rho(D, s);
-            halo_exchange(p.p, s);
-        }
+        if (!early) first_direction();
         double rel = 1.0;
         // The convergence test of iteration `it` is read back while the GPU already runs the
         // next iteration's apply / dot / xpay (speculatively: they only touch z, p, rho, beta,
