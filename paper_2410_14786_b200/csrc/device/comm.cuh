@@ -1,15 +1,14 @@
-// Multi-GPU communication of the distributed BDDC-PCG: NCCL over
-// NVLink/NVSwitch, one rank per B200. NCCL is loaded at run time (dlopen of
-// libnccl.so.2, preferring the copy torch already mapped), so the single-GPU library
-// carries no NCCL link dependency.
+// Multi-GPU communication of the distributed BDDC-PCG, one rank per B200.
+// NCCL is loaded at run time (dlopen of libnccl.so.2, preferring the copy torch already
+// mapped), so the single-GPU library carries no NCCL link dependency; it serves the setup
+// (A_ci gather, IPC handle exchange) and the BDDC_P2P=0 fallback.
 //
-// Per PCG iteration the distributed path issues (all on the solve stream):
-//   halo exchange of u0 and of p   grouped ncclSend/ncclRecv with the neighbour ranks
-//   interface exchange of h_i      grouped ncclSend/ncclRecv with the neighbour ranks
-//   gather of the c_i (r_c)        in-place ncclAllGather (padded per rank)
-//   3 scalar reductions            in-place ncclAllGather of one partial per rank, summed
-//                                  in rank order by the consuming kernel (deterministic,
-//                                  identical on every rank)
+// Per PCG iteration the distributed path exchanges: the halo of u0, the c_i (r_c), the
+// shared-interface h_i, p.q, r.r, and r.z with the halo of z. By default these ride on the
+// producing / consuming kernels (fused_comm.cuh, LL format over the IPC mappings below);
+// BDDC_FUSED_EX=0 uses the single-CTA flag-based exchange kernels declared here, BDDC_P2P=0
+// grouped ncclSend/ncclRecv and in-place ncclAllGather. Scalars are gathered as one partial
+// per rank and summed in rank order by the consumer (deterministic, identical on every rank).
 #pragma once
 
 #include <vector>
