@@ -289,13 +289,14 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         static const int min_kr = std::getenv("BDDC_MIN_CHUNK_ROWS") ? std::atoi(std::getenv("BDDC_MIN_CHUNK_ROWS")) : 8;
         auto chunk_rows_for = [&](const std::vector<index_t>& rows_per_node) {
             if (min_kr >= 32) return 32;
-            for (int k : {32, 16}) {
+            for (int k : {32, 16, 8}) {
                 if (k == 16 && min_kr >= 16) return 16;
+                if (k == 8 && min_kr >= 8) return 8;
                 std::int64_t chunks = 0;
                 for (index_t r : rows_per_node) chunks += (r + k - 1) / k;
                 if (chunks >= 2 * kSolveWarps) return k;
             }
-            return 8;
+            return 4;
         };
         auto singles = [](Chunks&& cs) {  // level-synchronous phase: every chunk is its own job
             Phase ph;
