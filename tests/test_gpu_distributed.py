@@ -19,8 +19,9 @@ def _gpus():
 
 @pytest.mark.parametrize("world,env", [(2, {}), (4, {}),
                                        (2, {"BDDC_FUSED_EX": "0"}),  # separate flag-based exchange kernels
-                                       (2, {"BDDC_P2P": "0"})],      # NCCL exchanges
-                         ids=["w2", "w4", "w2-exchange-kernels", "w2-nccl"])
+                                       (2, {"BDDC_P2P": "0"}),       # NCCL exchanges
+                                       (2, {"BDDC_SPLIT": "0", "BDDC_HARMONIC": "0"})],  # unpruned apply
+                         ids=["w2", "w4", "w2-exchange-kernels", "w2-nccl", "w2-unpruned"])
 def test_distributed_matches_single_gpu_and_reference(gpu, world, env):
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs (have {_gpus()})")
