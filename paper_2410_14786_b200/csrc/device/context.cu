@@ -86,6 +86,40 @@ void ensure_finite(const double* x, index_t n, const char* context) {
             throw std::invalid_argument(std::string(context) + ": non-finite entry at index " + std::to_string(i));
 }
 
+// Multi-GPU host entry points with a pinned (device-mapped) user buffer: the rank's runs
+// {local, global, length} are read from / written to host memory directly over PCIe by one
+// warp per run, with no host-side staging pass (gather_host / scatter_host).
+__global__ void __launch_bounds__(256) gather_runs_kernel(const index_t* __restrict__ runs, int n_runs,
+                                                          const double* __restrict__ g, double* __restrict__ l) {
+    const int lane = threadIdx.x & 31;
+    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_runs; k += (gridDim.x * blockDim.x) >> 5) {
+        const index_t lo = runs[3 * k], go = runs[3 * k + 1], len = runs[3 * k + 2];
+        for (index_t i = lane; i < len; i += 32) l[lo + i] = g[go + i];
+    }
+}
+
+__global__ void __launch_bounds__(256) scatter_runs_kernel(const index_t* __restrict__ runs, int n_runs, index_t n_rows,
+                                                           const double* __restrict__ l, double* __restrict__ g) {
+    const int lane = threadIdx.x & 31;
+    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_runs; k += (gridDim.x * blockDim.x) >> 5) {
+        const index_t lo = runs[3 * k], go = runs[3 * k + 1], len = runs[3 * k + 2];
+        if (lo >= n_rows) continue;
+        for (index_t i = lane; i < len; i += 32) g[go + i] = l[lo + i];
+    }
+}
+
+// Device address of a pinned, device-mapped host buffer (nullptr for pageable memory).
+const void* mapped_host_pointer(const void* p) {
+    static const bool on = !std::getenv("BDDC_ZERO_COPY") || std::atoi(std::getenv("BDDC_ZERO_COPY")) != 0;
+    if (!on) return nullptr;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // pcg.cpp:21-36
 void sampled_symmetry_check(const CsrMatrix& A) {
     if (A.nrows != A.ncols) throw std::invalid_argument("pcg: matrix must be square");
@@ -321,6 +355,21 @@ struct GpuContext::Impl {
             l = e;
         }
         BDDC_CUDA(cudaMallocHost(&stage, sizeof(double) * std::max<index_t>(n, 1)));
+        std::vector<index_t> flat;
+        for (const auto& r : runs) flat.insert(flat.end(), r.begin(), r.end());
+        runs_dev.upload(flat);
+    }
+    DBuf<index_t> runs_dev;
+    int runs_grid() const { return std::max(1, std::min<int>(148 * 4, static_cast<int>((runs.size() + 7) / 8))); }
+    // global (host, device-mapped) -> dst (device, all local entries)
+    void gather_mapped(const double* g, double* dst, cudaStream_t s) const {
+        gather_runs_kernel<<<runs_grid(), 256, 0, s>>>(runs_dev.p, static_cast<int>(runs.size()), g, dst);
+        BDDC_LAUNCHED();
+    }
+    // src rows (device) -> global (host, device-mapped)
+    void scatter_mapped(const double* src, double* g, cudaStream_t s) const {
+        scatter_runs_kernel<<<runs_grid(), 256, 0, s>>>(runs_dev.p, static_cast<int>(runs.size()), n_rows, src, g);
+        BDDC_LAUNCHED();
     }
     void gather_host(const double* g) const {  // global -> stage (all local entries)
         host_parallel(runs.size(), [&](std::size_t a, std::size_t b) {
@@ -1518,6 +1567,16 @@ void GpuContext::apply_host(const double* r, double* z) {
     ensure_finite(r, I.n_global, "bddc apply");
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {
+        const void* rm = mapped_host_pointer(r);
+        void* zm = const_cast<void*>(mapped_host_pointer(z));
+        if (rm && zm) {  // pinned user buffers: zero-copy gather / scatter over PCIe
+            I.gather_mapped(static_cast<const double*>(rm), I.vin.p, I.stream);
+            I.apply(I.vin.p, I.vout.p, I.stream);
+            I.scatter_mapped(I.vout.p, static_cast<double*>(zm), I.stream);
+            BDDC_CUDA(cudaStreamSynchronize(I.stream));
+            I.check_coarse(I.stream);
+            return;
+        }
         I.gather_host(r);
         BDDC_CUDA(cudaMemcpyAsync(I.vin.p, I.stage, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
         I.apply(I.vin.p, I.vout.p, I.stream);
@@ -1540,6 +1599,15 @@ SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x
     const index_t n = I.pb.decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {  // non-finite rhs entries: found on the devices, agreed over the ranks (pcg)
+        const void* bm = mapped_host_pointer(b);
+        void* xm = const_cast<void*>(mapped_host_pointer(x));
+        if (bm && xm) {  // pinned user buffers: zero-copy gather / scatter over PCIe
+            I.gather_mapped(static_cast<const double*>(bm), I.vin.p, I.stream);
+            SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);
+            I.scatter_mapped(I.vout.p, static_cast<double*>(xm), I.stream);
+            BDDC_CUDA(cudaStreamSynchronize(I.stream));
+            return rep;
+        }
         I.gather_host(b);
         BDDC_CUDA(cudaMemcpyAsync(I.vin.p, I.stage, sizeof(double) * n, cudaMemcpyHostToDevice, I.stream));
         SolveResult rep = I.pcg(I.vin.p, o, I.vout.p, precondition, I.stream);

@@ -84,6 +84,15 @@ def main():
         rep = pre.pcg_device(bl.data_ptr(), xl.data_ptr(), opts)
         res["device_matches_host"] = bool(np.array_equal(xl.cpu().numpy()[:n_rows], xd[rows])) and \
             rep.iterations == rd.iterations
+        # pinned (device-mapped) host buffers: zero-copy gather / scatter, same rows, same bits
+        b_pin = torch.from_numpy(b).pin_memory().numpy()
+        x_pin = torch.full((prob.global_dofs,), float("nan"), dtype=torch.float64).pin_memory().numpy()
+        xp, rp = pre.pcg(b_pin, opts, out=x_pin)
+        z_pin = _apply(pre, b_pin, torch.full((prob.global_dofs,), float("nan"),
+                                              dtype=torch.float64).pin_memory().numpy())
+        res["pinned_matches_pageable"] = bool(np.array_equal(xp[rows], xd[rows])) and \
+            bool(np.isnan(np.delete(xp, rows)).all()) and rp.iterations == rd.iterations and \
+            bool(np.array_equal(z_pin[rows], zd[rows])) and bool(np.isnan(np.delete(z_pin, rows)).all())
         if name == "k4m8":  # a non-finite rhs: every rank rejects it with the smallest global index
             from paper_2410_14786_b200 import InvalidArgument
             bad = b.copy()
@@ -100,7 +109,7 @@ def main():
         htol = 1e-7 if kappa[0] else 1e-10
         ok = (res["apply_bitwise"] and res["apply_untouched_elsewhere"] and rd.iterations == r1.iterations
               and res["history_err_vs_single"] <= htol and res["x_err_vs_single"] <= 1e-10
-              and res["device_matches_host"] and rd.converged and res.get("nonfinite_rejected", True)
+              and res["device_matches_host"] and res["pinned_matches_pageable"] and rd.converged and res.get("nonfinite_rejected", True)
               and res.get("usable_after_error", True))
         if "history_err_vs_reference" in res:
             ok = ok and res["history_err_vs_reference"] <= htol and abs(rd.iterations - res["iterations_reference"]) <= (
