@@ -127,6 +127,12 @@ typedef struct {
     int32_t max_interface;
     int64_t interior_dofs;        /* sum of n_I over subdomains */
     int64_t interior_apply_bytes; /* algorithmic FP64 bytes of the two interior solves of one apply */
+    int64_t graph_captures;       /* PCG iteration graphs captured so far (a repeated identical solve
+                                     re-uses them; host setup contexts: 0) */
+    int32_t coarse_mode;          /* coarse solve in effect: 0 dense replicated A_c^-1, 1 coarse CG */
+    int32_t switches;             /* bit mask of the BDDC_* environment switches set at creation
+                                     (bit i = bddc_switch_name(i)); 0 = all defaults */
+    double setup_device_seconds;  /* part of setup_seconds spent in device setup kernels */
 } bddc_stats;
 
 typedef struct {
@@ -179,6 +185,8 @@ typedef struct {
 
 const char* bddc_last_error(void);
 int32_t bddc_abi_version(void);
+/* Name of environment switch bit i of bddc_stats.switches (NULL past the last). */
+const char* bddc_switch_name(int32_t i);
 /* Kernel launches issued by this library in this process so far (all contexts). */
 int64_t bddc_kernel_launches(void);
 void bddc_default_gpu_options(bddc_gpu_options* opt);

@@ -335,9 +335,16 @@ class SolveReport:
     converged: bool = False
 
 
+def sequential_dot(a: np.ndarray, b: np.ndarray) -> float:
+    """dot exactly as vector_ops.hpp:15-22: one left-to-right running sum (np.cumsum is sequential;
+    no fused multiply-add, like the reference's -O3 x86-64 build)."""
+    return float(np.cumsum(a * b)[-1]) if a.size else 0.0
+
+
 def pcg(A, b, M=None, rel_tolerance=1e-8, abs_tolerance=0.0, max_iterations=1000,
-        record_history=False):
-    """pcg.cpp:40-109 (zero initial guess, recurrence residual)."""
+        record_history=False, dot=np.dot):
+    """pcg.cpp:40-109 (zero initial guess, recurrence residual). `dot` = np.dot (pairwise sums)
+    by default; `sequential_dot` reproduces the reference's summation order bit for bit."""
     if not rel_tolerance > 0.0 or abs_tolerance < 0.0:
         raise ValueError("pcg: tolerances must be positive")
     if max_iterations < 1:
@@ -348,7 +355,7 @@ def pcg(A, b, M=None, rel_tolerance=1e-8, abs_tolerance=0.0, max_iterations=1000
         raise ValueError("pcg rhs: non-finite entry at index %d" % int(np.argmin(np.isfinite(b))))
     rep = SolveReport()
     x = np.zeros_like(b)
-    norm_b = math.sqrt(float(np.dot(b, b)))
+    norm_b = math.sqrt(float(dot(b, b)))
     if record_history:
         rep.residual_history.append(1.0)
     if norm_b == 0.0:
@@ -357,19 +364,19 @@ def pcg(A, b, M=None, rel_tolerance=1e-8, abs_tolerance=0.0, max_iterations=1000
     r = b.copy()
     z = M(r) if M is not None else r.copy()
     p = z.copy()
-    rho = float(np.dot(r, z))
+    rho = float(dot(r, z))
     alphas, betas = [], []
     rel = 1.0
     for it in range(1, max_iterations + 1):
         q = As @ p
-        curv = float(np.dot(p, q))
+        curv = float(dot(p, q))
         if curv <= 0.0:
             raise RuntimeError("matrix not SPD")
         alpha = rho / curv
         alphas.append(alpha)
         x += alpha * p
         r -= alpha * q
-        rel = math.sqrt(float(np.dot(r, r))) / norm_b
+        rel = math.sqrt(float(dot(r, r))) / norm_b
         if record_history:
             rep.residual_history.append(rel)
         rep.iterations = it
@@ -379,7 +386,7 @@ def pcg(A, b, M=None, rel_tolerance=1e-8, abs_tolerance=0.0, max_iterations=1000
         if it == max_iterations:
             break
         z = M(r) if M is not None else r.copy()
-        rho_next = float(np.dot(r, z))
+        rho_next = float(dot(r, z))
         beta = rho_next / rho
         betas.append(beta)
         rho = rho_next

@@ -40,7 +40,7 @@ CONFIGS = {
     "k6m32": (6, 32, 1, "solve", ["--plain"]),
     "k8m32": (8, 32, 1, "history", ["--plain"]),
     "c1": (4, 64, 1, "solve", ["--plain"]),
-    "c2": (8, 100, 1, "history", ["--no-stages"]),
+    "c2": (8, 100, 1, "history", ["--no-stages", "--plain"]),  # C2 + C4 (plain CG, 1,649 its)
     "c2g4": (16, 100, 1, "history", ["--no-stages"]),   # C2 weak-scaling layout at 4 GPUs
     "c3": (24, 105, 1, "history", ["--no-stages"]),     # C3 strong scaling, 6,345,361 dofs
 }
@@ -55,7 +55,10 @@ BUNDLES = {
     "r16x8m8": (128, 64, 16, 8, 0.0, 0, 1, "solve"),
     "c5": (352, 352, 8, 8, 2.0, 0x5EED, 1, "history"),
     "c2g2": (1600, 800, 16, 8, 0.0, 0, 1, "history"),  # C2 weak-scaling layout at 2 GPUs
+    "c2g8": (3200, 1600, 32, 16, 0.0, 0, 1, "history"),  # C2 weak-scaling layout at 8 GPUs (n_c 1,441)
 }
+
+NO_PLAIN = {"c2g8"}  # plain CG at 5.1M dofs is ~5 min of reference time and adds nothing
 
 MAP_ARRAYS = ("subdomain_dofs", "subdomain_dofs_off", "interior_counts", "class_kind",
               "class_entity", "multiplicity", "primal_maps", "primal_maps_off",
@@ -72,7 +75,7 @@ def run(name: str) -> None:
     workers = str(min(8, os.cpu_count() or 1))
     if name in BUNDLES:
         cx, cy, kx, ky, dec, kseed, seed, kind = BUNDLES[name]
-        flags = ["--plain"]
+        flags = [] if name in NO_PLAIN else ["--plain"]
         sys.path.insert(0, REPO)
         from paper_2410_14786_b200 import Problem
 

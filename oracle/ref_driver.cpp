@@ -21,6 +21,7 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -241,10 +242,13 @@ int dump(const Problem& pr, const fs::path& dir, index_t workers, bool stages, b
 
 // Timed CPU reference: setup once, then `warmup` + `steps` full PCG solves.
 // Prints one JSON line with per-solve seconds.
-int bench(const Problem& pr, index_t workers, int steps, int warmup) {
+// plain = true: the reference's plain CG (empty PreconditionerFn, pcg.hpp:33-34; study.cpp
+// compare mode :123-135), no preconditioner setup.
+int bench(const Problem& pr, index_t workers, int steps, int warmup, bool plain) {
     const Decomposition& d = pr.decomposition;
     double t0 = now();
-    const Preconditioner P(pr.global_matrix, pr.local_matrices, d, pr.constraints, workers);
+    std::optional<Preconditioner> P;
+    if (!plain) P.emplace(pr.global_matrix, pr.local_matrices, d, pr.constraints, workers);
     const double setup_s = now() - t0;
     std::vector<double> times;
     int iterations = 0;
@@ -254,15 +258,16 @@ int bench(const Problem& pr, index_t workers, int steps, int warmup) {
         int napply = 0;
         double tapply = 0.0;
         t0 = now();
-        const SolveReport rep = pcg(pr.global_matrix, pr.rhs,
-                                    [&](std::span<const double> r, std::span<double> z) {
-                                        const double ta = now();
-                                        const std::vector<double> res = P.apply(r);
-                                        std::copy(res.begin(), res.end(), z.begin());
-                                        tapply += now() - ta;
-                                        ++napply;
-                                    },
-                                    outer(1e-8), x);
+        PreconditionerFn M;
+        if (P)
+            M = [&](std::span<const double> r, std::span<double> z) {
+                const double ta = now();
+                const std::vector<double> res = P->apply(r);
+                std::copy(res.begin(), res.end(), z.begin());
+                tapply += now() - ta;
+                ++napply;
+            };
+        const SolveReport rep = pcg(pr.global_matrix, pr.rhs, M, outer(1e-8), x);
         const double dt = now() - t0;
         if (s >= warmup) {
             times.push_back(dt);
@@ -288,8 +293,8 @@ void usage() {
                  "usage:\n"
                  "  ref_driver dump   <k> <m> <seed> <outdir> [workers] [--no-stages] [--plain]\n"
                  "  ref_driver dumpb  <manifest> <outdir> [workers] [--no-stages] [--plain]\n"
-                 "  ref_driver bench  <k> <m> <workers> <steps> <warmup>\n"
-                 "  ref_driver benchb <manifest> <workers> <steps> <warmup>\n"
+                 "  ref_driver bench  <k> <m> <workers> <steps> <warmup> [--plain]\n"
+                 "  ref_driver benchb <manifest> <workers> <steps> <warmup> [--plain]\n"
                  "  ref_driver export <k> <m> <seed> <outdir>\n");
 }
 
@@ -320,11 +325,11 @@ int main(int argc, char** argv) {
         }
         if (cmd == "bench" && argc >= 7) {
             const Problem pr = make_square(std::atoi(argv[2]), std::atoi(argv[3]), 1);
-            return bench(pr, std::atoi(argv[4]), std::atoi(argv[5]), std::atoi(argv[6]));
+            return bench(pr, std::atoi(argv[4]), std::atoi(argv[5]), std::atoi(argv[6]), has_flag(argc, argv, "--plain"));
         }
         if (cmd == "benchb" && argc >= 6) {
             const Problem pr = make_bundle(argv[2]);
-            return bench(pr, std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]));
+            return bench(pr, std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]), has_flag(argc, argv, "--plain"));
         }
         if (cmd == "export" && argc >= 6) {
             const index_t k = std::atoi(argv[2]), m = std::atoi(argv[3]);

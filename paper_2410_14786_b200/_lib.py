@@ -82,7 +82,8 @@ class Stats(C.Structure):
     _fields_ = [("setup_seconds", f64), ("factor_values", i64), ("interior_solve_bytes", i64),
                 ("apply_bytes", i64), ("n_subdomains", i32), ("global_dofs", i32), ("n_coarse", i32),
                 ("unique_subdomains", i32), ("max_interior", i32), ("max_interface", i32), ("interior_dofs", i64),
-                ("interior_apply_bytes", i64)]
+                ("interior_apply_bytes", i64), ("graph_captures", i64), ("coarse_mode", i32), ("switches", i32),
+                ("setup_device_seconds", f64)]
 
 
 class KernelTimes(C.Structure):
@@ -94,6 +95,7 @@ pd = P(f64)
 SIGNATURES = {
     "bddc_last_error": (C.c_char_p, []),
     "bddc_abi_version": (i32, []),
+    "bddc_switch_name": (C.c_char_p, [i32]),
     "bddc_kernel_launches": (i64, []),
     "bddc_default_gpu_options": (None, [P(GpuOptions)]),
     "bddc_default_solver_options": (None, [P(SolverOptions)]),

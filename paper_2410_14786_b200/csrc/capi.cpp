@@ -183,7 +183,8 @@ void copy_coarse(const CsrMatrix& A, int32_t* nnz, int32_t* rp, int32_t* ci, dou
 extern "C" {
 
 const char* bddc_last_error(void) { return g_last_error.c_str(); }
-int32_t bddc_abi_version(void) { return 2; }
+int32_t bddc_abi_version(void) { return 3; }
+const char* bddc_switch_name(int32_t i) { return env_switch_name(i); }
 
 int64_t bddc_kernel_launches(void) { return g_kernel_launches.load(); }
 
@@ -573,6 +574,10 @@ int bddc_gpu_get_stats(const bddc_gpu_ctx* c, bddc_stats* st) {
         st->global_dofs = g.problem().decomposition.global_dofs;
         st->n_coarse = g.problem().constraints.n_coarse;
         st->unique_subdomains = g.setup().unique_subdomains;
+        st->graph_captures = g.graph_captures();
+        st->coarse_mode = g.coarse_mode();
+        st->switches = g.switches();
+        st->setup_device_seconds = g.setup_device_seconds();
         for (const auto& sub : g.setup().subs) {
             st->interior_dofs += sub.n_interior;
             st->max_interior = std::max(st->max_interior, sub.n_interior);

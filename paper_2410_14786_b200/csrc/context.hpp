@@ -108,6 +108,10 @@ public:
     const BddcSetup& setup() const;
     const ProblemData& problem() const;
     double setup_seconds() const;
+    double setup_device_seconds() const;
+    std::int64_t graph_captures() const;
+    int coarse_mode() const;  // in effect (direct mode falls back to coarse CG above the dense cap)
+    int switches() const;     // env_switch_mask() at creation
     std::int64_t apply_bytes() const;       // algorithmic FP64 bytes per apply
     std::int64_t interior_apply_bytes() const;  // algorithmic bytes of the two interior solves of an apply
     std::int64_t interior_pass_bytes() const;  // stream bytes of one batched interior solve
@@ -124,6 +128,10 @@ private:
     struct Impl;
     std::unique_ptr<Impl> impl_;
 };
+
+// BDDC_* environment switches: bit i of the mask = switch i is set.
+const char* env_switch_name(int i);
+int env_switch_mask();
 
 std::optional<double> condition_estimate(const std::vector<double>& alphas,
                                          const std::vector<double>& betas);

@@ -137,6 +137,17 @@ void sampled_symmetry_check(const CsrMatrix& A) {
     }
 }
 
+// Every BDDC_* environment switch the library reads, in mask-bit order.
+const char* const kEnvSwitches[] = {
+    "BDDC_SPLIT", "BDDC_HARMONIC", "BDDC_GRAPH", "BDDC_FUSED_EX", "BDDC_P2P", "BDDC_COOP_COARSE",
+    "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
+    "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
+    "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS"};
+constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
+
+// Largest coarse dimension served by the dense replicated A_c^-1 (n_c^2 doubles per GPU, n_c
+// doubles of r_c in the K_i kernel's shared memory); above it the coarse solve is the coarse CG.
+constexpr index_t kDenseCoarseMax = 16384;
 }  // namespace
 
 struct GpuContext::Impl {
@@ -338,6 +349,9 @@ struct GpuContext::Impl {
     }
     // timing experiments only (wrong results): BDDC_NO_EXCHANGE=1 skips every exchange
     bool no_exchange = std::getenv("BDDC_NO_EXCHANGE") && std::atoi(std::getenv("BDDC_NO_EXCHANGE")) == 1;
+    std::int64_t graph_captures = 0;  // PCG iteration graphs captured (stats)
+    int switch_mask = 0;              // env_switch_mask() at creation (stats)
+    double setup_device_s = 0.0;      // device setup kernels (stats)
     std::vector<std::int32_t> halo_soff, halo_roff, iface_soff, iface_roff;
     index_t n_global = 0, n_rows = 0, n_owned = 0;
     std::string symmetry_error;  // distributed: global symmetry check done once at creation
@@ -947,6 +961,29 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaDeviceSynchronize());
     }
 
+    // smallest global index of a non-finite entry of v over the owned rows of every rank (a
+    // collective in the distributed case), 1e300 if there is none
+    double first_nonfinite_global(const double* v, cudaStream_t s) {
+        DBuf<int> bad;
+        bad.alloc(1);
+        device_first_nonfinite(dist() ? static_cast<int>(n_owned) : static_cast<int>(pb.decomposition.global_dofs), v,
+                               bad.p, s);
+        int idx = 0;
+        BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        double first = idx != 0x7fffffff ? static_cast<double>(global_index(idx)) : 1e300;
+        if (dist()) {  // each rank owns its rows
+            DBuf<double> all;
+            all.alloc(comm->world());
+            BDDC_CUDA(cudaMemcpy(all.p + comm->rank(), &first, sizeof(double), cudaMemcpyHostToDevice));
+            comm->allgather_inplace(all.p, 1, s);
+            std::vector<double> h(comm->world());
+            BDDC_CUDA(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+            BDDC_CUDA(cudaStreamSynchronize(s));
+            first = *std::min_element(h.begin(), h.end());
+        }
+        return first;
+    }
     index_t global_index(int local) const {
         return dist() && local >= 0 && local < static_cast<int>(plan->local_to_global.size()) ? plan->local_to_global[local]
                                                                                                : local;
@@ -1090,23 +1127,7 @@ struct GpuContext::Impl {
         }
         const double normb = pinned[0];
         if (!std::isfinite(normb)) {  // every rank sees the same ||b||: the decision is collective
-            DBuf<int> bad;
-            bad.alloc(1);
-            device_first_nonfinite(dist() ? static_cast<int>(n_owned) : static_cast<int>(n), b, bad.p, s);
-            int idx = 0;
-            BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-            BDDC_CUDA(cudaStreamSynchronize(s));
-            double first = idx != 0x7fffffff ? static_cast<double>(global_index(idx)) : 1e300;
-            if (dist()) {  // smallest global index over the ranks (each owns its rows)
-                DBuf<double> all;
-                all.alloc(comm->world());
-                BDDC_CUDA(cudaMemcpy(all.p + comm->rank(), &first, sizeof(double), cudaMemcpyHostToDevice));
-                comm->allgather_inplace(all.p, 1, s);
-                std::vector<double> h(comm->world());
-                BDDC_CUDA(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
-                BDDC_CUDA(cudaStreamSynchronize(s));
-                first = *std::min_element(h.begin(), h.end());
-            }
+            const double first = first_nonfinite_global(b, s);
             if (first < 1e300)  // else: finite entries whose squares overflow (the reference carries on)
                 throw std::invalid_argument("pcg rhs: non-finite entry at index " +
                                             std::to_string(static_cast<long long>(first)));
@@ -1156,7 +1177,11 @@ struct GpuContext::Impl {
         };
         if (graphed) {
             const bool prof = opt.profile;
-            if (!graphs.valid || std::memcmp(&graphs.key, &D, sizeof D) != 0 || graphs.precondition != precondition ||
+            // the cached graphs are keyed by the kernels' parameter block; its padding bytes (and
+            // those of the nested Publish blocks) are indeterminate, so they are zeroed first
+            PcgDevice key = D;
+            __builtin_clear_padding(&key);
+            if (!graphs.valid || std::memcmp(&graphs.key, &key, sizeof key) != 0 || graphs.precondition != precondition ||
                 graphs.profile != prof) {
                 graphs.reset();
                 graphs.a = capture(s, [&] { check_part(0); }, &graphs.a_kernels);
@@ -1215,7 +1240,8 @@ struct GpuContext::Impl {
                     }
                 }
                 graphs.b_graph = gb;
-                graphs.key = D;
+                std::memcpy(&graphs.key, &key, sizeof key);
+                ++graph_captures;
                 graphs.precondition = precondition;
                 graphs.profile = prof;
                 graphs.valid = true;
@@ -1258,15 +1284,15 @@ struct GpuContext::Impl {
                 BDDC_CUDA(cudaStreamSynchronize(s));
                 throw std::runtime_error("matrix not SPD");
             }
-            if (pinned[3] == 2.0) {
+            if (pinned[3] == 2.0 && precondition && !(pinned[2] != 0.0) && it < o.max_iterations) {
+                // the reference's next M(r) rejects a non-finite r (ensure_finite,
+                // preconditioner.cpp:229); a finite r whose norm overflowed carries on, and so
+                // does plain CG (no apply)
                 BDDC_CUDA(cudaStreamSynchronize(s));
-                DBuf<int> bad;
-                bad.alloc(1);
-                device_first_nonfinite(n, rd, bad.p, s);
-                int idx = 0;
-                BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-                BDDC_CUDA(cudaStreamSynchronize(s));
-                throw std::invalid_argument("bddc apply: non-finite entry at index " + std::to_string(global_index(idx)));
+                const double first = first_nonfinite_global(rd, s);  // collective over the ranks
+                if (first < 1e300)
+                    throw std::invalid_argument("bddc apply: non-finite entry at index " +
+                                                std::to_string(static_cast<long long>(first)));
             }
             rel = pinned[1];
             rep.iterations = it;
@@ -1335,6 +1361,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     }
     I.opt = opt;
     I.device = opt.device;
+    I.switch_mask = env_switch_mask();
+    if (I.no_exchange && !(std::getenv("BDDC_EXPERIMENTS") && std::atoi(std::getenv("BDDC_EXPERIMENTS")) == 1))
+        throw std::invalid_argument(
+            "BDDC_NO_EXCHANGE=1 skips every inter-GPU exchange (timing experiments, wrong results); "
+            "it needs BDDC_EXPERIMENTS=1");
+    // the dense replicated A_c^-1 only up to kDenseCoarseMax coarse dofs; the coarse CG beyond
+    if (I.opt.coarse_mode == 0 && I.pb.constraints.n_coarse > kDenseCoarseMax) I.opt.coarse_mode = 1;
     BDDC_CUDA(cudaSetDevice(I.device));
     const Decomposition& d = I.pb.decomposition;
     if (static_cast<index_t>(I.pb.local_matrices.size()) != d.n_subdomains ||
@@ -1344,7 +1377,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     FactorOptions fo;
     fo.leaf_size = opt.leaf_size;
     I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, I.pb.coords.empty() ? nullptr : I.pb.coords.data(),
-                         workers, fo, /*assemble=*/!I.plan);
+                         workers, fo, /*assemble=*/!I.plan, /*dense_inverse=*/I.opt.coarse_mode == 0);
     if (I.plan) {
         // A_c needs every subdomain's A_ci: gather the padded per-rank blocks over NCCL, then
         // assemble in ascending global subdomain order exactly like one GPU would
@@ -1378,9 +1411,12 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
             aci[j].assign(b0, b0 + np * np);
             blocks[j] = &aci[j];
         }
-        assemble_coarse(I.setup, blocks, P.primal_all, I.pb.constraints.n_coarse);
+        assemble_coarse(I.setup, blocks, P.primal_all, I.pb.constraints.n_coarse, I.opt.coarse_mode == 0);
         I.setup.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
+    // A_c not SPD: no dense inverse; the coarse CG then fails inside the apply exactly like the
+    // reference's (preconditioner.cpp:141-157 -> pcg "matrix not SPD")
+    if (I.opt.coarse_mode == 0 && I.setup.coarse_inverse.empty()) I.opt.coarse_mode = 1;
     int nsm = 148;
     BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
     // CTA pairs always: with more subdomains than SMs they run in waves, and halving the shared-
@@ -1685,6 +1721,18 @@ void GpuContext::stage_host(Stage st, const double* in0, const double* in1, cons
 const BddcSetup& GpuContext::setup() const { return impl_->setup; }
 const ProblemData& GpuContext::problem() const { return impl_->pb; }
 double GpuContext::setup_seconds() const { return impl_->setup.seconds; }
+double GpuContext::setup_device_seconds() const { return impl_->setup_device_s; }
+std::int64_t GpuContext::graph_captures() const { return impl_->graph_captures; }
+int GpuContext::coarse_mode() const { return impl_->opt.coarse_mode; }
+int GpuContext::switches() const { return impl_->switch_mask; }
+
+const char* env_switch_name(int i) { return i >= 0 && i < kNumEnvSwitches ? kEnvSwitches[i] : nullptr; }
+int env_switch_mask() {
+    int m = 0;
+    for (int i = 0; i < kNumEnvSwitches; ++i)
+        if (std::getenv(kEnvSwitches[i])) m |= 1 << i;
+    return m;
+}
 std::int64_t GpuContext::factor_values() const { return impl_->factor_vals; }
 std::int64_t GpuContext::interior_pass_bytes() const { return impl_->solve_stream_bytes; }
 int GpuContext::solve_parts() const { return impl_->launch.cluster; }

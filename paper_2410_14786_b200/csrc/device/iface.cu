@@ -122,6 +122,21 @@ __device__ __forceinline__ double coarse_entry(const IfaceParams& P, int q, std:
     return acc;
 }
 
+// h rows rb, rb + stride, ... (< r1) for n_primal > 32: lane-strided Phi_G x_c partial sums
+__device__ __noinline__ void wide_phi_rows(const IfaceParams& P, const SubdomainDesc& sd, const double* phig,
+                                           const double* xl, const double* kg, int rb, int r1, int r0, int stride,
+                                           int count, int lane) {
+    const int np = sd.n_primal;
+    for (int q = 0; q < count; ++q) {
+        const int row = rb + q * stride;
+        if (row >= r1) break;  // warp-uniform
+        double part = 0.0;
+        for (int j = lane; j < np; j += 32) part = fma(phig[row * np + j], xl[j], part);
+        const double c = warp_sum(part);
+        if (lane == 0) P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + kg[row - r0]);
+    }
+}
+
 __global__ void __launch_bounds__(kLocalThreads)
 iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
     pdl_trigger();
@@ -234,6 +249,10 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
         const double* phig = P.phig + sd.phig;
         constexpr int kB = 8;  // rows per batch: their Phi_G / weight loads issue together
         for (int rb = r0 + warp; rb < r1; rb += kB * kWarps) {
+            if (np > 32) {  // general constraint sets: more than one primal column per lane
+                wide_phi_rows(P, sd, phig, xl, kg, rb, r1, r0, kWarps, kB, lane);
+                continue;
+            }
             double ph[kB], w[kB];
 #pragma unroll
             for (int q = 0; q < kB; ++q) {

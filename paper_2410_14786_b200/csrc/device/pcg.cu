@@ -65,12 +65,14 @@ __global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevic
 
 // pcg.cpp:94-100: relative residual, history, convergence / failure flags (one thread)
 __device__ __forceinline__ void check_scalar(const PcgDevice& D, int it, double rr) {
-    if (D.scal[3] == 0.0) {
+    if (D.scal[3] != 1.0) {
         const double normb = D.scal[0];
         const double rel = sqrt(rr) / normb;
         D.hist[it] = rel;
         D.scal[1] = rel;
-        if (!isfinite(rel)) D.scal[3] = 2.0;
+        // 2 = this iteration's residual norm is not finite (the host decides: the reference
+        // throws only from the next apply's ensure_finite, preconditioner.cpp:229)
+        D.scal[3] = isfinite(rel) ? 0.0 : 2.0;
         if (rel <= D.rtol || (D.atol > 0.0 && rel * normb <= D.atol)) D.scal[2] = 1.0;
     }
     if (D.host_scal) {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     pdl_wait();
     const int it = *D.iter;
     const double pq = sum_ranks(D, D.red_a, D.red_a_n, 0, D.seq_pq, scratch);
-    if (!(pq > 0.0)) {  // pcg.cpp:75-78 "matrix not SPD"
+    if (pq <= 0.0) {  // pcg.cpp:75-78 "matrix not SPD" (a NaN curvature carries on, like the reference)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             D.scal[3] = 1.0;
             if (D.host_scal) reinterpret_cast<volatile double*>(D.host_scal)[3] = 1.0;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kVecThreads) check_kernel(const PcgDevice D, i
     pdl_trigger();
     pdl_wait();
     const int it = *D.iter;
-    if (D.scal[3] != 0.0) return;
+    if (D.scal[3] == 1.0) return;
     const double rr = sum_ranks(D, D.red_b, D.red_b_n, 1, D.seq_rr, scratch);
     if (threadIdx.x == 0) check_scalar(D, it, rr);
 }

@@ -229,7 +229,8 @@ void spd_inverse(std::vector<double>& a, index_t n, const char* what) {
 // assemble_coarse (preconditioner.cpp:68-98): triplets in ascending subdomain order, then
 // from_triplets (duplicates summed in input order); plus the dense inverse for the GEMV.
 void assemble_coarse(BddcSetup& out, const std::vector<const std::vector<double>*>& aci,
-                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse) {
+                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse,
+                     bool dense_inverse) {
     std::vector<Triplet> entries;
     const index_t nsub = static_cast<index_t>(aci.size());
     for (index_t i = 0; i < nsub; ++i) {
@@ -249,18 +250,24 @@ void assemble_coarse(BddcSetup& out, const std::vector<const std::vector<double>
             }
     }
     out.coarse_matrix = CsrMatrix::from_triplets(n_coarse, n_coarse, std::move(entries));
+    out.coarse_inverse.clear();
+    if (!dense_inverse) return;
     const index_t nc = n_coarse;
     out.coarse_inverse.assign(static_cast<std::size_t>(nc) * nc, 0.0);
     for (index_t r = 0; r < nc; ++r)
         for (index_t p = out.coarse_matrix.row_offsets[r]; p < out.coarse_matrix.row_offsets[r + 1]; ++p)
             out.coarse_inverse[static_cast<std::size_t>(r) * nc + out.coarse_matrix.col_indices[p]] =
                 out.coarse_matrix.values[p];
-    spd_inverse(out.coarse_inverse, nc, "coarse matrix");
+    try {
+        spd_inverse(out.coarse_inverse, nc, "coarse matrix");
+    } catch (const std::runtime_error&) {
+        out.coarse_inverse.clear();  // not SPD: the caller falls back to the coarse CG
+    }
 }
 
 BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& d,
                      const ConstraintSet& cs, const index_t* coords, index_t workers,
-                     const FactorOptions& fopt, bool assemble) {
+                     const FactorOptions& fopt, bool assemble, bool dense_inverse) {
     const auto t0 = std::chrono::steady_clock::now();
     const index_t nsub = d.n_subdomains;
     if (static_cast<index_t>(locals.size()) != nsub ||
@@ -315,7 +322,7 @@ BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& 
     if (assemble) {
         std::vector<const std::vector<double>*> blocks(nsub);
         for (index_t i = 0; i < nsub; ++i) blocks[i] = &out.subs[i].aci;
-        assemble_coarse(out, blocks, cs.primal_maps, cs.n_coarse);
+        assemble_coarse(out, blocks, cs.primal_maps, cs.n_coarse, dense_inverse);
     }
     out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return out;

@@ -41,14 +41,16 @@ struct BddcSetup {
 // (preconditioner.cpp:119-121).
 // assemble = false skips the coarse problem (multi-GPU: assembled after gathering every
 // rank's A_ci, see assemble_coarse).
+// dense_inverse = false skips A_c^-1 (coarse CG mode); a non-SPD A_c leaves it empty.
 BddcSetup bddc_setup(const std::vector<CsrMatrix>& locals, const Decomposition& d,
                      const ConstraintSet& cs, const index_t* coords, index_t workers,
-                     const FactorOptions& fopt = {}, bool assemble = true);
+                     const FactorOptions& fopt = {}, bool assemble = true, bool dense_inverse = true);
 
 // A_c = sum_i R_ci^T A_ci R_ci in ascending i (reference assemble_coarse,
 // preconditioner.cpp:68-98) and its dense inverse, into out.coarse_matrix / coarse_inverse.
 void assemble_coarse(BddcSetup& out, const std::vector<const std::vector<double>*>& aci,
-                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse);
+                     const std::vector<std::vector<index_t>>& primal_maps, index_t n_coarse,
+                     bool dense_inverse = true);
 
 // Dense helpers (row-major).
 // In-place inverse via LU with partial pivoting; throws "singular" on a zero pivot.

@@ -16,7 +16,7 @@ def test_library_exports_header_symbols():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
-    assert _lib.lib().bddc_abi_version() == 2
+    assert _lib.lib().bddc_abi_version() == 3
     assert _lib.lib().bddc_kernel_launches() == 0  # nothing launched on a CPU-only host
 
 

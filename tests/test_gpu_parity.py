@@ -7,7 +7,10 @@ additivity, coarse-CG failure (test_bddc.cpp:357-369), PCG KATs (test_krylov.cpp
 acceptance iteration counts (proj/test_output.txt:15). Reference outputs come from
 tests/golden (the unmodified reference) and from the CPU oracle for arbitrary inputs.
 Tolerances: apply / solution 1e-10 relative, residual histories 1e-10 (conftest.history_err),
-iterations exact (the +-1 budget of BASELINE.json is never needed).
+iterations exact. Two documented exceptions, each backed by a CPU test showing that the
+reference's own algorithm moves by more when only its summation order changes
+(tests/test_oracle_golden.py): h4m8's BDDC history (1e-7) and heterogeneous plain CG (iteration
+band of the pairwise vs sequential sums).
 """
 import numpy as np
 import pytest
@@ -132,11 +135,11 @@ def test_rectangular_and_heterogeneous_vs_reference(gpu, name):
     pre = Preconditioner(p)
     x, rep = pre.pcg(p.rhs(), OPTS)
     assert abs(rep.iterations - int(g["pcg_report"][0])) <= 1
-    # Heterogeneous coefficients amplify rounding: the CPU oracle itself (same algorithm,
-    # SuperLU instead of the reference's LU, coarse CG to 1e-12 like the reference) differs
-    # from the reference by 9.5e-9 on h4m8's history while the solutions agree to 1.5e-13.
-    # The history gate there is 1e-7; solutions keep the 1e-10 gate.
-    htol = 1e-7 if dm else 1e-10
+    # h4m8 alone keeps a 1e-7 history gate: changing only the summation order of the PCG dot
+    # products moves its history by more than 1e-9 on the CPU oracle itself
+    # (tests/test_oracle_golden.py::test_h4m8_history_sensitivity_is_intrinsic). C5 and the
+    # homogeneous bundles are held to the 1e-10 bar (C5 measures ~2e-12).
+    htol = H4M8_HISTORY_TOL if name == "h4m8" else 1e-10
     assert history_err(rep.residual_history, g["pcg_history"]) <= htol
     if "pcg_x" in g:
         assert np.abs(x - g["pcg_x"]).max() <= 1e-10 * np.abs(g["pcg_x"]).max()
@@ -145,6 +148,25 @@ def test_rectangular_and_heterogeneous_vs_reference(gpu, name):
         assert np.abs(x[::stride] - g["pcg_x_sample"]).max() <= 1e-10 * np.abs(g["pcg_x_sample"]).max()
     if "apply_rhs" in g:
         assert np.abs(pre.apply(p.rhs()) - g["apply_rhs"]).max() <= 1e-11 * np.abs(g["apply_rhs"]).max()
+    if "plain_report" in g:  # BASELINE configs[3] / C4 on the same problem: plain CG (empty M)
+        _, rp = pre.pcg(p.rhs(), OPTS, precondition=False)
+        assert rp.converged
+        if dm:
+            # heterogeneous plain CG is summation-order sensitive: the reference's own algorithm
+            # takes 1,943 (sequential sums) or 1,939 (pairwise) iterations on C5
+            # (test_oracle_golden.py::test_c5_plain_cg_summation_order_band); the GPU's
+            # fixed-tree reductions must land inside that band widened by 1
+            ref = int(g["plain_report"][0])
+            band = PLAIN_BAND.get(name, 1)
+            assert ref - band - 1 <= rp.iterations <= ref + 1, (rp.iterations, ref)
+        else:
+            assert rp.iterations == int(g["plain_report"][0])
+            assert history_err(rp.residual_history, g["plain_history"]) <= 1e-10
+
+
+H4M8_HISTORY_TOL = 1e-7
+# width of the summation-order band below the reference's plain-CG count (pairwise vs sequential)
+PLAIN_BAND = {"c5": 1943 - 1939, "h4m8": 157 - 156}
 
 
 @pytest.mark.parametrize("name", ["h4m8", "c5"])
@@ -159,7 +181,7 @@ def test_ingested_bundle_vs_reference(gpu, name, tmp_path):
     assert p.coords() is None
     x, rep = Preconditioner(p).pcg(p.rhs(), OPTS)
     assert abs(rep.iterations - int(g["pcg_report"][0])) <= 1
-    assert history_err(rep.residual_history, g["pcg_history"]) <= (1e-7 if dm else 1e-10)
+    assert history_err(rep.residual_history, g["pcg_history"]) <= (H4M8_HISTORY_TOL if name == "h4m8" else 1e-10)
     if "pcg_x" in g:
         assert np.abs(x - g["pcg_x"]).max() <= 1e-10 * np.abs(g["pcg_x"]).max()
     else:
@@ -180,6 +202,11 @@ def test_c2_weak_point_vs_reference(gpu):
     # size-independent property: the preconditioner is SPD on the Krylov vectors
     z = pre.apply(p.rhs())
     assert p.rhs() @ z > 0
+    # BASELINE configs[3] / C4: plain CG on the same problem, against the reference's plain CG
+    # (pcg.cpp:63-67 with an empty PreconditionerFn; study.cpp:123-135 compare mode)
+    xp, rp = pre.pcg(p.rhs(), OPTS, precondition=False)
+    assert rp.converged and rp.iterations == int(g["plain_report"][0]) == 1649
+    assert history_err(rp.residual_history, g["plain_history"]) <= 1e-10
 
 
 def test_coarse_cg_mode_matches_direct_and_fails_like_reference(gpu):
@@ -269,3 +296,31 @@ def test_c3_strong_scaling_point_vs_reference(gpu):
     assert history_err(rep.residual_history, g["pcg_history"]) <= 1e-10
     stride = int(g["pcg_x_sample_stride"][0])
     assert np.abs(x[::stride] - g["pcg_x_sample"]).max() <= 1e-10 * np.abs(g["pcg_x_sample"]).max()
+
+
+def test_wide_primal_sets_vs_oracle(gpu):
+    # n_primal > 32 (more than one coarse column per lane in the K_i kernel's
+    # Phi_G x_c). Every interface dof becomes a primal vertex constraint (n_primal 79 per
+    # subdomain at k=2, m=40); the reference / oracle accept arbitrary ConstraintSets
+    # (preconditioner.hpp:62-104).
+    prob = o.assemble_poisson(2, 2, 40)
+    d = prob.decomposition
+    gamma = sorted({int(g) for dofs, ni in zip(d.subdomain_dofs, d.interior_counts) for g in dofs[int(ni):]})
+    cid = {g: c for c, g in enumerate(gamma)}
+    mats, maps = [], []
+    for dofs, ni in zip(d.subdomain_dofs, d.interior_counts):
+        ni, nl = int(ni), len(dofs)
+        rows = np.arange(nl - ni, dtype=np.int32)
+        mats.append(o.Csr(nl - ni, nl, np.arange(nl - ni + 1, dtype=np.int32), np.arange(ni, nl, dtype=np.int32),
+                          np.ones(nl - ni)))
+        maps.append(np.array([cid[int(g)] for g in dofs[ni:]], dtype=np.int32))
+        assert rows.size > 32
+    cs = o.ConstraintSet(mats, maps, len(gamma))
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, d, cs)
+    tup = lambda m: (m.nrows, m.ncols, m.rowptr, m.cols, m.vals)  # noqa: E731
+    gp = Problem.from_arrays(tup(prob.global_matrix), [tup(m) for m in prob.local_matrices], d.subdomain_dofs,
+                             d.interior_counts, d.weights, [tup(m) for m in mats], maps, len(gamma))
+    pre = Preconditioner(gp)
+    r = o.study_rhs(d.global_dofs, 3)
+    zr = P.apply(r)
+    assert np.abs(pre.apply(r) - zr).max() <= 1e-10 * np.abs(zr).max()

@@ -55,3 +55,40 @@ def test_switch_keeps_parity(gpu, env):
         assert herr <= 1e-10, (name, herr)
         assert xerr <= 1e-10, (name, xerr)
         assert aerr <= 1e-11, (name, aerr)
+
+
+def test_switches_reported_and_no_exchange_guarded(gpu):
+    # the active BDDC_* switches are reported in the stats, and the wrong-results
+    # timing switch BDDC_NO_EXCHANGE=1 is refused unless BDDC_EXPERIMENTS=1 is also set
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2410_14786_b200 import Preconditioner, Problem, lib\n"
+            "p = Problem.poisson(16, 2)\n"
+            "try:\n    pre = Preconditioner(p)\nexcept Exception as e:\n    print('ERR', e); raise SystemExit(0)\n"
+            "st = pre.stats(); names = [lib().bddc_switch_name(i).decode() for i in range(32) "
+            "if st['switches'] >> i & 1]\nprint('OK', ','.join(names))\n") % ROOT
+    env = {k: v for k, v in os.environ.items() if not k.startswith("BDDC_")}
+    r = subprocess.run([sys.executable, "-c", code], env={**env, "BDDC_NO_EXCHANGE": "1"}, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "ERR" in r.stdout and "BDDC_EXPERIMENTS" in r.stdout
+    r = subprocess.run([sys.executable, "-c", code], env={**env, "BDDC_PDL": "1"}, capture_output=True, text=True,
+                       timeout=300)
+    assert r.stdout.strip().splitlines()[-1] == "OK BDDC_PDL"
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.stdout.strip().splitlines()[-1] == "OK"
+
+
+def test_repeated_solve_reuses_graphs(gpu):
+    # the cached PCG graphs are keyed by the kernels' parameter block (padding
+    # cleared); an identical second solve must not re-capture
+    sys.path.insert(0, ROOT)
+    from paper_2410_14786_b200 import Preconditioner, Problem, SolverOptions
+
+    p = Problem.poisson(128, 4)
+    pre = Preconditioner(p)
+    opts = SolverOptions(1e-8, 0.0, 10000, True)
+    pre.pcg(p.rhs(), opts)
+    n1 = pre.stats()["graph_captures"]
+    for _ in range(3):
+        pre.pcg(p.rhs(), opts)
+    assert n1 >= 1 and pre.stats()["graph_captures"] == n1
