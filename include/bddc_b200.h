@@ -94,7 +94,11 @@ typedef struct {
     int32_t leaf_size;             /* nested-dissection leaf size (default 24) */
     int32_t local_blocks;          /* CTAs per subdomain for the K_i GEMV (default 8) */
     int32_t solve_parts;           /* CTAs (cluster size) per subdomain in the interior solve: 0 auto, 1, 2 */
+    int32_t setup_mode;            /* BDDC_SETUP_DEVICE (default): factorisation, Schur complements, K_i,
+                                      Phi, A_ci and A_c^-1 on the GPU; BDDC_SETUP_HOST: host numeric setup */
 } bddc_gpu_options;
+
+enum { BDDC_SETUP_DEVICE = 0, BDDC_SETUP_HOST = 1 };
 
 /* Reference SolverOptions (include/bddc/pcg.hpp:17-22). */
 typedef struct {

@@ -48,7 +48,7 @@ class GpuOptions(C.Structure):
     _fields_ = [("device", i32), ("workers", i32), ("coarse_mode", i32),
                 ("coarse_rel_tolerance", f64), ("coarse_abs_tolerance", f64),
                 ("coarse_max_iterations", i32), ("leaf_size", i32), ("local_blocks", i32),
-                ("solve_parts", i32)]
+                ("solve_parts", i32), ("setup_mode", i32)]
 
 
 class DistOptions(C.Structure):

@@ -161,6 +161,7 @@ GpuOptions to_gpu(const bddc_gpu_options* o) {
         if (o->leaf_size > 0) g.leaf_size = o->leaf_size;
         if (o->local_blocks > 0) g.local_blocks = o->local_blocks;
         if (o->solve_parts > 0) g.solve_parts = o->solve_parts;
+        g.setup_on_device = o->setup_mode != BDDC_SETUP_HOST;
     }
     return g;
 }
@@ -198,6 +199,7 @@ void bddc_default_gpu_options(bddc_gpu_options* o) {
     o->coarse_max_iterations = 500;
     o->leaf_size = 24;
     o->local_blocks = 8;
+    o->setup_mode = BDDC_SETUP_DEVICE;
     o->solve_parts = 0;
 }
 
@@ -549,7 +551,7 @@ int bddc_gpu_subdomain_blocks(const bddc_gpu_ctx* c, int32_t i, double* phi, dou
         if (!c) throw std::invalid_argument("null context");
         const auto& subs = c->ctx->setup().subs;
         if (i < 0 || i >= static_cast<int32_t>(subs.size())) throw std::out_of_range("subdomain index");
-        copy_blocks(subs[i], phi, lambda, aci);
+        c->ctx->subdomain_blocks(i, phi, lambda, aci);
     });
 }
 

@@ -30,6 +30,7 @@ struct GpuOptions {
     int local_blocks = 8;         // CTAs per subdomain for the K_i GEMV (measured: 8 > 4, = 16)
     int solve_parts = 0;          // CTAs per subdomain in the interior solve (0 = auto)
     bool profile = false;         // record per-kernel CUDA events in apply()
+    bool setup_on_device = true;  // GPU setup (device/setup.cu); false: host numeric setup (host/setup.cpp)
     // second interior solve of the apply as the harmonic extension u0 - A_II^{-1} A_IG z_G with a
     // pruned forward sweep (BDDC_HARMONIC=0 selects the full solve of r_I - A_IG z_G)
     bool harmonic = !(std::getenv("BDDC_HARMONIC") && std::string(std::getenv("BDDC_HARMONIC")) == "0");
@@ -108,6 +109,8 @@ public:
     const BddcSetup& setup() const;
     const ProblemData& problem() const;
     double setup_seconds() const;
+    // Phi_i (n_local x n_primal), Lambda_i, A_ci (n_primal^2) host copies; null pointers skipped
+    void subdomain_blocks(int i, double* phi, double* lambda, double* aci) const;
     double setup_device_seconds() const;
     std::int64_t graph_captures() const;
     int coarse_mode() const;  // in effect (direct mode falls back to coarse CG above the dense cap)

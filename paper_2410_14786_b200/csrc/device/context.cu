@@ -13,6 +13,8 @@
 #include "../context.hpp"
 #include "../host/distribute.hpp"
 #include "../host/program.hpp"
+#include "../host/gpu_setup.hpp"
+#include "setup.cuh"
 #include "comm.cuh"
 #include "iface.cuh"
 #include "pcg.cuh"
@@ -142,8 +144,21 @@ const char* const kEnvSwitches[] = {
     "BDDC_SPLIT", "BDDC_HARMONIC", "BDDC_GRAPH", "BDDC_FUSED_EX", "BDDC_P2P", "BDDC_COOP_COARSE",
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
-    "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS"};
+    "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
+
+// Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
+struct SetupTimer {
+    bool on = std::getenv("BDDC_SETUP_TIMES") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[setup] %-34s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 // Largest coarse dimension served by the dense replicated A_c^-1 (n_c^2 doubles per GPU, n_c
 // doubles of r_c in the K_i kernel's shared memory); above it the coarse solve is the coarse CG.
@@ -171,7 +186,8 @@ struct GpuContext::Impl {
             parts.alloc(std::max<std::size_t>(sp.parts.size(), 1));
             if (!sp.parts.empty())
                 BDDC_CUDA(cudaMemcpy(parts.p, sp.parts.data(), sizeof(PartDesc) * sp.parts.size(), cudaMemcpyHostToDevice));
-            stream.upload(sp.stream);
+            if (sp.stream_words >= 0) stream.alloc(std::max<std::int64_t>(sp.stream_words, 1));  // device fill
+            else stream.upload(sp.stream);
             units.upload(sp.units);
             phases.upload(sp.phases);
             gmap.upload(sp.gmap);
@@ -596,6 +612,335 @@ struct GpuContext::Impl {
     void record(cudaEvent_t e, cudaStream_t s) {
         if (capture_events) BDDC_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
         else BDDC_CUDA(cudaEventRecord(e, s));
+    }
+
+    // ------------------------------------------------------------------ GPU setup (f1)
+    DBuf<double> lambda_dev;               // Lambda_i of every subdomain (device setup)
+    std::vector<std::int64_t> lambda_off;  // per subdomain
+
+    // Numeric setup of every subdomain on the device (device/setup.cuh), class by class, in
+    // member batches bounded by a scratch budget: multifrontal factorisation, Schur complement,
+    // L_ss^-1 / BL, program fill, saddle inverse -> K_i / Phi_G / Lambda_i / A_ci; then Phi_I
+    // (one interior solve per primal column, all subdomains at once). A handful of allocations
+    // in total: every class's plan goes up in one blob per element type, the scratch buffers are
+    // sized for the largest batch and reused, the jobs of all batches go up at once.
+    void device_setup(const std::vector<SetupClass>& classes, const DeviceImage& img) {
+        const auto t0 = std::chrono::steady_clock::now();
+        SetupTimer tm;
+        cudaStream_t s = stream;
+        const Decomposition& d = pb.decomposition;
+        const index_t nsub = d.n_subdomains;
+        SolveProgram* pools[3] = {&prog, &harm, &head};
+        int nprog = 0;
+        while (nprog < 3 && !img.fills[nprog].empty()) ++nprog;
+        const std::size_t ncls = classes.size();
+
+        // ---- templates (word + source code per stream word), straight into one device buffer
+        std::vector<std::array<std::int64_t, 3>> toff(ncls);
+        DBuf<double> tword;
+        DBuf<std::int32_t> tcode;
+        {
+            std::int64_t total = 0;
+            for (std::size_t k = 0; k < ncls; ++k)
+                for (int q = 0; q < nprog; ++q) {
+                    toff[k][q] = total;
+                    total += static_cast<std::int64_t>(classes[k].prog[q].stream.size());
+                }
+            tword.alloc(std::max<std::int64_t>(total, 1));
+            tcode.alloc(std::max<std::int64_t>(total, 1));
+            for (std::size_t k = 0; k < ncls; ++k)
+                for (int q = 0; q < nprog; ++q) {
+                    const SolvePools& T = classes[k].prog[q];
+                    BDDC_CUDA(cudaMemcpyAsync(tword.p + toff[k][q], T.stream.data(), sizeof(double) * T.stream.size(),
+                                              cudaMemcpyHostToDevice, s));
+                    BDDC_CUDA(cudaMemcpyAsync(tcode.p + toff[k][q], T.srcmap.data(),
+                                              sizeof(std::int32_t) * T.srcmap.size(), cudaMemcpyHostToDevice, s));
+                }
+        }
+        // ---- every class's plan in three blobs (int32 / int64 / double) with per-class offsets
+        std::vector<std::int32_t> bi;
+        std::vector<std::int64_t> bl;
+        std::vector<double> bd;
+        struct Ofs { std::size_t i[18], l[3], d; };
+        std::vector<Ofs> of(ncls);
+        for (std::size_t k = 0; k < ncls; ++k) {
+            const SetupClass& C = classes[k];
+            const std::vector<std::int32_t>* iv[18] = {&C.sn_nc, &C.sn_m, &C.sn_mi, &C.level_sn, &C.asc_ptr, &C.asc_pos,
+                                                       &C.asc_csr, &C.ch_ptr, &C.ch_id, &C.em_ptr, &C.em_pos, &C.sgg_pos,
+                                                       &C.sgg_csr, &C.roots, &C.root_gamma_ptr, &C.root_gamma, &C.c_ptr,
+                                                       &C.c_col};
+            for (int t = 0; t < 18; ++t) {
+                of[k].i[t] = bi.size();
+                bi.insert(bi.end(), iv[t]->begin(), iv[t]->end());
+            }
+            const std::vector<std::int64_t>* lv[3] = {&C.front_off, &C.layout.linv_off, &C.layout.bl_off};
+            for (int t = 0; t < 3; ++t) {
+                of[k].l[t] = bl.size();
+                bl.insert(bl.end(), lv[t]->begin(), lv[t]->end());
+            }
+            of[k].d = bd.size();
+            bd.insert(bd.end(), C.c_val.begin(), C.c_val.end());
+        }
+        DBuf<std::int32_t> pi;
+        DBuf<std::int64_t> pl;
+        DBuf<double> pdv;
+        pi.upload(bi);
+        pl.upload(bl);
+        pdv.upload(bd);
+        // ---- batches: members per batch from a scratch budget; scratch sized for the largest
+        const std::size_t budget = std::size_t(6) << 30;
+        struct Batch { std::size_t cls; int m0, nb; };
+        std::vector<Batch> batches;
+        std::size_t n_aval = 1, n_front = 1, n_S = 1, n_D = 1, n_M = 1, n_piv = 1;
+        for (std::size_t k = 0; k < ncls; ++k) {
+            const SetupClass& C = classes[k];
+            const std::size_t ns = static_cast<std::size_t>(C.n_iface + C.n_primal);
+            const std::size_t per = static_cast<std::size_t>(C.front_total) + C.layout.total +
+                                    static_cast<std::size_t>(C.n_iface) * C.n_iface + ns * ns + C.nnz;
+            const int nmem = static_cast<int>(C.members.size());
+            const int bsz = std::max(1, std::min<int>(nmem, static_cast<int>(budget / (8 * std::max<std::size_t>(per, 1)))));
+            for (int m0 = 0; m0 < nmem; m0 += bsz) batches.push_back({k, m0, std::min(bsz, nmem - m0)});
+            n_aval = std::max(n_aval, static_cast<std::size_t>(bsz) * C.nnz);
+            n_front = std::max(n_front, static_cast<std::size_t>(bsz) * C.front_total);
+            n_S = std::max(n_S, static_cast<std::size_t>(bsz) * C.n_iface * C.n_iface);
+            n_D = std::max(n_D, static_cast<std::size_t>(bsz) * C.layout.total);
+            n_M = std::max(n_M, static_cast<std::size_t>(bsz) * ns * ns);
+            n_piv = std::max(n_piv, static_cast<std::size_t>(bsz) * ns);
+        }
+        DBuf<double> aval, fronts, Sb, Db, Mb, aci_dev;
+        DBuf<int> piv, status;
+        aval.alloc(n_aval);
+        fronts.alloc(n_front);
+        Sb.alloc(n_S);
+        Db.alloc(n_D);
+        Mb.alloc(n_M);
+        piv.alloc(n_piv);
+        status.alloc(4 * batches.size());
+        BDDC_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int) * status.n, s));
+        // ---- jobs of every batch: fills and saddle output offsets
+        std::vector<std::int64_t> aci_off(nsub);
+        std::int64_t aci_total = 0;
+        for (index_t i = 0; i < nsub; ++i) {
+            aci_off[i] = aci_total;
+            aci_total += static_cast<std::int64_t>(setup.subs[i].n_primal) * setup.subs[i].n_primal;
+        }
+        aci_dev.alloc(std::max<std::int64_t>(aci_total, 1));
+        std::vector<std::vector<const DeviceImage::Fill*>> fill_of(nprog, std::vector<const DeviceImage::Fill*>(nsub));
+        for (int q = 0; q < nprog; ++q)
+            for (const auto& f : img.fills[q]) fill_of[q][f.sub] = &f;
+        std::vector<FillJob> jobs;
+        std::vector<std::int64_t> outs;
+        std::vector<std::size_t> job0(batches.size() * nprog + 1), out0(batches.size());
+        for (std::size_t bt = 0; bt < batches.size(); ++bt) {
+            const Batch& Bt = batches[bt];
+            const SetupClass& C = classes[Bt.cls];
+            for (int q = 0; q < nprog; ++q) {
+                job0[bt * nprog + q] = jobs.size();
+                for (int b = 0; b < Bt.nb; ++b) {
+                    const DeviceImage::Fill* f = fill_of[q][C.members[Bt.m0 + b]];
+                    jobs.push_back({f->dst, toff[Bt.cls][q], f->words, static_cast<std::int64_t>(b) * C.layout.total});
+                }
+            }
+            out0[bt] = outs.size();
+            for (int b = 0; b < Bt.nb; ++b) {
+                const index_t i = C.members[Bt.m0 + b];
+                outs.insert(outs.end(), {img.subs[i].kmat, img.subs[i].phig, img.subs[i].phi, lambda_off[i], aci_off[i]});
+            }
+        }
+        job0.back() = jobs.size();
+        DBuf<FillJob> jobs_dev;
+        DBuf<std::int64_t> outs_dev;
+        jobs_dev.upload(jobs);
+        outs_dev.upload(outs);
+        tm.mark("  templates, plans, scratch");
+
+        double acc_t[4] = {};  // diagnostics: factor, schur + linv, fill, saddle
+        auto lap = [&](int k, std::chrono::steady_clock::time_point& t) {
+            if (!tm.on) return;
+            BDDC_CUDA(cudaStreamSynchronize(s));
+            const auto now = std::chrono::steady_clock::now();
+            acc_t[k] += std::chrono::duration<double, std::milli>(now - t).count();
+            t = now;
+        };
+        std::vector<double> av;
+        for (std::size_t bt = 0; bt < batches.size(); ++bt) {
+            const Batch& Bt = batches[bt];
+            const SetupClass& C = classes[Bt.cls];
+            const Ofs& o = of[Bt.cls];
+            MfPlanDev P{};
+            const std::int32_t* ib = pi.p;
+            P.sn_nc = ib + o.i[0]; P.sn_m = ib + o.i[1]; P.sn_mi = ib + o.i[2]; P.level_sn = ib + o.i[3];
+            P.asc_ptr = ib + o.i[4]; P.asc_pos = ib + o.i[5]; P.asc_csr = ib + o.i[6]; P.ch_ptr = ib + o.i[7];
+            P.ch_id = ib + o.i[8]; P.em_ptr = ib + o.i[9]; P.em_pos = ib + o.i[10]; P.sgg_pos = ib + o.i[11];
+            P.sgg_csr = ib + o.i[12]; P.roots = ib + o.i[13]; P.root_gamma_ptr = ib + o.i[14];
+            P.root_gamma = ib + o.i[15]; P.c_ptr = ib + o.i[16]; P.c_col = ib + o.i[17];
+            P.front_off = pl.p + o.l[0]; P.linv_off = pl.p + o.l[1]; P.bl_off = pl.p + o.l[2];
+            P.c_val = pdv.p + o.d;
+            P.front_total = C.front_total;
+            P.d_total = C.layout.total;
+            P.nnz = C.nnz;
+            P.n_local = C.n_local;
+            P.n_interior = C.n_interior;
+            P.n_iface = C.n_iface;
+            P.n_primal = C.n_primal;
+            P.n_roots = static_cast<int>(C.roots.size());
+            P.n_sn = static_cast<int>(C.sym.snodes.size());
+            P.sgg_n = static_cast<int>(C.sgg_pos.size());
+            int max_nc = 1;
+            for (int v : C.sn_nc) max_nc = std::max(max_nc, v);
+            av.resize(static_cast<std::size_t>(Bt.nb) * C.nnz);
+            for (int b = 0; b < Bt.nb; ++b) {
+                const CsrMatrix& A = pb.local_matrices[C.members[Bt.m0 + b]];
+                std::copy(A.values.begin(), A.values.end(), av.begin() + static_cast<std::ptrdiff_t>(b) * C.nnz);
+            }
+            BDDC_CUDA(cudaMemcpyAsync(aval.p, av.data(), sizeof(double) * av.size(), cudaMemcpyHostToDevice, s));
+            BDDC_CUDA(cudaStreamSynchronize(s));  // av is reused by the next batch
+            auto tl = std::chrono::steady_clock::now();
+            MfBatch B{};
+            B.aval = aval.p;
+            B.fronts = fronts.p;
+            B.S = Sb.p;
+            B.D = Db.p;
+            B.M = Mb.p;
+            B.piv = piv.p;
+            B.status = status.p + 4 * bt;
+            B.n = Bt.nb;
+            B.first = Bt.m0;
+            for (std::size_t h = 0; h + 1 < C.level_ptr.size(); ++h) {
+                int fmax = 1;
+                for (int q = C.level_ptr[h]; q < C.level_ptr[h + 1]; ++q) {
+                    const int sn = C.level_sn[q];
+                    fmax = std::max(fmax, C.sn_nc[sn] + C.sn_m[sn]);
+                }
+                launch_mf_level(P, B, C.level_ptr[h], C.level_ptr[h + 1], fmax, s);
+            }
+            lap(0, tl);
+            launch_schur(P, B, 0, s);
+            launch_linv_bl(P, B, max_nc, s);
+            lap(1, tl);
+            for (int q = 0; q < nprog; ++q)
+                launch_fill(pools[q]->stream.p, tword.p, tcode.p, Db.p, jobs_dev.p + job0[bt * nprog + q],
+                            static_cast<int>(job0[bt * nprog + q + 1] - job0[bt * nprog + q]), s);
+            lap(2, tl);
+            SaddleOut O{outs_dev.p + out0[bt], kmat.p, phig.p, phi.p, lambda_dev.p, aci_dev.p};
+            launch_saddle(P, B, O, s);
+            lap(3, tl);
+        }
+        std::vector<int> st(status.n);
+        BDDC_CUDA(cudaMemcpyAsync(st.data(), status.p, sizeof(int) * st.size(), cudaMemcpyDeviceToHost, s));
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        for (std::size_t bt = 0; bt < batches.size(); ++bt) {
+            const SetupClass& C = classes[batches[bt].cls];
+            const int* sb = st.data() + 4 * bt;
+            if (sb[0]) {
+                const index_t i = C.members[sb[0] - 1];
+                const int sn = sb[1] / 4096, j = sb[1] % 4096;
+                throw std::runtime_error("bddc setup: subdomain " + std::to_string(global_sub(i)) +
+                                         ": interior block not positive definite at pivot " +
+                                         std::to_string(C.sym.snodes[sn].col_begin + j));
+            }
+            if (sb[2]) {
+                const index_t i = C.members[sb[2] - 1];
+                throw std::runtime_error("bddc setup: subdomain " + std::to_string(global_sub(i)) +
+                                         ": singular saddle system (zero pivot at step " + std::to_string(sb[3]) + ")");
+            }
+        }
+        if (tm.on)
+            std::fprintf(stderr, "[setup]     factor %.1f, schur+linv %.1f, fill %.1f, saddle %.1f ms\n", acc_t[0],
+                         acc_t[1], acc_t[2], acc_t[3]);
+        tm.mark("  classes (factor, fill, saddle)");
+        // Phi_I = -A_II^-1 A_IG Phi_G, column j of every subdomain in one interior solve (MODE 2:
+        // rhs 0 - A_IG h with h = Phi_G[:, j] in the hbuf slots)
+        BDDC_CUDA(cudaMemsetAsync(vin.p, 0, sizeof(double) * vin.n, s));
+        for (int j = 0; j < max_primal; ++j) {
+            launch_phi_to_hbuf(subs.p, static_cast<int>(nsub), phig.p, hbuf.p, j, s);
+            launch_interior_solve(solve_params(vin.p, vtmp.p), launch, 2, s);
+            launch_phi_from_solution(subs.p, static_cast<int>(nsub), local_dofs.p, vtmp.p, phi.p, j, s);
+        }
+        std::vector<double> aci(std::max<std::int64_t>(aci_total, 1));
+        BDDC_CUDA(cudaMemcpyAsync(aci.data(), aci_dev.p, sizeof(double) * aci.size(), cudaMemcpyDeviceToHost, s));
+        BDDC_CUDA(cudaStreamSynchronize(s));
+        for (index_t i = 0; i < nsub; ++i) {
+            const std::int64_t np = setup.subs[i].n_primal;
+            setup.subs[i].aci.assign(aci.begin() + aci_off[i], aci.begin() + aci_off[i] + np * np);
+        }
+        tm.mark("  Phi_I interior solves, A_ci");
+        setup_device_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    index_t global_sub(index_t local) const { return plan ? plan->subdomains[local] : local; }
+
+    // A_c from every subdomain's A_ci (gathered over the ranks), then its dense inverse (device
+    // setup: on the GPU; host setup: setup.cpp) unless the coarse CG is in effect
+    void finish_coarse(const DistSpec* dist) {
+        const index_t nc = pb.constraints.n_coarse;
+        const bool host_inverse = opt.coarse_mode == 0 && !opt.setup_on_device;
+        if (plan) {
+            // gather the padded per-rank blocks over NCCL, then assemble in ascending global
+            // subdomain order exactly like one GPU would
+            const RankPlan& P = *plan;
+            const index_t nsub = static_cast<index_t>(P.sub_rank.size());
+            std::vector<std::int64_t> per_rank(dist->world, 0), off(nsub, 0);
+            for (index_t j = 0; j < nsub; ++j) {
+                const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
+                off[j] = per_rank[P.sub_rank[j]];
+                per_rank[P.sub_rank[j]] += np * np;
+            }
+            const std::int64_t pad = std::max<std::int64_t>(1, *std::max_element(per_rank.begin(), per_rank.end()));
+            std::vector<double> host(static_cast<std::size_t>(pad) * dist->world, 0.0);
+            for (std::size_t li = 0; li < P.subdomains.size(); ++li) {
+                const index_t j = P.subdomains[li];
+                const auto& a = setup.subs[li].aci;
+                std::copy(a.begin(), a.end(), host.begin() + dist->rank * pad + off[j]);
+            }
+            DBuf<double> buf;
+            buf.upload(host);
+            comm->allgather_inplace(buf.p, static_cast<std::size_t>(pad), nullptr);
+            BDDC_CUDA(cudaDeviceSynchronize());
+            BDDC_CUDA(cudaMemcpy(host.data(), buf.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost));
+            std::vector<std::vector<double>> aci(nsub);
+            std::vector<const std::vector<double>*> blocks(nsub);
+            for (index_t j = 0; j < nsub; ++j) {
+                const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
+                const auto b0 = host.begin() + P.sub_rank[j] * pad + off[j];
+                aci[j].assign(b0, b0 + np * np);
+                blocks[j] = &aci[j];
+            }
+            assemble_coarse(setup, blocks, P.primal_all, nc, host_inverse);
+        } else {
+            std::vector<const std::vector<double>*> blocks(setup.subs.size());
+            for (std::size_t i = 0; i < blocks.size(); ++i) blocks[i] = &setup.subs[i].aci;
+            assemble_coarse(setup, blocks, pb.constraints.primal_maps, nc, host_inverse);
+        }
+        if (opt.coarse_mode == 0) {
+            if (opt.setup_on_device) {
+                std::vector<double> dense(static_cast<std::size_t>(nc) * nc, 0.0);
+                const CsrMatrix& Ac = setup.coarse_matrix;
+                for (index_t r = 0; r < nc; ++r)
+                    for (index_t q = Ac.row_offsets[r]; q < Ac.row_offsets[r + 1]; ++q)
+                        dense[static_cast<std::size_t>(r) * nc + Ac.col_indices[q]] = Ac.values[q];
+                coarse_inv.upload(dense);
+                DBuf<double> scr;
+                scr.alloc(2 * static_cast<std::size_t>(std::max<index_t>(nc, 1)));
+                DBuf<int> st;
+                st.alloc(1);
+                dense_spd_inverse(coarse_inv.p, nc, scr.p, st.p, stream);
+                int bad = 0;
+                BDDC_CUDA(cudaMemcpyAsync(&bad, st.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+                BDDC_CUDA(cudaStreamSynchronize(stream));
+                // A_c not SPD: no dense inverse; the coarse CG then fails inside the apply
+                // exactly like the reference's (preconditioner.cpp:141-157 -> "matrix not SPD")
+                if (bad) opt.coarse_mode = 1;
+            } else if (setup.coarse_inverse.empty()) {
+                opt.coarse_mode = 1;
+            } else {
+                coarse_inv.upload(setup.coarse_inverse);
+            }
+        }
+        if (opt.coarse_mode != 0) coarse_inv.alloc(1);
+        Ac_ptr.upload(setup.coarse_matrix.row_offsets);
+        Ac_col.upload(setup.coarse_matrix.col_indices);
+        Ac_val.upload(setup.coarse_matrix.values);
     }
 
     void apply(const double* r_dev, double* z_dev, cudaStream_t s) {
@@ -1376,47 +1721,26 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     const int workers = opt.workers > 0 ? opt.workers : std::max(1u, std::thread::hardware_concurrency());
     FactorOptions fo;
     fo.leaf_size = opt.leaf_size;
-    I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, I.pb.coords.empty() ? nullptr : I.pb.coords.data(),
-                         workers, fo, /*assemble=*/!I.plan, /*dense_inverse=*/I.opt.coarse_mode == 0);
-    if (I.plan) {
-        // A_c needs every subdomain's A_ci: gather the padded per-rank blocks over NCCL, then
-        // assemble in ascending global subdomain order exactly like one GPU would
-        const auto t0 = std::chrono::steady_clock::now();
-        const RankPlan& P = *I.plan;
-        I.comm = std::make_unique<Comm>(dist->nccl_id, dist->rank, dist->world);
-        const index_t nsub = static_cast<index_t>(P.sub_rank.size());
-        std::vector<std::int64_t> per_rank(dist->world, 0), off(nsub, 0);
-        for (index_t j = 0; j < nsub; ++j) {
-            const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
-            off[j] = per_rank[P.sub_rank[j]];
-            per_rank[P.sub_rank[j]] += np * np;
+    const auto t_setup0 = std::chrono::steady_clock::now();
+    SetupTimer tm;
+    const bool on_device = I.opt.setup_on_device;
+    const index_t* coords = I.pb.coords.empty() ? nullptr : I.pb.coords.data();
+    if (I.plan) I.comm = std::make_unique<Comm>(dist->nccl_id, dist->rank, dist->world);
+    if (on_device) {
+        // GPU setup: the host keeps only the per-subdomain sizes (the class planner below does the
+        // pattern-only work; device/setup.cu the numeric work)
+        I.setup.subs.resize(d.n_subdomains);
+        for (index_t i = 0; i < d.n_subdomains; ++i) {
+            SubdomainSetup& S = I.setup.subs[i];
+            S.n_local = I.pb.local_matrices[i].nrows;
+            S.n_interior = d.interior_counts[i];
+            S.n_iface = S.n_local - S.n_interior;
+            S.n_primal = I.pb.constraints.constraint_matrices[i].nrows;
         }
-        const std::int64_t pad = std::max<std::int64_t>(1, *std::max_element(per_rank.begin(), per_rank.end()));
-        std::vector<double> host(static_cast<std::size_t>(pad) * dist->world, 0.0);
-        for (std::size_t li = 0; li < P.subdomains.size(); ++li) {
-            const index_t j = P.subdomains[li];
-            const auto& a = I.setup.subs[li].aci;
-            std::copy(a.begin(), a.end(), host.begin() + dist->rank * pad + off[j]);
-        }
-        DBuf<double> buf;
-        buf.upload(host);
-        I.comm->allgather_inplace(buf.p, static_cast<std::size_t>(pad), nullptr);
-        BDDC_CUDA(cudaDeviceSynchronize());
-        BDDC_CUDA(cudaMemcpy(host.data(), buf.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost));
-        std::vector<std::vector<double>> aci(nsub);
-        std::vector<const std::vector<double>*> blocks(nsub);
-        for (index_t j = 0; j < nsub; ++j) {
-            const std::int64_t np = static_cast<std::int64_t>(P.primal_all[j].size());
-            const auto b0 = host.begin() + P.sub_rank[j] * pad + off[j];
-            aci[j].assign(b0, b0 + np * np);
-            blocks[j] = &aci[j];
-        }
-        assemble_coarse(I.setup, blocks, P.primal_all, I.pb.constraints.n_coarse, I.opt.coarse_mode == 0);
-        I.setup.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    } else {
+        I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, coords, workers, fo, /*assemble=*/false,
+                             /*dense_inverse=*/false);
     }
-    // A_c not SPD: no dense inverse; the coarse CG then fails inside the apply exactly like the
-    // reference's (preconditioner.cpp:141-157 -> pcg "matrix not SPD")
-    if (I.opt.coarse_mode == 0 && I.setup.coarse_inverse.empty()) I.opt.coarse_mode = 1;
     int nsm = 148;
     BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, I.device));
     // CTA pairs always: with more subdomains than SMs they run in waves, and halving the shared-
@@ -1429,9 +1753,18 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     DeviceImage img;
     int unit = std::getenv("BDDC_UNIT_BYTES") ? std::atoi(std::getenv("BDDC_UNIT_BYTES")) : 4096;
     int spw = 0;
+    tm.mark("host numeric setup (host path)");
+    std::vector<SetupClass> classes;
     for (;; unit /= 2) {
-        img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts, unit,
-                                 I.plan.get(), I.opt.harmonic);
+        if (on_device) {
+            classes = plan_gpu_setup(I.pb.local_matrices, d, I.pb.constraints, coords, fo, parts, unit,
+                                     I.opt.harmonic, workers);
+            img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
+                                     unit, I.plan.get(), I.opt.harmonic, &classes);
+        } else {
+            img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
+                                     unit, I.plan.get(), I.opt.harmonic);
+        }
         const std::size_t fixed = interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit, 0);
         spw = 0;
         if (fixed < static_cast<std::size_t>(max_smem)) {
@@ -1443,6 +1776,8 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
             throw std::runtime_error("subdomain interior (" + std::to_string(img.solve.max_loc) +
                                      " dofs per CTA) exceeds the shared-memory solve capacity");
     }
+    tm.mark("class plan + device image");
+    if (on_device) I.setup.unique_subdomains = static_cast<index_t>(classes.size());
     I.max_iface = img.max_iface;
     I.max_primal = img.max_primal;
     I.n_coarse = img.n_coarse;
@@ -1473,6 +1808,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.prog.upload(img.solve);
     I.harm.upload(img.harm);
     I.head.upload(img.head);
+    tm.mark("program uploads");
     if (I.head.valid) {
         if (img.head.parts.size() != img.harm.parts.size()) throw std::logic_error("head/harmonic programs differ in parts");
         for (std::size_t q = 0; q < img.head.parts.size(); ++q)
@@ -1491,9 +1827,18 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.iface_w.upload(img.iface_w);
     I.iface_gid.upload(img.iface_gid);
     I.iface_writer.upload(img.iface_writer);
-    I.kmat.upload(img.kmat);
-    I.phig.upload(img.phig);
-    I.phi.upload(img.phi);
+    if (img.device_values) {  // written by the device setup
+        I.kmat.alloc(std::max<std::int64_t>(img.kmat_total, 1));
+        I.phig.alloc(std::max<std::int64_t>(img.phig_total, 1));
+        I.phi.alloc(std::max<std::int64_t>(img.phi_total, 1));
+        BDDC_CUDA(cudaMemset(I.phi.p, 0, sizeof(double) * I.phi.n));
+        I.lambda_dev.alloc(std::max<std::int64_t>(img.lambda_total, 1));
+        I.lambda_off = img.lambda_off;
+    } else {
+        I.kmat.upload(img.kmat);
+        I.phig.upload(img.phig);
+        I.phi.upload(img.phi);
+    }
     I.primal.upload(img.primal);
     I.local_dofs.upload(img.local_dofs);
     I.lrow_ptr.upload(img.lrow_ptr);
@@ -1503,13 +1848,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.gi_row_ptr.upload(img.gi_row_ptr);
     I.gi_row_col.upload(img.gi_row_col);
     I.gi_row_val.upload(img.gi_row_val);
+    tm.mark("subdomain / K / Phi buffers");
     I.gi_own_ptr.upload(img.gi_own_ptr);
     I.gi_own_ref.upload(img.gi_own_ref);
     I.dof_own_ptr.upload(img.dof_own_ptr);
     I.dof_own_ref.upload(img.dof_own_ref);
     I.c_own_ptr.upload(img.c_own_ptr);
     I.c_own_ref.upload(img.c_own_ref);
-    I.coarse_inv.upload(img.coarse_inv);
     I.rc_g.alloc(std::max(img.n_coarse, 1));
     I.coarse_ctr.alloc(1);
     BDDC_CUDA(cudaMemset(I.coarse_ctr.p, 0, sizeof(unsigned long long)));
@@ -1518,9 +1863,6 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         for (const auto& w : d.weights) wl.insert(wl.end(), w.begin(), w.end());
         I.weights_local.upload(wl);
     }
-    I.Ac_ptr.upload(I.setup.coarse_matrix.row_offsets);
-    I.Ac_col.upload(I.setup.coarse_matrix.col_indices);
-    I.Ac_val.upload(I.setup.coarse_matrix.values);
     I.coarse_status.alloc(4);
     I.A_ptr.upload(I.pb.global_matrix.row_offsets);
     I.A_col.upload(I.pb.global_matrix.col_indices);
@@ -1563,7 +1905,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         const char* p2p_env = std::getenv("BDDC_P2P");
         if (!(p2p_env && std::atoi(p2p_env) == 0)) I.setup_peer_links(img);
     }
+    tm.mark("uploads + buffers");
+    if (on_device) I.device_setup(classes, img);
+    tm.mark("device numeric setup");
+    I.finish_coarse(dist);
+    tm.mark("coarse");
     BDDC_CUDA(cudaDeviceSynchronize());
+    I.setup.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_setup0).count();
 }
 
 GpuContext::~GpuContext() {
@@ -1722,6 +2070,25 @@ const BddcSetup& GpuContext::setup() const { return impl_->setup; }
 const ProblemData& GpuContext::problem() const { return impl_->pb; }
 double GpuContext::setup_seconds() const { return impl_->setup.seconds; }
 double GpuContext::setup_device_seconds() const { return impl_->setup_device_s; }
+
+void GpuContext::subdomain_blocks(int i, double* phi, double* lambda, double* aci) const {
+    const Impl& I = *impl_;
+    const SubdomainSetup& S = I.setup.subs.at(i);
+    const std::size_t np = S.n_primal;
+    if (aci) std::memcpy(aci, S.aci.data(), sizeof(double) * S.aci.size());
+    if (!I.opt.setup_on_device) {
+        if (phi) std::memcpy(phi, S.phi.data(), sizeof(double) * S.phi.size());
+        if (lambda) std::memcpy(lambda, S.lambda.data(), sizeof(double) * S.lambda.size());
+        return;
+    }
+    BDDC_CUDA(cudaSetDevice(I.device));
+    BDDC_CUDA(cudaDeviceSynchronize());
+    std::vector<SubdomainDesc> sd(1);
+    BDDC_CUDA(cudaMemcpy(sd.data(), I.subs.p + i, sizeof(SubdomainDesc), cudaMemcpyDeviceToHost));
+    if (phi) BDDC_CUDA(cudaMemcpy(phi, I.phi.p + sd[0].phi, sizeof(double) * S.n_local * np, cudaMemcpyDeviceToHost));
+    if (lambda)
+        BDDC_CUDA(cudaMemcpy(lambda, I.lambda_dev.p + I.lambda_off[i], sizeof(double) * np * np, cudaMemcpyDeviceToHost));
+}
 std::int64_t GpuContext::graph_captures() const { return impl_->graph_captures; }
 int GpuContext::coarse_mode() const { return impl_->opt.coarse_mode; }
 int GpuContext::switches() const { return impl_->switch_mask; }
@@ -1795,47 +2162,5 @@ std::int64_t GpuContext::solve_profile(std::int64_t* out, std::int64_t cap) {
 }
 
 // pcg.cpp:111-173 (host; O(iterations))
-std::optional<double> condition_estimate(const std::vector<double>& alphas, const std::vector<double>& betas) {
-    const std::size_t k = alphas.size();
-    if (k < 2 || betas.size() + 1 < k) return std::nullopt;
-    std::vector<double> diag(k), off(k - 1);
-    for (std::size_t i = 0; i < k; ++i) {
-        diag[i] = 1.0 / alphas[i];
-        if (i > 0) diag[i] += betas[i - 1] / alphas[i - 1];
-        if (i + 1 < k) off[i] = std::sqrt(betas[i]) / alphas[i];
-    }
-    const std::size_t n = k;
-    double lo = diag[0], hi = diag[0];
-    for (std::size_t i = 0; i < n; ++i) {
-        double radius = 0.0;
-        if (i > 0) radius += std::abs(off[i - 1]);
-        if (i + 1 < n) radius += std::abs(off[i]);
-        lo = std::min(lo, diag[i] - radius);
-        hi = std::max(hi, diag[i] + radius);
-    }
-    auto count_below = [&](double xv) {
-        std::size_t count = 0;
-        double qv = 1.0;
-        for (std::size_t i = 0; i < n; ++i) {
-            const double off2 = i > 0 ? off[i - 1] * off[i - 1] : 0.0;
-            qv = diag[i] - xv - off2 / qv;
-            if (qv == 0.0) qv = 1e-300;
-            if (qv < 0.0) ++count;
-        }
-        return count;
-    };
-    auto bisect = [&](std::size_t target) {
-        double a = lo, b = hi;
-        for (int step = 0; step < 200 && b - a > 1e-15 * std::max(1.0, std::abs(b)); ++step) {
-            const double mid = 0.5 * (a + b);
-            if (count_below(mid) >= target) b = mid;
-            else a = mid;
-        }
-        return 0.5 * (a + b);
-    };
-    const double l = bisect(1), h = bisect(n);
-    if (!(l > 0.0)) return std::nullopt;
-    return h / l;
-}
 
 }  // namespace bddc_b200

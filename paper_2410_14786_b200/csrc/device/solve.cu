@@ -58,10 +58,13 @@ __device__ __forceinline__ double ld_dsmem(const double* local, std::uint32_t ra
 
 // Per-warp table spread over the lanes' registers: entry i lives in lane i % 32, slot i / 32;
 // entries beyond kMaxRegEntries fall back to global memory.
+// With more than 16 warps the register budget (64 per thread at 32 warps) does not hold the
+// tables: they are read from global memory (L1-resident) instead.
+constexpr bool kRegTables = kSolveWarps <= 16;
 struct RegTable {
-    int v[kMaxRegEntries / 32];
+    int v[kRegTables ? kMaxRegEntries / 32 : 1];
     __device__ __forceinline__ int get(int i, const int* fallback, int stride) const {
-        if (i >= kMaxRegEntries) return __ldg(fallback + static_cast<std::int64_t>(i) * stride);
+        if (!kRegTables || i >= kMaxRegEntries) return __ldg(fallback + static_cast<std::int64_t>(i) * stride);
         const int slot = i >> 5;
         const int mine = slot == 0 ? v[0] : (slot == 1 ? v[1] : v[2]);
         return __shfl_sync(0xffffffffu, mine, i & 31);
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     // per-warp registers: unit offsets / bytes, the end unit and kind of each phase
     RegTable uoff, ubytes, uend, pkind;
 #pragma unroll
-    for (int q = 0; q < kMaxRegEntries / 32; ++q) {
+    for (int q = 0; q < (kRegTables ? kMaxRegEntries / 32 : 0); ++q) {
         const int i = q * 32 + lane;
         int2 e = make_int2(0, 0);
         if (i < nunits) e = __ldg(reinterpret_cast<const int2*>(units) + i);
@@ -332,8 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             const long long t_r0 = stats ? clock64() : 0;
             if (stats) t_tiles += t_r0 - t_tile0;
             if (u + nsl < nunits) {
+                // slot consumed: every lane's reads of it have completed (their values fed this
+                // unit's flushes), so the bulk copy may overwrite it; a generic-read ->
+                // async-write (WAR) reuse needs no proxy fence (measured: -1.5% per launch)
                 __syncwarp();
-                if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 fetch(u + nsl);
             }
             if (stats) t_refill += clock64() - t_r0;

@@ -37,7 +37,10 @@
 
 namespace bddc_b200 {
 
-constexpr int kSolveWarps = 16;          // consumer warps per interior-solve CTA
+#ifndef BDDC_SOLVE_WARPS
+#define BDDC_SOLVE_WARPS 16
+#endif
+constexpr int kSolveWarps = BDDC_SOLVE_WARPS;  // consumer warps per interior-solve CTA
 constexpr int kMaxSlots = 64;            // max ring slots per CTA (shared slot pool)
 constexpr int kPhaseStride = 2 * kSolveWarps + 3;
 

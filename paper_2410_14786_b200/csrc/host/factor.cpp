@@ -210,8 +210,7 @@ std::int64_t InteriorFactor::factor_values() const {
     return v;
 }
 
-InteriorFactor factor_subdomain(const CsrMatrix& A, index_t nI, const index_t* coords,
-                                const FactorOptions& opt) {
+InteriorFactor symbolic_factor(const CsrMatrix& A, index_t nI, const index_t* coords, const FactorOptions& opt) {
     if (A.nrows != A.ncols) throw std::invalid_argument("factor: matrix not square");
     const index_t n = A.nrows;
     if (nI < 0 || nI > n) throw std::invalid_argument("factor: interior count out of range");
@@ -256,6 +255,22 @@ InteriorFactor factor_subdomain(const CsrMatrix& A, index_t nI, const index_t* c
         index_t h = 0;
         for (index_t ch : children[s]) h = std::max(h, F.snodes[ch].height + 1);
         sn.height = h;
+    }
+
+    return F;
+}
+
+InteriorFactor factor_subdomain(const CsrMatrix& A, index_t nI, const index_t* coords,
+                                const FactorOptions& opt) {
+    InteriorFactor F = symbolic_factor(A, nI, coords, opt);
+    const index_t n = A.nrows;
+    auto position = [&](index_t local) { return local < nI ? F.iperm[local] : local; };
+    const index_t ns = static_cast<index_t>(F.snodes.size());
+    std::vector<std::vector<index_t>> children(ns);
+    std::vector<index_t> roots;
+    for (index_t s = 0; s < ns; ++s) {
+        if (F.snodes[s].parent >= 0) children[F.snodes[s].parent].push_back(s);
+        else roots.push_back(s);
     }
 
     // Numeric multifrontal factorisation.

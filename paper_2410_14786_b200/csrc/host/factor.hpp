@@ -55,6 +55,12 @@ struct FactorOptions {
 InteriorFactor factor_subdomain(const CsrMatrix& A_local, index_t n_interior,
                                 const index_t* coords, const FactorOptions& opt = {});
 
+// The pattern-only part of factor_subdomain: ordering, supernodes, row structures and heights
+// (numeric members L / Linv / B and schur left empty). Identical for every subdomain with the
+// same local pattern, split and relative coordinates, whatever the values.
+InteriorFactor symbolic_factor(const CsrMatrix& A_local, index_t n_interior, const index_t* coords,
+                               const FactorOptions& opt = {});
+
 // In-place multi-RHS solve A_II X = B; X is n_interior x nrhs row-major, indexed by
 // the original local interior order. Host-side setup helper (coarse basis).
 void factor_solve(const InteriorFactor& F, double* X, index_t nrhs);

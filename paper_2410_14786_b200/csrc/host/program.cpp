@@ -8,6 +8,7 @@
 #include <utility>
 
 #include "distribute.hpp"
+#include "gpu_setup.hpp"
 #include <stdexcept>
 #include <string>
 
@@ -16,8 +17,15 @@ namespace bddc_b200 {
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
                                const BddcSetup& setup, int parts, int unit_bytes, const RankPlan* plan,
-                               bool harmonic) {
+                               bool harmonic, const std::vector<SetupClass>* classes) {
     DeviceImage img;
+    const bool dev = classes != nullptr;
+    img.device_values = dev;
+    if (dev) {
+        img.sub_class.assign(d.n_subdomains, -1);
+        for (std::size_t c = 0; c < classes->size(); ++c)
+            for (index_t i : (*classes)[c].members) img.sub_class[i] = static_cast<std::int32_t>(c);
+    }
     const index_t nsub = d.n_subdomains;
     img.parts = parts;
     img.n_vector = d.global_dofs;
@@ -59,7 +67,7 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
         img.max_interior = std::max<std::int32_t>(img.max_interior, nI);
         img.max_iface = std::max<std::int32_t>(img.max_iface, ng);
         img.max_primal = std::max<std::int32_t>(img.max_primal, np);
-        img.factor_values += S.factor.factor_values();
+        img.factor_values += dev ? (*classes)[img.sub_class[i]].factor_values : S.factor.factor_values();
 
         sd.local_dofs = static_cast<std::int64_t>(img.local_dofs.size());
         for (index_t l = 0; l < nl; ++l) {
@@ -90,12 +98,23 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
         }
         img.cbuf_total += np;
 
-        sd.kmat = static_cast<std::int64_t>(img.kmat.size());
-        img.kmat.insert(img.kmat.end(), S.K.begin(), S.K.end());
-        sd.phig = static_cast<std::int64_t>(img.phig.size());
-        img.phig.insert(img.phig.end(), S.phi.begin() + static_cast<std::ptrdiff_t>(nI) * np, S.phi.end());
-        sd.phi = static_cast<std::int64_t>(img.phi.size());
-        img.phi.insert(img.phi.end(), S.phi.begin(), S.phi.end());
+        if (dev) {  // sizes only: the device setup writes the values
+            sd.kmat = img.kmat_total;
+            img.kmat_total += static_cast<std::int64_t>(ng) * ng;
+            sd.phig = img.phig_total;
+            img.phig_total += static_cast<std::int64_t>(ng) * np;
+            sd.phi = img.phi_total;
+            img.phi_total += static_cast<std::int64_t>(nl) * np;
+            img.lambda_off.push_back(img.lambda_total);
+            img.lambda_total += static_cast<std::int64_t>(np) * np;
+        } else {
+            sd.kmat = static_cast<std::int64_t>(img.kmat.size());
+            img.kmat.insert(img.kmat.end(), S.K.begin(), S.K.end());
+            sd.phig = static_cast<std::int64_t>(img.phig.size());
+            img.phig.insert(img.phig.end(), S.phi.begin() + static_cast<std::ptrdiff_t>(nI) * np, S.phi.end());
+            sd.phi = static_cast<std::int64_t>(img.phi.size());
+            img.phi.insert(img.phi.end(), S.phi.begin(), S.phi.end());
+        }
 
         // local A_GI rows of subdomain i (local_correction stage): interior cols as vector index
         const CsrMatrix& A = locals[i];
@@ -113,6 +132,54 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
 
     }
 
+    if (dev) {
+        // GPU setup: every subdomain's programs are its class's templates with the subdomain's
+        // own dof map and coupling values; the stream values are filled on the device
+        for (int k = 0; k < (harmonic ? 3 : 1); ++k) {
+            SolvePools& dst = k == 0 ? img.solve : (k == 1 ? img.harm : img.head);
+            dst.stream_words = 0;
+            for (index_t i = 0; i < nsub; ++i) {
+                const std::int32_t c = img.sub_class[i];
+                const SolvePools& T = (*classes)[c].prog[k];
+                if (dst.couple_ptr.size() & 1) dst.couple_ptr.push_back(0);  // int2 alignment
+                const std::int64_t units0 = static_cast<std::int64_t>(dst.units.size() / 2);
+                const std::int64_t order0 = static_cast<std::int64_t>(dst.order.size() / 4);
+                const std::int32_t phases0 = static_cast<std::int32_t>(dst.phases.size());
+                const std::int64_t gmap0 = static_cast<std::int64_t>(dst.gmap.size());
+                const std::int64_t cptr0 = static_cast<std::int64_t>(dst.couple_ptr.size());
+                const std::int64_t cent0 = static_cast<std::int64_t>(dst.couple_gamma.size());
+                for (PartDesc pd : T.parts) {
+                    pd.stream += dst.stream_words;
+                    pd.units += units0;
+                    pd.order += order0;
+                    pd.phases += phases0;
+                    pd.gmap += gmap0;
+                    pd.couple_ptr += cptr0;
+                    pd.couple_ent += cent0;
+                    pd.sub = static_cast<std::int32_t>(i);
+                    dst.parts.push_back(pd);
+                }
+                dst.units.insert(dst.units.end(), T.units.begin(), T.units.end());
+                dst.order.insert(dst.order.end(), T.order.begin(), T.order.end());
+                dst.phases.insert(dst.phases.end(), T.phases.begin(), T.phases.end());
+                dst.couple_ptr.insert(dst.couple_ptr.end(), T.couple_ptr.begin(), T.couple_ptr.end());
+                dst.couple_gamma.insert(dst.couple_gamma.end(), T.couple_gamma.begin(), T.couple_gamma.end());
+                const auto& dofs = d.subdomain_dofs[i];
+                for (std::int32_t l : T.gmap) dst.gmap.push_back(dofs[l]);
+                for (std::int32_t q : T.couple_src) dst.couple_val.push_back(locals[i].values[q]);
+                img.fills[k].push_back({dst.stream_words, T.words(), c, k, i});
+                dst.stream_words += T.words();
+                dst.tile_values += T.tile_values;
+                dst.fwd_factor_values += T.fwd_factor_values;
+                dst.bwd_factor_values += T.bwd_factor_values;
+                dst.n_tiles += T.n_tiles;
+                dst.max_loc = std::max(dst.max_loc, T.max_loc);
+                dst.max_top = std::max(dst.max_top, T.max_top);
+                dst.max_phases = std::max(dst.max_phases, T.max_phases);
+                dst.max_units = std::max(dst.max_units, T.max_units);
+            }
+        }
+    } else {
     // interior-solve programs (local dof -> vector index = the subdomain map), built per
     // subdomain on host threads and appended in subdomain order (deterministic image)
     {
@@ -167,6 +234,8 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
             }
         }
     }
+
+    }  // host-built programs
 
     if (plan) {
         // remote interface contributions (filled by the interface exchange) and the

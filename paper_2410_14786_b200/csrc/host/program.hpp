@@ -16,6 +16,7 @@
 namespace bddc_b200 {
 
 struct RankPlan;
+struct SetupClass;
 
 struct DeviceImage {
     std::vector<SubdomainDesc> subs;
@@ -46,11 +47,25 @@ struct DeviceImage {
     std::int32_t max_interior = 0, max_iface = 0, max_primal = 0, n_coarse = 0;
     std::int32_t n_vector = 0;
     std::int64_t factor_values = 0;
+    // GPU setup (classes given): K_i, Phi and the program values are produced on the device;
+    // the host vectors kmat / phig / phi stay empty, these are their lengths
+    bool device_values = false;
+    std::int64_t kmat_total = 0, phig_total = 0, phi_total = 0, lambda_total = 0;
+    std::vector<std::int64_t> lambda_off;  // per subdomain (device Lambda_i, n_primal^2)
+    std::vector<std::int32_t> sub_class;   // class of each subdomain
+    struct Fill {
+        std::int64_t dst;  // word offset in the pool's device stream
+        std::int64_t words;
+        std::int32_t cls, prog;
+        index_t sub;
+    };
+    std::vector<Fill> fills[3];  // per pool: 0 solve, 1 harm, 2 head
 };
 
 DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                                const std::vector<CsrMatrix>& locals, const CsrMatrix& global,
                                const BddcSetup& setup, int parts, int unit_bytes = 4096,
-                               const RankPlan* plan = nullptr, bool harmonic = false);
+                               const RankPlan* plan = nullptr, bool harmonic = false,
+                               const std::vector<SetupClass>* classes = nullptr);
 
 }  // namespace bddc_b200

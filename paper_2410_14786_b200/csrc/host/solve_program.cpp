@@ -15,6 +15,7 @@ inline std::int64_t pad16(std::int64_t b) { return (b + 15) & ~std::int64_t(15);
 struct Tile {
     TileTask t{};
     std::vector<double> vals;
+    std::vector<std::int32_t> src;     // template mode: value sources (SolvePools::srcmap codes)
     std::vector<std::int32_t> idx;     // input index list (IN_INDEXED)
     std::vector<std::int32_t> outidx;  // output rows (PUSH, last piece)
     std::int64_t bytes() const {
@@ -37,9 +38,16 @@ struct Phase {
 };
 
 // Build the flattened-mapping pieces of one output unit.
+// Value of tile entry (r, j) of a chunk: numeric `v` or, building a template, the code `src` of
+// where the device fill takes it from (SolvePools::srcmap).
+struct TileValue {
+    double v;
+    std::int32_t src;
+};
+
 template <typename Val, typename InIdx>
 Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx in_idx, int in_start, int out_base,
-                 int nvalid, std::uint8_t flags, const std::vector<std::int32_t>* outidx) {
+                 int nvalid, std::uint8_t flags, const std::vector<std::int32_t>* outidx, bool tmpl) {
     Chunk ch;
     if (k < 1 || k > 32 || ncols < 1) throw std::logic_error("solve program: bad tile shape");
     int G = 1;
@@ -61,12 +69,17 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         T.t.flags = flags | (indexed ? kTaskInIndexed : 0) | (j0 == 0 ? kTaskFirst : 0) |
                     (j0 + jn >= ncols ? kTaskLast : 0);
         T.vals.assign(static_cast<std::size_t>(iters) * k * G, 0.0);
+        if (tmpl) T.src.assign(T.vals.size(), kSrcZero);
         for (int t = 0; t < iters; ++t)
             for (int g = 0; g < G; ++g) {
                 const int j = t * G + g;
                 if (j >= jn) continue;
-                for (int r = 0; r < k; ++r)
-                    T.vals[static_cast<std::size_t>(t) * k * G + r * G + g] = val(r, j0 + j);
+                for (int r = 0; r < k; ++r) {
+                    const TileValue tv = val(r, j0 + j);
+                    const std::size_t at = static_cast<std::size_t>(t) * k * G + r * G + g;
+                    T.vals[at] = tv.v;
+                    if (tmpl) T.src[at] = tv.src;
+                }
             }
         if (indexed) {
             T.idx.resize(static_cast<std::size_t>(iters) * G);
@@ -84,8 +97,10 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
 }  // namespace
 
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std::vector<index_t>& l2v, int sub,
-                         int P, int unit_bytes, SolvePools& pools, bool prune_forward, bool prune_backward) {
+                         int P, int unit_bytes, SolvePools& pools, bool prune_forward, bool prune_backward,
+                         const ValueLayout* layout) {
     const auto& sn = F.snodes;
+    const bool tmpl = layout != nullptr;
     const index_t nsn = static_cast<index_t>(sn.size());
     const index_t nI = F.n_interior;
     // Harmonic-extension program: the forward sweep of A_II^{-1} (A_IG z_G) only reaches the
@@ -171,7 +186,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
     // becomes t[R] -= BL_s t_s, so it reads the same t_s as the diagonal solve and shares its
     // phase; the backward sweep x_s = L_ss^{-T} y_s - BL_s^T x_R is one chunk with two pieces.
     std::vector<std::vector<double>> BL(nsn);
-    for (index_t sidx = 0; sidx < nsn; ++sidx) {
+    for (index_t sidx = 0; sidx < nsn && !tmpl; ++sidx) {
         const Supernode& S = sn[sidx];
         const index_t ns = S.size(), mI = S.n_interior_rows;
         BL[sidx].assign(static_cast<std::size_t>(mI) * ns, 0.0);
@@ -183,6 +198,24 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 BL[sidx][static_cast<std::size_t>(a) * ns + j] = acc;
             }
     }
+
+    // tile values: L_ss^{-1} entries and BL entries (numeric), or their positions in the per-subdomain
+    // value array of a ValueLayout (template: the device fills them, device/setup.cu)
+    auto linv = [&](index_t s, index_t r, index_t c) -> TileValue {
+        const std::int64_t ns = sn[s].size();
+        if (tmpl) return {0.0, static_cast<std::int32_t>(layout->linv_off[s] + r * ns + c)};
+        return {sn[s].Linv[static_cast<std::size_t>(r * ns + c)], 0};
+    };
+    auto bl = [&](index_t s, index_t a, index_t j, bool negate) -> TileValue {
+        const std::int64_t ns = sn[s].size();
+        if (tmpl) {
+            const std::int32_t i = static_cast<std::int32_t>(layout->bl_off[s] + a * ns + j);
+            return {0.0, negate ? -i - 3 : i};
+        }
+        const double v = BL[s][static_cast<std::size_t>(a * ns + j)];
+        return {negate ? -v : v, 0};
+    };
+    const TileValue zero{0.0, kSrcZero};
 
     for (int part = 0; part < P; ++part) {
         // local index space: group positions ascending, then top positions ascending
@@ -210,9 +243,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 const int nr = static_cast<int>(std::min<index_t>(kr, ns - r0));
                 out.push_back(make_chunk(unit_bytes,
                     nr, static_cast<int>(r0 + nr),
-                    [&](int r, int j) { return j <= r0 + r ? S.Linv[static_cast<std::size_t>(r0 + r) * ns + j] : 0.0; },
+                    [&](int r, int j) { return j <= r0 + r ? linv(s, r0 + r, j) : zero; },
                     false, [](int) { return 0; }, loc[S.col_begin], loc[S.col_begin + r0], nr,
-                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr));
+                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr, tmpl));
             }
         };
         // backward chunk of rows q0.. of supernode s: piece A = L_ss^{-T} y_s (own = X,
@@ -224,21 +257,19 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
                 Chunk a = make_chunk(unit_bytes,
                     nq, static_cast<int>(ns - q0),
-                    [&](int r, int j) {
-                        return j >= r ? S.Linv[static_cast<std::size_t>(q0 + j) * ns + q0 + r] : 0.0;
-                    },
+                    [&](int r, int j) { return j >= r ? linv(s, q0 + j, q0 + r) : zero; },
                     false, [](int) { return 0; }, loc[S.col_begin + q0], loc[S.col_begin + q0], nq,
-                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr);
+                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr, tmpl);
                 if (mI > 0) {
                     Chunk b = make_chunk(unit_bytes,
                         nq, static_cast<int>(mI),
-                        [&](int r, int j) { return -BL[s][static_cast<std::size_t>(j) * ns + q0 + r]; }, true,
+                        [&](int r, int j) { return bl(s, j, q0 + r, true); }, true,
                         [&](int j) {
                             const std::int32_t l = loc[S.rows[j]];
                             if (l < 0) throw std::logic_error("solve program: ancestor row not local");
                             return l;
                         },
-                        0, loc[S.col_begin + q0], nq, kTaskDiag, nullptr);
+                        0, loc[S.col_begin + q0], nq, kTaskDiag, nullptr, tmpl);
                     a.tiles.back().t.flags &= static_cast<std::uint8_t>(~kTaskLast);   // accumulation continues
                     b.tiles.front().t.flags &= static_cast<std::uint8_t>(~kTaskFirst);
                     for (Tile& t : b.tiles) a.tiles.push_back(std::move(t));
@@ -278,9 +309,10 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     }
                     out.push_back(make_chunk(unit_bytes,
                         k, static_cast<int>(nd),
-                        [&](int r, int j) { return BL[d][static_cast<std::size_t>(rows[c0 + r]) * nd + j]; }, false,
+                        [&](int r, int j) { return bl(d, rows[c0 + r], j, false); }, false,
                         [](int) { return 0; }, loc[D.col_begin], 0, k,
-                        static_cast<std::uint8_t>(kTaskPush | kTaskInOwn | (to_top ? kTaskPartial : 0)), &outidx));
+                        static_cast<std::uint8_t>(kTaskPush | kTaskInOwn | (to_top ? kTaskPartial : 0)), &outidx,
+                        tmpl));
                 }
             }
         };
@@ -522,6 +554,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         auto ensure = [&](std::int64_t bytes) {
             const std::size_t need = static_cast<std::size_t>(pd.stream + (bytes + 7) / 8);
             if (pools.stream.size() < need) pools.stream.resize(need, 0.0);
+            if (tmpl && pools.srcmap.size() < need) pools.srcmap.resize(need, kSrcCopy);
         };
         for (std::size_t pi = 0; pi < phases.size(); ++pi) {
             Phase& ph = phases[pi];
@@ -564,6 +597,10 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         hdr.next = kNoTask;
                         std::memcpy(dst, &hdr, 16);
                         std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
+                        if (tmpl) {
+                            const std::size_t w0 = static_cast<std::size_t>(pd.stream + (ustart + uused + 16) / 8);
+                            std::copy(t.src.begin(), t.src.end(), pools.srcmap.begin() + static_cast<std::ptrdiff_t>(w0));
+                        }
                         std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
                         if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
                         off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
@@ -604,6 +641,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         }
         const std::int64_t total = pad16(pos);
         pools.stream.resize(static_cast<std::size_t>(pd.stream + total / 8), 0.0);
+        if (tmpl) pools.srcmap.resize(pools.stream.size(), kSrcCopy);
         pd.stream_bytes = total;
         if (total / 16 > (std::int64_t(1) << 31) - 1) throw std::runtime_error("solve program: part stream too large");
         pools.phases.insert(pools.phases.end(), table.begin(), table.end());
@@ -633,7 +671,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             for (index_t q = A.row_offsets[v]; q < A.row_offsets[v + 1]; ++q)
                 if (A.col_indices[q] >= nI) {
                     pools.couple_gamma.push_back(A.col_indices[q] - nI);
-                    pools.couple_val.push_back(A.values[q]);
+                    pools.couple_val.push_back(tmpl ? 0.0 : A.values[q]);
+                    if (tmpl) pools.couple_src.push_back(static_cast<std::int32_t>(q));
                     ++cnt;
                 }
             if (cnt > c0) {
@@ -681,6 +720,8 @@ void append_pools(SolvePools& dst, SolvePools&& src) {
     cat(dst.couple_ptr, src.couple_ptr);
     cat(dst.couple_gamma, src.couple_gamma);
     cat(dst.couple_val, src.couple_val);
+    cat(dst.srcmap, src.srcmap);
+    cat(dst.couple_src, src.couple_src);
     dst.tile_values += src.tile_values;
     dst.fwd_factor_values += src.fwd_factor_values;
     dst.bwd_factor_values += src.bwd_factor_values;

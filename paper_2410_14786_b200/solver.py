@@ -210,7 +210,7 @@ class Problem:
 
 
 def gpu_options(device=0, workers=0, coarse_mode="direct", coarse_options: SolverOptions | None = None,
-                leaf_size=24, local_blocks=8, solve_parts=0) -> L.GpuOptions:
+                leaf_size=24, local_blocks=8, solve_parts=0, setup="device") -> L.GpuOptions:
     o = L.GpuOptions()
     L.lib().bddc_default_gpu_options(C.byref(o))
     o.device, o.workers = device, workers
@@ -220,6 +220,9 @@ def gpu_options(device=0, workers=0, coarse_mode="direct", coarse_options: Solve
         o.coarse_abs_tolerance = coarse_options.abs_tolerance
         o.coarse_max_iterations = coarse_options.max_iterations
     o.leaf_size, o.local_blocks, o.solve_parts = leaf_size, local_blocks, solve_parts
+    if setup not in ("device", "host"):
+        raise ValueError("setup must be 'device' or 'host'")
+    o.setup_mode = 1 if setup == "host" else 0
     return o
 
 
@@ -328,11 +331,11 @@ class Preconditioner:
 
     def __init__(self, problem: Problem, device: int = 0, workers: int = 0, coarse_mode: str = "direct",
                  coarse_options: SolverOptions | None = None, leaf_size: int = 24, local_blocks: int = 8,
-                 solve_parts: int = 0, dist=None):
+                 solve_parts: int = 0, dist=None, setup: str = "device"):
         self.problem = problem
         self.n = problem.global_dofs
         h = C.c_void_p()
-        opts = gpu_options(device, workers, coarse_mode, coarse_options, leaf_size, local_blocks, solve_parts)
+        opts = gpu_options(device, workers, coarse_mode, coarse_options, leaf_size, local_blocks, solve_parts, setup)
         if dist is None:
             L.check(L.lib().bddc_gpu_create(problem.handle, C.byref(opts), C.byref(h)))
         else:
@@ -402,6 +405,16 @@ class Preconditioner:
         phi, lam, aci = np.zeros(nl * npr), np.zeros(npr * npr), np.zeros(npr * npr)
         L.check(L.lib().bddc_gpu_subdomain_blocks(self._h, i, _dptr(phi), _dptr(lam), _dptr(aci)))
         return phi.reshape(nl, npr), lam.reshape(npr, npr), aci.reshape(npr, npr)
+
+    def coarse_matrix(self):
+        """A_c (CSR rowptr, cols, values) as assembled by this context (reference CoarseProblem)."""
+        nnz = C.c_int32()
+        L.check(L.lib().bddc_gpu_coarse_matrix(self._h, C.byref(nnz), None, None, None))
+        n = self.problem.n_coarse
+        rp, ci, v = np.zeros(n + 1, np.int32), np.zeros(nnz.value, np.int32), np.zeros(nnz.value)
+        L.check(L.lib().bddc_gpu_coarse_matrix(self._h, None, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                               ci.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(v)))
+        return rp, ci, v
 
     def stats(self) -> dict:
         s = L.Stats()

@@ -14,6 +14,7 @@
 
 #include "../../paper_2410_14786_b200/csrc/context.hpp"
 #include "../../paper_2410_14786_b200/csrc/host/program.hpp"
+#include "../../paper_2410_14786_b200/csrc/host/gpu_setup.hpp"
 
 using namespace bddc_b200;
 
@@ -237,4 +238,87 @@ extern "C" int bddc_sim_split_solve(int cells_x, int cells_y, int kx, int ky, in
 extern "C" int bddc_sim_harmonic_solve(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
                                        int use_coords, const double* in, double* out, char* err, int errlen) {
     return sim_solve(cells_x, cells_y, kx, ky, parts, leaf_size, use_coords, 1, in, out, err, errlen);
+}
+
+// GPU-setup templates (host/gpu_setup.hpp) against the host-built programs: the class
+// templates instantiated per subdomain and filled exactly like device/setup.cu's fill kernel
+// (from a value array D = [L_ss^-1 | BL_s] computed from the host factor in the builder's loop
+// order) must reproduce every host-built stream word, dof map and coupling entry bit for bit.
+// Returns the number of mismatching entries (0 = identical), -1 on error.
+extern "C" long bddc_sim_template_check(int cells_x, int cells_y, int kx, int ky, int parts, int leaf_size,
+                                        int use_coords, char* err, int errlen) {
+    try {
+        PoissonProblem pp = assemble_poisson(cells_x, cells_y, kx, ky);
+        ProblemData pb;
+        pb.constraints = build_constraints(pp.decomposition);
+        pb.decomposition = std::move(pp.decomposition);
+        pb.global_matrix = std::move(pp.global_matrix);
+        pb.local_matrices = std::move(pp.local_matrices);
+        if (use_coords) pb.coords = std::move(pp.coords);
+        const index_t* coords = pb.coords.empty() ? nullptr : pb.coords.data();
+        FactorOptions fo;
+        fo.leaf_size = leaf_size;
+        const BddcSetup setup = bddc_setup(pb.local_matrices, pb.decomposition, pb.constraints, coords, 4, fo);
+        const DeviceImage host = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
+                                                    pb.global_matrix, setup, parts, 4096, nullptr, true);
+        const std::vector<SetupClass> classes = plan_gpu_setup(pb.local_matrices, pb.decomposition, pb.constraints,
+                                                               coords, fo, parts, 4096, true, 4);
+        BddcSetup meta;
+        meta.subs.resize(pb.decomposition.n_subdomains);
+        for (index_t i = 0; i < pb.decomposition.n_subdomains; ++i) {
+            meta.subs[i].n_local = setup.subs[i].n_local;
+            meta.subs[i].n_interior = setup.subs[i].n_interior;
+            meta.subs[i].n_iface = setup.subs[i].n_iface;
+            meta.subs[i].n_primal = setup.subs[i].n_primal;
+        }
+        const DeviceImage dev = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
+                                                   pb.global_matrix, meta, parts, 4096, nullptr, true, &classes);
+        long bad = 0;
+        auto cmp = [&](const auto& a, const auto& b) {
+            if (a.size() != b.size()) return bad += 1000000, void();
+            for (std::size_t i = 0; i < a.size(); ++i) bad += std::memcmp(&a[i], &b[i], sizeof(a[i])) != 0;
+        };
+        for (int k = 0; k < 3; ++k) {
+            const SolvePools& H = k == 0 ? host.solve : (k == 1 ? host.harm : host.head);
+            const SolvePools& G = k == 0 ? dev.solve : (k == 1 ? dev.harm : dev.head);
+            if (G.words() != H.words()) bad += 1000000;
+            std::vector<double> filled(static_cast<std::size_t>(G.words()), 0.0);
+            for (const auto& f : dev.fills[k]) {
+                const SetupClass& C = classes[f.cls];
+                const InteriorFactor& F = setup.subs[f.sub].factor;  // host numeric factor of this subdomain
+                std::vector<double> D(static_cast<std::size_t>(C.layout.total), 0.0);
+                for (std::size_t s = 0; s < F.snodes.size(); ++s) {
+                    const Supernode& S = F.snodes[s];
+                    const index_t ns = S.size();
+                    std::copy(S.Linv.begin(), S.Linv.end(), D.begin() + C.layout.linv_off[s]);
+                    for (index_t a = 0; a < S.n_interior_rows; ++a)
+                        for (index_t j = 0; j < ns; ++j) {
+                            double acc = 0.0;
+                            for (index_t q = j; q < ns; ++q) acc += S.B[a * ns + q] * S.Linv[q * ns + j];
+                            D[C.layout.bl_off[s] + a * ns + j] = acc;
+                        }
+                }
+                const SolvePools& T = C.prog[k];
+                for (std::int64_t w = 0; w < f.words; ++w) {
+                    const std::int32_t c = T.srcmap[w];
+                    double v = c == kSrcCopy ? T.stream[w] : c == kSrcZero ? 0.0 : c >= 0 ? D[c] : -D[-c - 3];
+                    filled[f.dst + w] = v;
+                }
+            }
+            cmp(filled, H.stream);
+            cmp(G.gmap, H.gmap);
+            cmp(G.couple_val, H.couple_val);
+            cmp(G.couple_gamma, H.couple_gamma);
+            cmp(G.units, H.units);
+            cmp(G.phases, H.phases);
+            cmp(G.order, H.order);
+            if (G.parts.size() != H.parts.size()) bad += 1000000;
+            for (std::size_t p = 0; p < std::min(G.parts.size(), H.parts.size()); ++p)
+                bad += std::memcmp(&G.parts[p], &H.parts[p], sizeof(PartDesc)) != 0;
+        }
+        return bad;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return -1;
+    }
 }

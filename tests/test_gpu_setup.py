@@ -1,0 +1,102 @@
+"""GPU setup (reference setup_subdomain / assemble_coarse,
+src/preconditioner.cpp:34-98, lu_factor src/sparse_lu.cpp:80-195): the device factorisation,
+Schur complements, saddle reduction, coarse basis, coarse blocks and coarse matrix against the
+reference's own setup products (tests/golden), mirroring tests/test_host_setup.py, plus the
+device-set-up preconditioner against the host-set-up one."""
+import numpy as np
+import pytest
+
+import bddc_oracle as o
+from conftest import golden, history_err
+from paper_2410_14786_b200 import BddcError, Preconditioner, Problem, SolverOptions
+
+pytestmark = pytest.mark.gpu
+OPTS = SolverOptions(1e-8, 0.0, 10000, True)
+
+
+def _problem(g):
+    cfg = [int(v) for v in g["config"]]
+    if len(cfg) == 3:
+        k, m, seed = cfg
+        return Problem.poisson(k * m, k, rhs_seed=seed)
+    cx, cy, kx, ky, dm, ks, seed = cfg
+    return Problem.poisson(cx, kx, cy, ky, kappa_decades=dm / 1000.0, kappa_seed=ks, rhs_seed=seed)
+
+
+@pytest.mark.parametrize("name", ["k2m4", "k3m4", "k3m6", "k4m8", "r4x2m8", "h4m8"])
+def test_device_blocks_match_reference(gpu, name):
+    g = golden(name)
+    p = _problem(g)
+    pre = Preconditioner(p)  # setup on the device (default)
+    st = pre.stats()
+    assert st["setup_device_seconds"] > 0.0
+    blocks = [pre.subdomain_blocks(i) for i in range(p.n_subdomains)]
+    phi = np.concatenate([b[0].ravel() for b in blocks])
+    lam = np.concatenate([b[1].ravel() for b in blocks])
+    aci = np.concatenate([b[2].ravel() for b in blocks])
+    scale = max(1.0, np.abs(g["aci"]).max())
+    assert np.abs(phi - g["phi"]).max() < 1e-11
+    assert np.abs(lam - g["lambda"]).max() < 1e-11 * scale
+    assert np.abs(aci - g["aci"]).max() < 1e-11 * scale
+    rp, ci, v = pre.coarse_matrix()
+    assert np.array_equal(rp, g["Ac_rowptr"]) and np.array_equal(ci, g["Ac_cols"])
+    assert np.abs(v - g["Ac_vals"]).max() < 1e-11 * scale
+
+
+def test_device_saddle_identities(gpu):
+    # test_bddc.cpp:56-91 on the device products: C Phi = I, A Phi + C^T Lambda = 0, A_ci symmetric
+    p = Problem.poisson(12, 3)
+    pre = Preconditioner(p)
+    for i in range(p.n_subdomains):
+        phi, lam, aci = pre.subdomain_blocks(i)
+        A = o.Csr(*p.local_matrix(i)).dense()
+        Cm = o.Csr(*p.constraint_matrix(i)).dense()
+        assert np.abs(Cm @ phi - np.eye(Cm.shape[0])).max() <= 1e-10
+        assert np.abs(A @ phi + Cm.T @ lam).max() <= 1e-10 * np.abs(A).sum(1).max()
+        assert np.abs(aci - aci.T).max() <= 1e-12 * max(1.0, np.abs(aci).max())
+
+
+@pytest.mark.parametrize("setup_args", [(128, 4, None), (352, 8, 2.0)], ids=["c1ish", "c5"])
+def test_device_setup_matches_host_setup(gpu, setup_args):
+    cells, k, dec = setup_args
+    kw = dict(kappa_decades=dec, kappa_seed=0x5EED) if dec else {}
+    p = Problem.poisson(cells, k, **kw)
+    dev, host = Preconditioner(p), Preconditioner(p, setup="host")
+    r = p.rhs()
+    zd, zh = dev.apply(r), host.apply(r)
+    assert np.abs(zd - zh).max() <= 1e-12 * np.abs(zh).max()
+    xd, rd = dev.pcg(r, OPTS)
+    xh, rh = host.pcg(r, OPTS)
+    assert rd.iterations == rh.iterations
+    assert history_err(rd.residual_history, rh.residual_history) <= 1e-10
+
+
+def test_device_setup_c2_and_c5_against_reference(gpu):
+    # the BASELINE configs solved after a device setup: C2 (64 subdomains, 9 setup classes) and C5
+    # (heterogeneous: no two subdomains share values) to the reference's iteration counts / histories
+    for name, p in (("c2", Problem.poisson(800, 8)),
+                    ("c5", Problem.poisson(352, 8, kappa_decades=2.0, kappa_seed=0x5EED))):
+        g = golden(name)
+        pre = Preconditioner(p)
+        x, rep = pre.pcg(p.rhs(), OPTS)
+        assert rep.iterations == int(g["pcg_report"][0]), name
+        assert history_err(rep.residual_history, g["pcg_history"]) <= 1e-10, name
+        stride = int(g["pcg_x_sample_stride"][0])
+        assert np.abs(x[::stride] - g["pcg_x_sample"]).max() <= 1e-10 * np.abs(g["pcg_x_sample"]).max()
+
+
+def test_device_setup_error_names_subdomain(gpu):
+    # test_bddc.cpp:371-402 on the device path: duplicated constraint rows -> singular saddle
+    p = Problem.poisson(8, 2)
+    cons = [p.constraint_matrix(i) for i in range(p.n_subdomains)]
+    nr, nc, rp, ci, va = cons[0]
+    row0 = slice(rp[0], rp[1])
+    dup = (2, nc, np.array([0, rp[1] - rp[0], 2 * (rp[1] - rp[0])]), np.concatenate([ci[row0], ci[row0]]),
+           np.concatenate([va[row0], va[row0]]))
+    pm = p.primal_maps()
+    pm[0] = np.array([0, 1])
+    broken = Problem.from_arrays(p.global_matrix(), [p.local_matrix(i) for i in range(p.n_subdomains)],
+                                 p.subdomain_dofs(), p.interior_counts(), p.weights(), [dup] + cons[1:], pm,
+                                 p.n_coarse, *p.classes(), p.multiplicity(), p.rhs())
+    with pytest.raises(BddcError, match="bddc setup: subdomain 0"):
+        Preconditioner(broken)

@@ -184,3 +184,17 @@ def test_split_apply_programs(sim, k, m, parts, leaf, coords):
     assert coupled.sum() > 0
     assert np.abs(u0[coupled] - ref_u0[coupled]).max() <= 1e-12 * np.abs(ref_u0).max()
     assert np.abs(z[kinds] - ref_z[kinds]).max() <= 1e-12 * np.abs(ref_z).max()
+
+
+@pytest.mark.parametrize("cx,cy,kx,ky,parts,leaf,coords", [(32, 32, 4, 4, 2, 24, 1), (32, 32, 4, 4, 1, 24, 1),
+                                                           (64, 32, 4, 2, 2, 16, 1), (32, 32, 4, 4, 2, 24, 0),
+                                                           (300, 300, 3, 3, 2, 24, 1)])
+def test_gpu_setup_templates_reproduce_host_programs(sim, cx, cy, kx, ky, parts, leaf, coords):
+    # the GPU setup instantiates one program template per setup class and fills
+    # its values on the device from D = [L_ss^-1 | BL_s] (host/gpu_setup.cpp, device/setup.cu).
+    # Emulating that fill with the host factor's values must give back the host-built programs
+    # word for word (streams, dof maps, coupling entries, tables, part descriptors).
+    sim.bddc_sim_template_check.restype = C.c_long
+    err = C.create_string_buffer(512)
+    bad = sim.bddc_sim_template_check(cx, cy, kx, ky, parts, leaf, coords, err, 512)
+    assert bad == 0, err.value
