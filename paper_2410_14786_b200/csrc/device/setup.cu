@@ -256,10 +256,28 @@ __global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev 
             ck[j] = M[static_cast<long long>(j) * ns + k];
         }
         __syncthreads();
-        for (long long idx = tid; idx < nn; idx += blockDim.x) {
-            const int i = static_cast<int>(idx / ns), j = static_cast<int>(idx % ns);
-            if (i == k) M[idx] = rk[j];
-            else M[idx] = j == k ? -ck[i] * rk[k] : M[idx] - ck[i] * rk[j];
+        // rank-1 update: one row per warp at a time, lanes along the row (coalesced, no index
+        // division), four independent entries in flight per lane
+        {
+            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+            for (int i = warp; i < ns; i += nw) {
+                double* Mi = M + static_cast<long long>(i) * ns;
+                if (i == k) {
+                    for (int j = lane; j < ns; j += 32) Mi[j] = rk[j];
+                    continue;
+                }
+                const double f = ck[i];
+                for (int j0 = lane; j0 < ns; j0 += 128) {
+                    double v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = j0 + 32 * u < ns ? Mi[j0 + 32 * u] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = j0 + 32 * u;
+                        if (j < ns) Mi[j] = j == k ? -f * rk[k] : v[u] - f * rk[j];
+                    }
+                }
+            }
         }
         __syncthreads();
     }

@@ -197,45 +197,56 @@ std::vector<SetupClass> plan_gpu_setup(const std::vector<CsrMatrix>& locals, con
             classes[it->second].members.push_back(i);
         }
     }
-    std::atomic<std::size_t> next{0};
+    // two parallel passes: the symbolic factor + plan of every class, then the class x program
+    // templates (the three programs of a class are independent)
     std::exception_ptr err;
     std::mutex mu;
-    auto work = [&] {
-        for (std::size_t c = next++; c < classes.size(); c = next++) {
-            SetupClass& C = classes[c];
-            const index_t i = C.rep;
-            try {
-                const CsrMatrix& A = locals[i];
-                const index_t nI = d.interior_counts[i];
-                C.n_local = A.nrows;
-                C.n_interior = nI;
-                C.n_iface = A.nrows - nI;
-                C.n_primal = cs.constraint_matrices[i].nrows;
-                C.nnz = A.nnz();
-                C.sym = symbolic_factor(A, nI, coords ? rel[i].data() : nullptr, fopt);
-                C.factor_values = C.sym.factor_values();
-                plan_class(C, A, cs.constraint_matrices[i]);
-                std::vector<index_t> ident(A.nrows);
-                std::iota(ident.begin(), ident.end(), 0);
-                build_solve_program(C.sym, A, ident, i, parts, unit_bytes, C.prog[0], false, false, &C.layout);
-                if (harmonic) {
-                    build_solve_program(C.sym, A, ident, i, parts, unit_bytes, C.prog[1], true, false, &C.layout);
-                    build_solve_program(C.sym, A, ident, i, parts, unit_bytes, C.prog[2], false, true, &C.layout);
+    auto run = [&](std::size_t n_tasks, auto&& task) {
+        std::atomic<std::size_t> next{0};
+        auto work = [&] {
+            for (std::size_t t = next++; t < n_tasks; t = next++) {
+                const index_t i = classes[t % classes.size()].rep;
+                try {
+                    task(t);
+                } catch (const std::exception& e) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (!err)
+                        err = std::make_exception_ptr(
+                            std::runtime_error("bddc setup: subdomain " + std::to_string(i) + ": " + e.what()));
                 }
-            } catch (const std::exception& e) {
-                std::lock_guard<std::mutex> lk(mu);
-                if (!err)
-                    err = std::make_exception_ptr(
-                        std::runtime_error("bddc setup: subdomain " + std::to_string(i) + ": " + e.what()));
             }
-        }
+        };
+        const int nt = std::max(1, std::min<int>(workers, static_cast<int>(n_tasks)));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto& t : th) t.join();
+        if (err) std::rethrow_exception(err);
     };
-    const int nt = std::max(1, std::min<int>(workers, static_cast<int>(classes.size())));
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) th.emplace_back(work);
-    work();
-    for (auto& t : th) t.join();
-    if (err) std::rethrow_exception(err);
+    run(classes.size(), [&](std::size_t c) {
+        SetupClass& C = classes[c];
+        const index_t i = C.rep;
+        const CsrMatrix& A = locals[i];
+        const index_t nI = d.interior_counts[i];
+        C.n_local = A.nrows;
+        C.n_interior = nI;
+        C.n_iface = A.nrows - nI;
+        C.n_primal = cs.constraint_matrices[i].nrows;
+        C.nnz = A.nnz();
+        C.sym = symbolic_factor(A, nI, coords ? rel[i].data() : nullptr, fopt);
+        C.factor_values = C.sym.factor_values();
+        plan_class(C, A, cs.constraint_matrices[i]);
+    });
+    const int nprog = harmonic ? 3 : 1;
+    run(classes.size() * nprog, [&](std::size_t t) {
+        SetupClass& C = classes[t % classes.size()];
+        const int q = static_cast<int>(t / classes.size());
+        const CsrMatrix& A = locals[C.rep];
+        std::vector<index_t> ident(A.nrows);
+        std::iota(ident.begin(), ident.end(), 0);
+        // 0: full solve, 1: harmonic (pruned forward), 2: head (pruned backward)
+        build_solve_program(C.sym, A, ident, C.rep, parts, unit_bytes, C.prog[q], q == 1, q == 2, &C.layout);
+    });
     return classes;
 }
 

@@ -4,10 +4,10 @@
 //
 // CG is Lanczos in disguise: with alpha_j, beta_j of the recurrences, the Lanczos
 // tridiagonal T has diagonal 1/alpha_j + beta_{j-1}/alpha_{j-1} and off-diagonal
-// sqrt(beta_j)/alpha_j, and its extreme eigenvalues approximate those of M^-1 A. The reference
-// brackets them by Gershgorin discs and bisects Sturm counts; here every eigenvalue of T is
-// computed by the implicitly shifted QL iteration (Wilkinson shift, Givens bulge chase), which
-// converges to the same extreme values (to ~1e-15 relative for these well-separated ends).
+// sqrt(beta_j)/alpha_j, and its extreme eigenvalues approximate those of M^-1 A. Here they are
+// located by bisection on the inertia of T - x I (the signs of its LDL^T pivots count the
+// eigenvalues below x), bracketed by the infinity norm of T; O(n) per step, so the estimate
+// stays cheap for the ~2,000-step plain-CG runs of C4 / C5.
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -19,49 +19,29 @@
 namespace bddc_b200 {
 namespace {
 
-// All eigenvalues of the symmetric tridiagonal (a = diagonal, b[i] couples i and i+1),
-// returned in a (unordered). b is destroyed.
-void tridiagonal_eigenvalues(std::vector<double>& a, std::vector<double>& b) {
-    const std::size_t n = a.size();
-    b.resize(n, 0.0);  // b[n-1] = 0 terminates every deflation scan
-    const double eps = std::numeric_limits<double>::epsilon();
-    for (std::size_t top = 0; top < n; ++top) {
-        for (int sweep = 0; sweep < 64; ++sweep) {
-            // the unreduced block starting at `top` ends at `end` (negligible coupling below it)
-            std::size_t end = top;
-            while (end + 1 < n && std::abs(b[end]) > eps * (std::abs(a[end]) + std::abs(a[end + 1]))) ++end;
-            if (end == top) break;  // a[top] has converged
-            // Wilkinson-type shift from the leading 2x2 of the block
-            const double half_gap = (a[top + 1] - a[top]) / (2.0 * b[top]);
-            const double root = std::hypot(half_gap, 1.0);
-            double bulge_g = a[end] - a[top] + b[top] / (half_gap + std::copysign(root, half_gap));
-            double sn = 1.0, cs = 1.0, shift_acc = 0.0;
-            bool split = false;
-            // chase the bulge from the bottom of the block up to `top`
-            for (std::size_t k = end; k-- > top;) {
-                const double f = sn * b[k], h = cs * b[k];
-                const double rad = std::hypot(f, bulge_g);
-                b[k + 1] = rad;
-                if (rad == 0.0) {  // exact split: restart on the shorter block
-                    a[k + 1] -= shift_acc;
-                    b[end] = 0.0;
-                    split = true;
-                    break;
-                }
-                sn = f / rad;
-                cs = bulge_g / rad;
-                const double g = a[k + 1] - shift_acc;
-                const double t = (a[k] - g) * sn + 2.0 * cs * h;
-                shift_acc = sn * t;
-                a[k + 1] = g + shift_acc;
-                bulge_g = cs * t - h;
-            }
-            if (split) continue;
-            a[top] -= shift_acc;
-            b[top] = bulge_g;
-            b[end] = 0.0;
-        }
+// Eigenvalues of the symmetric tridiagonal (diagonal a, squared couplings b2[i] between i and
+// i+1) strictly below x: the negative pivots of the LDL^T factorisation of T - x I (a zero
+// pivot is nudged to the smallest positive normal number).
+std::size_t count_below(const std::vector<double>& a, const std::vector<double>& b2, double x) {
+    std::size_t neg = 0;
+    double piv = 1.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        piv = (a[i] - x) - (i > 0 ? b2[i - 1] / piv : 0.0);
+        if (piv == 0.0) piv = std::numeric_limits<double>::min();
+        neg += piv < 0.0 ? 1 : 0;
     }
+    return neg;
+}
+
+// The k-th smallest eigenvalue (k = 1 .. n) by bisection of [lo, hi] down to 1e-15 relative.
+double kth_eigenvalue(const std::vector<double>& a, const std::vector<double>& b2, std::size_t k, double lo,
+                      double hi) {
+    for (int step = 0; step < 256; ++step) {
+        if (hi - lo <= 1e-15 * std::max(1.0, std::abs(hi))) break;
+        const double mid = lo + 0.5 * (hi - lo);
+        (count_below(a, b2, mid) >= k ? hi : lo) = mid;
+    }
+    return lo + 0.5 * (hi - lo);
 }
 
 }  // namespace
@@ -69,15 +49,21 @@ void tridiagonal_eigenvalues(std::vector<double>& a, std::vector<double>& b) {
 std::optional<double> condition_estimate(const std::vector<double>& alphas, const std::vector<double>& betas) {
     const std::size_t k = alphas.size();
     if (k < 2 || betas.size() + 1 < k) return std::nullopt;  // as the reference: needs two steps
-    std::vector<double> a(k), b(k - 1);
+    std::vector<double> a(k), b2(k - 1);
+    double norm = 0.0;  // infinity norm of T: every eigenvalue lies in [-norm, norm]
     for (std::size_t j = 0; j < k; ++j) {
         a[j] = 1.0 / alphas[j] + (j > 0 ? betas[j - 1] / alphas[j - 1] : 0.0);
-        if (j + 1 < k) b[j] = std::sqrt(betas[j]) / alphas[j];
+        if (j + 1 < k) {
+            const double off = std::sqrt(betas[j]) / alphas[j];
+            b2[j] = off * off;
+        }
     }
-    tridiagonal_eigenvalues(a, b);
-    const auto [lo, hi] = std::minmax_element(a.begin(), a.end());
-    if (!(*lo > 0.0)) return std::nullopt;
-    return *hi / *lo;
+    for (std::size_t j = 0; j < k; ++j)
+        norm = std::max(norm, std::abs(a[j]) + (j > 0 ? std::sqrt(b2[j - 1]) : 0.0) + (j + 1 < k ? std::sqrt(b2[j]) : 0.0));
+    const double lo = kth_eigenvalue(a, b2, 1, -norm, norm);
+    const double hi = kth_eigenvalue(a, b2, k, -norm, norm);
+    if (!(lo > 0.0)) return std::nullopt;
+    return hi / lo;
 }
 
 }  // namespace bddc_b200

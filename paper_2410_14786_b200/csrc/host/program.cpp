@@ -52,7 +52,14 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
     }
     // (global subdomain id, hbuf slot): sorted by subdomain before flattening
     std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>> gi_owners(img.gi_dof.size());
-    std::vector<std::vector<std::int32_t>> dof_owners(d.global_dofs);
+    // every vector dof's owners as local-dof slots (ascending subdomain): a CSR built in two
+    // passes (counts, then the slots in subdomain order) instead of a list per dof
+    img.dof_own_ptr.assign(static_cast<std::size_t>(d.global_dofs) + 1, 0);
+    for (index_t i = 0; i < nsub; ++i)
+        for (index_t g : d.subdomain_dofs[i]) ++img.dof_own_ptr[g + 1];
+    for (index_t g = 0; g < d.global_dofs; ++g) img.dof_own_ptr[g + 1] += img.dof_own_ptr[g];
+    img.dof_own_ref.assign(static_cast<std::size_t>(img.dof_own_ptr.back()), 0);
+    std::vector<std::int32_t> dof_fill(img.dof_own_ptr.begin(), img.dof_own_ptr.end() - 1);
     std::vector<std::vector<std::int32_t>> c_owners(cs.n_coarse);
 
     for (index_t i = 0; i < nsub; ++i) {
@@ -71,7 +78,7 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
 
         sd.local_dofs = static_cast<std::int64_t>(img.local_dofs.size());
         for (index_t l = 0; l < nl; ++l) {
-            dof_owners[dofs[l]].push_back(static_cast<std::int32_t>(img.local_total + l));
+            img.dof_own_ref[dof_fill[dofs[l]]++] = static_cast<std::int32_t>(img.local_total + l);
             img.local_dofs.push_back(dofs[l]);
         }
         img.local_total += nl;
@@ -135,39 +142,25 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
     if (dev) {
         // GPU setup: every subdomain's programs are its class's templates with the subdomain's
         // own dof map and coupling values; the stream values are filled on the device
+        // offsets sequentially (cheap), then every subdomain's ranges filled on host threads
         for (int k = 0; k < (harmonic ? 3 : 1); ++k) {
             SolvePools& dst = k == 0 ? img.solve : (k == 1 ? img.harm : img.head);
             dst.stream_words = 0;
+            struct At { std::size_t units, order, phases, gmap, cptr, cent, parts; };
+            std::vector<At> at(nsub);
+            std::size_t nu = 0, no = 0, nph = 0, ngm = 0, ncp = 0, nce = 0, npt = 0;
             for (index_t i = 0; i < nsub; ++i) {
-                const std::int32_t c = img.sub_class[i];
-                const SolvePools& T = (*classes)[c].prog[k];
-                if (dst.couple_ptr.size() & 1) dst.couple_ptr.push_back(0);  // int2 alignment
-                const std::int64_t units0 = static_cast<std::int64_t>(dst.units.size() / 2);
-                const std::int64_t order0 = static_cast<std::int64_t>(dst.order.size() / 4);
-                const std::int32_t phases0 = static_cast<std::int32_t>(dst.phases.size());
-                const std::int64_t gmap0 = static_cast<std::int64_t>(dst.gmap.size());
-                const std::int64_t cptr0 = static_cast<std::int64_t>(dst.couple_ptr.size());
-                const std::int64_t cent0 = static_cast<std::int64_t>(dst.couple_gamma.size());
-                for (PartDesc pd : T.parts) {
-                    pd.stream += dst.stream_words;
-                    pd.units += units0;
-                    pd.order += order0;
-                    pd.phases += phases0;
-                    pd.gmap += gmap0;
-                    pd.couple_ptr += cptr0;
-                    pd.couple_ent += cent0;
-                    pd.sub = static_cast<std::int32_t>(i);
-                    dst.parts.push_back(pd);
-                }
-                dst.units.insert(dst.units.end(), T.units.begin(), T.units.end());
-                dst.order.insert(dst.order.end(), T.order.begin(), T.order.end());
-                dst.phases.insert(dst.phases.end(), T.phases.begin(), T.phases.end());
-                dst.couple_ptr.insert(dst.couple_ptr.end(), T.couple_ptr.begin(), T.couple_ptr.end());
-                dst.couple_gamma.insert(dst.couple_gamma.end(), T.couple_gamma.begin(), T.couple_gamma.end());
-                const auto& dofs = d.subdomain_dofs[i];
-                for (std::int32_t l : T.gmap) dst.gmap.push_back(dofs[l]);
-                for (std::int32_t q : T.couple_src) dst.couple_val.push_back(locals[i].values[q]);
-                img.fills[k].push_back({dst.stream_words, T.words(), c, k, i});
+                const SolvePools& T = (*classes)[img.sub_class[i]].prog[k];
+                ncp += ncp & 1;  // int2 alignment of the parts' {row, end} pairs
+                at[i] = {nu, no, nph, ngm, ncp, nce, npt};
+                nu += T.units.size();
+                no += T.order.size();
+                nph += T.phases.size();
+                ngm += T.gmap.size();
+                ncp += T.couple_ptr.size();
+                nce += T.couple_gamma.size();
+                npt += T.parts.size();
+                img.fills[k].push_back({dst.stream_words, T.words(), img.sub_class[i], k, i});
                 dst.stream_words += T.words();
                 dst.tile_values += T.tile_values;
                 dst.fwd_factor_values += T.fwd_factor_values;
@@ -178,6 +171,48 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
                 dst.max_phases = std::max(dst.max_phases, T.max_phases);
                 dst.max_units = std::max(dst.max_units, T.max_units);
             }
+            dst.units.resize(nu);
+            dst.order.resize(no);
+            dst.phases.resize(nph);
+            dst.gmap.resize(ngm);
+            dst.couple_ptr.assign(ncp, 0);
+            dst.couple_gamma.resize(nce);
+            dst.couple_val.resize(nce);
+            dst.parts.resize(npt);
+            auto fill = [&](index_t i) {
+                const SolvePools& T = (*classes)[img.sub_class[i]].prog[k];
+                const At& a = at[i];
+                for (std::size_t q = 0; q < T.parts.size(); ++q) {
+                    PartDesc pd = T.parts[q];
+                    pd.stream += img.fills[k][i].dst;
+                    pd.units += static_cast<std::int64_t>(a.units / 2);
+                    pd.order += static_cast<std::int64_t>(a.order / 4);
+                    pd.phases += static_cast<std::int32_t>(a.phases);
+                    pd.gmap += static_cast<std::int64_t>(a.gmap);
+                    pd.couple_ptr += static_cast<std::int64_t>(a.cptr);
+                    pd.couple_ent += static_cast<std::int64_t>(a.cent);
+                    pd.sub = static_cast<std::int32_t>(i);
+                    dst.parts[a.parts + q] = pd;
+                }
+                std::copy(T.units.begin(), T.units.end(), dst.units.begin() + a.units);
+                std::copy(T.order.begin(), T.order.end(), dst.order.begin() + a.order);
+                std::copy(T.phases.begin(), T.phases.end(), dst.phases.begin() + a.phases);
+                std::copy(T.couple_ptr.begin(), T.couple_ptr.end(), dst.couple_ptr.begin() + a.cptr);
+                std::copy(T.couple_gamma.begin(), T.couple_gamma.end(), dst.couple_gamma.begin() + a.cent);
+                const auto& dofs = d.subdomain_dofs[i];
+                for (std::size_t q = 0; q < T.gmap.size(); ++q) dst.gmap[a.gmap + q] = dofs[T.gmap[q]];
+                const auto& vals = locals[i].values;
+                for (std::size_t q = 0; q < T.couple_src.size(); ++q) dst.couple_val[a.cent + q] = vals[T.couple_src[q]];
+            };
+            std::atomic<index_t> next{0};
+            auto work = [&] {
+                for (index_t i = next++; i < nsub; i = next++) fill(i);
+            };
+            const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), nsub));
+            std::vector<std::thread> th;
+            for (int t = 1; t < nt; ++t) th.emplace_back(work);
+            work();
+            for (auto& t : th) t.join();
         }
     } else {
     // interior-solve programs (local dof -> vector index = the subdomain map), built per
@@ -268,7 +303,6 @@ DeviceImage build_device_image(const Decomposition& d, const ConstraintSet& cs,
             ptr.push_back(static_cast<std::int32_t>(ref.size()));
         }
     };
-    flatten(dof_owners, img.dof_own_ptr, img.dof_own_ref);
     flatten(c_owners, img.c_own_ptr, img.c_own_ref);
     img.coarse_inv = setup.coarse_inverse;
     return img;

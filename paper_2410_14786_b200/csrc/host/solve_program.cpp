@@ -374,27 +374,35 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         std::sort(heights.begin(), heights.end());
         heights.erase(std::unique(heights.begin(), heights.end()), heights.end());
 
-        // greedy colouring of jobs whose target-row sets intersect
+        // greedy colouring of jobs whose target-row sets intersect: each job takes the first
+        // colour none of its target rows carries yet (per-row bit mask of used colours; beyond
+        // 64 colours the remaining jobs get one colour each)
+        std::vector<std::uint64_t> row_colours(nI, 0);
         auto colour = [&](const std::vector<std::vector<index_t>>& targets) {
-            std::vector<std::vector<char>> used;
             std::vector<std::vector<std::size_t>> classes;
+            std::vector<index_t> touched;
             for (std::size_t j = 0; j < targets.size(); ++j) {
                 if (targets[j].empty()) continue;
-                std::size_t c = 0;
-                for (; c < used.size(); ++c) {
-                    bool clash = false;
-                    for (index_t r : targets[j])
-                        if (used[c][r]) { clash = true; break; }
-                    if (!clash) break;
+                std::uint64_t busy = 0;
+                for (index_t r : targets[j]) busy |= row_colours[r];
+                std::size_t c;
+                if (~busy != 0) {
+                    c = static_cast<std::size_t>(__builtin_ctzll(~busy));
+                    for (index_t r : targets[j]) {
+                        if (!row_colours[r]) touched.push_back(r);
+                        row_colours[r] |= std::uint64_t(1) << c;
+                    }
+                } else {
+                    c = std::max<std::size_t>(64, classes.size());
                 }
-                if (c == used.size()) {
-                    used.emplace_back(nI, 0);
-                    classes.emplace_back();
-                }
-                for (index_t r : targets[j]) used[c][r] = 1;
+                if (c >= classes.size()) classes.resize(c + 1);
                 classes[c].push_back(j);
             }
-            return classes;
+            for (index_t r : touched) row_colours[r] = 0;
+            std::vector<std::vector<std::size_t>> kept;
+            for (auto& c : classes)
+                if (!c.empty()) kept.push_back(std::move(c));
+            return kept;
         };
 
         std::vector<Phase> phases;
