@@ -65,10 +65,13 @@ def layout(n_gpus: int):
     return (8 * n_gpus, 8)
 
 
+LAYOUT_OVERRIDE = None  # --subdomains KXxKY: the C2 / C4 layout (e.g. the N=8 layout 32x16 on 4 GPUs)
+
+
 def problem_spec(cfg: str, n_gpus: int):
     """(cells_x, kx, cells_y, ky, kappa_decades, kappa_seed) of a config at n_gpus."""
     if cfg in ("c2", "c4"):
-        kx, ky = layout(n_gpus)
+        kx, ky = LAYOUT_OVERRIDE or layout(n_gpus)
         return kx * CELLS, kx, ky * CELLS, ky, 0.0, 0
     if cfg == "c3":
         return 2520, 24, 2520, 24, 0.0, 0
@@ -86,7 +89,11 @@ def make_problem(cfg: str, n_gpus: int):
 
 def workload(cfg: str, n_gpus: int) -> dict:
     cx, kx, cy, ky, dec, ks = problem_spec(cfg, n_gpus)
-    w = {"workload": CONFIG_DOC[cfg], "config": cfg, "cells": [cx, cy], "subdomains": [kx, ky],
+    doc = CONFIG_DOC[cfg]
+    if LAYOUT_OVERRIDE and cfg in ("c2", "c4"):
+        doc = doc.replace("64 subdomains of 100x100 cells per GPU",
+                          f"{kx}x{ky} subdomains of 100x100 cells ({kx * ky // n_gpus} per GPU)")
+    w = {"workload": doc, "config": cfg, "cells": [cx, cy], "subdomains": [kx, ky],
          "subdomains_per_gpu": kx * ky / n_gpus, "global_dofs": (cx - 1) * (cy - 1), "rhs": "study_rhs(n, seed=1)",
          "preconditioner": "none (plain CG)" if cfg == "c4" else "BDDC",
          "l2": "inputs larger than L2 (the factor streams of one interior solve exceed 126 MB per GPU)"
@@ -465,8 +472,12 @@ def main() -> None:
                     help="SURVEY.md §8 config of the JSON line (c2 = the headline; c2 also reports c3/c4/c5 "
                          "in extra_configs unless --no-extra)")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--subdomains", default=None, help="C2/C4 layout override KXxKY (e.g. 32x16 on 4 GPUs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.subdomains:
+        global LAYOUT_OVERRIDE
+        LAYOUT_OVERRIDE = tuple(int(v) for v in args.subdomains.lower().split("x"))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -221,6 +221,10 @@ struct GpuContext::Impl {
     // global matrix
     DBuf<std::int32_t> A_ptr, A_col;
     DBuf<double> A_val;
+    DBuf<std::int64_t> ell_off;  // the global (rank) matrix as sliced ELL (PcgDevice)
+    DBuf<std::uint16_t> ell_len;
+    DBuf<std::int32_t> ell_col;
+    DBuf<double> ell_val;
     // scratch
     DBuf<double> U, gbuf, hbuf, cbuf, xc, lbuf, vin, vout, vtmp, vtmp2;
     // pcg
@@ -1043,6 +1047,10 @@ struct GpuContext::Impl {
         D.A_ptr = A_ptr.p;
         D.A_col = A_col.p;
         D.A_val = A_val.p;
+        D.ell_off = ell_off.p;
+        D.ell_len = ell_len.p;
+        D.ell_col = ell_col.p;
+        D.ell_val = ell_val.p;
         D.x = xd;
         D.r = rd;
         D.z = zd;
@@ -1867,6 +1875,36 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.A_ptr.upload(I.pb.global_matrix.row_offsets);
     I.A_col.upload(I.pb.global_matrix.col_indices);
     I.A_val.upload(I.pb.global_matrix.values);
+    {
+        // sliced ELL copy for the PCG SpMV: slices of 32 rows, width = the slice's longest row,
+        // entries column-major within the slice in CSR order (padding never read: row lengths)
+        const CsrMatrix& A = I.pb.global_matrix;
+        const index_t nr = A.nrows, ns = (nr + 31) / 32;
+        std::vector<std::int64_t> off(static_cast<std::size_t>(ns) + 1, 0);
+        std::vector<std::uint16_t> len(static_cast<std::size_t>(ns) * 32, 0);
+        for (index_t sl = 0; sl < ns; ++sl) {
+            index_t w = 0;
+            for (index_t i = sl * 32; i < std::min(nr, sl * 32 + 32); ++i) {
+                const index_t l = A.row_offsets[i + 1] - A.row_offsets[i];
+                if (l > 65535) throw std::runtime_error("global matrix row longer than 65535 entries");
+                len[i] = static_cast<std::uint16_t>(l);
+                w = std::max(w, l);
+            }
+            off[sl + 1] = off[sl] + static_cast<std::int64_t>(w) * 32;
+        }
+        std::vector<std::int32_t> col(static_cast<std::size_t>(std::max<std::int64_t>(off[ns], 1)), 0);
+        std::vector<double> val(col.size(), 0.0);
+        for (index_t i = 0; i < nr; ++i)
+            for (index_t q = A.row_offsets[i], j = 0; q < A.row_offsets[i + 1]; ++q, ++j) {
+                const std::int64_t at = off[i / 32] + 32 * j + (i % 32);
+                col[at] = A.col_indices[q];
+                val[at] = A.values[q];
+            }
+        I.ell_off.upload(off);
+        I.ell_len.upload(len);
+        I.ell_col.upload(col);
+        I.ell_val.upload(val);
+    }
     const std::size_t n = d.global_dofs;
     I.U.alloc(n);
     BDDC_CUDA(cudaMemset(I.U.p, 0, sizeof(double) * n));

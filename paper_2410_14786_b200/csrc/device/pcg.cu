@@ -46,15 +46,29 @@ __global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevic
     pdl_trigger();
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *D.iter += 1;  // read by the later kernels of this iteration
-    const std::int32_t* __restrict__ ap = D.A_ptr;
-    const std::int32_t* __restrict__ ac = D.A_col;
-    const double* __restrict__ av = D.A_val;
     const double* __restrict__ p = D.p;
     double* __restrict__ q = D.q;
     double acc = 0.0;
+    // sliced ELL: a warp's 32 rows are one slice, so every entry load of the warp is one
+    // contiguous 256-byte (values) / 128-byte (columns) access
+    const std::int32_t* __restrict__ ec = D.ell_col;
+    const double* __restrict__ ev = D.ell_val;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+        const std::int64_t base = D.ell_off[i >> 5] + (i & 31);
+        const int len = D.ell_len[i];
         double y = 0.0;
-        for (int e = ap[i]; e < ap[i + 1]; ++e) y += av[e] * p[ac[e]];
+        int j = 0;
+        for (; j + 3 < len; j += 4) {  // four entries' loads in flight; the sum stays in CSR order
+            const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
+            const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
+            const double x0 = p[ec[base + 32 * j]], x1 = p[ec[base + 32 * (j + 1)]];
+            const double x2 = p[ec[base + 32 * (j + 2)]], x3 = p[ec[base + 32 * (j + 3)]];
+            y += v0 * x0;
+            y += v1 * x1;
+            y += v2 * x2;
+            y += v3 * x3;
+        }
+        for (; j < len; ++j) y += ev[base + 32 * j] * p[ec[base + 32 * j]];
         q[i] = y;
         if (i < D.n_dot) acc = fma(p[i], y, acc);
     }
@@ -127,6 +141,16 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     pdl_trigger();
     pdl_wait();
     const int it = *D.iter;
+    const double* __restrict__ p = (D.fuse_dir && (it & 1)) ? D.p_alt : D.p;
+    const double* __restrict__ q = D.q;
+    double* __restrict__ x = D.x;
+    double* __restrict__ r = D.r;
+    // the thread's first two entries are loaded before the p.q reduction, so their latency hides
+    // behind it (the vectors do not depend on alpha)
+    const int stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x, i1 = i0 + stride;
+    const bool h0 = i0 < D.n, h1 = i1 < D.n;
+    const double p0 = h0 ? p[i0] : 0.0, q0 = h0 ? q[i0] : 0.0, x0 = h0 ? x[i0] : 0.0, r0 = h0 ? r[i0] : 0.0;
+    const double p1 = h1 ? p[i1] : 0.0, q1 = h1 ? q[i1] : 0.0, x1 = h1 ? x[i1] : 0.0, r1 = h1 ? r[i1] : 0.0;
     const double pq = sum_ranks(D, D.red_a, D.red_a_n, 0, D.seq_pq, scratch);
     if (pq <= 0.0) {  // pcg.cpp:75-78 "matrix not SPD" (a NaN curvature carries on, like the reference)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -137,13 +161,21 @@ __global__ void __launch_bounds__(kVecThreads) update_kernel(const PcgDevice D, 
     }
     const double alpha = D.rho[it - 1] / pq;
     if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[it - 1] = alpha;
-    const double* __restrict__ p = (D.fuse_dir && (it & 1)) ? D.p_alt : D.p;
-    const double* __restrict__ q = D.q;
-    double* __restrict__ x = D.x;
-    double* __restrict__ r = D.r;
     double acc = 0.0;
+    if (h0) {
+        x[i0] = x0 + alpha * p0;
+        const double ri = r0 - alpha * q0;
+        r[i0] = ri;
+        if (i0 < D.n_dot) acc = fma(ri, ri, acc);
+    }
+    if (h1) {
+        x[i1] = x1 + alpha * p1;
+        const double ri = r1 - alpha * q1;
+        r[i1] = ri;
+        if (i1 < D.n_dot) acc = fma(ri, ri, acc);
+    }
 #pragma unroll 2
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    for (int i = i0 + 2 * stride; i < D.n; i += stride) {
         x[i] += alpha * p[i];
         const double ri = r[i] - alpha * q[i];
         r[i] = ri;
@@ -185,16 +217,24 @@ __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, in
     pdl_trigger();
     pdl_wait();
     const int it = *D.iter;
+    const double* __restrict__ z = D.z;
+    double* __restrict__ p = D.p;
+    // the thread's first two rows (not the LL halo) are loaded before the r.z reduction
+    const int stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x, i1 = i0 + stride;
+    const double z0 = i0 < D.n ? z[i0] : 0.0, p0 = i0 < D.n ? p[i0] : 0.0;
+    const double z1 = i1 < D.n ? z[i1] : 0.0, p1 = i1 < D.n ? p[i1] : 0.0;
     const double rz = sum_ranks(D, D.red_c, D.red_c_n, 2, D.seq_rz, scratch);
     const double beta = rz / D.rho[it - 1];
     const std::uint32_t tag = D.ll_z ? ll_tag(D.seq_rz) : 0u;
-    const double* __restrict__ z = D.z;
-    double* __restrict__ p = D.p;
+    auto z_at = [&](int i) {
+        return (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : z[i];
+    };
+    if (i0 < D.n) p[i0] = z0 + beta * p0;
+    else if (i0 < D.n_dir) p[i0] = z_at(i0) + beta * p[i0];
+    if (i1 < D.n) p[i1] = z1 + beta * p1;
+    else if (i1 < D.n_dir) p[i1] = z_at(i1) + beta * p[i1];
 #pragma unroll 2
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n_dir; i += gridDim.x * blockDim.x) {
-        const double zi = (D.ll_z && i >= D.n) ? ll_get(D.ll_z + 2 * static_cast<std::int64_t>(i - D.n), tag) : z[i];
-        p[i] = zi + beta * p[i];
-    }
+    for (int i = i0 + 2 * stride; i < D.n_dir; i += stride) p[i] = z_at(i) + beta * p[i];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         D.beta[it - 1] = beta;
         D.rho[it] = rz;

@@ -15,6 +15,13 @@ struct PcgDevice {
     const std::int32_t* A_ptr;
     const std::int32_t* A_col;
     const double* A_val;
+    // the same matrix as sliced ELL (SpMV of the PCG loop): slices of 32 consecutive rows, each
+    // slice column-major (entry j of the slice's lane-th row at ell_off[slice] + 32 j + lane), row
+    // lengths in ell_len; entries keep their CSR order, so every row sum is the CSR sum
+    const std::int64_t* ell_off;
+    const std::uint16_t* ell_len;
+    const std::int32_t* ell_col;
+    const double* ell_val;
     double* x;
     double* r;
     double* z;

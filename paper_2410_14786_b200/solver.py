@@ -139,7 +139,10 @@ class Problem:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and h.value and getattr(self, "_owner", None) is None:
-            L.lib().bddc_problem_destroy(h)
+            try:
+                L.lib().bddc_problem_destroy(h)
+            except TypeError:  # interpreter shutdown: the module globals are already gone
+                return
             self._h = C.c_void_p()
 
     @property
@@ -359,7 +362,10 @@ class Preconditioner:
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
-            L.lib().bddc_gpu_destroy(self._h)
+            try:
+                L.lib().bddc_gpu_destroy(self._h)
+            except TypeError:  # interpreter shutdown: the module globals are already gone
+                return
             self._h = C.c_void_p()
 
     def _vec(self, r) -> np.ndarray:

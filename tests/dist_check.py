@@ -38,7 +38,11 @@ def main():
             ("c2g2", (1600, 800, 16, 8))]
     if world >= 4:
         cfgs.append(("c2g4", (1600, 1600, 16, 16)))
-    if os.environ.get("DIST_CHECK_C3"):
+        # the N=8 weak-scaling layout (32x16 subdomains, n_c = 1,441: the cooperative coarse grid)
+        # at 128 subdomains per GPU on the 4 GPUs reachable here
+        cfgs.append(("c2g8", (3200, 1600, 32, 16)))
+    # C3 strong scaling (6.35M dofs, 24x24 subdomains) split over the ranks (DIST_CHECK_C3=0 skips)
+    if os.environ.get("DIST_CHECK_C3", "1") != "0":
         cfgs.append(("c3", (2520, 2520, 24, 24)))
     failures = []
     for name, cfg in cfgs:
@@ -104,16 +108,17 @@ def main():
             except InvalidArgument as e:
                 res["nonfinite_rejected"] = f"non-finite entry at index {j}" in str(e)
             res["usable_after_error"] = pre.pcg(b, opts)[1].iterations == rd.iterations
-        # heterogeneous coefficients amplify the reordered dot products of the distributed PCG
-        # (and the reference itself is only 1e-8-stable there, test_gpu_parity): 1e-7 on histories
-        htol = 1e-7 if kappa[0] else 1e-10
+        # h4m8 alone is summation-order sensitive beyond 1e-10 (the CPU oracle moves by more than
+        # 1e-9 when only its dot-product order changes: test_oracle_golden.py::
+        # test_h4m8_history_sensitivity_is_intrinsic); C5 and the rest are held to 1e-10
+        htol = 1e-7 if name == "h4m8" else 1e-10
         ok = (res["apply_bitwise"] and res["apply_untouched_elsewhere"] and rd.iterations == r1.iterations
               and res["history_err_vs_single"] <= htol and res["x_err_vs_single"] <= 1e-10
               and res["device_matches_host"] and res["pinned_matches_pageable"] and rd.converged and res.get("nonfinite_rejected", True)
               and res.get("usable_after_error", True))
         if "history_err_vs_reference" in res:
             ok = ok and res["history_err_vs_reference"] <= htol and abs(rd.iterations - res["iterations_reference"]) <= (
-                1 if kappa[0] else 0)
+                1 if name == "h4m8" else 0)
         if "x_err_vs_reference" in res:
             ok = ok and res["x_err_vs_reference"] <= 1e-10
         res["ok"] = bool(ok)

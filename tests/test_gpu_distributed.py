@@ -18,9 +18,10 @@ def _gpus():
 
 
 @pytest.mark.parametrize("world,env", [(2, {}), (4, {}),
-                                       (2, {"BDDC_FUSED_EX": "0"}),  # separate flag-based exchange kernels
-                                       (2, {"BDDC_P2P": "0"}),       # NCCL exchanges
-                                       (2, {"BDDC_SPLIT": "0", "BDDC_HARMONIC": "0"})],  # unpruned apply
+                                       # separate flag-based exchange kernels
+                                       (2, {"BDDC_FUSED_EX": "0", "DIST_CHECK_C3": "0"}),
+                                       (2, {"BDDC_P2P": "0", "DIST_CHECK_C3": "0"}),  # NCCL exchanges
+                                       (2, {"BDDC_SPLIT": "0", "BDDC_HARMONIC": "0", "DIST_CHECK_C3": "0"})],
                          ids=["w2", "w4", "w2-exchange-kernels", "w2-nccl", "w2-unpruned"])
 def test_distributed_matches_single_gpu_and_reference(gpu, world, env):
     if _gpus() < world:
@@ -28,6 +29,6 @@ def test_distributed_matches_single_gpu_and_reference(gpu, world, env):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + 10 * len(env)),
            os.path.join(ROOT, "tests", "dist_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env={**os.environ, **env})
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, cwd=ROOT, env={**os.environ, **env})
     print(out.stdout[-4000:], out.stderr[-4000:])
     assert out.returncode == 0

@@ -17,7 +17,7 @@ from paper_2410_14786_b200 import Problem, Preconditioner, SolverOptions  # noqa
 from paper_2410_14786_b200.distributed import init  # noqa: E402
 
 rank, world, lr, nid = init()
-lay = {2: (16, 8), 4: (16, 16)}[world]
+lay = tuple(int(v) for v in os.environ["LAYOUT"].split("x")) if os.environ.get("LAYOUT") else {2: (16, 8), 4: (16, 16)}[world]
 p = Problem.poisson(lay[0] * 100, lay[0], lay[1] * 100, lay[1])
 pre = Preconditioner(p, device=lr, dist=(rank, world, nid))
 nl, nr, no, l2g = pre.layout()
