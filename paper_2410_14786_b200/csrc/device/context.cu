@@ -1757,13 +1757,19 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     (void)nsm;
     // TMA unit size: the largest for which every warp gets at least two ring slots next to
     // the vectors (BDDC_UNIT_BYTES overrides, for experiments)
-    const int max_smem = max_solve_smem(I.device) - kSolveStaticSmemReserve;
+    // four parts per subdomain aim at two co-resident CTAs per SM (the SM's 228 KB shared)
+    const int ctas_per_sm = parts >= 4 ? 2 : 1;
+    const int max_smem = std::min(max_solve_smem(I.device), 228 * 1024 / ctas_per_sm - 1024) - kSolveStaticSmemReserve;
     DeviceImage img;
-    int unit = std::getenv("BDDC_UNIT_BYTES") ? std::atoi(std::getenv("BDDC_UNIT_BYTES")) : 4096;
+    // candidate unit sizes (multiples of 128 bytes, largest first); BDDC_UNIT_BYTES pins one
+    std::vector<int> units = {4096, 3584, 3072, 2560, 2048, 1920, 1792, 1536, 1280, 1024};
+    if (std::getenv("BDDC_UNIT_BYTES")) units = {std::atoi(std::getenv("BDDC_UNIT_BYTES"))};
+    std::size_t ui = 0;
+    int unit = units[0];
     int spw = 0;
     tm.mark("host numeric setup (host path)");
     std::vector<SetupClass> classes;
-    for (;; unit /= 2) {
+    for (;; unit = units[++ui]) {
         if (on_device) {
             classes = plan_gpu_setup(I.pb.local_matrices, d, I.pb.constraints, coords, fo, parts, unit,
                                      I.opt.harmonic, workers);
@@ -1780,7 +1786,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
             spw = fit >= 8 ? 8 : fit >= 4 ? 4 : fit >= 2 ? 2 : 0;
         }
         if (spw >= 2) break;
-        if (unit <= 1024)
+        if (ui + 1 >= units.size())
             throw std::runtime_error("subdomain interior (" + std::to_string(img.solve.max_loc) +
                                      " dofs per CTA) exceeds the shared-memory solve capacity");
     }

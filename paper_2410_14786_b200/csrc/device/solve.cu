@@ -190,15 +190,18 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         uend.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + kSolveWarps + warp) : 0;
         pkind.v[q] = i < n_phases ? __ldg(gtable + i * kPhaseStride + 2 * kSolveWarps) : 0;
     }
-    auto fetch = [&](int u) {  // whole warp calls; lane 0 issues unit u into its slot
-        const int o16 = uoff.get(u, units, 2);
-        const int nb = ubytes.get(u, units + 1, 2);
+    auto issue = [&](int u, int o16, int nb) {  // lane 0 issues unit u into its slot
         if (lane == 0) {
             const int s = u & (nsl - 1);
             mbar_expect_tx(&my_bars[s], static_cast<std::uint32_t>(nb));
             bulk_g2s(my_ring + s * unit, src + static_cast<std::int64_t>(o16) * 16, static_cast<std::uint32_t>(nb),
                      &my_bars[s]);
         }
+    };
+    auto fetch = [&](int u) {  // whole warp calls (the table lookups are warp shuffles)
+        const int o16 = uoff.get(u, units, 2);
+        const int nb = ubytes.get(u, units + 1, 2);
+        issue(u, o16, nb);
     };
     for (int u = 0; u < nsl && u < nunits; ++u) fetch(u);
     // everything above reads only the program (immutable): it overlaps the predecessor's tail
@@ -354,14 +357,18 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
         if (CLUSTER > 1 && (kind & kPhaseCombine)) {
             cluster_sync_all();
-            // t_top = (t - Q_rank0) - Q_rank1 : identical arithmetic in both CTAs
+            // t_top = ((t - Q_rank0) - Q_rank1) - ... : identical arithmetic in every CTA
             const int cb = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 1);
             const int ce = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 2);
             for (int l = cb + tid; l < ce; l += kThreads) {
                 const int qi = l - pdr.n_group;
-                const double q0 = pdr.rank == 0 ? Q[qi] : ld_dsmem(&Q[qi], 0);
-                const double q1 = pdr.rank == 1 ? Q[qi] : ld_dsmem(&Q[qi], 1);
-                T[l] = (T[l] - q0) - q1;
+                double q[CLUSTER];
+#pragma unroll
+                for (int r = 0; r < CLUSTER; ++r) q[r] = pdr.rank == r ? Q[qi] : ld_dsmem(&Q[qi], r);
+                double t = T[l];
+#pragma unroll
+                for (int r = 0; r < CLUSTER; ++r) t -= q[r];
+                T[l] = t;
             }
             __syncthreads();
         }
@@ -447,7 +454,12 @@ void launch_interior_solve(SolveParams P, const SolveLaunch& L, int mode, cudaSt
     if (L.n_parts <= 0) return;
     P.unit_bytes = L.unit_bytes;
     P.slot_shift = L.slot_shift;
-    if (L.cluster == 2) {
+    if (L.cluster == 4) {
+        if (mode == 0) launch_one<0, 4>(P, L, stream);
+        else if (mode == 1) launch_one<1, 4>(P, L, stream);
+        else if (mode == 2) launch_one<2, 4>(P, L, stream);
+        else launch_one<3, 4>(P, L, stream);
+    } else if (L.cluster == 2) {
         if (mode == 0) launch_one<0, 2>(P, L, stream);
         else if (mode == 1) launch_one<1, 2>(P, L, stream);
         else if (mode == 2) launch_one<2, 2>(P, L, stream);

@@ -130,7 +130,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         if (fwd[sidx]) pools.fwd_factor_values += v;
         if (bwdm[sidx]) pools.bwd_factor_values += v;
     }
-    if (P < 1 || P > 2) throw std::invalid_argument("solve program: parts must be 1 or 2");
+    if (P != 1 && P != 2 && P != 4) throw std::invalid_argument("solve program: parts must be 1, 2 or 4");
 
     // ---- tree and group assignment (P = 2: halves below the top separator chain)
     std::vector<std::vector<index_t>> children(nsn);
@@ -145,26 +145,29 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         weight[s] += ns * (ns + 1) + 2 * ns * sn[s].n_interior_rows;
         if (sn[s].parent >= 0) weight[sn[s].parent] += weight[s];
     }
+    // parts: the heaviest subtree of the frontier is expanded into its children (it joins the
+    // shared top, solved redundantly by every part after the partial sums are combined) until
+    // the frontier holds at least P subtrees; those are dealt to the P parts by weight (LPT)
     std::vector<int> group(nsn, 0);
-    if (P == 2) {
-        std::vector<index_t> tops, split_children;
-        if (roots.size() == 1) {
-            index_t cur = roots[0];
-            while (true) {
-                tops.push_back(cur);
-                if (children[cur].size() == 1) { cur = children[cur][0]; continue; }
-                split_children = children[cur];
-                break;
-            }
-        } else {
-            split_children = roots;
+    if (P > 1) {
+        std::vector<index_t> tops, frontier = roots;
+        while (static_cast<int>(frontier.size()) < P) {
+            auto heavy = std::max_element(frontier.begin(), frontier.end(), [&](index_t a, index_t b) {
+                return weight[a] != weight[b] ? weight[a] < weight[b] : a > b;
+            });
+            const index_t h = *heavy;
+            if (children[h].empty()) break;  // too few subtrees: some parts stay empty
+            frontier.erase(heavy);
+            tops.push_back(h);
+            for (index_t c : children[h]) frontier.push_back(c);
         }
+        std::vector<index_t> split_children = frontier;
         std::sort(split_children.begin(), split_children.end(),
                   [&](index_t a, index_t b) { return weight[a] != weight[b] ? weight[a] > weight[b] : a < b; });
-        std::int64_t load[2] = {0, 0};
+        std::vector<std::int64_t> load(P, 0);
         std::vector<int> gsub(nsn, -2);
         for (index_t c : split_children) {
-            const int g = load[0] <= load[1] ? 0 : 1;
+            const int g = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
             load[g] += weight[c];
             gsub[c] = g;
         }
@@ -480,8 +483,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             if (first) phases.push_back(std::move(diag_phase));
             kr = 32;
         }
-        // ---------------- exchange the partial sums into the shared top (P = 2)
-        if (P == 2) {
+        // ---------------- exchange the partial sums into the shared top (P > 1)
+        if (P > 1) {
             Phase comb;
             comb.kind = kPhaseCombine;
             comb.comb_begin = n_group;
