@@ -691,36 +691,60 @@ struct GpuContext::Impl {
         pi.upload(bi);
         pl.upload(bl);
         pdv.upload(bd);
-        // ---- batches: members per batch from a scratch budget; scratch sized for the largest
+        // ---- batches: members per batch from a scratch budget. When every class's first batch
+        // fits the budget at once, the classes get disjoint scratch and a stream each and run
+        // concurrently (their pipelines are independent); otherwise they share the scratch in turn.
         const std::size_t budget = std::size_t(6) << 30;
         struct Batch { std::size_t cls; int m0, nb; };
         std::vector<Batch> batches;
-        std::size_t n_aval = 1, n_front = 1, n_S = 1, n_D = 1, n_M = 1, n_piv = 1;
+        std::vector<int> bsz(ncls);
+        std::vector<std::array<std::size_t, 6>> need(ncls);  // aval, fronts, S, D, M, piv per class
+        std::size_t total_bytes = 0;
         for (std::size_t k = 0; k < ncls; ++k) {
             const SetupClass& C = classes[k];
             const std::size_t ns = static_cast<std::size_t>(C.n_iface + C.n_primal);
             const std::size_t per = static_cast<std::size_t>(C.front_total) + C.layout.total +
                                     static_cast<std::size_t>(C.n_iface) * C.n_iface + ns * ns + C.nnz;
             const int nmem = static_cast<int>(C.members.size());
-            const int bsz = std::max(1, std::min<int>(nmem, static_cast<int>(budget / (8 * std::max<std::size_t>(per, 1)))));
-            for (int m0 = 0; m0 < nmem; m0 += bsz) batches.push_back({k, m0, std::min(bsz, nmem - m0)});
-            n_aval = std::max(n_aval, static_cast<std::size_t>(bsz) * C.nnz);
-            n_front = std::max(n_front, static_cast<std::size_t>(bsz) * C.front_total);
-            n_S = std::max(n_S, static_cast<std::size_t>(bsz) * C.n_iface * C.n_iface);
-            n_D = std::max(n_D, static_cast<std::size_t>(bsz) * C.layout.total);
-            n_M = std::max(n_M, static_cast<std::size_t>(bsz) * ns * ns);
-            n_piv = std::max(n_piv, static_cast<std::size_t>(bsz) * ns);
+            bsz[k] = std::max(1, std::min<int>(nmem, static_cast<int>(budget / (8 * std::max<std::size_t>(per, 1)))));
+            for (int m0 = 0; m0 < nmem; m0 += bsz[k]) batches.push_back({k, m0, std::min(bsz[k], nmem - m0)});
+            const std::size_t b = static_cast<std::size_t>(bsz[k]);
+            need[k] = {b * C.nnz, b * C.front_total, b * C.n_iface * C.n_iface, b * C.layout.total, b * ns * ns, b * ns};
+            total_bytes += 8 * (need[k][0] + need[k][1] + need[k][2] + need[k][3] + need[k][4]) + 4 * need[k][5];
         }
+        const bool concurrent = total_bytes <= budget && ncls > 1;
+        std::vector<std::array<std::size_t, 6>> base(ncls, std::array<std::size_t, 6>{});
+        std::array<std::size_t, 6> tot{1, 1, 1, 1, 1, 1};
+        for (std::size_t k = 0; k < ncls; ++k)
+            for (int t = 0; t < 6; ++t) {
+                if (concurrent) {
+                    base[k][t] = tot[t] - 1;
+                    tot[t] += need[k][t];
+                } else {
+                    tot[t] = std::max(tot[t], need[k][t] + 1);
+                }
+            }
         DBuf<double> aval, fronts, Sb, Db, Mb, aci_dev;
         DBuf<int> piv, status;
-        aval.alloc(n_aval);
-        fronts.alloc(n_front);
-        Sb.alloc(n_S);
-        Db.alloc(n_D);
-        Mb.alloc(n_M);
-        piv.alloc(n_piv);
+        aval.alloc(tot[0]);
+        fronts.alloc(tot[1]);
+        Sb.alloc(tot[2]);
+        Db.alloc(tot[3]);
+        Mb.alloc(tot[4]);
+        piv.alloc(tot[5]);
         status.alloc(4 * batches.size());
         BDDC_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int) * status.n, s));
+        struct Streams {
+            std::vector<cudaStream_t> v;
+            ~Streams() {
+                for (cudaStream_t q : v) cudaStreamDestroy(q);
+            }
+        } cs;
+        cs.v.resize(concurrent ? ncls : 1);
+        for (auto& q : cs.v) BDDC_CUDA(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+        Event ready;  // the class streams start after the work queued on s so far
+        BDDC_CUDA(cudaEventRecord(ready.e, s));
+        for (cudaStream_t q : cs.v) BDDC_CUDA(cudaStreamWaitEvent(q, ready.e, 0));
         // ---- jobs of every batch: fills and saddle output offsets
         std::vector<std::int64_t> aci_off(nsub);
         std::int64_t aci_total = 0;
@@ -761,16 +785,19 @@ struct GpuContext::Impl {
         double acc_t[4] = {};  // diagnostics: factor, schur + linv, fill, saddle
         auto lap = [&](int k, std::chrono::steady_clock::time_point& t) {
             if (!tm.on) return;
-            BDDC_CUDA(cudaStreamSynchronize(s));
+            BDDC_CUDA(cudaDeviceSynchronize());  // (diagnostics: serialises the class streams)
             const auto now = std::chrono::steady_clock::now();
             acc_t[k] += std::chrono::duration<double, std::milli>(now - t).count();
             t = now;
         };
-        std::vector<double> av;
+        std::vector<std::vector<double>> avs(ncls);
         for (std::size_t bt = 0; bt < batches.size(); ++bt) {
             const Batch& Bt = batches[bt];
             const SetupClass& C = classes[Bt.cls];
             const Ofs& o = of[Bt.cls];
+            cudaStream_t s = cs.v[concurrent ? Bt.cls : 0];  // this class's stream
+            const auto& bk = base[Bt.cls];
+            std::vector<double>& av = avs[Bt.cls];
             MfPlanDev P{};
             const std::int32_t* ib = pi.p;
             P.sn_nc = ib + o.i[0]; P.sn_m = ib + o.i[1]; P.sn_mi = ib + o.i[2]; P.level_sn = ib + o.i[3];
@@ -797,16 +824,16 @@ struct GpuContext::Impl {
                 const CsrMatrix& A = pb.local_matrices[C.members[Bt.m0 + b]];
                 std::copy(A.values.begin(), A.values.end(), av.begin() + static_cast<std::ptrdiff_t>(b) * C.nnz);
             }
-            BDDC_CUDA(cudaMemcpyAsync(aval.p, av.data(), sizeof(double) * av.size(), cudaMemcpyHostToDevice, s));
-            BDDC_CUDA(cudaStreamSynchronize(s));  // av is reused by the next batch
+            // (pageable source: the call returns once av is staged, so the next batch may refill it)
+            BDDC_CUDA(cudaMemcpyAsync(aval.p + bk[0], av.data(), sizeof(double) * av.size(), cudaMemcpyHostToDevice, s));
             auto tl = std::chrono::steady_clock::now();
             MfBatch B{};
-            B.aval = aval.p;
-            B.fronts = fronts.p;
-            B.S = Sb.p;
-            B.D = Db.p;
-            B.M = Mb.p;
-            B.piv = piv.p;
+            B.aval = aval.p + bk[0];
+            B.fronts = fronts.p + bk[1];
+            B.S = Sb.p + bk[2];
+            B.D = Db.p + bk[3];
+            B.M = Mb.p + bk[4];
+            B.piv = piv.p + bk[5];
             B.status = status.p + 4 * bt;
             B.n = Bt.nb;
             B.first = Bt.m0;
@@ -823,12 +850,17 @@ struct GpuContext::Impl {
             launch_linv_bl(P, B, max_nc, s);
             lap(1, tl);
             for (int q = 0; q < nprog; ++q)
-                launch_fill(pools[q]->stream.p, tword.p, tcode.p, Db.p, jobs_dev.p + job0[bt * nprog + q],
+                launch_fill(pools[q]->stream.p, tword.p, tcode.p, B.D, jobs_dev.p + job0[bt * nprog + q],
                             static_cast<int>(job0[bt * nprog + q + 1] - job0[bt * nprog + q]), s);
             lap(2, tl);
             SaddleOut O{outs_dev.p + out0[bt], kmat.p, phig.p, phi.p, lambda_dev.p, aci_dev.p};
             launch_saddle(P, B, O, s);
             lap(3, tl);
+        }
+        for (cudaStream_t q : cs.v) {  // join the class streams back into s
+            Event done;
+            BDDC_CUDA(cudaEventRecord(done.e, q));
+            BDDC_CUDA(cudaStreamWaitEvent(s, done.e, 0));
         }
         std::vector<int> st(status.n);
         BDDC_CUDA(cudaMemcpyAsync(st.data(), status.p, sizeof(int) * st.size(), cudaMemcpyDeviceToHost, s));
