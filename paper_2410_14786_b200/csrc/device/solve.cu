@@ -304,12 +304,32 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             if (MODE == 0) {
                 for (int l = tid; l < n_loc; l += kThreads) S.y_out[pdr.gmap + l] = X[l];
             } else {
-                for (int l = tid; l < n_loc; l += kThreads) X[l] = __ldg(S.y_in + pdr.gmap + l) - X[l];
+                // X = y0 - X: eight y0 loads in flight per thread (a dependent chain of global
+                // loads here cost ~24k cycles per launch, ~10% of the harmonic solve)
+                const double* y0 = S.y_in + pdr.gmap;
+                for (int l0 = tid; l0 < n_loc; l0 += 8 * kThreads) {
+                    double yv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int l = l0 + q * kThreads;
+                        yv[q] = l < n_loc ? __ldg(y0 + l) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int l = l0 + q * kThreads;
+                        if (l < n_loc) X[l] = yv[q] - X[l];
+                    }
+                }
                 __syncthreads();
             }
+            if (stats && blockIdx.x == 0 && tid == 0)
+                S.stats[static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 + 2 * 256 * kSolveWarps + 3] =
+                    clock64() - t_start;
         }
         double* own = (kind & kPhaseBackward) ? X : T;
         double* other = (kind & kPhaseBackward) ? T : X;
+        const long long t_ph0 = stats ? clock64() : 0;
+        const long long n_tiles0 = n_tiles;
         for (; u < u_end; ++u) {
             const int s = u & (nsl - 1);
             if constexpr (stats) {
@@ -348,6 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
         if constexpr (stats) {
             const long long t0 = clock64();
+            if (blockIdx.x == 0 && lane == 0 && ph < 256) {  // CTA 0: per (phase, warp) busy cycles and tiles
+                long long* pw = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256;
+                pw[ph * kSolveWarps + warp] = t0 - t_ph0;
+                pw[256 * kSolveWarps + ph * kSolveWarps + warp] = n_tiles - n_tiles0;
+            }
             __syncthreads();
             t_bar += clock64() - t0;
             if (blockIdx.x == 0 && tid == 0)  // phase timeline of CTA 0
@@ -356,7 +381,10 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             __syncthreads();
         }
         if (CLUSTER > 1 && (kind & kPhaseCombine)) {
+            long long* mk = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 + 2 * 256 * kSolveWarps;
+            if (stats && blockIdx.x == 0 && tid == 0) mk[0] = clock64() - t_start;
             cluster_sync_all();
+            if (stats && blockIdx.x == 0 && tid == 0) mk[1] = clock64() - t_start;
             // t_top = ((t - Q_rank0) - Q_rank1) - ... : identical arithmetic in every CTA
             const int cb = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 1);
             const int ce = __ldg(gtable + ph * kPhaseStride + 2 * kSolveWarps + 2);
@@ -371,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 T[l] = t;
             }
             __syncthreads();
+            if (stats && blockIdx.x == 0 && tid == 0) mk[2] = clock64() - t_start;
         }
     }
 

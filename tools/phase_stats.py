@@ -1,0 +1,43 @@
+"""Per-phase accounting of the interior solve (dev tool; BDDC_SOLVE_STATS=1): for CTA 0 of the
+apply's last interior-solve launch (the harmonic program), each phase's duration, the busiest and
+mean warp busy cycles and tiles, so the barrier waits split into imbalance vs critical path."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2410_14786_b200 import Preconditioner, Problem  # noqa: E402
+
+W = int(os.environ.get("WARPS", 16))
+p = Problem.poisson(800, 8)
+pre = Preconditioner(p)
+s = torch.cuda.Stream()
+r = torch.tensor(p.rhs(), device="cuda")
+z = torch.empty_like(r)
+for _ in range(3):
+    pre.apply_device(r.data_ptr(), z.data_ptr(), s.cuda_stream)
+torch.cuda.synchronize()
+raw = pre.solve_profile()
+nparts = 128
+tl = raw[nparts * W * 8: nparts * W * 8 + 256]
+pw = raw[nparts * W * 8 + 256: nparts * W * 8 + 256 + 256 * W].reshape(256, W)
+nt = raw[nparts * W * 8 + 256 + 256 * W: nparts * W * 8 + 256 + 2 * 256 * W].reshape(256, W)
+nph = int((tl > 0).sum())
+prev = 0
+tot_dur = tot_max = tot_mean = 0
+print(" ph   dur   busy_max  busy_mean  tiles_max tiles_mean")
+for ph in range(nph):
+    dur = int(tl[ph] - prev) if tl[ph] > prev else 0
+    prev = max(prev, int(tl[ph]))
+    bm, bmean = int(pw[ph].max()), float(pw[ph].mean())
+    tot_dur += dur
+    tot_max += bm
+    tot_mean += bmean
+    print(f"{ph:3d} {dur:6d} {bm:9d} {bmean:10.0f} {int(nt[ph].max()):9d} {nt[ph].mean():10.1f}")
+mk = raw[nparts * W * 8 + 256 + 2 * 256 * W: nparts * W * 8 + 256 + 2 * 256 * W + 8]
+print("markers (cycles since start): before cluster sync", mk[0], "after", mk[1], "after combine", mk[2],
+      "after split switch", mk[3], "| timeline at the combine phase end", [int(t) for t in tl[:nph] if 0 < t <= mk[0]][-1:])
+print(f"sum: duration {tot_dur}, sum of busiest warps {tot_max}, sum of mean busy {tot_mean:.0f}")
