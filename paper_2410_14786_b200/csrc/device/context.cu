@@ -144,7 +144,8 @@ const char* const kEnvSwitches[] = {
     "BDDC_SPLIT", "BDDC_HARMONIC", "BDDC_GRAPH", "BDDC_FUSED_EX", "BDDC_P2P", "BDDC_COOP_COARSE",
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
-    "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES"};
+    "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
+    "BDDC_PRUNED_JOBS"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.

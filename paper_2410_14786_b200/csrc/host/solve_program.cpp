@@ -12,6 +12,10 @@ namespace {
 
 inline std::int64_t pad16(std::int64_t b) { return (b + 15) & ~std::int64_t(15); }
 
+// Subtree jobs per warp in the pruned sweeps (the harmonic program's forward, the head program's
+// backward); 0 = level-synchronous like the full sweeps.
+constexpr double kPrunedJobsPerWarp = 0.0;
+
 struct Tile {
     TileTask t{};
     std::vector<double> vals;
@@ -119,8 +123,17 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         for (index_t sidx = 0; sidx < nsn; ++sidx)  // postorder: children before parents
             if (fwd[sidx] && sn[sidx].parent >= 0) fwd[sn[sidx].parent] = 1;
     }
-    // active = coupled to the interface or an ancestor of such a supernode
-    const std::vector<char> active = fwd;
+    // active = coupled to the interface or an ancestor of such a supernode (the supernodes the
+    // pruned sweeps visit; computed for every program, it also steers the part split below)
+    std::vector<char> active(nsn, 0);
+    for (index_t sidx = 0; sidx < nsn; ++sidx)
+        for (index_t c = sn[sidx].col_begin; c < sn[sidx].col_end && !active[sidx]; ++c) {
+            const index_t v = F.perm[c];
+            for (index_t q = A.row_offsets[v]; q < A.row_offsets[v + 1]; ++q)
+                if (A.col_indices[q] >= nI) { active[sidx] = 1; break; }
+        }
+    for (index_t sidx = 0; sidx < nsn; ++sidx)
+        if (active[sidx] && sn[sidx].parent >= 0) active[sn[sidx].parent] = 1;
     std::vector<char> bwdm(nsn, 1);
     if (prune_backward) bwdm = active;
     if (!prune_forward) std::fill(fwd.begin(), fwd.end(), 1);
@@ -139,38 +152,85 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         if (sn[s].parent >= 0) children[sn[s].parent].push_back(s);
         else roots.push_back(s);
     }
-    std::vector<std::int64_t> weight(nsn, 0);
+    std::vector<std::int64_t> weight(nsn, 0), aweight(nsn, 0);  // subtree values: all / active only
     for (index_t s = 0; s < nsn; ++s) {
         const std::int64_t ns = sn[s].size();
-        weight[s] += ns * (ns + 1) + 2 * ns * sn[s].n_interior_rows;
-        if (sn[s].parent >= 0) weight[sn[s].parent] += weight[s];
+        const std::int64_t own = ns * (ns + 1) + 2 * ns * sn[s].n_interior_rows;
+        weight[s] += own;
+        aweight[s] += active[s] ? own : 0;
+        if (sn[s].parent >= 0) {
+            weight[sn[s].parent] += weight[s];
+            aweight[sn[s].parent] += aweight[s];
+        }
     }
     // parts: the heaviest subtree of the frontier is expanded into its children (it joins the
     // shared top, solved redundantly by every part after the partial sums are combined) until
     // the frontier holds at least P subtrees; those are dealt to the P parts by weight (LPT)
     std::vector<int> group(nsn, 0);
     if (P > 1) {
-        std::vector<index_t> tops, frontier = roots;
-        while (static_cast<int>(frontier.size()) < P) {
-            auto heavy = std::max_element(frontier.begin(), frontier.end(), [&](index_t a, index_t b) {
-                return weight[a] != weight[b] ? weight[a] < weight[b] : a > b;
-            });
-            const index_t h = *heavy;
-            if (children[h].empty()) break;  // too few subtrees: some parts stay empty
-            frontier.erase(heavy);
-            tops.push_back(h);
-            for (index_t c : children[h]) frontier.push_back(c);
-        }
-        std::vector<index_t> split_children = frontier;
+        auto expand = [&](int target, std::vector<index_t>& tops) {
+            std::vector<index_t> frontier = roots;
+            while (static_cast<int>(frontier.size()) < target) {
+                auto heavy = std::max_element(frontier.begin(), frontier.end(), [&](index_t a, index_t b) {
+                    return weight[a] != weight[b] ? weight[a] < weight[b] : a > b;
+                });
+                const index_t h = *heavy;
+                if (children[h].empty()) break;  // too few subtrees: some parts stay empty
+                frontier.erase(heavy);
+                tops.push_back(h);
+                for (index_t c : children[h]) frontier.push_back(c);
+            }
+            return frontier;
+        };
+        std::vector<index_t> tops;
+        std::vector<index_t> split_children = expand(P, tops);
         std::sort(split_children.begin(), split_children.end(),
                   [&](index_t a, index_t b) { return weight[a] != weight[b] ? weight[a] > weight[b] : a < b; });
-        std::vector<std::int64_t> load(P, 0);
         std::vector<int> gsub(nsn, -2);
-        for (index_t c : split_children) {
-            const int g = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-            load[g] += weight[c];
-            gsub[c] = g;
+        std::vector<int> part_of(split_children.size(), 0);
+        {
+            std::vector<std::int64_t> load(P, 0);
+            for (std::size_t i = 0; i < split_children.size(); ++i) {
+                const int g = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+                load[g] += weight[split_children[i]];
+                part_of[i] = g;
+            }
         }
+        // Two parts whose ACTIVE work (what the pruned sweeps visit) is badly unbalanced — a
+        // subdomain touching the interface on one or two sides only, e.g. a corner — wait for each
+        // other at the combine of every pruned launch. Split one level deeper instead (the two
+        // separators above the quarters join the redundant top) and pair the quarters so that
+        // both the full and the active work are balanced, when that is clearly better.
+        auto imbalance = [&](const std::vector<index_t>& kids, const std::vector<int>& part, int np) {
+            std::vector<double> w(np, 0.0), a(np, 0.0);
+            for (std::size_t i = 0; i < kids.size(); ++i) {
+                w[part[i]] += static_cast<double>(weight[kids[i]]);
+                a[part[i]] += static_cast<double>(aweight[kids[i]]);
+            }
+            const double wt = std::accumulate(w.begin(), w.end(), 0.0), at = std::accumulate(a.begin(), a.end(), 0.0);
+            return std::max(wt > 0 ? *std::max_element(w.begin(), w.end()) * np / wt : 1.0,
+                            at > 0 ? *std::max_element(a.begin(), a.end()) * np / at : 1.0);
+        };
+        if (P == 2 && imbalance(split_children, part_of, 2) > 1.25) {
+            std::vector<index_t> tops4;
+            std::vector<index_t> kids4 = expand(4, tops4);
+            if (kids4.size() == 4) {
+                std::vector<int> best;
+                double best_v = imbalance(split_children, part_of, 2);
+                for (int mate = 1; mate < 4; ++mate) {  // quarter 0 with quarter `mate`
+                    std::vector<int> pt(4, 1);
+                    pt[0] = pt[mate] = 0;
+                    const double v = imbalance(kids4, pt, 2);
+                    if (v < best_v - 0.1) { best_v = v; best = pt; }
+                }
+                if (!best.empty()) {
+                    split_children = kids4;
+                    part_of = best;
+                    tops = tops4;
+                }
+            }
+        }
+        for (std::size_t i = 0; i < split_children.size(); ++i) gsub[split_children[i]] = part_of[i];
         for (index_t t : tops) gsub[t] = -1;
         for (index_t s = nsn - 1; s >= 0; --s) {
             if (gsub[s] != -2) { group[s] = gsub[s]; continue; }
@@ -344,38 +404,54 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
 
         // ---- subtree-to-warp mapping: below the cut every warp solves whole subtrees ("jobs")
         // sequentially with no CTA barrier; only the levels above the cut are level-synchronous.
-        std::vector<char> local(nsn, 0);
-        std::vector<index_t> job_roots;
-        {
+        // The forward and backward sweeps have their own cut: a pruned sweep (few supernodes per
+        // level: the boundary band and its ancestors) can trade its level barriers for warp-local
+        // chains, a full sweep keeps the levels (measured: the serial chains of full subtrees cost
+        // more than the barriers they save)
+        struct JobSet {
+            std::vector<char> local;
+            std::vector<std::vector<index_t>> job_nodes;  // postorder
+            std::vector<index_t> job_of, heights;         // heights above the cut
+        };
+        auto make_jobs = [&](double jpw, bool by_active) {
+            JobSet J;
+            J.local.assign(nsn, 0);
+            const std::vector<std::int64_t>& wt = by_active ? aweight : weight;
+            std::vector<index_t> job_roots;
             std::int64_t total = 0;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && (sn[s].parent < 0 || !in_group(sn[s].parent))) total += weight[s];
-            // subtree jobs per warp (BDDC_JOBS_PER_WARP); off by default: measured on B200 the
-            // serial per-warp chain of a subtree costs more than the level barriers it saves
-            const char* jpw_env = std::getenv("BDDC_JOBS_PER_WARP");
-            const double jpw = jpw_env ? std::atof(jpw_env) : 0.0;
-            const std::int64_t tau = jpw > 0 ? std::max<std::int64_t>(1, static_cast<std::int64_t>(total / (jpw * kSolveWarps))) : 0;
+                if (in_group(s) && (sn[s].parent < 0 || !in_group(sn[s].parent))) total += wt[s];
+            const std::int64_t tau =
+                jpw > 0 ? std::max<std::int64_t>(1, static_cast<std::int64_t>(total / (jpw * kSolveWarps))) : 0;
             for (index_t s = nsn - 1; s >= 0; --s) {  // parents before children
                 if (!in_group(s)) continue;
                 const index_t p = sn[s].parent;
-                const bool parent_local = p >= 0 && in_group(p) && local[p];
-                if (parent_local) { local[s] = 1; continue; }
-                if (weight[s] <= tau) { local[s] = 1; job_roots.push_back(s); }
+                const bool parent_local = p >= 0 && in_group(p) && J.local[p];
+                if (parent_local) { J.local[s] = 1; continue; }
+                if (tau > 0 && wt[s] <= tau) { J.local[s] = 1; job_roots.push_back(s); }
             }
             std::sort(job_roots.begin(), job_roots.end());
-        }
-        std::vector<index_t> job_of(nsn, -1);
-        std::vector<std::vector<index_t>> job_nodes(job_roots.size());  // postorder
-        for (std::size_t j = 0; j < job_roots.size(); ++j) job_of[job_roots[j]] = static_cast<index_t>(j);
-        for (index_t s = nsn - 1; s >= 0; --s)
-            if (local[s] && job_of[s] < 0) job_of[s] = job_of[sn[s].parent];
-        for (index_t s = 0; s < nsn; ++s)
-            if (local[s]) job_nodes[job_of[s]].push_back(s);
-        std::vector<index_t> heights;  // above the cut
-        for (index_t s = 0; s < nsn; ++s)
-            if (in_group(s) && !local[s]) heights.push_back(sn[s].height);
-        std::sort(heights.begin(), heights.end());
-        heights.erase(std::unique(heights.begin(), heights.end()), heights.end());
+            J.job_of.assign(nsn, -1);
+            J.job_nodes.resize(job_roots.size());
+            for (std::size_t j = 0; j < job_roots.size(); ++j) J.job_of[job_roots[j]] = static_cast<index_t>(j);
+            for (index_t s = nsn - 1; s >= 0; --s)
+                if (J.local[s] && J.job_of[s] < 0) J.job_of[s] = J.job_of[sn[s].parent];
+            for (index_t s = 0; s < nsn; ++s)
+                if (J.local[s]) J.job_nodes[J.job_of[s]].push_back(s);
+            for (index_t s = 0; s < nsn; ++s)
+                if (in_group(s) && !J.local[s]) J.heights.push_back(sn[s].height);
+            std::sort(J.heights.begin(), J.heights.end());
+            J.heights.erase(std::unique(J.heights.begin(), J.heights.end()), J.heights.end());
+            return J;
+        };
+        // BDDC_JOBS_PER_WARP: subtree jobs in every sweep (experiments); BDDC_PRUNED_JOBS: jobs per
+        // warp in the pruned sweeps only
+        const char* jpw_env = std::getenv("BDDC_JOBS_PER_WARP");
+        const char* pj_env = std::getenv("BDDC_PRUNED_JOBS");
+        const double jpw_all = jpw_env ? std::atof(jpw_env) : 0.0;
+        const double jpw_pruned = pj_env ? std::atof(pj_env) : kPrunedJobsPerWarp;
+        const JobSet jf = make_jobs(prune_forward && jpw_all <= 0 ? jpw_pruned : jpw_all, prune_forward && jpw_all <= 0);
+        const JobSet jb = make_jobs(prune_backward && jpw_all <= 0 ? jpw_pruned : jpw_all, prune_backward && jpw_all <= 0);
 
         // greedy colouring of jobs whose target-row sets intersect: each job takes the first
         // colour none of its target rows carries yet (per-row bit mask of used colours; beyond
@@ -414,22 +490,22 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             // (1) warp-local subtrees: diag + pushes inside the subtree, postorder
             Phase ph;
             ph.kind = kPhaseChained;
-            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
+            for (std::size_t j = 0; j < jf.job_nodes.size(); ++j) {
                 Chunks job;
-                for (index_t s : job_nodes[j]) {
+                for (index_t s : jf.job_nodes[j]) {
                     if (!fwd[s]) continue;
                     diag_fwd(s, job);
-                    push_fwd(s, job, false, [&](index_t r) { return local[owner[r]] && job_of[owner[r]] == (index_t)j; });
+                    push_fwd(s, job, false, [&](index_t r) { return jf.local[owner[r]] && jf.job_of[owner[r]] == (index_t)j; });
                 }
                 ph.jobs.push_back(std::move(job));
             }
             phases.push_back(std::move(ph));
             // (2) pushes leaving each subtree, jobs coloured by target rows
-            std::vector<std::vector<index_t>> targets(job_nodes.size());
-            std::vector<Chunks> ext(job_nodes.size());
-            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
-                auto outside = [&](index_t r) { return !(local[owner[r]] && job_of[owner[r]] == (index_t)j); };
-                for (index_t s : job_nodes[j]) {
+            std::vector<std::vector<index_t>> targets(jf.job_nodes.size());
+            std::vector<Chunks> ext(jf.job_nodes.size());
+            for (std::size_t j = 0; j < jf.job_nodes.size(); ++j) {
+                auto outside = [&](index_t r) { return !(jf.local[owner[r]] && jf.job_of[owner[r]] == (index_t)j); };
+                for (index_t s : jf.job_nodes[j]) {
                     if (!fwd[s]) continue;
                     push_fwd(s, ext[j], false, outside);
                     for (index_t a = 0; a < sn[s].n_interior_rows; ++a)
@@ -443,11 +519,11 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             }
         }
         // (3) levels above the cut, level-synchronous
-        for (index_t h : heights) {
+        for (index_t h : jf.heights) {
             Chunks b;
             std::vector<index_t> nodes, nrows, mrows;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == h && fwd[s]) {
+                if (in_group(s) && !jf.local[s] && sn[s].height == h && fwd[s]) {
                     nodes.push_back(s);
                     nrows.push_back(sn[s].size());
                     mrows.push_back(sn[s].n_interior_rows);
@@ -514,14 +590,14 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             pb2.kind = kPhaseBackward;
             phases.push_back(std::move(pb2));
         }
-        for (auto hit = heights.rbegin(); hit != heights.rend(); ++hit) {
+        for (auto hit = jb.heights.rbegin(); hit != jb.heights.rend(); ++hit) {
             Chunks a, b;
             std::vector<index_t> nrows;
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == *hit && bwdm[s]) nrows.push_back(sn[s].size());
+                if (in_group(s) && !jb.local[s] && sn[s].height == *hit && bwdm[s]) nrows.push_back(sn[s].size());
             kr = chunk_rows_for(nrows);
             for (index_t s = 0; s < nsn; ++s)
-                if (in_group(s) && !local[s] && sn[s].height == *hit && bwdm[s]) bwd(s, b);
+                if (in_group(s) && !jb.local[s] && sn[s].height == *hit && bwdm[s]) bwd(s, b);
             kr = 32;
             (void)a;
             Phase pb2 = singles(std::move(b));
@@ -531,9 +607,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         {
             Phase ph;
             ph.kind = kPhaseBackward | kPhaseChained;
-            for (std::size_t j = 0; j < job_nodes.size(); ++j) {
+            for (std::size_t j = 0; j < jb.job_nodes.size(); ++j) {
                 Chunks job;
-                for (auto it = job_nodes[j].rbegin(); it != job_nodes[j].rend(); ++it)
+                for (auto it = jb.job_nodes[j].rbegin(); it != jb.job_nodes[j].rend(); ++it)
                     if (bwdm[*it]) bwd(*it, job);
                 ph.jobs.push_back(std::move(job));
             }

@@ -41,3 +41,9 @@ mk = raw[nparts * W * 8 + 256 + 2 * 256 * W: nparts * W * 8 + 256 + 2 * 256 * W 
 print("markers (cycles since start): before cluster sync", mk[0], "after", mk[1], "after combine", mk[2],
       "after split switch", mk[3], "| timeline at the combine phase end", [int(t) for t in tl[:nph] if 0 < t <= mk[0]][-1:])
 print(f"sum: duration {tot_dur}, sum of busiest warps {tot_max}, sum of mean busy {tot_mean:.0f}")
+# per-CTA totals (cycles from start to the end of the phase loop, busiest warp), slowest first
+w = raw[:nparts * W * 8].reshape(nparts, W, 8)
+tot = w[:, :, 0].max(axis=1)
+order = np.argsort(-tot)
+print("slowest CTAs (subdomain, rank, cycles):", [(int(c) // 2, int(c) % 2, int(tot[c])) for c in order[:8]])
+print("fastest CTAs:", [(int(c) // 2, int(c) % 2, int(tot[c])) for c in order[-4:]], "median", int(np.median(tot)))
