@@ -1835,8 +1835,8 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     for (const PartDesc& pd : img.solve.parts) I.solve_stream_bytes += pd.stream_bytes;
     for (const PartDesc& pd : img.harm.parts) I.harm_stream_bytes += pd.stream_bytes;
     I.harm_fwd_values = img.harm.parts.empty() ? I.factor_vals : img.harm.fwd_factor_values;
-    I.k_values = static_cast<std::int64_t>(img.kmat.size());
-    I.phig_values = static_cast<std::int64_t>(img.phig.size());
+    I.k_values = img.device_values ? img.kmat_total : static_cast<std::int64_t>(img.kmat.size());
+    I.phig_values = img.device_values ? img.phig_total : static_cast<std::int64_t>(img.phig.size());
     I.ginnz = static_cast<std::int64_t>(img.gi_row_val.size());
     for (const auto& v : img.solve.couple_val) (void)v;
     I.couple_nnz = static_cast<std::int64_t>(img.solve.couple_val.size());

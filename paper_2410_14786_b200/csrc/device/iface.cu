@@ -92,7 +92,10 @@ coarse_direct_kernel(const IfaceParams P) {
 }
 
 constexpr int kLocalThreads = 256;
-constexpr int kLocalRows = 4;  // rows per warp in flight (8 independent loads per lane)
+#ifndef BDDC_LOCAL_ROWS
+#define BDDC_LOCAL_ROWS 4
+#endif
+constexpr int kLocalRows = BDDC_LOCAL_ROWS;  // rows per warp in flight (2 * kLocalRows independent loads per lane)
 
 // h_i = W_i (Phi_Gi x_c[map_i] + K_i g_i) (with_coarse) or h_i = K_i g_i. Each streaming warp
 // handles kLocalRows rows of K_i at once so every lane keeps 2 * kLocalRows loads in flight;
