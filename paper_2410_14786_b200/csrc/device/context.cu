@@ -162,8 +162,9 @@ struct SetupTimer {
 };
 
 // Largest coarse dimension served by the dense replicated A_c^-1 (n_c^2 doubles per GPU, n_c
-// doubles of r_c in the K_i kernel's shared memory); above it the coarse solve is the coarse CG.
-constexpr index_t kDenseCoarseMax = 16384;
+// doubles of r_c in the K_i kernel's shared memory, and an O(n_c^3) Gauss-Jordan inverse whose
+// rank-1 passes stream n_c^2 doubles each); above it the coarse solve is the coarse CG.
+constexpr index_t kDenseCoarseMax = 4096;
 }  // namespace
 
 struct GpuContext::Impl {
