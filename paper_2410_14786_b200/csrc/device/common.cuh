@@ -58,7 +58,7 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
 // Speculative launches of the pipelined PCG loop pass the solver's scalar block: a set
 // converged (scal[2]) or error (scal[3]) flag turns the kernel into a no-op.
 __device__ __forceinline__ bool skip_launch(const double* scal) {
-    return scal != nullptr && (scal[2] != 0.0 || scal[3] != 0.0);
+    return scal != nullptr && (scal[2] != 0.0 || scal[3] == 1.0);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
