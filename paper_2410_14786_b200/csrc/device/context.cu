@@ -145,7 +145,7 @@ const char* const kEnvSwitches[] = {
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
-    "BDDC_PRUNED_JOBS"};
+    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
@@ -236,6 +236,10 @@ struct GpuContext::Impl {
     double* pinned_dev = nullptr;  // the same buffer, mapped (update's fused check writes it)
     DBuf<std::uint64_t> solo_seq;  // one GPU: grid tickets of update's fused check and dir_spmv
     DBuf<unsigned int> solo_ticket;
+    DBuf<unsigned int> plain_bar;  // grid barrier of the one-launch plain CG
+    // plain CG on one GPU as one cooperative launch (BDDC_PLAIN_LOOP=0: the per-kernel loop)
+    bool use_plain_loop = !(std::getenv("BDDC_PLAIN_LOOP") && std::atoi(std::getenv("BDDC_PLAIN_LOOP")) == 0);
+    int plain_loop_ok = -1;  // occupancy check, once
     DBuf<double> p_alt;            // second direction buffer (pcg_dir_spmv)
     // BDDC_DIR_SPMV=1: fuse p = z + beta p into the SpMV. Off by default: measured on B200 the
     // on-the-fly p entries (two extra gathers per nonzero) cost more than the xpay pass saves
@@ -1525,7 +1529,38 @@ struct GpuContext::Impl {
             return rep;
         }
         if (!early) first_direction();
+        auto finish = [&](double rel) -> SolveResult {
+            rep.final_relative_residual = rel;
+            const int k = rep.iterations;
+            std::vector<double> al(k), be(std::max(0, k - 1));
+            if (k) BDDC_CUDA(cudaMemcpyAsync(al.data(), alpha.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+            if (k > 1) BDDC_CUDA(cudaMemcpyAsync(be.data(), beta.p, sizeof(double) * (k - 1), cudaMemcpyDeviceToHost, s));
+            if (o.record_history && k) {
+                rep.history.resize(k + 1);
+                BDDC_CUDA(cudaMemcpyAsync(rep.history.data() + 1, hist.p + 1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+            }
+            BDDC_CUDA(cudaStreamSynchronize(s));
+            rep.condition_estimate = condition_estimate(al, be);
+            return rep;
+        };
         double rel = 1.0;
+        if (!precondition && !dist() && use_plain_loop) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            BDDC_CUDA(cudaStreamIsCapturing(s, &cs));
+            if (plain_loop_ok < 0) plain_loop_ok = pcg_plain_loop_fits(D.grid) ? 1 : 0;
+            if (cs == cudaStreamCaptureStatusNone && plain_loop_ok == 1) {
+                if (!plain_bar.p) plain_bar.alloc(1);
+                D.p_alt = p_alt.p;  // p_k alternates between p and p_alt
+                pcg_plain_loop(D, o.max_iterations, plain_bar.p, s);
+                BDDC_CUDA(cudaMemcpyAsync(pinned, scal.p, sizeof(double) * 5, cudaMemcpyDeviceToHost, s));
+                BDDC_CUDA(cudaStreamSynchronize(s));
+                if (pinned[3] == 1.0) throw std::runtime_error("matrix not SPD");
+                rel = pinned[1];
+                rep.iterations = static_cast<int>(pinned[4]);
+                rep.converged = pinned[2] != 0.0;
+                return finish(rel);
+            }
+        }
         // The convergence test of iteration `it` is read back while the GPU already runs the
         // next iteration's apply / dot / xpay (speculatively: they only touch z, p, rho, beta,
         // which are unused once the loop stops), so the host round trip leaves no bubble.
@@ -1707,18 +1742,7 @@ struct GpuContext::Impl {
                 }
             }
         }
-        rep.final_relative_residual = rel;
-        const int k = rep.iterations;
-        std::vector<double> al(k), be(std::max(0, k - 1));
-        if (k) BDDC_CUDA(cudaMemcpyAsync(al.data(), alpha.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-        if (k > 1) BDDC_CUDA(cudaMemcpyAsync(be.data(), beta.p, sizeof(double) * (k - 1), cudaMemcpyDeviceToHost, s));
-        if (o.record_history && k) {
-            rep.history.resize(k + 1);
-            BDDC_CUDA(cudaMemcpyAsync(rep.history.data() + 1, hist.p + 1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-        }
-        BDDC_CUDA(cudaStreamSynchronize(s));
-        rep.condition_estimate = condition_estimate(al, be);
-        return rep;
+        return finish(rel);
     }
 };
 

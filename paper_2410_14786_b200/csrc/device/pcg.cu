@@ -241,6 +241,115 @@ __global__ void __launch_bounds__(kVecThreads) xpay_kernel(const PcgDevice D, in
     }
 }
 
+// Grid-wide barrier of a cooperative (all CTAs resident) launch: a monotonic arrival counter,
+// released by each CTA's thread 0 after the CTA's writes, acquired before the CTA proceeds.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// Plain CG on one GPU (pcg.cpp:61-109 with z = r): the whole iteration loop in ONE cooperative
+// launch, two grid barriers per iteration instead of four kernels and a host read-back of the
+// convergence flags. Phase 1 is dir_spmv's: p_k = r + beta p_{k-1} formed on the fly for the
+// columns each row reads (p_k in p_alt for odd k, p for even k), q = A p_k, p.q; phase 2 is
+// update's. The partials and their fixed-order sums (every CTA sums the same grid partials in the
+// same order, so every CTA takes the same decisions) and every expression are those of the
+// launch-per-kernel loop, so the iterates are bitwise identical. The vectors change inside the
+// launch and are read through the coherent path (no __restrict__ / non-coherent loads); only
+// the matrix is. scal[4] = iterations done.
+__global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevice D, int max_it, unsigned int* bar) {
+    __shared__ double scratch[kVecThreads / 32];
+    unsigned int target = 0;
+    const int stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const std::int32_t* __restrict__ ec = D.ell_col;
+    const double* __restrict__ ev = D.ell_val;
+    double* q = D.q;
+    double* x = D.x;
+    double* r = D.r;
+    const double normb = D.scal[0];
+    double rho = D.rho[0];
+    double beta = 0.0;
+    for (int it = 1;; ++it) {
+        double* pn = (it & 1) ? D.p_alt : D.p;
+        const double* po = (it & 1) ? D.p : D.p_alt;
+        const bool first = it == 1;  // p_1 = z = r
+        auto p_at = [&](int j) { return first ? r[j] : r[j] + beta * po[j]; };
+        double acc = 0.0;
+        for (int i = i0; i < D.n; i += stride) {
+            const std::int64_t base = D.ell_off[i >> 5] + (i & 31);
+            const int len = D.ell_len[i];
+            double y = 0.0;
+            int j = 0;
+            for (; j + 3 < len; j += 4) {
+                const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
+                const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
+                const double x0 = p_at(ec[base + 32 * j]), x1 = p_at(ec[base + 32 * (j + 1)]);
+                const double x2 = p_at(ec[base + 32 * (j + 2)]), x3 = p_at(ec[base + 32 * (j + 3)]);
+                y += v0 * x0;
+                y += v1 * x1;
+                y += v2 * x2;
+                y += v3 * x3;
+            }
+            for (; j < len; ++j) y += ev[base + 32 * j] * p_at(ec[base + 32 * j]);
+            const double pi = p_at(i);
+            pn[i] = pi;
+            q[i] = y;
+            if (i < D.n_dot) acc = fma(pi, y, acc);
+        }
+        acc = block_sum<kVecThreads>(acc, scratch);
+        if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
+        grid_barrier(bar, target);
+        // alpha, x += alpha p, r -= alpha q, r.r (update_kernel; p_k[i] of the thread's own rows)
+        const double pq = sum_partials(D.part_a, gridDim.x, scratch);
+        if (pq <= 0.0) {  // pcg.cpp:75-78 "matrix not SPD"
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                D.scal[3] = 1.0;
+                D.scal[4] = it;
+            }
+            return;
+        }
+        const double alpha = rho / pq;
+        if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[it - 1] = alpha;
+        acc = 0.0;
+        for (int i = i0; i < D.n; i += stride) {
+            x[i] += alpha * pn[i];
+            const double ri = r[i] - alpha * q[i];
+            r[i] = ri;
+            if (i < D.n_dot) acc = fma(ri, ri, acc);
+        }
+        acc = block_sum<kVecThreads>(acc, scratch);
+        if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
+        grid_barrier(bar, target);
+        // convergence (check_scalar), beta for the next direction (xpay_kernel)
+        const double rr = sum_partials(D.part_b, gridDim.x, scratch);
+        const double rel = sqrt(rr) / normb;
+        const bool done = rel <= D.rtol || (D.atol > 0.0 && rel * normb <= D.atol);
+        beta = rr / rho;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            D.hist[it] = rel;
+            D.scal[1] = rel;
+            D.scal[3] = isfinite(rel) ? 0.0 : 2.0;  // a non-finite residual carries on (no apply)
+            if (done) D.scal[2] = 1.0;
+            D.scal[4] = it;
+            if (!done && it < max_it) {
+                D.beta[it - 1] = beta;
+                D.rho[it] = rr;
+            }
+        }
+        if (done || it == max_it) return;
+        rho = rr;
+    }
+}
+
 __global__ void __launch_bounds__(kVecThreads) spmv_kernel(int n, const std::int32_t* __restrict__ ptr,
                                                            const std::int32_t* __restrict__ col,
                                                            const double* __restrict__ val,
@@ -317,5 +426,27 @@ void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_
 }
 
 int pcg_grid_for(int n) { return vec_grid(n); }
+bool pcg_plain_loop_fits(int grid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    BDDC_CUDA(cudaGetDevice(&dev));
+    BDDC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plain_cg_kernel, kVecThreads, 0));
+    return grid <= per_sm * sms;
+}
+void pcg_plain_loop(const PcgDevice& D, int max_iterations, unsigned int* barrier, cudaStream_t s) {
+    BDDC_CUDA(cudaMemsetAsync(barrier, 0, sizeof(unsigned int), s));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(D.grid);
+    cfg.blockDim = dim3(kVecThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BDDC_CUDA(cudaLaunchKernelEx(&cfg, plain_cg_kernel, D, max_iterations, barrier));
+    BDDC_LAUNCHED();
+}
+
 
 }  // namespace bddc_b200

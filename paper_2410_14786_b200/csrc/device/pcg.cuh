@@ -83,6 +83,10 @@ void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const 
 void device_axpby(int n, double a, const double* x, double b, const double* y, double* out,
                   cudaStream_t s);  // out = a x + b y
 int pcg_grid_for(int n);
+// plain CG (no preconditioner, one GPU) as one cooperative launch over D.grid CTAs: iterations
+// 1..max_iterations from rho[0] and p = r; scal[1..4] = rel, converged, error code, iterations
+bool pcg_plain_loop_fits(int grid);
+void pcg_plain_loop(const PcgDevice& D, int max_iterations, unsigned int* barrier, cudaStream_t s);
 // Smallest index of a non-finite entry, or -1 (writes to *dev_result).
 void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_t s);
 

@@ -92,3 +92,51 @@ def test_repeated_solve_reuses_graphs(gpu):
     for _ in range(3):
         pre.pcg(p.rhs(), opts)
     assert n1 >= 1 and pre.stats()["graph_captures"] == n1
+
+
+PLAIN_SCRIPT = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, ROOT)
+from paper_2410_14786_b200 import Preconditioner, Problem, SolverOptions
+out = {}
+cases = {"c2": Problem.poisson(800, 8), "kappa": Problem.poisson(240, 4, kappa_decades=4.0, kappa_seed=7)}
+for name, p in cases.items():
+    pre = Preconditioner(p)
+    for cap in (10000, 7):
+        x, rep = pre.pcg(p.rhs(), SolverOptions(1e-8, 0.0, cap, True), precondition=False)
+        out[f"{name}/{cap}"] = [rep.iterations, bool(rep.converged), [float(h).hex() for h in rep.residual_history],
+                                hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
+                                float(rep.condition_estimate).hex()]
+# symmetric, not SPD (the negated Laplacian): pcg.cpp:75-78 at the first iteration
+p = Problem.poisson(32, 2)
+nr, nc, rp, ci, va = p.global_matrix()
+neg = Problem.from_arrays((nr, nc, rp, ci, -va), [p.local_matrix(i) for i in range(p.n_subdomains)],
+                          p.subdomain_dofs(), p.interior_counts(), p.weights(),
+                          [p.constraint_matrix(i) for i in range(p.n_subdomains)], p.primal_maps(), p.n_coarse,
+                          rhs=p.rhs())
+try:
+    Preconditioner(neg).pcg(neg.rhs(), SolverOptions(1e-8, 0.0, 100, True), precondition=False)
+    out["neg"] = "no error"
+except Exception as e:
+    out["neg"] = str(e)
+print(json.dumps(out))
+""".replace("ROOT", repr(ROOT))
+
+
+def test_plain_cg_one_launch_matches_kernel_loop(gpu):
+    # plain CG on one GPU runs as one cooperative launch (pcg.cu plain_cg_kernel); its phases are
+    # the per-kernel loop's (BDDC_PLAIN_LOOP=0), so histories, x and the Lanczos estimate are
+    # bitwise identical, at convergence and at the iteration cap, and "not SPD" is raised alike
+    env = {k: v for k, v in os.environ.items() if not k.startswith("BDDC_")}
+    res = []
+    for extra in ({}, {"BDDC_PLAIN_LOOP": "0"}):
+        r = subprocess.run([sys.executable, "-c", PLAIN_SCRIPT], env={**env, **extra}, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    one, loop = res
+    assert one == loop
+    assert one["c2/10000"][0] == 1649 and one["c2/10000"][1]
+    assert one["c2/7"][0] == 7 and not one["c2/7"][1] and len(one["c2/7"][2]) == 8
+    assert "matrix not SPD" in one["neg"]
