@@ -145,7 +145,7 @@ const char* const kEnvSwitches[] = {
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
-    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP"};
+    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
@@ -704,7 +704,7 @@ struct GpuContext::Impl {
         struct Batch { std::size_t cls; int m0, nb; };
         std::vector<Batch> batches;
         std::vector<int> bsz(ncls);
-        std::vector<std::array<std::size_t, 6>> need(ncls);  // aval, fronts, S, D, M, piv per class
+        std::vector<std::array<std::size_t, 6>> need(ncls);  // aval, fronts, S, D, M, row/column maps per class
         std::size_t total_bytes = 0;
         for (std::size_t k = 0; k < ncls; ++k) {
             const SetupClass& C = classes[k];
@@ -715,7 +715,7 @@ struct GpuContext::Impl {
             bsz[k] = std::max(1, std::min<int>(nmem, static_cast<int>(budget / (8 * std::max<std::size_t>(per, 1)))));
             for (int m0 = 0; m0 < nmem; m0 += bsz[k]) batches.push_back({k, m0, std::min(bsz[k], nmem - m0)});
             const std::size_t b = static_cast<std::size_t>(bsz[k]);
-            need[k] = {b * C.nnz, b * C.front_total, b * C.n_iface * C.n_iface, b * C.layout.total, b * ns * ns, b * ns};
+            need[k] = {b * C.nnz, b * C.front_total, b * C.n_iface * C.n_iface, b * C.layout.total, b * ns * ns, 2 * b * ns};
             total_bytes += 8 * (need[k][0] + need[k][1] + need[k][2] + need[k][3] + need[k][4]) + 4 * need[k][5];
         }
         const bool concurrent = total_bytes <= budget && ncls > 1;
@@ -1831,8 +1831,10 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         if (on_device) {
             classes = plan_gpu_setup(I.pb.local_matrices, d, I.pb.constraints, coords, fo, parts, unit,
                                      I.opt.harmonic, workers);
+            tm.mark("  class plan (symbolic, templates)");
             img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
                                      unit, I.plan.get(), I.opt.harmonic, &classes);
+            tm.mark("  device image");
         } else {
             img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
                                      unit, I.plan.get(), I.opt.harmonic);
@@ -1936,6 +1938,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         I.weights_local.upload(wl);
     }
     I.coarse_status.alloc(4);
+    tm.mark("  coarse-owner maps, weights");
     I.A_ptr.upload(I.pb.global_matrix.row_offsets);
     I.A_col.upload(I.pb.global_matrix.col_indices);
     I.A_val.upload(I.pb.global_matrix.values);
@@ -1956,19 +1959,18 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
             }
             off[sl + 1] = off[sl] + static_cast<std::int64_t>(w) * 32;
         }
-        std::vector<std::int32_t> col(static_cast<std::size_t>(std::max<std::int64_t>(off[ns], 1)), 0);
-        std::vector<double> val(col.size(), 0.0);
-        for (index_t i = 0; i < nr; ++i)
-            for (index_t q = A.row_offsets[i], j = 0; q < A.row_offsets[i + 1]; ++q, ++j) {
-                const std::int64_t at = off[i / 32] + 32 * j + (i % 32);
-                col[at] = A.col_indices[q];
-                val[at] = A.values[q];
-            }
+        // the entries are scattered on the device from the CSR upload above
+        const std::size_t words = static_cast<std::size_t>(std::max<std::int64_t>(off[ns], 1));
         I.ell_off.upload(off);
         I.ell_len.upload(len);
-        I.ell_col.upload(col);
-        I.ell_val.upload(val);
+        I.ell_col.alloc(words);
+        I.ell_val.alloc(words);
+        BDDC_CUDA(cudaMemsetAsync(I.ell_col.p, 0, sizeof(std::int32_t) * words, I.stream));
+        BDDC_CUDA(cudaMemsetAsync(I.ell_val.p, 0, sizeof(double) * words, I.stream));
+        device_csr_to_sliced_ell(static_cast<int>(nr), I.A_ptr.p, I.A_col.p, I.A_val.p, I.ell_off.p, I.ell_col.p,
+                                 I.ell_val.p, I.stream);
     }
+    tm.mark("  global matrix, sliced ELL");
     const std::size_t n = d.global_dofs;
     I.U.alloc(n);
     BDDC_CUDA(cudaMemset(I.U.p, 0, sizeof(double) * n));

@@ -372,6 +372,20 @@ __global__ void __launch_bounds__(kVecThreads) nonfinite_kernel(int n, const dou
         if (!isfinite(x[i])) atomicMin(res, i);
 }
 
+__global__ void __launch_bounds__(kVecThreads) csr_to_ell_kernel(int n, const std::int32_t* __restrict__ ptr,
+                                                                const std::int32_t* __restrict__ col,
+                                                                const double* __restrict__ val,
+                                                                const std::int64_t* __restrict__ off,
+                                                                std::int32_t* ell_col, double* ell_val) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const std::int64_t base = off[i >> 5] + (i & 31);
+        for (int e = ptr[i], j = 0; e < ptr[i + 1]; ++e, ++j) {
+            ell_col[base + 32 * j] = col[e];
+            ell_val[base + 32 * j] = val[e];
+        }
+    }
+}
+
 int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecThreads, 148 * 4)); }
 
 }  // namespace
@@ -426,6 +440,12 @@ void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_
 }
 
 int pcg_grid_for(int n) { return vec_grid(n); }
+void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
+                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s) {
+    if (n <= 0) return;
+    csr_to_ell_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, off, ell_col, ell_val);
+    BDDC_LAUNCHED();
+}
 bool pcg_plain_loop_fits(int grid) {
     int dev = 0, sms = 0, per_sm = 0;
     BDDC_CUDA(cudaGetDevice(&dev));

@@ -83,6 +83,9 @@ void device_spmv(int n, const std::int32_t* ptr, const std::int32_t* col, const 
 void device_axpby(int n, double a, const double* x, double b, const double* y, double* out,
                   cudaStream_t s);  // out = a x + b y
 int pcg_grid_for(int n);
+// sliced ELL from CSR (entry j of row i at off[i / 32] + 32 j + i % 32, CSR order kept)
+void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
+                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s);
 // plain CG (no preconditioner, one GPU) as one cooperative launch over D.grid CTAs: iterations
 // 1..max_iterations from rho[0] and p = r; scal[1..4] = rel, converged, error code, iterations
 bool pcg_plain_loop_fits(int grid);

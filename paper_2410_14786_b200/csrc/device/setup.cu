@@ -5,6 +5,7 @@
 #include "setup.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace bddc_b200 {
 namespace {
@@ -180,17 +181,16 @@ __device__ double block_max(double v, double* red) {
 // pivoting (the first row of largest |entry|, setup.cpp dense_inverse's rule; singular when the
 // pivot is below 1e-13 of the largest entry), column interchanges undone at the end; then the
 // blocks out to the image.
-__global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev P, const MfBatch B,
-                                                                const SaddleOut O) {
+__global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev P, const MfBatch B) {
     __shared__ double red[32];
     __shared__ int redi[32];
     __shared__ int s_piv;
     __shared__ double s_best;
     extern __shared__ double sh[];  // row k, column k
     const int b = blockIdx.x, tid = threadIdx.x;
-    const int ng = P.n_iface, np = P.n_primal, ns = ng + np, nI = P.n_interior;
+    const int ng = P.n_iface, np = P.n_primal, ns = ng + np;
     double* M = B.M + static_cast<long long>(b) * ns * ns;
-    int* piv = B.piv + static_cast<long long>(b) * ns;
+    int* piv = B.piv + static_cast<long long>(b) * 2 * ns + ns;  // (the row map's half: identity, below)
     const double* S = B.S + static_cast<long long>(b) * ng * ng;
     const long long nn = static_cast<long long>(ns) * ns;
     for (long long idx = tid; idx < nn; idx += blockDim.x) {
@@ -292,31 +292,210 @@ __global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev 
             }
         __syncthreads();
     }
+    // rows and columns are in place: identity maps for the output kernel
+    int* map = B.piv + static_cast<long long>(b) * 2 * ns;
+    for (int i = tid; i < ns; i += blockDim.x) map[i] = i;
+    __syncthreads();
+    for (int i = tid; i < ns; i += blockDim.x) map[ns + i] = i;
+}
+
+// The same Gauss-Jordan inverse, blocked: the pivots of a block of KB columns are taken on a
+// shared-memory copy of those columns (the panel), and the rest of the matrix receives the
+// block's KB rank-1 updates in one pass afterwards. Each entry still gets saddle_kernel's
+// updates in pivot order with its expressions (x - f rk[j]; the pivot row replaced by rk), so the
+// inverse is bitwise the same; the matrix is read and written once per block instead of once
+// per pivot. For pivot k of the block, the pivot row outside the panel is brought up to date
+// from the block's earlier pivot rows (Rb) and multipliers (F). Row interchanges are a
+// permutation (logical position -> physical row), column interchanges a composed map; the
+// output kernel reads the inverse through both (map[0..ns) rows, map[ns..2ns) columns).
+constexpr int kGjThreads = 1024;
+
+std::size_t gj_blocked_smem(int ns, int kb) {
+    return sizeof(double) * 3 * static_cast<std::size_t>(ns) * kb + sizeof(int) * 3 * static_cast<std::size_t>(ns);
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfPlanDev P, const MfBatch B) {
+    extern __shared__ double sh[];
+    __shared__ double red[32];
+    __shared__ int redi[32];
+    __shared__ int s_piv;
+    __shared__ double s_best;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int ng = P.n_iface, np = P.n_primal, ns = ng + np;
+    double* M = B.M + static_cast<long long>(b) * ns * ns;
+    const double* S = B.S + static_cast<long long>(b) * ng * ng;
+    double* Pn = sh;                                    // [ns][KB] panel, physical rows
+    double* F = Pn + static_cast<std::size_t>(ns) * KB;  // [ns][KB] multipliers f of the block's pivots
+    double* Rb = F + static_cast<std::size_t>(ns) * KB;  // [KB][ns] the block's pivot rows rk
+    int* perm = reinterpret_cast<int*>(Rb + static_cast<std::size_t>(ns) * KB);
+    int* pos = perm + ns;
+    int* piv = pos + ns;
+    const long long nn = static_cast<long long>(ns) * ns;
+    for (long long idx = tid; idx < nn; idx += blockDim.x) {
+        const int r = static_cast<int>(idx / ns), c = static_cast<int>(idx % ns);
+        M[idx] = r < ng && c < ng ? S[static_cast<long long>(r) * ng + c] : 0.0;
+    }
+    for (int i = tid; i < ns; i += blockDim.x) perm[i] = pos[i] = i;
+    __syncthreads();
+    for (int r = tid; r < np; r += blockDim.x)
+        for (int e = P.c_ptr[r]; e < P.c_ptr[r + 1]; ++e) {
+            const int g = P.c_col[e];
+            M[static_cast<long long>(ng + r) * ns + g] += P.c_val[e];
+            M[static_cast<long long>(g) * ns + ng + r] += P.c_val[e];
+        }
+    __syncthreads();
+    double mx = 0.0;
+    for (long long idx = tid; idx < nn; idx += blockDim.x) mx = fmax(mx, fabs(M[idx]));
+    const double scale = block_max(mx, red);
+    bool failed = false;
+    for (int k0 = 0; k0 < ns && !failed; k0 += KB) {
+        const int kb = min(KB, ns - k0);
+        for (int idx = tid; idx < ns * kb; idx += blockDim.x) {
+            const int r = idx / kb, c = idx % kb;
+            Pn[r * KB + c] = M[static_cast<long long>(r) * ns + k0 + c];
+        }
+        __syncthreads();
+        for (int c = 0; c < kb; ++c) {
+            const int k = k0 + c;
+            double best = -1.0;
+            int bi = k;
+            for (int i = k + tid; i < ns; i += blockDim.x) {
+                const double a = fabs(Pn[perm[i] * KB + c]);
+                if (a > best) { best = a; bi = i; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if ((tid & 31) == 0) { red[tid >> 5] = best; redi[tid >> 5] = bi; }
+            __syncthreads();
+            if (tid == 0) {
+                double bb = red[0];
+                int bx = redi[0];
+                for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+                    if (red[w] > bb || (red[w] == bb && redi[w] < bx)) { bb = red[w]; bx = redi[w]; }
+                s_best = bb;
+                s_piv = bx;
+                if ((bb > 1e-13 * scale) && isfinite(bb)) {
+                    piv[k] = bx;
+                    const int qk = perm[k], qp = perm[bx];
+                    perm[k] = qp;
+                    perm[bx] = qk;
+                    pos[qp] = k;
+                    pos[qk] = bx;
+                }
+            }
+            __syncthreads();
+            if (!(s_best > 1e-13 * scale) || !isfinite(s_best)) {
+                if (tid == 0) report(B.status, 2, B.first + b, k);
+                failed = true;
+                break;
+            }
+            const int q = perm[k];
+            const double pv = Pn[q * KB + c];
+            // the pivot row rk: panel entries current, the others brought up to date from the
+            // block's earlier pivots (q was not one of them)
+            double* rk = Rb + static_cast<std::size_t>(c) * ns;
+            for (int j = tid; j < ns; j += blockDim.x) {
+                double v;
+                if (j >= k0 && j < k0 + kb) {
+                    v = Pn[q * KB + (j - k0)];
+                } else {
+                    v = M[static_cast<long long>(q) * ns + j];
+                    for (int cc = 0; cc < c; ++cc) v = v - F[q * KB + cc] * Rb[static_cast<std::size_t>(cc) * ns + j];
+                }
+                rk[j] = j == k ? 1.0 / pv : v / pv;
+            }
+            for (int r = tid; r < ns; r += blockDim.x) F[r * KB + c] = Pn[r * KB + c];
+            __syncthreads();
+            // the panel's update (saddle_kernel's expressions)
+            for (int idx = tid; idx < ns * kb; idx += blockDim.x) {
+                const int r = idx / kb, cj = idx % kb, j = k0 + cj;
+                if (r == q) {
+                    Pn[r * KB + cj] = rk[j];
+                } else {
+                    const double f = F[r * KB + c];
+                    Pn[r * KB + cj] = j == k ? -f * rk[k] : Pn[r * KB + cj] - f * rk[j];
+                }
+            }
+            __syncthreads();
+        }
+        if (failed) break;
+        // the block's updates to the columns outside the panel, in pivot order; the panel back
+        for (long long idx = tid; idx < nn; idx += blockDim.x) {
+            const int r = static_cast<int>(idx / ns), j = static_cast<int>(idx % ns);
+            if (j >= k0 && j < k0 + kb) {
+                M[idx] = Pn[r * KB + (j - k0)];
+                continue;
+            }
+            const int pr = pos[r] - k0;  // the block step at which r was the pivot row, if any
+            double v = M[idx];
+            for (int cc = 0; cc < kb; ++cc) {
+                const double rj = Rb[static_cast<std::size_t>(cc) * ns + j];
+                v = cc == pr ? rj : v - F[r * KB + cc] * rj;
+            }
+            M[idx] = v;
+        }
+        __syncthreads();
+    }
+    if (failed) return;
+    // row map (logical -> physical) and the composed column interchanges (undone in reverse)
+    int* map = B.piv + static_cast<long long>(b) * 2 * ns;
+    for (int i = tid; i < ns; i += blockDim.x) map[i] = perm[i];
+    if (tid == 0) {
+        int* sig = map + ns;
+        for (int c = 0; c < ns; ++c) sig[c] = c;
+        for (int k = ns - 1; k >= 0; --k) {
+            const int p = piv[k];
+            if (p != k) {
+                const int t = sig[k];
+                sig[k] = sig[p];
+                sig[p] = t;
+            }
+        }
+    }
+}
+
+// The blocks of the saddle inverse out to the image (M: the inverse, logical row order), and
+// A_ci = Phi^T A Phi = Phi_G^T (S Phi_G).
+__global__ void __launch_bounds__(kSaddleThreads) saddle_out_kernel(const MfPlanDev P, const MfBatch B,
+                                                                    const SaddleOut O) {
+    extern __shared__ double sh[];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int ng = P.n_iface, np = P.n_primal, ns = ng + np, nI = P.n_interior;
+    const double* Mp = B.M + static_cast<long long>(b) * ns * ns;
+    const double* S = B.S + static_cast<long long>(b) * ng * ng;
+    if (B.status[2] != 0) return;  // a singular saddle matrix: the setup throws
+    // the inverse's entry (r, c) through the row / column maps of the elimination
+    const int* rmap = B.piv + static_cast<long long>(b) * 2 * ns;
+    const int* cmap = rmap + ns;
+    auto Minv = [&](int r, int c) { return Mp[static_cast<long long>(rmap[r]) * ns + cmap[c]]; };
     const std::int64_t* off = O.off + 5 * static_cast<long long>(b);
     double* K = O.kmat + off[0];
     for (long long idx = tid; idx < static_cast<long long>(ng) * ng; idx += blockDim.x) {
         const int r = static_cast<int>(idx / ng), c = static_cast<int>(idx % ng);
-        K[idx] = M[static_cast<long long>(r) * ns + c];
+        K[idx] = Minv(r, c);
     }
     for (int idx = tid; idx < ng * np; idx += blockDim.x) {
         const int g = idx / np, j = idx % np;
-        const double v = M[static_cast<long long>(g) * ns + ng + j];
+        const double v = Minv(g, ng + j);
         O.phig[off[1] + idx] = v;
         O.phi[off[2] + static_cast<long long>(nI + g) * np + j] = v;
     }
     for (int idx = tid; idx < np * np; idx += blockDim.x) {
         const int r = idx / np, c = idx % np;
-        O.lambda[off[3] + idx] = M[static_cast<long long>(ng + r) * ns + ng + c];
+        O.lambda[off[3] + idx] = Minv(ng + r, ng + c);
     }
-    // A_ci = Phi^T A Phi = Phi_G^T (S Phi_G): W = S Phi_G in shared memory (rows of S in order),
-    // then one warp per entry (lane-strided over the interface, fixed butterfly)
+    // W = S Phi_G in shared memory (rows of S in order), then one warp per A_ci entry
+    // (lane-strided over the interface, fixed butterfly)
     double* W = sh;
-    __syncthreads();
     for (int idx = tid; idx < ng * np; idx += blockDim.x) {
         const int g = idx / np, c = idx % np;
         const double* Sg = S + static_cast<long long>(g) * ng;
         double acc = 0.0;
-        for (int h = 0; h < ng; ++h) acc = fma(Sg[h], M[static_cast<long long>(h) * ns + ng + c], acc);
+        for (int h = 0; h < ng; ++h) acc = fma(Sg[h], Minv(h, ng + c), acc);
         W[idx] = acc;
     }
     __syncthreads();
@@ -324,7 +503,7 @@ __global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev 
     for (int e = warp; e < np * np; e += blockDim.x >> 5) {
         const int r = e / np, c = e % np;
         double acc = 0.0;
-        for (int g = lane; g < ng; g += 32) acc = fma(M[static_cast<long long>(g) * ns + ng + r], W[g * np + c], acc);
+        for (int g = lane; g < ng; g += 32) acc = fma(Minv(g, ng + r), W[g * np + c], acc);
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) O.aci[off[4] + e] = acc;
     }
@@ -400,11 +579,28 @@ void launch_fill(double* dst, const double* tmpl, const std::int32_t* srcmap, co
 
 void launch_saddle(const MfPlanDev& P, const MfBatch& B, const SaddleOut& O, cudaStream_t s) {
     if (B.n <= 0) return;
-    const std::size_t smem = sizeof(double) * std::max<std::size_t>(2 * static_cast<std::size_t>(P.n_iface + P.n_primal),
-                                                                    static_cast<std::size_t>(P.n_iface) * P.n_primal);
-    if (smem > 48 * 1024)
-        BDDC_CUDA(cudaFuncSetAttribute(saddle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    saddle_kernel<<<B.n, kSaddleThreads, smem, s>>>(P, B, O);
+    const int ns = P.n_iface + P.n_primal;
+    static const bool global_gj = std::getenv("BDDC_SADDLE_GLOBAL") && std::atoi(std::getenv("BDDC_SADDLE_GLOBAL")) == 1;
+    constexpr std::size_t kMaxSmem = 220 * 1024;
+    if (!global_gj && gj_blocked_smem(ns, 16) <= kMaxSmem) {
+        const std::size_t smem = gj_blocked_smem(ns, 16);
+        BDDC_CUDA(cudaFuncSetAttribute(saddle_gj_blocked_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        saddle_gj_blocked_kernel<16><<<B.n, kGjThreads, smem, s>>>(P, B);
+    } else if (!global_gj && gj_blocked_smem(ns, 4) <= kMaxSmem) {
+        const std::size_t smem = gj_blocked_smem(ns, 4);
+        BDDC_CUDA(cudaFuncSetAttribute(saddle_gj_blocked_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        saddle_gj_blocked_kernel<4><<<B.n, kGjThreads, smem, s>>>(P, B);
+    } else {
+        const std::size_t smem = sizeof(double) * 2 * static_cast<std::size_t>(ns);
+        if (smem > 48 * 1024)
+            BDDC_CUDA(cudaFuncSetAttribute(saddle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        saddle_kernel<<<B.n, kSaddleThreads, smem, s>>>(P, B);
+    }
+    BDDC_LAUNCHED();
+    const std::size_t out_smem = sizeof(double) * std::max<std::size_t>(1, static_cast<std::size_t>(P.n_iface) * P.n_primal);
+    if (out_smem > 48 * 1024)
+        BDDC_CUDA(cudaFuncSetAttribute(saddle_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out_smem));
+    saddle_out_kernel<<<B.n, kSaddleThreads, out_smem, s>>>(P, B, O);
     BDDC_LAUNCHED();
 }
 

@@ -100,3 +100,40 @@ def test_device_setup_error_names_subdomain(gpu):
                                  p.n_coarse, *p.classes(), p.multiplicity(), p.rhs())
     with pytest.raises(BddcError, match="bddc setup: subdomain 0"):
         Preconditioner(broken)
+
+
+SADDLE_SCRIPT = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, ROOT)
+from paper_2410_14786_b200 import Preconditioner, Problem
+out = {}
+for name, p in (("c2", Problem.poisson(800, 8)), ("kappa", Problem.poisson(240, 4, 180, 3, kappa_decades=3.0))):
+    pre = Preconditioner(p)
+    h = hashlib.sha256()
+    for i in range(p.n_subdomains):
+        for blk in pre.subdomain_blocks(i):
+            h.update(np.ascontiguousarray(blk).tobytes())
+    h.update(np.ascontiguousarray(pre.apply(p.rhs())).tobytes())  # K_i enters the apply
+    out[name] = h.hexdigest()
+print(json.dumps(out))
+""".replace("ROOT", repr(__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))))
+
+
+def test_cluster_saddle_inverse_is_bitwise_the_global_one(gpu):
+    # the saddle Gauss-Jordan with the matrix in a CTA cluster's shared memory (setup.cu
+    # saddle_gj_cluster_kernel) and the global-memory one (BDDC_SADDLE_GLOBAL=1) make the same
+    # pivot choices and updates: Phi, Lambda, A_ci and the apply (K_i) are bitwise identical
+    import json
+    import os
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if not k.startswith("BDDC_")}
+    res = []
+    for extra in ({}, {"BDDC_SADDLE_GLOBAL": "1"}):
+        r = subprocess.run([sys.executable, "-c", SADDLE_SCRIPT], env={**env, **extra}, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
