@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kSaddleThreads) saddle_kernel(const MfPlanDev 
 // from the block's earlier pivot rows (Rb) and multipliers (F). Row interchanges are a
 // permutation (logical position -> physical row), column interchanges a composed map; the
 // output kernel reads the inverse through both (map[0..ns) rows, map[ns..2ns) columns).
-constexpr int kGjThreads = 1024;
+constexpr int kGjThreads = 512;
 
 std::size_t gj_blocked_smem(int ns, int kb) {
     return sizeof(double) * 3 * static_cast<std::size_t>(ns) * kb + sizeof(int) * 3 * static_cast<std::size_t>(ns);
@@ -332,10 +332,9 @@ __global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfP
     int* pos = perm + ns;
     int* piv = pos + ns;
     const long long nn = static_cast<long long>(ns) * ns;
-    for (long long idx = tid; idx < nn; idx += blockDim.x) {
-        const int r = static_cast<int>(idx / ns), c = static_cast<int>(idx % ns);
-        M[idx] = r < ng && c < ng ? S[static_cast<long long>(r) * ng + c] : 0.0;
-    }
+    for (int r = tid >> 5; r < ns; r += blockDim.x >> 5)
+        for (int c = tid & 31; c < ns; c += 32)
+            M[static_cast<long long>(r) * ns + c] = r < ng && c < ng ? S[static_cast<long long>(r) * ng + c] : 0.0;
     for (int i = tid; i < ns; i += blockDim.x) perm[i] = pos[i] = i;
     __syncthreads();
     for (int r = tid; r < np; r += blockDim.x)
@@ -349,11 +348,17 @@ __global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfP
     for (long long idx = tid; idx < nn; idx += blockDim.x) mx = fmax(mx, fabs(M[idx]));
     const double scale = block_max(mx, red);
     bool failed = false;
+#ifdef GJ_PROF
+    long long t_search = 0, t_rk = 0, t_panel = 0, t_trail = 0, t0p = clock64(), tq;
+#define GJ_T(acc) do { __syncthreads(); tq = clock64(); acc += tq - t0p; t0p = tq; } while (0)
+#else
+#define GJ_T(acc) do { } while (0)
+#endif
     for (int k0 = 0; k0 < ns && !failed; k0 += KB) {
         const int kb = min(KB, ns - k0);
-        for (int idx = tid; idx < ns * kb; idx += blockDim.x) {
-            const int r = idx / kb, c = idx % kb;
-            Pn[r * KB + c] = M[static_cast<long long>(r) * ns + k0 + c];
+        for (int idx = tid; idx < ns * KB; idx += blockDim.x) {
+            const int r = idx / KB, c = idx % KB;
+            if (c < kb) Pn[r * KB + c] = M[static_cast<long long>(r) * ns + k0 + c];
         }
         __syncthreads();
         for (int c = 0; c < kb; ++c) {
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfP
                 failed = true;
                 break;
             }
+            GJ_T(t_search);
             const int q = perm[k];
             const double pv = Pn[q * KB + c];
             // the pivot row rk: panel entries current, the others brought up to date from the
@@ -410,9 +416,11 @@ __global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfP
             }
             for (int r = tid; r < ns; r += blockDim.x) F[r * KB + c] = Pn[r * KB + c];
             __syncthreads();
+            GJ_T(t_rk);
             // the panel's update (saddle_kernel's expressions)
-            for (int idx = tid; idx < ns * kb; idx += blockDim.x) {
-                const int r = idx / kb, cj = idx % kb, j = k0 + cj;
+            for (int idx = tid; idx < ns * KB; idx += blockDim.x) {
+                const int r = idx / KB, cj = idx % KB, j = k0 + cj;
+                if (cj >= kb) continue;
                 if (r == q) {
                     Pn[r * KB + cj] = rk[j];
                 } else {
@@ -421,25 +429,92 @@ __global__ void __launch_bounds__(kGjThreads) saddle_gj_blocked_kernel(const MfP
                 }
             }
             __syncthreads();
+            GJ_T(t_panel);
         }
         if (failed) break;
-        // the block's updates to the columns outside the panel, in pivot order; the panel back
-        for (long long idx = tid; idx < nn; idx += blockDim.x) {
-            const int r = static_cast<int>(idx / ns), j = static_cast<int>(idx % ns);
-            if (j >= k0 && j < k0 + kb) {
-                M[idx] = Pn[r * KB + (j - k0)];
-                continue;
+        // the block's updates to the columns outside the panel, in pivot order; the panel back.
+        // A warp per row (its multipliers in registers), lanes along the row, four columns in
+        // flight per lane; the block's pivot rows take the replacing branch
+        {
+            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+            for (int r = warp; r < ns; r += nw) {
+                double* Mr = M + static_cast<long long>(r) * ns;
+                const int pr = pos[r] - k0;  // the block step at which r was the pivot row, if any
+                if (pr >= 0 && pr < kb) {
+                    for (int j = lane; j < ns; j += 32) {
+                        if (j >= k0 && j < k0 + kb) {
+                            Mr[j] = Pn[r * KB + (j - k0)];
+                            continue;
+                        }
+                        double v = Mr[j];
+                        for (int cc = 0; cc < kb; ++cc) {
+                            const double rj = Rb[static_cast<std::size_t>(cc) * ns + j];
+                            v = cc == pr ? rj : v - F[r * KB + cc] * rj;
+                        }
+                        Mr[j] = v;
+                    }
+                    continue;
+                }
+                double f[KB];
+#pragma unroll
+                for (int cc = 0; cc < KB; ++cc) f[cc] = cc < kb ? F[r * KB + cc] : 0.0;
+                constexpr int TW = KB == 16 ? 18 : 1;  // the whole row in registers (ns <= 32 TW)
+                if (ns <= 32 * TW && TW > 1) {
+                    double v[TW];
+#pragma unroll
+                    for (int t = 0; t < TW; ++t) {
+                        const int j = lane + 32 * t;
+                        v[t] = j < ns ? Mr[j] : 0.0;
+                    }
+#pragma unroll
+                    for (int cc = 0; cc < KB; ++cc) {
+                        if (cc < kb) {
+                            const double* Rc = Rb + static_cast<std::size_t>(cc) * ns;
+#pragma unroll
+                            for (int t = 0; t < TW; ++t) {
+                                const int j = lane + 32 * t;
+                                if (j < ns) v[t] = v[t] - f[cc] * Rc[j];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < TW; ++t) {
+                        const int j = lane + 32 * t;
+                        if (j < ns) Mr[j] = (j >= k0 && j < k0 + kb) ? Pn[r * KB + (j - k0)] : v[t];
+                    }
+                    continue;
+                }
+                for (int j0 = lane; j0 < ns; j0 += 128) {
+                    double v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = j0 + 32 * u;
+                        v[u] = j < ns ? Mr[j] : 0.0;
+                    }
+#pragma unroll
+                    for (int cc = 0; cc < KB; ++cc) {
+                        if (cc < kb) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int j = j0 + 32 * u;
+                                if (j < ns) v[u] = v[u] - f[cc] * Rb[static_cast<std::size_t>(cc) * ns + j];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = j0 + 32 * u;
+                        if (j < ns) Mr[j] = (j >= k0 && j < k0 + kb) ? Pn[r * KB + (j - k0)] : v[u];
+                    }
+                }
             }
-            const int pr = pos[r] - k0;  // the block step at which r was the pivot row, if any
-            double v = M[idx];
-            for (int cc = 0; cc < kb; ++cc) {
-                const double rj = Rb[static_cast<std::size_t>(cc) * ns + j];
-                v = cc == pr ? rj : v - F[r * KB + cc] * rj;
-            }
-            M[idx] = v;
         }
         __syncthreads();
+        GJ_T(t_trail);
     }
+#ifdef GJ_PROF
+    if (tid == 0 && b == 0) printf("gj ns %d search %lld rk %lld panel %lld trail %lld\n", ns, t_search, t_rk, t_panel, t_trail);
+#endif
     if (failed) return;
     // row map (logical -> physical) and the composed column interchanges (undone in reverse)
     int* map = B.piv + static_cast<long long>(b) * 2 * ns;
