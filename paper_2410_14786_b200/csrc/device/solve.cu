@@ -73,64 +73,98 @@ struct RegTable {
 
 // One tile GEMV (device_format.hpp): k <= 32 rows, G = 2^lg column groups, lane = r*G + g
 // owns row r and columns j = t*G + g; values are stored iteration-major, value(r, t*G + g)
-// at [t*k*G + r*G + g], so every iteration is one contiguous, conflict-free shared-memory
-// read per lane. Written for a short issue path (most tiles hold ~5 values per lane): no
-// divergent guard around the loop (lanes beyond k*G read in-bounds slack and are masked
-// before the reduction), a 4-way body with predicated tails, pointer increments only. The
-// G partial sums of a row are reduced with an xor butterfly inside the row's lane group; the
-// row total accumulates into `acc` and is flushed by the group's first lane.
-__device__ __forceinline__ void tile_task(const int4 h, const unsigned char* tile, double* own, double* other,
-                                          double* Q, double& acc, int lane) {
+// at [t*S + r*G + g] (S = k*G), so every iteration is one contiguous, conflict-free
+// shared-memory read per lane. Written for a short issue path (most tiles hold ~5 values per
+// lane): no divergent guard around the loop (lanes beyond k*G read in-bounds slack and are
+// masked before the reduction), a 4-way body with predicated tails, pointer increments only.
+// The G partial sums of a row are reduced with an xor butterfly inside the row's lane group;
+// the row total accumulates into `acc` and is flushed by the group's first lane.
+// PAIR: a pair step (two half-warp tiles, device_format.hpp): lanes 16-31 run tile B with
+// its own header; the values interleave with stride S = kG_A + kG_B; each half loops over its
+// own iteration count.
+template <bool PAIR, bool PROF = false>
+__device__ __forceinline__ void tile_task(const int4 hA, const int4 hB, const unsigned char* tile, double* own,
+                                          double* other, double* Q, double& acc, int lane,
+                                          long long* tp = nullptr) {
+    long long tq = PROF ? clock64() : 0;
+#define TILE_T(i) do { if constexpr (PROF) { const long long t_ = clock64(); tp[i] += t_ - tq; tq = t_; } } while (0)
+    const bool hi = PAIR && lane >= 16;
+    const int4 h = hi ? hB : hA;
+    const int sl = PAIR ? (lane & 15) : lane;
     const int k = h.w & 0xff, lg = (h.w >> 8) & 0xff, flags = (h.w >> 16) & 0xff;
     const int iters = static_cast<unsigned>(h.z) >> 16;
     const int G = 1 << lg, kG = k << lg;
-    const int g = lane & (G - 1), r = lane >> lg;
+    const int g = sl & (G - 1), r = sl >> lg;
     const double* in = (flags & kTaskInOwn) ? own : other;
-    const double* M = reinterpret_cast<const double*>(tile) + lane;
-    const int vbytes = (iters * kG * 8 + 15) & ~15;
+    int S = kG, itmax = iters, Gmax = G, ioff = 0, ibytes = 0, ooff = 0;
+    const bool indexed = flags & kTaskInIndexed;
+    if constexpr (PAIR) {
+        const int kA = hA.w & 0xff, lgA = (hA.w >> 8) & 0xff, itA = static_cast<unsigned>(hA.z) >> 16;
+        const int lgB = (hB.w >> 8) & 0xff, itB = static_cast<unsigned>(hB.z) >> 16;
+        const int kGA = kA << lgA;
+        S = kGA + ((hB.w & 0xff) << lgB);
+        itmax = max(itA, itB);
+        Gmax = 1 << max(lgA, lgB);
+        const int ia = indexed ? ((itA << lgA) * 4 + 15) & ~15 : 0;
+        ioff = hi ? ia : 0;
+        ibytes = indexed ? ia + (((itB << lgB) * 4 + 15) & ~15) : 0;
+        // B's output rows follow A's (A has a list when it is a push)
+        ooff = hi && (((hA.w >> 16) & (kTaskPush | kTaskLast)) == (kTaskPush | kTaskLast)) ? ((kA * 4 + 15) & ~15) : 0;
+    } else {
+        ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
+    }
+    const int voff = PAIR && hi ? S - kG : 0;  // B's values start kG_A doubles into an iteration
+    const double* M = reinterpret_cast<const double*>(tile) + voff + sl;
+    const int vbytes = (itmax * S * 8 + 15) & ~15;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int full = iters & ~3, rem = iters & 3;
-    if (flags & kTaskInIndexed) {
-        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes) + g;
+    TILE_T(0);
+    if (indexed) {
+        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes + ioff) + g;
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], in[ix[0]], s0);
-            s1 = fma(M[kG], in[ix[G]], s1);
-            s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
-            s3 = fma(M[3 * kG], in[ix[3 * G]], s3);
-            M += 4 * kG;
+            s1 = fma(M[S], in[ix[G]], s1);
+            s2 = fma(M[2 * S], in[ix[2 * G]], s2);
+            s3 = fma(M[3 * S], in[ix[3 * G]], s3);
+            M += 4 * S;
             ix += 4 * G;
         }
         if (rem > 0) s0 = fma(M[0], in[ix[0]], s0);
-        if (rem > 1) s1 = fma(M[kG], in[ix[G]], s1);
-        if (rem > 2) s2 = fma(M[2 * kG], in[ix[2 * G]], s2);
+        if (rem > 1) s1 = fma(M[S], in[ix[G]], s1);
+        if (rem > 2) s2 = fma(M[2 * S], in[ix[2 * G]], s2);
     } else {
         const double* v = in + h.y + g;
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], v[0], s0);
-            s1 = fma(M[kG], v[G], s1);
-            s2 = fma(M[2 * kG], v[2 * G], s2);
-            s3 = fma(M[3 * kG], v[3 * G], s3);
-            M += 4 * kG;
+            s1 = fma(M[S], v[G], s1);
+            s2 = fma(M[2 * S], v[2 * G], s2);
+            s3 = fma(M[3 * S], v[3 * G], s3);
+            M += 4 * S;
             v += 4 * G;
         }
         if (rem > 0) s0 = fma(M[0], v[0], s0);
-        if (rem > 1) s1 = fma(M[kG], v[G], s1);
-        if (rem > 2) s2 = fma(M[2 * kG], v[2 * G], s2);
+        if (rem > 1) s1 = fma(M[S], v[G], s1);
+        if (rem > 2) s2 = fma(M[2 * S], v[2 * G], s2);
     }
     // per-lane partial sums accumulate over the pieces of a chunk (same k, hence same G and
-    // lane -> row map); the row's lane group is reduced once, at its last piece
-    acc = ((flags & kTaskFirst) ? 0.0 : acc) + (lane < kG ? (s0 + s1) + (s2 + s3) : 0.0);
+    // lane -> row map); the row's lane group is reduced once, at its last piece (a pair's two
+    // halves are in lockstep: both or neither are last)
+    TILE_T(1);
+    acc = ((flags & kTaskFirst) ? 0.0 : acc) + (sl < kG ? (s0 + s1) + (s2 + s3) : 0.0);
     if (!(flags & kTaskLast)) return;
 #pragma unroll 1
-    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = Gmax >> 1; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, acc, off);
+        if (!PAIR || off < G) acc += o;
+    }
+    TILE_T(2);
     if (g == 0) {
         const int nvalid = static_cast<unsigned>(h.w) >> 24;
         if (flags & kTaskPush) {
             if (r < k) {
-                const int ibytes = (flags & kTaskInIndexed) ? ((iters * G * 4 + 15) & ~15) : 0;
-                const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes)[r];
+                const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes + ooff)[r];
                 if (flags & kTaskPartial) Q[o] += acc;
                 else own[o] -= acc;
             }
@@ -140,6 +174,9 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
             else own[out] -= acc;
         }
     }
+    if constexpr (PROF) __syncwarp();  // (the flush's lanes, timed together)
+    TILE_T(3);
+#undef TILE_T
 }
 
 template <int MODE, int CLUSTER, bool STATS>
@@ -204,6 +241,13 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         issue(u, o16, nb);
     };
     for (int u = 0; u < nsl && u < nunits; ++u) fetch(u);
+    // the table entry of the next refill (unit nsl, then one ahead of each refill): looked up a
+    // unit early so the lookup's latency is off the refill's path
+    int nx_o16 = 0, nx_nb = 0;
+    if (nsl < nunits) {
+        nx_o16 = uoff.get(nsl, units, 2);
+        nx_nb = ubytes.get(nsl, units + 1, 2);
+    }
     // everything above reads only the program (immutable): it overlaps the predecessor's tail
     // under programmatic dependent launch; from here on the inputs are the predecessors'
     pdl_wait();
@@ -293,12 +337,20 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
 
     constexpr bool stats = STATS;
     long long t_start = stats ? clock64() : 0, t_wait = 0, t_bar = 0, t_refill = 0, t_tiles = 0, n_tiles = 0;
+    long long tprof[4] = {0, 0, 0, 0};  // STATS: decode, loop, reduction, flush cycles
     double acc = 0.0;
     int u = 0;  // next unit of this warp
     bool split_done = !(MODE == 0 ? S.y_out : (MODE == 3 ? S.y_in : nullptr));
+    // phase kind and end unit, looked up a phase ahead
+    int nx_kind = pkind.get(0, gtable + 2 * kSolveWarps, kPhaseStride);
+    int nx_end = uend.get(0, gtable + kSolveWarps + warp, kPhaseStride);
     for (int ph = 0; ph < n_phases; ++ph) {
-        const int kind = pkind.get(ph, gtable + 2 * kSolveWarps, kPhaseStride);
-        const int u_end = uend.get(ph, gtable + kSolveWarps + warp, kPhaseStride);
+        const int kind = nx_kind;
+        const int u_end = nx_end;
+        if (ph + 1 < n_phases) {
+            nx_kind = pkind.get(ph + 1, gtable + 2 * kSolveWarps, kPhaseStride);
+            nx_end = uend.get(ph + 1, gtable + kSolveWarps + warp, kPhaseStride);
+        }
         if (!split_done && (kind & kPhaseBackward)) {  // forward sweep complete: X = y (block-uniform)
             split_done = true;
             if (MODE == 0) {
@@ -329,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         double* own = (kind & kPhaseBackward) ? X : T;
         double* other = (kind & kPhaseBackward) ? T : X;
         const long long t_ph0 = stats ? clock64() : 0;
-        const long long n_tiles0 = n_tiles;
+        const long long n_tiles0 = n_tiles, t_wait0 = t_wait, t_tiles0 = t_tiles, t_refill0 = t_refill;
         for (; u < u_end; ++u) {
             const int s = u & (nsl - 1);
             if constexpr (stats) {
@@ -342,14 +394,22 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             const unsigned char* ubuf = my_ring + s * unit;
             std::uint32_t cur = 0;
             const long long t_tile0 = stats ? clock64() : 0;
+            // a step's first 32 bytes: its header and, for a pair step, B's header (a single
+            // tile's first values otherwise; every tile holds at least 16 bytes of values)
             int4 hdr4 = *reinterpret_cast<const int4*>(ubuf);
+            int4 hdr4b = *reinterpret_cast<const int4*>(ubuf + 16);
             while (true) {
                 if (stats) ++n_tiles;
-                const int4 h = hdr4;
-                const unsigned char* tile = ubuf + (cur << 4) + 16;
+                const int4 h = hdr4, hb = hdr4b;
+                const bool pair = (h.w >> 16) & kTaskPair;
+                const unsigned char* tile = ubuf + (cur << 4) + (pair ? 32 : 16);
                 cur = static_cast<std::uint32_t>(h.x);
-                if (cur != kNoTask) hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));  // next header early
-                tile_task(h, tile, own, other, Q, acc, lane);
+                if (cur != kNoTask) {  // next headers early
+                    hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));
+                    hdr4b = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + 16);
+                }
+                if (pair) tile_task<true, STATS>(h, hb, tile, own, other, Q, acc, lane, tprof);
+                else tile_task<false, STATS>(h, h, tile, own, other, Q, acc, lane, tprof);
                 if ((kind & kPhaseChained) && ((h.w >> 16) & kTaskLast))
                     __syncwarp();  // a later tile of this warp's job reads what was just written
                 if (cur == kNoTask) break;
@@ -362,7 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 // unit's flushes), so the bulk copy may overwrite it; a generic-read ->
                 // async-write (WAR) reuse needs no proxy fence (measured: -1.5% per launch)
                 __syncwarp();
-                fetch(u + nsl);
+                issue(u + nsl, nx_o16, nx_nb);
+                if (u + nsl + 1 < nunits) {
+                    nx_o16 = uoff.get(u + nsl + 1, units, 2);
+                    nx_nb = ubytes.get(u + nsl + 1, units + 1, 2);
+                }
             }
             if (stats) t_refill += clock64() - t_r0;
         }
@@ -372,6 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 long long* pw = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256;
                 pw[ph * kSolveWarps + warp] = t0 - t_ph0;
                 pw[256 * kSolveWarps + ph * kSolveWarps + warp] = n_tiles - n_tiles0;
+                pw[2 * 256 * kSolveWarps + 8 + ph * kSolveWarps + warp] = t_wait - t_wait0;  // mbarrier waits
+                pw[3 * 256 * kSolveWarps + 8 + ph * kSolveWarps + warp] = t_tiles - t_tiles0;  // tile processing
+                pw[4 * 256 * kSolveWarps + 8 + ph * kSolveWarps + warp] = t_refill - t_refill0;  // refills
             }
             __syncthreads();
             t_bar += clock64() - t0;
@@ -412,6 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         o[4] = t_refill;
         o[5] = t_tiles;
         o[6] = n_tiles;
+        if (STATS && blockIdx.x == 0) {  // CTA 0: tile sub-phases (decode, loop, reduction, flush)
+            long long* tpo = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 + 5 * 256 * kSolveWarps + 8;
+            for (int i = 0; i < 4; ++i) tpo[warp * 4 + i] = tprof[i];
+        }
     }
     for (int l0 = tid; l0 < pdr.n_write; l0 += 4 * kThreads) {
         int gi[4];

@@ -31,6 +31,16 @@
 //   PULL : own[out_base + r]   -= acc     u_s = x_s - L_{R_s,s}^T y[R_s] (backward)
 // Input column j is in[in_ref + j] (contiguous) or in[idx[j]] (IN_INDEXED).
 // Pushes of one phase never share a target row (supernodes are coloured per height).
+//
+// Pair steps: two independent tiles A and B with k <= 16 rows each run side by side, A on
+// lanes 0-15 and B on lanes 16-31 (lane - 16 = r*G_B + g), each with its own G (k*G <= 16),
+// iteration count, input, flags and outputs, so a warp pays one header decode, one loop and
+// one butterfly for both. Layout: header A (kTaskPair set; A.next links the unit), header B,
+// values iteration-major with stride S = k_A*G_A + k_B*G_B (A's lanes then B's), for
+// max(iters_A, iters_B) iterations (the shorter tile's slots are zero and never read), then
+// A's and B's index lists (IN_INDEXED: both or neither; 16-byte aligned each), then A's and
+// B's output-row lists (those that have one). Chunks of several pieces are paired piece by
+// piece (both FIRST/LAST in lockstep).
 #pragma once
 
 #include <cstdint>
@@ -52,6 +62,7 @@ enum TaskFlags : std::uint8_t {
     kTaskPush = 16,      // own[outidx[r]] -= acc (outidx after the values / index list)
     kTaskPartial = 32,   // with PUSH: Q[outidx[r]] += acc
     kTaskInOwn = 64,     // inputs from own (else from other)
+    kTaskPair = 128,     // a pair step: two half-warp tiles (layout below)
 };
 
 enum PhaseKind : std::int32_t {

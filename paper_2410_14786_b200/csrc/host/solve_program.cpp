@@ -18,6 +18,7 @@ constexpr double kPrunedJobsPerWarp = 0.0;
 
 struct Tile {
     TileTask t{};
+    int jn = 0;                        // columns of this piece
     std::vector<double> vals;
     std::vector<std::int32_t> src;     // template mode: value sources (SolvePools::srcmap codes)
     std::vector<std::int32_t> idx;     // input index list (IN_INDEXED)
@@ -64,6 +65,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         const int jn = std::min(per, ncols - j0);
         const int iters = tile_iters(jn, G);
         Tile T;
+        T.jn = jn;
         T.t.in_ref = indexed ? 0u : static_cast<std::uint32_t>(in_start + j0);
         T.t.out_base = static_cast<std::uint16_t>(out_base);
         T.t.iters = static_cast<std::uint16_t>(iters);
@@ -96,6 +98,49 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         ch.tiles.push_back(std::move(T));
     }
     return ch;
+}
+
+// The tile re-laid out for G2 column groups (same rows, columns and index list; one half of a
+// pair step uses k * G2 <= 16 lanes).
+Tile regroup(const Tile& T, int G2) {
+    const int k = T.t.nrows, G = 1 << T.t.groups, kG = k * G;
+    Tile R;
+    R.t = T.t;
+    R.jn = T.jn;
+    R.outidx = T.outidx;
+    const int it2 = tile_iters(T.jn, G2);
+    R.t.iters = static_cast<std::uint16_t>(it2);
+    R.t.groups = static_cast<std::uint8_t>(__builtin_ctz(static_cast<unsigned>(G2)));
+    R.vals.assign(static_cast<std::size_t>(it2) * k * G2, 0.0);
+    if (!T.src.empty()) R.src.assign(R.vals.size(), kSrcZero);
+    for (int j = 0; j < T.jn; ++j)
+        for (int r = 0; r < k; ++r) {
+            const std::size_t o = static_cast<std::size_t>(j / G) * kG + r * G + j % G;
+            const std::size_t n = static_cast<std::size_t>(j / G2) * k * G2 + r * G2 + j % G2;
+            R.vals[n] = T.vals[o];
+            if (!T.src.empty()) R.src[n] = T.src[o];
+        }
+    if (!T.idx.empty()) {
+        R.idx.resize(static_cast<std::size_t>(it2) * G2);
+        for (int j = 0; j < it2 * G2; ++j) R.idx[j] = T.idx[std::min(j, T.jn - 1)];
+    }
+    return R;
+}
+
+int half_groups(int k) {
+    int G = 1;
+    while (k * G * 2 <= 16) G *= 2;
+    return G;
+}
+
+// Bytes of a pair step (device_format.hpp): two headers, the interleaved values (iteration
+// stride kG_A + kG_B, max(iters) iterations), the two index lists, the two output-row lists.
+std::int64_t pair_bytes(const Tile& A, const Tile& B) {
+    const int ia = A.t.iters, ib = B.t.iters;
+    const std::int64_t S = static_cast<std::int64_t>(A.t.nrows << A.t.groups) + (B.t.nrows << B.t.groups);
+    return 32 + pad16(std::max(ia, ib) * S * 8) + pad16(static_cast<std::int64_t>(A.idx.size()) * 4) +
+           pad16(static_cast<std::int64_t>(B.idx.size()) * 4) + pad16(static_cast<std::int64_t>(A.outidx.size()) * 4) +
+           pad16(static_cast<std::int64_t>(B.outidx.size()) * 4);
 }
 
 }  // namespace
@@ -381,6 +426,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         };
         auto all_rows = [](index_t) { return true; };
         // chunk rows for a level: the largest of 32/16/8 giving at least 2 chunks per warp
+        // BDDC_PAIR_TILES=0: no pair steps (experiments)
+        static const bool pair_tiles = !std::getenv("BDDC_PAIR_TILES") || std::atoi(std::getenv("BDDC_PAIR_TILES")) != 0;
         static const int min_kr = std::getenv("BDDC_MIN_CHUNK_ROWS") ? std::atoi(std::getenv("BDDC_MIN_CHUNK_ROWS")) : 8;
         auto chunk_rows_for = [&](const std::vector<index_t>& rows_per_node) {
             if (min_kr >= 32) return 32;
@@ -670,36 +717,120 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     pos = ustart + pad16(uused);
                     ustart = -1;
                 };
+                // this warp's chunks of the phase; outside chained phases (tiles independent),
+                // chunks of <= 16 rows are paired piece by piece into half-warp pair steps
+                std::vector<Chunk*> chs;
                 for (index_t c : per_warp[w])
-                    for (Chunk& ch : ph.jobs[c])
-                    for (Tile& t : ch.tiles) {
-                        const std::int64_t nb = 16 + t.bytes();
-                        if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
-                        if (ustart >= 0 && uused + nb > unit_bytes) close_unit();
-                        if (ustart < 0) { ustart = pos; uused = 0; last_hdr = -1; }
-                        ensure(ustart + uused + nb);
-                        char* base = reinterpret_cast<char*>(pools.stream.data() + pd.stream);
-                        char* dst = base + ustart + uused;
-                        TileTask hdr = t.t;
-                        hdr.next = kNoTask;
-                        std::memcpy(dst, &hdr, 16);
-                        std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
-                        if (tmpl) {
-                            const std::size_t w0 = static_cast<std::size_t>(pd.stream + (ustart + uused + 16) / 8);
-                            std::copy(t.src.begin(), t.src.end(), pools.srcmap.begin() + static_cast<std::ptrdiff_t>(w0));
-                        }
-                        std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
-                        if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
-                        off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
-                        if (!t.outidx.empty()) std::memcpy(dst + off, t.outidx.data(), t.outidx.size() * 4);
-                        if (last_hdr >= 0)
-                            reinterpret_cast<TileTask*>(base + ustart + last_hdr)->next =
-                                static_cast<std::uint32_t>(uused / 16);
-                        last_hdr = uused;
-                        uused += nb;
-                        pools.tile_values += static_cast<std::int64_t>(t.vals.size());
-                        ++pools.n_tiles;
+                    for (Chunk& ch : ph.jobs[c]) chs.push_back(&ch);
+                std::vector<int> mate(chs.size(), -1);
+                std::vector<std::vector<Tile>> half(chs.size());
+                if (pair_tiles && !(ph.kind & kPhaseChained)) {
+                    std::vector<int> cand;
+                    for (std::size_t i = 0; i < chs.size(); ++i) {
+                        bool ok = !chs[i]->tiles.empty();
+                        for (const Tile& t : chs[i]->tiles) ok = ok && t.t.nrows <= 16;
+                        if (!ok) continue;
+                        for (const Tile& t : chs[i]->tiles) half[i].push_back(regroup(t, half_groups(t.t.nrows)));
+                        cand.push_back(static_cast<int>(i));
                     }
+                    constexpr std::uint8_t kShape = kTaskInIndexed | kTaskFirst | kTaskLast;
+                    auto shape_less = [&](int a, int b) {
+                        const auto& A = half[a];
+                        const auto& B = half[b];
+                        if (A.size() != B.size()) return A.size() < B.size();
+                        for (std::size_t q = 0; q < A.size(); ++q)
+                            if ((A[q].t.flags & kShape) != (B[q].t.flags & kShape))
+                                return (A[q].t.flags & kShape) < (B[q].t.flags & kShape);
+                        for (std::size_t q = 0; q < A.size(); ++q)
+                            if (A[q].t.iters != B[q].t.iters) return A[q].t.iters < B[q].t.iters;
+                        return a < b;
+                    };
+                    std::sort(cand.begin(), cand.end(), shape_less);
+                    for (std::size_t q = 0; q + 1 < cand.size();) {
+                        const int a = cand[q], b = cand[q + 1];
+                        bool ok = half[a].size() == half[b].size();
+                        for (std::size_t p = 0; ok && p < half[a].size(); ++p)
+                            ok = (half[a][p].t.flags & kShape) == (half[b][p].t.flags & kShape) &&
+                                 pair_bytes(half[a][p], half[b][p]) <= unit_bytes;
+                        if (!ok) { ++q; continue; }
+                        mate[a] = b;
+                        mate[b] = a;
+                        q += 2;
+                    }
+                }
+                auto place = [&](std::int64_t nb) {  // a step of nb bytes in the current unit
+                    if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
+                    if (ustart >= 0 && uused + nb > unit_bytes) close_unit();
+                    if (ustart < 0) { ustart = pos; uused = 0; last_hdr = -1; }
+                    ensure(ustart + uused + nb);
+                    char* base = reinterpret_cast<char*>(pools.stream.data() + pd.stream);
+                    if (last_hdr >= 0)
+                        reinterpret_cast<TileTask*>(base + ustart + last_hdr)->next = static_cast<std::uint32_t>(uused / 16);
+                    last_hdr = uused;
+                    char* dst = base + ustart + uused;
+                    const std::size_t w0 = static_cast<std::size_t>(pd.stream + (ustart + uused) / 8);
+                    uused += nb;
+                    return std::make_pair(dst, w0);
+                };
+                for (std::size_t i = 0; i < chs.size(); ++i) {
+                    if (mate[i] >= 0 && mate[i] < static_cast<int>(i)) continue;  // emitted with its mate
+                    if (mate[i] < 0) {
+                        for (Tile& t : chs[i]->tiles) {
+                            auto [dst, w0] = place(16 + t.bytes());
+                            TileTask hdr = t.t;
+                            hdr.next = kNoTask;
+                            std::memcpy(dst, &hdr, 16);
+                            std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
+                            if (tmpl) std::copy(t.src.begin(), t.src.end(), pools.srcmap.begin() + static_cast<std::ptrdiff_t>(w0 + 2));
+                            std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
+                            if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
+                            off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
+                            if (!t.outidx.empty()) std::memcpy(dst + off, t.outidx.data(), t.outidx.size() * 4);
+                            pools.tile_values += static_cast<std::int64_t>(t.vals.size());
+                            ++pools.n_tiles;
+                        }
+                        continue;
+                    }
+                    const std::size_t j = static_cast<std::size_t>(mate[i]);
+                    for (std::size_t p = 0; p < half[i].size(); ++p) {
+                        const Tile& A = half[i][p];
+                        const Tile& B = half[j][p];
+                        auto [dst, w0] = place(pair_bytes(A, B));
+                        TileTask ha = A.t, hb = B.t;
+                        ha.next = kNoTask;
+                        hb.next = 0;
+                        ha.flags |= kTaskPair;
+                        hb.flags |= kTaskPair;
+                        std::memcpy(dst, &ha, 16);
+                        std::memcpy(dst + 16, &hb, 16);
+                        const int kga = A.t.nrows << A.t.groups, kgb = B.t.nrows << B.t.groups, S = kga + kgb;
+                        const int ia = A.t.iters, ib = B.t.iters, im = std::max(ia, ib);
+                        double* V = reinterpret_cast<double*>(dst + 32);
+                        for (int t = 0; t < im; ++t) {
+                            for (int l = 0; l < kga; ++l) {
+                                const std::size_t at = static_cast<std::size_t>(t) * S + l;
+                                V[at] = t < ia ? A.vals[static_cast<std::size_t>(t) * kga + l] : 0.0;
+                                if (tmpl) pools.srcmap[w0 + 4 + at] = t < ia ? A.src[static_cast<std::size_t>(t) * kga + l] : kSrcZero;
+                            }
+                            for (int l = 0; l < kgb; ++l) {
+                                const std::size_t at = static_cast<std::size_t>(t) * S + kga + l;
+                                V[at] = t < ib ? B.vals[static_cast<std::size_t>(t) * kgb + l] : 0.0;
+                                if (tmpl) pools.srcmap[w0 + 4 + at] = t < ib ? B.src[static_cast<std::size_t>(t) * kgb + l] : kSrcZero;
+                            }
+                        }
+                        std::int64_t off = 32 + pad16(static_cast<std::int64_t>(im) * S * 8);
+                        for (const Tile* T : {&A, &B}) {
+                            if (!T->idx.empty()) std::memcpy(dst + off, T->idx.data(), T->idx.size() * 4);
+                            off += pad16(static_cast<std::int64_t>(T->idx.size()) * 4);
+                        }
+                        for (const Tile* T : {&A, &B}) {
+                            if (!T->outidx.empty()) std::memcpy(dst + off, T->outidx.data(), T->outidx.size() * 4);
+                            off += pad16(static_cast<std::int64_t>(T->outidx.size()) * 4);
+                        }
+                        pools.tile_values += static_cast<std::int64_t>(im) * S;
+                        pools.n_tiles += 2;
+                    }
+                }
                 close_unit();
                 row[kSolveWarps + w] = static_cast<std::int32_t>(wunits[w].size() / 2);
             }

@@ -35,43 +35,66 @@ void run_phase(const SolvePools& sp, PartState& st) {
     std::vector<double>& other = (kind & kPhaseBackward) ? st.T : st.X;
     const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
     for (int w = 0; w < kSolveWarps; ++w) {
-        double acc[32] = {0};
+        double acc[2][32] = {{0}};  // per sub-tile (a pair step's halves), per row
         const int ua = st.ph == 0 ? 0 : sp.phases[pd.phases + (st.ph - 1) * kPhaseStride + kSolveWarps + w];
         const int ub = row[kSolveWarps + w];
         for (int u = ua; u < ub; ++u)
         for (std::uint32_t cur = 0; cur != kNoTask;) {
             const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + u)];
             const char* ubase = base + std::int64_t(ue[0]) * 16;
-            TileTask task;
-            std::memcpy(&task, ubase + std::int64_t(cur) * 16, 16);
-            const char* tb = ubase + std::int64_t(cur) * 16 + 16;
-            cur = task.next;
-            const int k = task.nrows, G = 1 << task.groups, iters = task.iters;
-            const double* M = reinterpret_cast<const double*>(tb);
-            const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + pad16i(iters * k * G * 8));
-            const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(
-                tb + pad16i(iters * k * G * 8) + ((task.flags & kTaskInIndexed) ? pad16i(iters * G * 4) : 0));
-            if (task.flags & kTaskFirst)
-                for (double& a : acc) a = 0.0;
-            const std::vector<double>& in = (task.flags & kTaskInOwn) ? own : other;
-            for (int r = 0; r < k; ++r) {
-                double s = 0.0;
-                for (int it = 0; it < iters; ++it)
-                    for (int g = 0; g < G; ++g) {
-                        const int j = it * G + g;
-                        const double v = (task.flags & kTaskInIndexed) ? in.at(ix[j]) : in.at(task.in_ref + j);
-                        s += M[it * k * G + r * G + g] * v;
-                    }
-                acc[r] += s;
+            TileTask hd[2];
+            std::memcpy(&hd[0], ubase + std::int64_t(cur) * 16, 16);
+            const bool pair = hd[0].flags & kTaskPair;
+            if (pair) std::memcpy(&hd[1], ubase + std::int64_t(cur) * 16 + 16, 16);
+            const char* tb = ubase + std::int64_t(cur) * 16 + (pair ? 32 : 16);
+            cur = hd[0].next;
+            const int nsub = pair ? 2 : 1;
+            // step geometry (device_format.hpp): value stride S, iterations, list offsets
+            int S = 0, im = 0;
+            for (int q = 0; q < nsub; ++q) {
+                S += hd[q].nrows << hd[q].groups;
+                im = std::max<int>(im, hd[q].iters);
             }
-            if (task.flags & kTaskLast)
-                for (int r = 0; r < task.nvalid; ++r) {
-                    if (task.flags & kTaskDiag) other.at(task.out_base + r) = acc[r];
-                    else if (task.flags & kTaskPush) {
-                        if (task.flags & kTaskPartial) st.Q.at(ox[r]) += acc[r];
-                        else own.at(ox[r]) -= acc[r];
-                    } else own.at(task.out_base + r) -= acc[r];
+            std::int64_t ioff[2] = {0, 0}, ooff[2] = {0, 0};
+            std::int64_t off = pad16i(im * S * 8);
+            for (int q = 0; q < nsub; ++q) {
+                ioff[q] = off;
+                if (hd[q].flags & kTaskInIndexed) off += pad16i(hd[q].iters * (1 << hd[q].groups) * 4);
+            }
+            for (int q = 0; q < nsub; ++q) {
+                ooff[q] = off;
+                if ((hd[q].flags & kTaskPush) && (hd[q].flags & kTaskLast)) off += pad16i(hd[q].nrows * 4);
+            }
+            int voff = 0;
+            for (int q = 0; q < nsub; ++q) {
+                const TileTask& task = hd[q];
+                const int k = task.nrows, G = 1 << task.groups, iters = task.iters;
+                const double* M = reinterpret_cast<const double*>(tb);
+                const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + ioff[q]);
+                const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(tb + ooff[q]);
+                if (task.flags & kTaskFirst)
+                    for (double& a : acc[q]) a = 0.0;
+                const std::vector<double>& in = (task.flags & kTaskInOwn) ? own : other;
+                for (int r = 0; r < k; ++r) {
+                    double s = 0.0;
+                    for (int it = 0; it < iters; ++it)
+                        for (int g = 0; g < G; ++g) {
+                            const int j = it * G + g;
+                            const double v = (task.flags & kTaskInIndexed) ? in.at(ix[j]) : in.at(task.in_ref + j);
+                            s += M[it * S + voff + r * G + g] * v;
+                        }
+                    acc[q][r] += s;
                 }
+                if (task.flags & kTaskLast)
+                    for (int r = 0; r < task.nvalid; ++r) {
+                        if (task.flags & kTaskDiag) other.at(task.out_base + r) = acc[q][r];
+                        else if (task.flags & kTaskPush) {
+                            if (task.flags & kTaskPartial) st.Q.at(ox[r]) += acc[q][r];
+                            else own.at(ox[r]) -= acc[q][r];
+                        } else own.at(task.out_base + r) -= acc[q][r];
+                    }
+                voff += k * G;
+            }
         }
     }
 }

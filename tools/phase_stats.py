@@ -25,10 +25,13 @@ nparts = 128
 tl = raw[nparts * W * 8: nparts * W * 8 + 256]
 pw = raw[nparts * W * 8 + 256: nparts * W * 8 + 256 + 256 * W].reshape(256, W)
 nt = raw[nparts * W * 8 + 256 + 256 * W: nparts * W * 8 + 256 + 2 * 256 * W].reshape(256, W)
+wt = raw[nparts * W * 8 + 256 + 2 * 256 * W + 8: nparts * W * 8 + 256 + 3 * 256 * W + 8].reshape(256, W)
+tt = raw[nparts * W * 8 + 256 + 3 * 256 * W + 8: nparts * W * 8 + 256 + 4 * 256 * W + 8].reshape(256, W)
+rf = raw[nparts * W * 8 + 256 + 4 * 256 * W + 8: nparts * W * 8 + 256 + 5 * 256 * W + 8].reshape(256, W)
 nph = int((tl > 0).sum())
 prev = 0
 tot_dur = tot_max = tot_mean = 0
-print(" ph   dur   busy_max  busy_mean  tiles_max tiles_mean")
+print(" ph   dur   busy_max  busy_mean  tiles_max tiles_mean  wait_max wait_mean  tile@max refill@max")
 for ph in range(nph):
     dur = int(tl[ph] - prev) if tl[ph] > prev else 0
     prev = max(prev, int(tl[ph]))
@@ -36,7 +39,8 @@ for ph in range(nph):
     tot_dur += dur
     tot_max += bm
     tot_mean += bmean
-    print(f"{ph:3d} {dur:6d} {bm:9d} {bmean:10.0f} {int(nt[ph].max()):9d} {nt[ph].mean():10.1f}")
+    print(f"{ph:3d} {dur:6d} {bm:9d} {bmean:10.0f} {int(nt[ph].max()):9d} {nt[ph].mean():10.1f} "
+          f"{int(wt[ph].max()):9d} {wt[ph].mean():9.0f} {int(tt[ph][pw[ph].argmax()]):9d} {int(rf[ph][pw[ph].argmax()]):9d}")
 mk = raw[nparts * W * 8 + 256 + 2 * 256 * W: nparts * W * 8 + 256 + 2 * 256 * W + 8]
 print("markers (cycles since start): before cluster sync", mk[0], "after", mk[1], "after combine", mk[2],
       "after split switch", mk[3], "| timeline at the combine phase end", [int(t) for t in tl[:nph] if 0 < t <= mk[0]][-1:])
@@ -47,3 +51,7 @@ tot = w[:, :, 0].max(axis=1)
 order = np.argsort(-tot)
 print("slowest CTAs (subdomain, rank, cycles):", [(int(c) // 2, int(c) % 2, int(tot[c])) for c in order[:8]])
 print("fastest CTAs:", [(int(c) // 2, int(c) % 2, int(tot[c])) for c in order[-4:]], "median", int(np.median(tot)))
+tp = raw[nparts * W * 8 + 256 + 5 * 256 * W + 8: nparts * W * 8 + 256 + 5 * 256 * W + 8 + 4 * W].reshape(W, 4)
+print("CTA 0 tile sub-phase cycles per warp (decode, loop, reduction, flush):")
+for w_ in range(W):
+    print("  warp", w_, [int(v) for v in tp[w_]])

@@ -37,7 +37,7 @@ int main(int argc, char** argv) {
                 (long long)F.factor_values(), (long long)pools.n_tiles, (long long)pools.tile_values);
     std::map<std::tuple<int, int, int>, std::pair<long long, long long>> hist;  // (k, G, flags) -> tiles, values
     std::map<int, std::pair<long long, long long>> by_iters;
-    long long ntile = 0, nval = 0;
+    long long ntile = 0, nval = 0, nsteps = 0, npairs = 0;
     for (const PartDesc& pd : pools.parts) {
         std::printf("part %d: n_loc %d n_top %d phases %d units %d\n", pd.rank, pd.n_loc, pd.n_top, pd.n_phases,
                     pd.n_units);
@@ -49,6 +49,14 @@ int main(int argc, char** argv) {
                 for (std::uint32_t cur = 0; cur != kNoTask;) {
                     TileTask t;
                     std::memcpy(&t, ub + std::int64_t(cur) * 16, 16);
+                    ++nsteps;
+                    if (t.flags & kTaskPair) {  // a pair step: count its B tile too
+                        ++npairs;
+                        TileTask b;
+                        std::memcpy(&b, ub + std::int64_t(cur) * 16 + 16, 16);
+                        ntile++;
+                        nval += (long long)b.iters * b.nrows * (1 << b.groups);
+                    }
                     cur = t.next;
                     const int G = 1 << t.groups;
                     const long long v = (long long)t.iters * t.nrows * G;
@@ -63,7 +71,8 @@ int main(int argc, char** argv) {
                 }
             }
     }
-    std::printf("tiles %lld values %lld (%.1f per tile)\n", ntile, nval, double(nval) / ntile);
+    std::printf("tiles %lld values %lld (%.1f per tile), warp steps %lld (%lld pair steps)\n", ntile, nval,
+                double(nval) / ntile, nsteps, npairs);
     std::printf("%4s %3s %5s %8s %10s %8s\n", "k", "G", "flags", "tiles", "values", "v/tile");
     for (auto& [key, c] : hist)
         if (c.first * 200 > ntile)
