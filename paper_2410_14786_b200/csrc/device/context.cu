@@ -145,7 +145,7 @@ const char* const kEnvSwitches[] = {
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
-    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL"};
+    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
@@ -239,6 +239,16 @@ struct GpuContext::Impl {
     DBuf<unsigned int> plain_bar;  // grid barrier of the one-launch plain CG
     // plain CG on one GPU as one cooperative launch (BDDC_PLAIN_LOOP=0: the per-kernel loop)
     bool use_plain_loop = !(std::getenv("BDDC_PLAIN_LOOP") && std::atoi(std::getenv("BDDC_PLAIN_LOOP")) == 0);
+    // K_i stored as packed symmetric 32 x 32 tiles, one CTA per subdomain (BDDC_K_FULL=1: the
+    // row-major K_i and local_blocks CTAs per subdomain)
+    bool kpacked = !(std::getenv("BDDC_K_FULL") && std::atoi(std::getenv("BDDC_K_FULL")) == 1);
+    // BDDC_STEP=1 (experiment, measured slower: two grid barriers over 592 CTAs cost more than
+    // the graph's kernel boundaries): xpay + SpMV + update of a BDDC-PCG iteration on one GPU as
+    // one cooperative launch
+    bool use_step = std::getenv("BDDC_STEP") && std::atoi(std::getenv("BDDC_STEP")) == 1;
+    int step_ok = -1;
+    DBuf<unsigned long long> step_bar;
+    DBuf<double> kpart;  // packed K_i: per tile two 32-vectors of partial sums
     int plain_loop_ok = -1;  // occupancy check, once
     DBuf<double> p_alt;            // second direction buffer (pcg_dir_spmv)
     // BDDC_DIR_SPMV=1: fuse p = z + beta p into the SpMV. Off by default: measured on B200 the
@@ -502,6 +512,37 @@ struct GpuContext::Impl {
     std::int32_t max_loc = 0, max_top = 0;
     DBuf<long long> dbg_buf;
 
+    // K_i (row-major, written by the setup) -> packed symmetric tiles (iface.cu); the subdomain
+    // descriptors' kmat offsets then index the packed array
+    void pack_k(const DeviceImage& img) {
+        const int nsub = static_cast<int>(img.subs.size());
+        std::vector<SubdomainDesc> subs_h = img.subs;
+        std::vector<std::int64_t> full_off(nsub), sym_off(nsub);
+        std::vector<std::int32_t> ngs(nsub);
+        std::int64_t total = 0;
+        for (int i = 0; i < nsub; ++i) {
+            full_off[i] = subs_h[i].kmat;
+            ngs[i] = subs_h[i].n_iface;
+            sym_off[i] = total;
+            subs_h[i].kmat = total;
+            total += sym_k_values(ngs[i]);
+        }
+        DBuf<std::int64_t> d_full, d_sym;
+        DBuf<std::int32_t> d_ng;
+        d_full.upload(full_off);
+        d_sym.upload(sym_off);
+        d_ng.upload(ngs);
+        DBuf<double> packed;
+        packed.alloc(std::max<std::int64_t>(total, 1));
+        launch_pack_sym_k(kmat.p, d_full.p, packed.p, d_sym.p, d_ng.p, nsub, nullptr);
+        BDDC_CUDA(cudaDeviceSynchronize());
+        std::swap(kmat.p, packed.p);
+        std::swap(kmat.n, packed.n);
+        kpart.alloc(std::max<std::int64_t>(total / 16, 1) + 1024);  // (+ diagnostics slots)
+        if (nsub) BDDC_CUDA(cudaMemcpy(subs.p, subs_h.data(), sizeof(SubdomainDesc) * nsub, cudaMemcpyHostToDevice));
+        k_values = total;
+    }
+
     IfaceParams iface_params() const {
         IfaceParams P{};
         P.skip = apply_skip;
@@ -516,6 +557,9 @@ struct GpuContext::Impl {
         P.gi_row_col = gi_row_col.p;
         P.gi_row_val = gi_row_val.p;
         P.kmat = kmat.p;
+        P.kpacked = kpacked ? 1 : 0;
+        P.kcluster = coop_coarse ? 1 : 2;
+        P.kpart = kpart.p;
         P.phig = phig.p;
         P.primal = primal.p;
         P.n_coarse = n_coarse;
@@ -1282,12 +1326,20 @@ struct GpuContext::Impl {
             }
             std::vector<std::int32_t> wc(std::max<std::int64_t>(img.cbuf_total, 1), -1);
             std::vector<std::int32_t> wh(std::max<std::int64_t>(img.hbuf_total, 1), -1);
-            const int bps = opt.local_blocks;
+            // CTAs per subdomain of the K_i kernel and the h rows each produces
+            const int bps = kpacked ? iface_params().kcluster : opt.local_blocks;
             for (std::size_t b = 0; b < img.subs.size(); ++b) {
                 const SubdomainDesc& sd = img.subs[b];
                 for (int j = 0; j < sd.n_primal; ++j) wc[sd.cbuf + j] = static_cast<std::int32_t>(b);
                 const int rows_per = (sd.n_iface + bps - 1) / bps;
-                for (int g = 0; g < sd.n_iface; ++g) wh[sd.hbuf + g] = static_cast<std::int32_t>(b * bps + g / rows_per);
+                for (int g = 0; g < sd.n_iface; ++g) {
+                    int c = g / rows_per;
+                    if (kpacked) {
+                        c = 0;
+                        while (c + 1 < bps && g >= sym_rows_begin(sd.n_iface, bps, c + 1)) ++c;
+                    }
+                    wh[sd.hbuf + g] = static_cast<std::int32_t>(b * bps + c);
+                }
             }
             const int nsub = static_cast<int>(img.subs.size());
             {
@@ -1451,6 +1503,12 @@ struct GpuContext::Impl {
         }
         // p = z + beta p fused into the next iteration's SpMV (no xpay pass, no init_rho)
         const bool dirspmv = use_dir_spmv && precondition && fused_dot && (!dist() || frz);
+        if (step_ok < 0) step_ok = pcg_step_fits(D.grid) ? 1 : 0;
+        const bool stepfuse = use_step && step_ok == 1 && !dist() && precondition && fused_dot && fcheck && !dirspmv;
+        if (stepfuse && !step_bar.p) {
+            step_bar.alloc(1);
+            BDDC_CUDA(cudaMemset(step_bar.p, 0, sizeof(unsigned long long)));
+        }
         if (dirspmv) {
             D.fuse_dir = 1;
             D.p_alt = p_alt.p;
@@ -1497,8 +1555,8 @@ struct GpuContext::Impl {
                 check_coarse(s);
             }
             if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-            if (dirspmv) {
-                // rho[0] and p_1 = z are formed by the first dir_spmv
+            if (dirspmv || stepfuse) {
+                // rho[0] and p_1 = z are formed by the first dir_spmv / pcg_step
             } else if (fused_dir) {
                 if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
                 pcg_init_rho(D, s);
@@ -1576,8 +1634,8 @@ struct GpuContext::Impl {
             if (precondition) apply_rz();
             apply_skip = nullptr;
             if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-            if (dirspmv) {
-                // p = z + beta p happens inside the next dir_spmv
+            if (dirspmv || stepfuse) {
+                // p = z + beta p happens inside the next dir_spmv / pcg_step
             } else if (fused_dir) {
                 if (!frz) gather_rz_with_z_halo(rz_part, rz_grid, s);
                 pcg_xpay(D, it, s);
@@ -1588,6 +1646,10 @@ struct GpuContext::Impl {
             }
         };
         auto check_part = [&](int it) {
+            if (stepfuse) {
+                pcg_step(D, step_bar.p, s);  // xpay + SpMV + update + check
+                return;
+            }
             if (dirspmv) pcg_dir_spmv(D, s);
             else pcg_spmv_dot(D, s);
             if (!fpcg) gather_partial(part_a.p, D.grid, gath_a.p, s);
@@ -1735,7 +1797,7 @@ struct GpuContext::Impl {
                     check_coarse(s);
                 }
                 if (!fused_dot) pcg_dot(D, rd, zd, part_a.p, s);
-                if (!dirspmv) {
+                if (!dirspmv && !stepfuse) {
                     gather_partial(rz_part, rz_grid, gath_c.p, s);
                     pcg_xpay(D, it, s);
                     halo_exchange(p.p, s);
@@ -2012,6 +2074,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     tm.mark("uploads + buffers");
     if (on_device) I.device_setup(classes, img);
     tm.mark("device numeric setup");
+    if (I.kpacked) I.pack_k(img);
     I.finish_coarse(dist);
     tm.mark("coarse");
     BDDC_CUDA(cudaDeviceSynchronize());

@@ -276,6 +276,199 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
 }
 
 
+// Packed symmetric K_i (kpacked): a cluster of kcluster CTAs per subdomain streams the stored
+// tiles (a, b), a <= b, of the 32 x 32 tiling of K_i once each (K_i is symmetric: the lower tiles
+// are the upper ones transposed) and forms both of their products: u_ab = K_ab g_b for the rows
+// of block a and, off the diagonal, v_ab = K_ab^T g_a for the rows of block b. A warp holds a
+// tile's 32 rows (lane = column: every row load is one coalesced 256-byte read); v is a
+// lane-local column sum, u a reduce-scatter of the 32 row products over the lanes (recursive
+// halving, 31 shuffles). The partials go to kpart; after a cluster barrier each CTA sums, for its
+// row blocks (sym_rows_begin), the partials in a fixed order (b ascending: v_ba for b < a, u_ab
+// for b >= a), so the result is deterministic. Half the K_i bytes of a row-major GEMV. r_c is
+// formed by all threads while the first tiles' loads are in flight; every CTA of the cluster
+// forms the x_c rows its Phi_G rows need.
+constexpr int kSymThreads = 512;
+constexpr int kSymWarps = kSymThreads / 32;
+
+__device__ __forceinline__ int sym_tile(int a, int b, int nt) { return a * nt - a * (a - 1) / 2 + (b - a); }
+
+// xl[j] = (A_c^{-1} r_c)[primal j] for j = first, first + stride, ... (a warp per row)
+__device__ __forceinline__ void coarse_rows(const IfaceParams& P, const SubdomainDesc& sd, const double* rc, double* xl,
+                                            int first, int stride, int lane) {
+    const int nc = P.n_coarse;
+    for (int j = first; j < sd.n_primal; j += stride) {
+        const double* row = P.coarse_inv + static_cast<std::size_t>(P.primal[sd.primal + j]) * nc;
+        double acc = 0.0;
+        for (int k = lane; k < nc; k += 32) acc = fma(row[k], rc[k], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) xl[j] = acc;
+    }
+}
+
+#ifdef SYM_PROF
+#define SYM_T(i) do { ts_[i] = clock64() - t0_; } while (0)
+#else
+#define SYM_T(i) do { } while (0)
+#endif
+template <int CLUSTER>
+__global__ void __launch_bounds__(kSymThreads) iface_local_sym_kernel(const IfaceParams P, int with_coarse) {
+    const long long t0_ = clock64();
+    long long ts_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    (void)t0_;
+    (void)ts_;
+    pdl_trigger();
+    pdl_wait();
+    if (skip_launch(P.skip)) return;  // uniform over the cluster
+    extern __shared__ double sm[];
+    const int sub = blockIdx.x / CLUSTER, crank = blockIdx.x % CLUSTER;
+    const SubdomainDesc& sd = P.subs[sub];
+    const int ng = sd.n_iface, np = sd.n_primal, nc = P.n_coarse;
+    const int nt = (ng + 31) >> 5;
+    double* g = sm;                                   // nt * 32, zero padded
+    double* xl = g + nt * 32;
+    double* rc = xl + ((P.max_primal + 1) & ~1);
+    double* kg = rc + (with_coarse == 2 ? ((nc + 1) & ~1) : 0);  // K_i g_i (nt * 32)
+    for (int k = threadIdx.x; k < nt * 32; k += blockDim.x) g[k] = k < ng ? P.gbuf[sd.hbuf + k] : 0.0;
+    __syncthreads();
+    SYM_T(0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* K = P.kmat + sd.kmat;
+    double* part = P.kpart + sd.kmat / 16;
+    const int ntiles = nt * (nt + 1) / 2;
+    const std::uint32_t tag_c = with_coarse == 2 && P.ll_c ? ll_tag(P.seq_c) : 0u;
+    constexpr int kStride = CLUSTER * kSymWarps;
+    int t = crank * kSymWarps + warp;
+    double x[32];
+    if (t < ntiles) {  // the first tile's loads, in flight while r_c is formed
+#pragma unroll
+        for (int r = 0; r < 32; ++r) x[r] = ld_stream(K + static_cast<std::int64_t>(t) * 1024 + 32 * r + lane);
+    }
+    if (with_coarse == 2) {
+        if (P.coarse_ctr) {
+            // this CTA's share of r_c (every owner's c_i, ascending subdomain) to rc_g, then arrive
+            const int q0 = static_cast<int>(static_cast<long long>(nc) * blockIdx.x / gridDim.x);
+            const int q1 = static_cast<int>(static_cast<long long>(nc) * (blockIdx.x + 1) / gridDim.x);
+            for (int q = q0 + threadIdx.x; q < q1; q += kSymThreads) P.rc_g[q] = coarse_entry(P, q, tag_c);
+            __threadfence();  // each writer's entries visible GPU-wide before the CTA arrives
+        } else {
+            for (int q = threadIdx.x; q < nc; q += kSymThreads) rc[q] = coarse_entry(P, q, tag_c);
+        }
+    }
+    SYM_T(1);
+    int a = 0, row_end = nt;  // tile t = (a, b): the tiles of row a are [row_end - (nt - a), row_end)
+    for (; t < ntiles; t += kStride) {
+        while (t >= row_end) row_end += nt - ++a;
+        const int b = a + (t - (row_end - (nt - a)));
+        if (a != b) {
+            const double* ga = g + a * 32;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+            for (int r = 0; r < 32; r += 4) {
+                v0 = fma(x[r], ga[r], v0);
+                v1 = fma(x[r + 1], ga[r + 1], v1);
+                v2 = fma(x[r + 2], ga[r + 2], v2);
+                v3 = fma(x[r + 3], ga[r + 3], v3);
+            }
+            part[static_cast<std::int64_t>(t) * 64 + 32 + lane] = (v0 + v1) + (v2 + v3);
+        }
+        const double gb = g[b * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) x[r] *= gb;
+        // reduce-scatter: after the step of width w a lane keeps the half of its 2w values
+        // selected by its bit w, plus the partner's copy of that half; lane l ends with row l
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+            const bool up = lane & w;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const double send = up ? x[i] : x[i + w];
+                const double keep = up ? x[i + w] : x[i];
+                x[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+            }
+        }
+        part[static_cast<std::int64_t>(t) * 64 + lane] = x[0];
+        if (t + kStride < ntiles) {
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                x[r] = ld_stream(K + static_cast<std::int64_t>(t + kStride) * 1024 + 32 * r + lane);
+        }
+    }
+    SYM_T(2);
+    // every partial of the subdomain written (and this CTA's r_c complete)
+    if (CLUSTER > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        __syncthreads();
+    }
+    SYM_T(3);
+    if (with_coarse == 2 && P.coarse_ctr) {
+        if (threadIdx.x == 0) {  // grid barrier (monotonic counter, see iface_local_kernel)
+            __threadfence();
+            atomicAdd(P.coarse_ctr, 1ull);
+            const unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr);
+            const unsigned long long target = (seen + gridDim.x - 1) / gridDim.x * gridDim.x;
+            while (*reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr) < target) {
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < nc; q += blockDim.x) rc[q] = __ldcg(P.rc_g + q);
+        __syncthreads();
+    }
+    // this CTA's row blocks: K_i g_i from the partials in a fixed order, and the x_c rows
+    const int a0 = sym_rows_begin(ng, CLUSTER, crank) / 32, a1 = (sym_rows_begin(ng, CLUSTER, crank + 1) + 31) / 32;
+    for (int ab = a0 + warp; ab < a1; ab += kSymWarps) {
+        double acc = 0.0;
+        for (int bb = 0; bb < nt; ++bb)
+            acc += bb < ab ? part[static_cast<std::int64_t>(sym_tile(bb, ab, nt)) * 64 + 32 + lane]
+                           : part[static_cast<std::int64_t>(sym_tile(ab, bb, nt)) * 64 + lane];
+        kg[ab * 32 + lane] = acc;
+    }
+    if (with_coarse == 2) coarse_rows(P, sd, rc, xl, warp, kSymWarps, lane);
+    if (with_coarse == 1)
+        for (int j = threadIdx.x; j < np; j += blockDim.x) xl[j] = P.xc[P.primal[sd.primal + j]];
+    __syncthreads();
+    SYM_T(4);
+    const int r0 = sym_rows_begin(ng, CLUSTER, crank), r1 = sym_rows_begin(ng, CLUSTER, crank + 1);
+    if (!with_coarse) {
+        for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) P.hbuf[sd.hbuf + k] = kg[k];
+    } else {
+        // h = W (Phi_G x_c + K g): a thread per row (its Phi_G row's loads in flight together)
+        const double* phig = P.phig + sd.phig;
+        for (int row = r0 + threadIdx.x; row < r1; row += kSymThreads) {
+            const double* ph = phig + static_cast<std::int64_t>(row) * np;
+            double c = 0.0;
+            for (int j = 0; j < np; ++j) c = fma(ph[j], xl[j], c);
+            P.hbuf[sd.hbuf + row] = P.iface_w[sd.iface + row] * (c + kg[row]);
+        }
+    }
+    SYM_T(5);
+    // the partials stay alive until every CTA of the cluster has read them
+    if (CLUSTER > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    publish<kSymThreads>(P.pub_h);
+    SYM_T(6);
+#ifdef SYM_PROF
+    if ((blockIdx.x / CLUSTER == 0 || blockIdx.x / CLUSTER == 27) && (threadIdx.x & 31) == 0)
+        printf("sym cta %d warp %d: %lld %lld %lld %lld %lld %lld %lld\n", blockIdx.x, threadIdx.x >> 5, ts_[0], ts_[1],
+               ts_[2], ts_[3], ts_[4], ts_[5], ts_[6]);
+#endif
+}
+
+__global__ void pack_sym_k_kernel(const double* __restrict__ full, const std::int64_t* __restrict__ full_off,
+                                  double* packed, const std::int64_t* __restrict__ sym_off,
+                                  const std::int32_t* __restrict__ ngs) {
+    const int sub = blockIdx.x, ng = ngs[sub], nt = (ng + 31) >> 5;
+    const double* K = full + full_off[sub];
+    double* out = packed + sym_off[sub];
+    for (int a = 0, t = 0; a < nt; ++a)
+        for (int b = a; b < nt; ++b, ++t)
+            for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+                const int row = a * 32 + (e >> 5), col = b * 32 + (e & 31);
+                out[static_cast<std::int64_t>(t) * 1024 + e] =
+                    row < ng && col < ng ? K[static_cast<std::int64_t>(row) * ng + col] : 0.0;
+            }
+}
+
 // ---------------------------------------------------------------- stage hooks
 constexpr int kStageThreads = 256;
 
@@ -460,7 +653,34 @@ void launch_coarse_direct(const IfaceParams& P, cudaStream_t s) {
     BDDC_LAUNCHED();
 }
 
+std::size_t sym_smem(const IfaceParams& P, int coarse) {
+    const std::size_t nt = (P.max_iface + 31) / 32;
+    return sizeof(double) * (64 * nt + P.max_primal + 4 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0));
+}
+
+std::int64_t sym_k_values(int ng) {
+    const std::int64_t nt = (ng + 31) / 32;
+    return nt * (nt + 1) / 2 * 1024;
+}
+
+void launch_pack_sym_k(const double* full, const std::int64_t* full_off, double* packed, const std::int64_t* sym_off,
+                       const std::int32_t* ng, int n_subdomains, cudaStream_t s) {
+    if (n_subdomains <= 0) return;
+    pack_sym_k_kernel<<<n_subdomains, 256, 0, s>>>(full, full_off, packed, sym_off, ng);
+    BDDC_LAUNCHED();
+}
+
 bool iface_local_cooperative_fits(const IfaceParams& P, int blocks_per_sub, int device) {
+    if (P.kpacked) {  // the cooperative K_i grid runs one CTA per subdomain
+        const std::size_t smem = sym_smem(P, 2);
+        if (smem > 48 * 1024)
+            BDDC_CUDA(cudaFuncSetAttribute(iface_local_sym_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0, nsm = 0, coop = 0;
+        BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iface_local_sym_kernel<1>, kSymThreads, smem));
+        BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        BDDC_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+        return coop && static_cast<long long>(per_sm) * nsm >= P.n_subdomains;
+    }
     const std::size_t smem =
         sizeof(double) * (P.max_iface + P.max_primal + 6 + static_cast<std::size_t>(P.n_coarse) +
                           (P.max_iface + blocks_per_sub - 1) / blocks_per_sub);
@@ -474,6 +694,40 @@ bool iface_local_cooperative_fits(const IfaceParams& P, int blocks_per_sub, int 
 }
 
 void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s, int coarse) {
+    if (P.kpacked) {  // kcluster CTAs per subdomain (blocks_per_sub does not apply)
+        const std::size_t smem = sym_smem(P, coarse);
+        const bool coop = coarse == 2 && P.coarse_ctr;
+        auto go = [&](auto kern) {
+            if (smem > 48 * 1024) BDDC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(P.n_subdomains * P.kcluster);
+            cfg.blockDim = dim3(kSymThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[2];
+            int na = 0;
+            if (coop) {
+                attr[na].id = cudaLaunchAttributeCooperative;
+                attr[na++].val.cooperative = 1;
+            } else if (P.kcluster > 1) {
+                attr[na].id = cudaLaunchAttributeClusterDimension;
+                attr[na].val.clusterDim.x = P.kcluster;
+                attr[na].val.clusterDim.y = 1;
+                attr[na++].val.clusterDim.z = 1;
+            }
+            if (!coop && pdl_enabled()) {
+                attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[na++].val.programmaticStreamSerializationAllowed = 1;
+            }
+            cfg.attrs = attr;
+            cfg.numAttrs = na;
+            BDDC_CUDA(cudaLaunchKernelEx(&cfg, kern, P, coarse));
+        };
+        if (P.kcluster == 2) go(iface_local_sym_kernel<2>);
+        else go(iface_local_sym_kernel<1>);
+        BDDC_LAUNCHED();
+        return;
+    }
     const std::size_t smem =
         sizeof(double) * (P.max_iface + P.max_primal + 6 + (coarse == 2 ? static_cast<std::size_t>(P.n_coarse) : 0) +
                           (P.max_iface + blocks_per_sub - 1) / blocks_per_sub);

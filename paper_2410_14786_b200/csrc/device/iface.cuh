@@ -27,8 +27,13 @@ struct IfaceParams {
     const std::int32_t* gi_row_ptr;
     const std::int32_t* gi_row_col;
     const double* gi_row_val;
-    // dense blocks
+    // dense blocks. kpacked: K_i stored as its upper triangle of 32 x 32 tiles (iface.cu,
+    // pack_sym_k), applied by one CTA per subdomain; kpart: per tile two 32-vectors of partial
+    // sums (kmat offset / 16)
     const double* kmat;
+    int kpacked;
+    int kcluster;  // packed: CTAs per subdomain (a thread-block cluster); 1 for the cooperative grid
+    double* kpart;
     const double* phig;
     const std::int32_t* primal;
     // coarse
@@ -109,5 +114,17 @@ void launch_iface_local(const IfaceParams& P, int blocks_per_sub, cudaStream_t s
 // Whether the fused-coarse K_i grid (n_subdomains * blocks_per_sub CTAs) can be co-resident on
 // `device` (cooperative launch, one r_c per GPU); otherwise every CTA forms r_c itself.
 bool iface_local_cooperative_fits(const IfaceParams& P, int blocks_per_sub, int device);
+// Packed K_i kernel: the first h row of CTA c of a subdomain's cluster of C (whole 32-row blocks)
+__host__ __device__ inline int sym_rows_begin(int ng, int C, int c) {
+    const int nt = (ng + 31) / 32;
+    const int r = (c * nt / C) * 32;
+    return r < ng ? r : ng;
+}
+// Doubles of subdomain K_i (n_iface = ng) in the packed symmetric layout: the tiles (a, b),
+// a <= b, of the zero-padded ceil(ng / 32)^2 tiling, 1024 row-major values each.
+std::int64_t sym_k_values(int ng);
+// Packs every subdomain's row-major K_i (full_off) into the tiled upper triangle (sym_off).
+void launch_pack_sym_k(const double* full, const std::int64_t* full_off, double* packed, const std::int64_t* sym_off,
+                       const std::int32_t* ng, int n_subdomains, cudaStream_t s);
 
 }  // namespace bddc_b200

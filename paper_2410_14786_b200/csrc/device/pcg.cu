@@ -350,6 +350,111 @@ __global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevic
     }
 }
 
+// Grid barrier on a monotonic 64-bit counter (no reset between launches): the k-th arrival of
+// a barrier round falls in [m * grid, (m + 1) * grid) for one m, the round ends at (m + 1) * grid.
+__device__ __forceinline__ void grid_sync_mono(unsigned long long* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long v = atomicAdd(ctr, 1ull);
+        const unsigned long long target = (v / gridDim.x + 1) * gridDim.x;
+        unsigned long long c;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(ctr) : "memory");
+        } while (c < target);
+    }
+    __syncthreads();
+}
+
+// One BDDC-PCG iteration's vector work on one GPU as ONE cooperative launch (pcg.cpp:65-104):
+// phase 0 is xpay_kernel's (beta = r.z / rho from the harmonic solve's partials, p = z + beta p;
+// p = z and rho_0 for the first direction), phase 1 spmv_dot_kernel's (q = A p, p.q), phase 2
+// update_kernel's (alpha, x += alpha p, r -= alpha q, r.r, the fused convergence check in the
+// grid's last CTA, which also advances the iteration counter). Grid barriers between the phases
+// instead of kernel boundaries; every expression and fixed-order partial sum is the per-kernel
+// loop's, so the iterates are bitwise identical to it.
+__global__ void __launch_bounds__(kVecThreads, 4) pcg_step_kernel(const PcgDevice D, unsigned long long* bar) {
+    __shared__ double scratch[kVecThreads / 32];
+    const int km1 = *D.iter, k = km1 + 1;
+    const int stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    {
+        // phase 0: the direction (the thread's first rows' loads before the r.z reduction)
+        double* p = D.p;
+        const double* z = D.z;
+        const double z0 = i0 < D.n ? z[i0] : 0.0, p0 = i0 < D.n && km1 > 0 ? p[i0] : 0.0;
+        const double rz = sum_partials(D.red_c, D.red_c_n, scratch);
+        const double beta = km1 > 0 ? rz / D.rho[km1 - 1] : 0.0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            D.rho[km1] = rz;
+            if (km1 > 0) D.beta[km1 - 1] = beta;
+        }
+        if (i0 < D.n) p[i0] = km1 > 0 ? z0 + beta * p0 : z0;
+        for (int i = i0 + stride; i < D.n; i += stride) p[i] = km1 > 0 ? z[i] + beta * p[i] : z[i];
+    }
+    grid_sync_mono(bar);
+    {
+        // phase 1: q = A p (sliced ELL, CSR order), p.q
+        const double* p = D.p;
+        double* q = D.q;
+        const std::int32_t* __restrict__ ec = D.ell_col;
+        const double* __restrict__ ev = D.ell_val;
+        double acc = 0.0;
+        for (int i = i0; i < D.n; i += stride) {
+            const std::int64_t base = D.ell_off[i >> 5] + (i & 31);
+            const int len = D.ell_len[i];
+            double y = 0.0;
+            int j = 0;
+            for (; j + 3 < len; j += 4) {
+                const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
+                const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
+                const double x0 = p[ec[base + 32 * j]], x1 = p[ec[base + 32 * (j + 1)]];
+                const double x2 = p[ec[base + 32 * (j + 2)]], x3 = p[ec[base + 32 * (j + 3)]];
+                y += v0 * x0;
+                y += v1 * x1;
+                y += v2 * x2;
+                y += v3 * x3;
+            }
+            for (; j < len; ++j) y += ev[base + 32 * j] * p[ec[base + 32 * j]];
+            q[i] = y;
+            if (i < D.n_dot) acc = fma(p[i], y, acc);
+        }
+        acc = block_sum<kVecThreads>(acc, scratch);
+        if (threadIdx.x == 0) D.part_a[blockIdx.x] = acc;
+    }
+    grid_sync_mono(bar);
+    {
+        // phase 2: update_kernel's
+        const double* p = D.p;
+        const double* q = D.q;
+        double* x = D.x;
+        double* r = D.r;
+        const double pq = sum_partials(D.part_a, gridDim.x, scratch);
+        if (pq <= 0.0) {  // pcg.cpp:75-78 "matrix not SPD"
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                D.scal[3] = 1.0;
+                if (D.host_scal) reinterpret_cast<volatile double*>(D.host_scal)[3] = 1.0;
+                *D.iter = k;
+            }
+            return;
+        }
+        const double alpha = D.rho[km1] / pq;
+        if (blockIdx.x == 0 && threadIdx.x == 0) D.alpha[km1] = alpha;
+        double acc = 0.0;
+        for (int i = i0; i < D.n; i += stride) {
+            x[i] += alpha * p[i];
+            const double ri = r[i] - alpha * q[i];
+            r[i] = ri;
+            if (i < D.n_dot) acc = fma(ri, ri, acc);
+        }
+        acc = block_sum<kVecThreads>(acc, scratch);
+        if (threadIdx.x == 0) D.part_b[blockIdx.x] = acc;
+        if (publish<kVecThreads>(D.pub_rr) && threadIdx.x == 0) {  // the grid's last CTA
+            check_scalar(D, k, D.pub_rr.red[0]);
+            *D.iter = k;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kVecThreads) spmv_kernel(int n, const std::int32_t* __restrict__ ptr,
                                                            const std::int32_t* __restrict__ col,
                                                            const double* __restrict__ val,
@@ -444,6 +549,26 @@ void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t
                               const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s) {
     if (n <= 0) return;
     csr_to_ell_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, off, ell_col, ell_val);
+    BDDC_LAUNCHED();
+}
+bool pcg_step_fits(int grid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    BDDC_CUDA(cudaGetDevice(&dev));
+    BDDC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_step_kernel, kVecThreads, 0));
+    return grid <= per_sm * sms;
+}
+void pcg_step(const PcgDevice& D, unsigned long long* barrier, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(D.grid);
+    cfg.blockDim = dim3(kVecThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BDDC_CUDA(cudaLaunchKernelEx(&cfg, pcg_step_kernel, D, barrier));
     BDDC_LAUNCHED();
 }
 bool pcg_plain_loop_fits(int grid) {

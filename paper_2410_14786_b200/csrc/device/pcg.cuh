@@ -88,6 +88,10 @@ void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t
                               const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s);
 // plain CG (no preconditioner, one GPU) as one cooperative launch over D.grid CTAs: iterations
 // 1..max_iterations from rho[0] and p = r; scal[1..4] = rel, converged, error code, iterations
+// one BDDC-PCG iteration's xpay + SpMV + update (+ fused check) on one GPU as one cooperative
+// launch over D.grid CTAs (monotonic grid-barrier counter, zeroed once)
+bool pcg_step_fits(int grid);
+void pcg_step(const PcgDevice& D, unsigned long long* barrier, cudaStream_t s);
 bool pcg_plain_loop_fits(int grid);
 void pcg_plain_loop(const PcgDevice& D, int max_iterations, unsigned int* barrier, cudaStream_t s);
 // Smallest index of a non-finite entry, or -1 (writes to *dev_result).

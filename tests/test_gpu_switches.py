@@ -41,6 +41,9 @@ CASES = [
     {"BDDC_DIR_SPMV": "1"},         # p = z + beta p fused into the SpMV
     {"BDDC_PDL": "1"},              # programmatic dependent launch
     {"BDDC_PROFILE_STRIDE": "1"},   # (profiling off here; the stride must not change results)
+    {"BDDC_STEP": "1"},             # xpay / SpMV / update as one cooperative launch
+    {"BDDC_K_FULL": "1"},           # row-major K_i, local_blocks CTAs per subdomain
+    {"BDDC_PAIR_TILES": "0"},       # no pair steps in the interior-solve programs
 ]
 
 
@@ -107,7 +110,7 @@ for name, p in cases.items():
         x, rep = pre.pcg(p.rhs(), SolverOptions(1e-8, 0.0, cap, True), precondition=False)
         out[f"{name}/{cap}"] = [rep.iterations, bool(rep.converged), [float(h).hex() for h in rep.residual_history],
                                 hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
-                                float(rep.condition_estimate).hex()]
+                                None if rep.condition_estimate is None else float(rep.condition_estimate).hex()]
 # symmetric, not SPD (the negated Laplacian): pcg.cpp:75-78 at the first iteration
 p = Problem.poisson(32, 2)
 nr, nc, rp, ci, va = p.global_matrix()
@@ -140,3 +143,38 @@ def test_plain_cg_one_launch_matches_kernel_loop(gpu):
     assert one["c2/10000"][0] == 1649 and one["c2/10000"][1]
     assert one["c2/7"][0] == 7 and not one["c2/7"][1] and len(one["c2/7"][2]) == 8
     assert "matrix not SPD" in one["neg"]
+
+
+STEP_SCRIPT = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, ROOT)
+from paper_2410_14786_b200 import Preconditioner, Problem, SolverOptions
+out = {}
+for name, args in (("c2", (800, 8)), ("k4m8", (32, 4))):
+    p = Problem.poisson(*args, rhs_seed=1)
+    pre = Preconditioner(p)
+    for cap in (10000, 5):
+        x, rep = pre.pcg(p.rhs(), SolverOptions(1e-8, 0.0, cap, True))
+        out[f"{name}/{cap}"] = [rep.iterations, rep.converged, [float(h).hex() for h in rep.residual_history],
+                                hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
+                                None if rep.condition_estimate is None else float(rep.condition_estimate).hex()]
+print(json.dumps(out))
+""".replace("ROOT", repr(ROOT))
+
+
+def test_pcg_step_one_launch_matches_kernel_loop(gpu):
+    # BDDC_STEP=1: xpay + SpMV + update (+ check) of each BDDC-PCG iteration run as one cooperative
+    # launch (pcg.cu pcg_step_kernel); its phases are the per-kernel loop's, so histories, x and
+    # the Lanczos estimate are bitwise identical, at convergence and at the cap
+    env = {k: v for k, v in os.environ.items() if not k.startswith("BDDC_")}
+    res = []
+    for extra in ({"BDDC_STEP": "1"}, {}):
+        r = subprocess.run([sys.executable, "-c", STEP_SCRIPT], env={**env, **extra}, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    one, loop = res
+    assert one == loop
+    assert one["c2/10000"][0] == 11 and one["c2/10000"][1]
+    assert one["c2/5"][0] == 5 and not one["c2/5"][1]
