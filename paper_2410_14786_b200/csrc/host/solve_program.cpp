@@ -6,6 +6,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 namespace bddc_b200 {
 namespace {
@@ -426,6 +427,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         };
         auto all_rows = [](index_t) { return true; };
         // chunk rows for a level: the largest of 32/16/8 giving at least 2 chunks per warp
+        // forward levels: pushes sharing target rows chained into one warp job (up to kMaxChain
+        // chunks) instead of coloured into phases; BDDC_MAX_CHAIN=0: colouring only (experiments)
+        static const std::size_t kMaxChain = std::getenv("BDDC_MAX_CHAIN") ? std::atoi(std::getenv("BDDC_MAX_CHAIN")) : 8;
         // BDDC_PAIR_TILES=0: no pair steps (experiments)
         static const bool pair_tiles = !std::getenv("BDDC_PAIR_TILES") || std::atoi(std::getenv("BDDC_PAIR_TILES")) != 0;
         static const int min_kr = std::getenv("BDDC_MIN_CHUNK_ROWS") ? std::atoi(std::getenv("BDDC_MIN_CHUNK_ROWS")) : 8;
@@ -593,6 +597,42 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     pushes.back().push_back(std::move(cs[c]));
                 }
             }
+            // Pushes sharing target rows are chained into one warp job (their flushes ordered by
+            // the warp) instead of coloured into separate phases, when no chain gets longer than
+            // kMaxChain chunks: one phase per level instead of one per colour class (measured:
+            // C2 -1% at 8; all levels of the pruned sweeps and most of the full sweeps qualify).
+            if (kMaxChain > 0 && !pushes.empty()) {
+                std::vector<std::size_t> parent(pushes.size());
+                std::iota(parent.begin(), parent.end(), 0);
+                auto find = [&](std::size_t x) {
+                    while (parent[x] != x) x = parent[x] = parent[parent[x]];
+                    return x;
+                };
+                std::unordered_map<index_t, std::size_t> row_job;
+                for (std::size_t j = 0; j < targets.size(); ++j)
+                    for (index_t r : targets[j]) {
+                        auto [it, fresh] = row_job.emplace(r, j);
+                        if (!fresh) parent[find(j)] = find(it->second);
+                    }
+                std::vector<std::vector<std::size_t>> comps(pushes.size());
+                for (std::size_t j = 0; j < pushes.size(); ++j) comps[find(j)].push_back(j);
+                std::size_t longest = 0;
+                for (const auto& c : comps) longest = std::max(longest, c.size());
+                if (longest <= kMaxChain) {
+                    Phase pp = std::move(diag_phase);
+                    for (const auto& c : comps) {
+                        if (c.empty()) continue;
+                        pp.jobs.emplace_back();
+                        for (std::size_t j : c) pp.jobs.back().push_back(std::move(pushes[j][0]));
+                        if (c.size() > 1) pp.kind = kPhaseChained;
+                    }
+                    phases.push_back(std::move(pp));
+                    kr = 32;
+                    continue;
+                }
+                // (a level with a longer chain keeps the colouring: chaining part of it only
+                // lengthens the first phase, measured +2%)
+            }
             // the diagonal solves read the same final t_s as the pushes (and write X): they
             // share the first colour class's phase
             bool first = true;
@@ -720,14 +760,18 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                 // this warp's chunks of the phase; outside chained phases (tiles independent),
                 // chunks of <= 16 rows are paired piece by piece into half-warp pair steps
                 std::vector<Chunk*> chs;
+                std::vector<char> solo;  // the chunk is a job of its own (chained phases: pairable)
                 for (index_t c : per_warp[w])
-                    for (Chunk& ch : ph.jobs[c]) chs.push_back(&ch);
+                    for (Chunk& ch : ph.jobs[c]) {
+                        chs.push_back(&ch);
+                        solo.push_back(ph.jobs[c].size() == 1);
+                    }
                 std::vector<int> mate(chs.size(), -1);
                 std::vector<std::vector<Tile>> half(chs.size());
-                if (pair_tiles && !(ph.kind & kPhaseChained)) {
+                if (pair_tiles) {
                     std::vector<int> cand;
                     for (std::size_t i = 0; i < chs.size(); ++i) {
-                        bool ok = !chs[i]->tiles.empty();
+                        bool ok = !chs[i]->tiles.empty() && (solo[i] || !(ph.kind & kPhaseChained));
                         for (const Tile& t : chs[i]->tiles) ok = ok && t.t.nrows <= 16;
                         if (!ok) continue;
                         for (const Tile& t : chs[i]->tiles) half[i].push_back(regroup(t, half_groups(t.t.nrows)));

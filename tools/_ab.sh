@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 for rnd in $(seq 1 ${ROUNDS:-3}); do
 for v in ${VARIANTS:-default}; do
-  if [ "$v" = default ]; then envs=""; else envs="$v"; fi
+  if [ "$v" = default ]; then envs=""; else envs="${v//+/ }"; fi
   env $envs timeout 600 python bench.py --no-cpu-baseline --no-extra --steps ${STEPS:-30} ${BENCH_ARGS} > gpurun_out/ab.jsonl 2>gpurun_out/ab.err
   python -c "
 import json; d=json.loads(open('gpurun_out/ab.jsonl').read().strip().splitlines()[-1])
