@@ -192,8 +192,11 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);  // [warp][kMaxWarpSlots]
     const int ldn = (S.max_loc + 64 + 1) & ~1;
     double* T = reinterpret_cast<double*>(bars + kSolveWarps * kMaxWarpSlots);
-    double* X = T + ldn;
-    double* Q = X + ldn;
+    // X follows this part's T at the part's own stride (device_format.hpp: a merged backward
+    // tile addresses both through one index list relative to T)
+    const int ldn_p = part_ldn(pdr.n_loc);
+    double* X = T + ldn_p;
+    double* Q = T + 2 * ldn;
     double* ZG = Q + ((S.max_top + 1) & ~1);
     unsigned char* glut = reinterpret_cast<unsigned char*>(ZG + ((S.max_iface + 1) & ~1));  // spare 1 KB
     // offset arithmetic on smem_raw (not through an integer cast) keeps the shared address
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     const std::int32_t* gmap = S.gmap + pdr.gmap;
     const int n_loc = pdr.n_loc, n_top = pdr.n_top;
     // rhs gather: four independent index/value loads in flight per thread
-    for (int l0 = tid; l0 < ldn; l0 += 4 * kThreads) {
+    for (int l0 = tid; l0 < ldn_p; l0 += 4 * kThreads) {
         int gi[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int l = l0 + q * kThreads;
-            if (l < ldn) {
+            if (l < ldn_p) {
                 T[l] = gv[q];
                 X[l] = 0.0;  // padded columns of a tile read finite zeros
             }

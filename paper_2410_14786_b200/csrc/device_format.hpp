@@ -29,6 +29,8 @@
 //   PUSH : own[outidx[r]]      -= acc     t[R_d] -= L_{R_d,d} x_d (forward off-diagonal)
 //          Q[outidx[r]]        += acc     (PARTIAL: this CTA's contribution into the top)
 //   PULL : own[out_base + r]   -= acc     u_s = x_s - L_{R_s,s}^T y[R_s] (backward)
+// A backward chunk is one indexed DIAG tile over [L_ss^{-T} | -BL_s^T]: its index list is
+// relative to T (= other) and reaches y_s in X as part_ldn(n_loc) + j.
 // Input column j is in[in_ref + j] (contiguous) or in[idx[j]] (IN_INDEXED).
 // Pushes of one phase never share a target row (supernodes are coloured per height).
 //
@@ -93,6 +95,9 @@ inline constexpr int tile_value_bytes(int nrows, int ncols, int groups) {
     return tile_iters(ncols, groups) * nrows * groups * 8;
 }
 inline constexpr int pad16i(int b) { return (b + 15) & ~15; }
+// Shared-memory stride of a part's vectors: X = T + part_ldn(n_loc) (64 zero slack entries
+// after the local rows), so one index list relative to T reaches both (merged backward tiles).
+inline constexpr int part_ldn(int n_loc) { return (n_loc + 64 + 1) & ~1; }
 
 // Phase table entry (kPhaseStride int32):
 //   [0 .. W-1]      first unit of each warp in this phase (index into the warp's unit list)

@@ -357,34 +357,30 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr, tmpl));
             }
         };
-        // backward chunk of rows q0.. of supernode s: piece A = L_ss^{-T} y_s (own = X,
-        // contiguous), piece B = -BL_s^T x_R (other = T, indexed); flush T[s rows] = acc
+        // backward chunk of rows q0.. of supernode s: one tile over [L_ss^{-T} y_s | -BL_s^T x_R]
+        // (ns - q0 + mI columns), indexed relative to T (= other in the backward sweep): y_s
+        // lives in X = T + part_ldn(n_loc), x_R in T; flush T[s rows] = acc
+        const std::int32_t xoff = part_ldn(n_loc);
         auto bwd = [&](index_t s, Chunks& out) {
             const Supernode& S = sn[s];
             const index_t ns = S.size(), mI = S.n_interior_rows;
             for (index_t q0 = 0; q0 < ns; q0 += kr) {
                 const int nq = static_cast<int>(std::min<index_t>(kr, ns - q0));
-                Chunk a = make_chunk(unit_bytes,
-                    nq, static_cast<int>(ns - q0),
-                    [&](int r, int j) { return j >= r ? linv(s, q0 + j, q0 + r) : zero; },
-                    false, [](int) { return 0; }, loc[S.col_begin + q0], loc[S.col_begin + q0], nq,
-                    static_cast<std::uint8_t>(kTaskDiag | kTaskInOwn), nullptr, tmpl);
-                if (mI > 0) {
-                    Chunk b = make_chunk(unit_bytes,
-                        nq, static_cast<int>(mI),
-                        [&](int r, int j) { return bl(s, j, q0 + r, true); }, true,
-                        [&](int j) {
-                            const std::int32_t l = loc[S.rows[j]];
-                            if (l < 0) throw std::logic_error("solve program: ancestor row not local");
-                            return l;
-                        },
-                        0, loc[S.col_begin + q0], nq, kTaskDiag, nullptr, tmpl);
-                    a.tiles.back().t.flags &= static_cast<std::uint8_t>(~kTaskLast);   // accumulation continues
-                    b.tiles.front().t.flags &= static_cast<std::uint8_t>(~kTaskFirst);
-                    for (Tile& t : b.tiles) a.tiles.push_back(std::move(t));
-                    a.cost += b.cost;
-                }
-                out.push_back(std::move(a));
+                const int na = static_cast<int>(ns - q0);
+                out.push_back(make_chunk(unit_bytes,
+                    nq, na + static_cast<int>(mI),
+                    [&](int r, int j) {
+                        if (j < na) return j >= r ? linv(s, q0 + j, q0 + r) : zero;
+                        return bl(s, j - na, q0 + r, true);
+                    },
+                    true,
+                    [&](int j) {
+                        if (j < na) return xoff + loc[S.col_begin + q0 + j];
+                        const std::int32_t l = loc[S.rows[j - na]];
+                        if (l < 0) throw std::logic_error("solve program: ancestor row not local");
+                        return l;
+                    },
+                    0, loc[S.col_begin + q0], nq, kTaskDiag, nullptr, tmpl));
             }
         };
         // t[R_d] -= L_{R_d,d} x_d restricted to the target rows accepted by `take`: rows in the

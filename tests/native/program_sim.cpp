@@ -75,12 +75,18 @@ void run_phase(const SolvePools& sp, PartState& st) {
                 if (task.flags & kTaskFirst)
                     for (double& a : acc[q]) a = 0.0;
                 const std::vector<double>& in = (task.flags & kTaskInOwn) ? own : other;
+                // T-relative indices at or past part_ldn(n_loc) address X (merged backward tiles)
+                const int ldn_p = part_ldn(pd.n_loc);
+                auto fetch = [&](int idx) -> double {
+                    if (&in == &st.T && idx >= ldn_p) return st.X.at(idx - ldn_p);
+                    return in.at(idx);
+                };
                 for (int r = 0; r < k; ++r) {
                     double s = 0.0;
                     for (int it = 0; it < iters; ++it)
                         for (int g = 0; g < G; ++g) {
                             const int j = it * G + g;
-                            const double v = (task.flags & kTaskInIndexed) ? in.at(ix[j]) : in.at(task.in_ref + j);
+                            const double v = (task.flags & kTaskInIndexed) ? fetch(ix[j]) : fetch(task.in_ref + j);
                             s += M[it * S + voff + r * G + g] * v;
                         }
                     acc[q][r] += s;
