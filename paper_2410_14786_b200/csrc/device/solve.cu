@@ -342,14 +342,19 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     long long t_start = stats ? clock64() : 0, t_wait = 0, t_bar = 0, t_refill = 0, t_tiles = 0, n_tiles = 0;
     long long tprof[4] = {0, 0, 0, 0};  // STATS: decode, loop, reduction, flush cycles
     double acc = 0.0;
-    int u = 0;  // next unit of this warp
+    int u = 0;                // this warp's current unit (ring slot u & (nsl - 1))
+    int done = 0;             // steps processed (the phase table holds cumulative step counts)
+    bool fresh = true;        // unit u not yet waited on
+    std::uint32_t cur = 0;    // offset (16 B) of the next step in unit u
+    const unsigned char* ubuf = my_ring;
+    int4 hdr4 = make_int4(0, 0, 0, 0), hdr4b = hdr4;
     bool split_done = !(MODE == 0 ? S.y_out : (MODE == 3 ? S.y_in : nullptr));
-    // phase kind and end unit, looked up a phase ahead
+    // phase kind and end step count, looked up a phase ahead
     int nx_kind = pkind.get(0, gtable + 2 * kSolveWarps, kPhaseStride);
     int nx_end = uend.get(0, gtable + kSolveWarps + warp, kPhaseStride);
     for (int ph = 0; ph < n_phases; ++ph) {
         const int kind = nx_kind;
-        const int u_end = nx_end;
+        const int s_end = nx_end;
         if (ph + 1 < n_phases) {
             nx_kind = pkind.get(ph + 1, gtable + 2 * kSolveWarps, kPhaseStride);
             nx_end = uend.get(ph + 1, gtable + kSolveWarps + warp, kPhaseStride);
@@ -385,53 +390,60 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         double* other = (kind & kPhaseBackward) ? T : X;
         const long long t_ph0 = stats ? clock64() : 0;
         const long long n_tiles0 = n_tiles, t_wait0 = t_wait, t_tiles0 = t_tiles, t_refill0 = t_refill;
-        for (; u < u_end; ++u) {
-            const int s = u & (nsl - 1);
-            if constexpr (stats) {
-                const long long t0 = clock64();
-                mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
-                t_wait += clock64() - t0;
-            } else {
-                mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+        // this phase's steps: the warp's step stream runs on across phases and units (a unit
+        // is waited on at its first step and refilled after its last)
+        while (done < s_end) {
+            if (fresh) {
+                const int s = u & (nsl - 1);
+                if constexpr (stats) {
+                    const long long t0 = clock64();
+                    mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+                    t_wait += clock64() - t0;
+                } else {
+                    mbar_wait(&my_bars[s], (u >> slot_shift) & 1);
+                }
+                ubuf = my_ring + s * unit;
+                cur = 0;
+                // a step's first 32 bytes: its header and, for a pair step, B's header (a single
+                // tile's first values otherwise; every tile holds at least 16 bytes of values)
+                hdr4 = *reinterpret_cast<const int4*>(ubuf);
+                hdr4b = *reinterpret_cast<const int4*>(ubuf + 16);
+                fresh = false;
             }
-            const unsigned char* ubuf = my_ring + s * unit;
-            std::uint32_t cur = 0;
             const long long t_tile0 = stats ? clock64() : 0;
-            // a step's first 32 bytes: its header and, for a pair step, B's header (a single
-            // tile's first values otherwise; every tile holds at least 16 bytes of values)
-            int4 hdr4 = *reinterpret_cast<const int4*>(ubuf);
-            int4 hdr4b = *reinterpret_cast<const int4*>(ubuf + 16);
-            while (true) {
-                if (stats) ++n_tiles;
-                const int4 h = hdr4, hb = hdr4b;
-                const bool pair = (h.w >> 16) & kTaskPair;
-                const unsigned char* tile = ubuf + (cur << 4) + (pair ? 32 : 16);
-                cur = static_cast<std::uint32_t>(h.x);
-                if (cur != kNoTask) {  // next headers early
-                    hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));
-                    hdr4b = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + 16);
-                }
-                if (pair) tile_task<true, STATS>(h, hb, tile, own, other, Q, acc, lane, tprof);
-                else tile_task<false, STATS>(h, h, tile, own, other, Q, acc, lane, tprof);
-                if ((kind & kPhaseChained) && ((h.w >> 16) & kTaskLast))
-                    __syncwarp();  // a later tile of this warp's job reads what was just written
-                if (cur == kNoTask) break;
+            if (stats) ++n_tiles;
+            const int4 h = hdr4, hb = hdr4b;
+            const bool pair = (h.w >> 16) & kTaskPair;
+            const unsigned char* tile = ubuf + (cur << 4) + (pair ? 32 : 16);
+            cur = static_cast<std::uint32_t>(h.x);
+            if (cur != kNoTask) {  // next headers early
+                hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));
+                hdr4b = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + 16);
             }
-            // slot consumed: refill it with the unit nsl ahead
-            const long long t_r0 = stats ? clock64() : 0;
-            if (stats) t_tiles += t_r0 - t_tile0;
-            if (u + nsl < nunits) {
-                // slot consumed: every lane's reads of it have completed (their values fed this
-                // unit's flushes), so the bulk copy may overwrite it; a generic-read ->
-                // async-write (WAR) reuse needs no proxy fence (measured: -1.5% per launch)
-                __syncwarp();
-                issue(u + nsl, nx_o16, nx_nb);
-                if (u + nsl + 1 < nunits) {
-                    nx_o16 = uoff.get(u + nsl + 1, units, 2);
-                    nx_nb = ubytes.get(u + nsl + 1, units + 1, 2);
+            if (pair) tile_task<true, STATS>(h, hb, tile, own, other, Q, acc, lane, tprof);
+            else tile_task<false, STATS>(h, h, tile, own, other, Q, acc, lane, tprof);
+            if ((kind & kPhaseChained) && ((h.w >> 16) & kTaskLast))
+                __syncwarp();  // a later tile of this warp's job reads what was just written
+            ++done;
+            if (stats) t_tiles += clock64() - t_tile0;
+            if (cur == kNoTask) {
+                // unit u consumed: refill its slot with the unit nsl ahead
+                const long long t_r0 = stats ? clock64() : 0;
+                if (u + nsl < nunits) {
+                    // every lane's reads of the slot have completed (their values fed this
+                    // unit's flushes), so the bulk copy may overwrite it; a generic-read ->
+                    // async-write (WAR) reuse needs no proxy fence (measured: -1.5% per launch)
+                    __syncwarp();
+                    issue(u + nsl, nx_o16, nx_nb);
+                    if (u + nsl + 1 < nunits) {
+                        nx_o16 = uoff.get(u + nsl + 1, units, 2);
+                        nx_nb = ubytes.get(u + nsl + 1, units + 1, 2);
+                    }
                 }
+                ++u;
+                fresh = true;
+                if (stats) t_refill += clock64() - t_r0;
             }
-            if (stats) t_refill += clock64() - t_r0;
         }
         if constexpr (stats) {
             const long long t0 = clock64();

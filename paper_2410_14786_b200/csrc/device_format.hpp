@@ -9,7 +9,7 @@
 // is processed redundantly by both after one exchange of partial sums through
 // distributed shared memory). Each part is
 //   * per warp, a sequence of "units" in HBM (<= unit_bytes each, whole tiles with their
-//     16-byte headers, one phase per unit); every warp prefetches its own units into a
+//     16-byte headers, filled across phases); every warp prefetches its own units into a
 //     private double-buffered shared-memory ring with cp.async.bulk (TMA bulk copies)
 //     and its own mbarriers, so streaming never waits on other warps and continues
 //     across the phase barriers;
@@ -100,8 +100,9 @@ inline constexpr int pad16i(int b) { return (b + 15) & ~15; }
 inline constexpr int part_ldn(int n_loc) { return (n_loc + 64 + 1) & ~1; }
 
 // Phase table entry (kPhaseStride int32):
-//   [0 .. W-1]      first unit of each warp in this phase (index into the warp's unit list)
-//   [W .. 2W-1]     end unit (exclusive)
+//   [0 .. W-1]      steps of each warp before this phase (cumulative)
+//   [W .. 2W-1]     steps of each warp up to the end of this phase (a warp's steps fill its
+//                   units in order across phases: a unit may hold several phases' steps)
 //   [2W]            kind (PhaseKind bits)
 //   [2W+1, 2W+2]    combine range of local rows [begin, end) (kPhaseCombine, runs after the phase)
 // Unit list of a part: for warp w, entries [warp_base[w], warp_base[w+1]) of int2

@@ -721,11 +721,18 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         std::vector<std::int32_t> table(phases.size() * kPhaseStride, 0);
         std::vector<std::vector<std::int32_t>> wunits(kSolveWarps);  // per warp: {offset16, bytes} pairs
         std::vector<std::int32_t> porder;                             // producer order (int4 entries)
-        auto ensure = [&](std::int64_t bytes) {
-            const std::size_t need = static_cast<std::size_t>(pd.stream + (bytes + 7) / 8);
-            if (pools.stream.size() < need) pools.stream.resize(need, 0.0);
-            if (tmpl && pools.srcmap.size() < need) pools.srcmap.resize(need, kSrcCopy);
+        // Each warp's steps fill its units in order ACROSS phases (a unit closes only when the
+        // next step does not fit): a warp with one small tile per phase refills once per ~4 KB,
+        // not once per phase. The phase table holds cumulative step counts per warp.
+        struct Unit {
+            std::vector<double> words;
+            std::vector<std::int32_t> src;  // template mode: srcmap codes of the words
+            std::int64_t used = 0, last_hdr = -1;
+            int opened = 0;                 // phase in which the unit was opened
         };
+        std::vector<Unit> open_unit(kSolveWarps);
+        std::vector<std::vector<Unit>> units_of(kSolveWarps);
+        std::vector<std::int32_t> steps_of(kSolveWarps, 0);
         for (std::size_t pi = 0; pi < phases.size(); ++pi) {
             Phase& ph = phases[pi];
             std::vector<std::int64_t> jcost(ph.jobs.size(), 0);
@@ -744,15 +751,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             std::int32_t* row = &table[pi * kPhaseStride];
             for (int w = 0; w < kSolveWarps; ++w) {
                 std::sort(per_warp[w].begin(), per_warp[w].end());
-                row[w] = static_cast<std::int32_t>(wunits[w].size() / 2);
-                std::int64_t ustart = -1, uused = 0, last_hdr = -1;
-                auto close_unit = [&]() {
-                    if (ustart < 0) return;
-                    wunits[w].push_back(static_cast<std::int32_t>(ustart / 16));
-                    wunits[w].push_back(static_cast<std::int32_t>(uused));
-                    pos = ustart + pad16(uused);
-                    ustart = -1;
-                };
+                row[w] = steps_of[w];
                 // this warp's chunks of the phase; outside chained phases (tiles independent),
                 // chunks of <= 16 rows are paired piece by piece into half-warp pair steps
                 std::vector<Chunk*> chs;
@@ -798,30 +797,38 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         q += 2;
                     }
                 }
-                auto place = [&](std::int64_t nb) {  // a step of nb bytes in the current unit
+                // a step of nb bytes in this warp's open unit: {bytes, srcmap codes of its words}
+                auto place = [&](std::int64_t nb) {
                     if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
-                    if (ustart >= 0 && uused + nb > unit_bytes) close_unit();
-                    if (ustart < 0) { ustart = pos; uused = 0; last_hdr = -1; }
-                    ensure(ustart + uused + nb);
-                    char* base = reinterpret_cast<char*>(pools.stream.data() + pd.stream);
-                    if (last_hdr >= 0)
-                        reinterpret_cast<TileTask*>(base + ustart + last_hdr)->next = static_cast<std::uint32_t>(uused / 16);
-                    last_hdr = uused;
-                    char* dst = base + ustart + uused;
-                    const std::size_t w0 = static_cast<std::size_t>(pd.stream + (ustart + uused) / 8);
-                    uused += nb;
-                    return std::make_pair(dst, w0);
+                    Unit& U = open_unit[w];
+                    if (U.used > 0 && U.used + nb > unit_bytes) {
+                        units_of[w].push_back(std::move(U));
+                        U = Unit{};
+                    }
+                    if (U.used == 0) U.opened = static_cast<int>(pi);
+                    const std::size_t need = static_cast<std::size_t>((U.used + nb + 7) / 8);
+                    if (U.words.size() < need) U.words.resize(need, 0.0);
+                    if (tmpl && U.src.size() < need) U.src.resize(need, kSrcCopy);
+                    char* base = reinterpret_cast<char*>(U.words.data());
+                    if (U.last_hdr >= 0)
+                        reinterpret_cast<TileTask*>(base + U.last_hdr)->next = static_cast<std::uint32_t>(U.used / 16);
+                    U.last_hdr = U.used;
+                    char* dst = base + U.used;
+                    std::int32_t* src = tmpl ? U.src.data() + U.used / 8 : nullptr;
+                    U.used += nb;
+                    ++steps_of[w];
+                    return std::make_pair(dst, src);
                 };
                 for (std::size_t i = 0; i < chs.size(); ++i) {
                     if (mate[i] >= 0 && mate[i] < static_cast<int>(i)) continue;  // emitted with its mate
                     if (mate[i] < 0) {
                         for (Tile& t : chs[i]->tiles) {
-                            auto [dst, w0] = place(16 + t.bytes());
+                            auto [dst, srcw] = place(16 + t.bytes());
                             TileTask hdr = t.t;
                             hdr.next = kNoTask;
                             std::memcpy(dst, &hdr, 16);
                             std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
-                            if (tmpl) std::copy(t.src.begin(), t.src.end(), pools.srcmap.begin() + static_cast<std::ptrdiff_t>(w0 + 2));
+                            if (tmpl) std::copy(t.src.begin(), t.src.end(), srcw + 2);
                             std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
                             if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
                             off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
@@ -835,7 +842,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     for (std::size_t p = 0; p < half[i].size(); ++p) {
                         const Tile& A = half[i][p];
                         const Tile& B = half[j][p];
-                        auto [dst, w0] = place(pair_bytes(A, B));
+                        auto [dst, srcw] = place(pair_bytes(A, B));
                         TileTask ha = A.t, hb = B.t;
                         ha.next = kNoTask;
                         hb.next = 0;
@@ -850,12 +857,12 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                             for (int l = 0; l < kga; ++l) {
                                 const std::size_t at = static_cast<std::size_t>(t) * S + l;
                                 V[at] = t < ia ? A.vals[static_cast<std::size_t>(t) * kga + l] : 0.0;
-                                if (tmpl) pools.srcmap[w0 + 4 + at] = t < ia ? A.src[static_cast<std::size_t>(t) * kga + l] : kSrcZero;
+                                if (tmpl) srcw[4 + at] = t < ia ? A.src[static_cast<std::size_t>(t) * kga + l] : kSrcZero;
                             }
                             for (int l = 0; l < kgb; ++l) {
                                 const std::size_t at = static_cast<std::size_t>(t) * S + kga + l;
                                 V[at] = t < ib ? B.vals[static_cast<std::size_t>(t) * kgb + l] : 0.0;
-                                if (tmpl) pools.srcmap[w0 + 4 + at] = t < ib ? B.src[static_cast<std::size_t>(t) * kgb + l] : kSrcZero;
+                                if (tmpl) srcw[4 + at] = t < ib ? B.src[static_cast<std::size_t>(t) * kgb + l] : kSrcZero;
                             }
                         }
                         std::int64_t off = 32 + pad16(static_cast<std::int64_t>(im) * S * 8);
@@ -871,31 +878,34 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         pools.n_tiles += 2;
                     }
                 }
-                close_unit();
-                row[kSolveWarps + w] = static_cast<std::int32_t>(wunits[w].size() / 2);
-            }
-            // producer order for this phase: warps' units interleaved by cumulative bytes
-            {
-                std::vector<std::int32_t> cur(kSolveWarps), endu(kSolveWarps);
-                std::vector<std::int64_t> done_bytes(kSolveWarps, 0);
-                for (int w = 0; w < kSolveWarps; ++w) { cur[w] = row[w]; endu[w] = row[kSolveWarps + w]; }
-                while (true) {
-                    int best = -1;
-                    for (int w = 0; w < kSolveWarps; ++w)
-                        if (cur[w] < endu[w] && (best < 0 || done_bytes[w] < done_bytes[best])) best = w;
-                    if (best < 0) break;
-                    const std::int32_t k = cur[best]++;
-                    const std::int32_t off16 = wunits[best][2 * k], nb = wunits[best][2 * k + 1];
-                    porder.push_back(off16);
-                    porder.push_back(nb);
-                    porder.push_back(best | (static_cast<std::int32_t>(pi) << 8));
-                    porder.push_back(k);
-                    done_bytes[best] += nb;
-                }
+                row[kSolveWarps + w] = steps_of[w];
             }
             row[2 * kSolveWarps] = ph.kind;
             row[2 * kSolveWarps + 1] = ph.comb_begin;
             row[2 * kSolveWarps + 2] = ph.comb_end;
+        }
+        // the units into the part's stream, warp after warp ({offset16, bytes} per unit; the
+        // producer-order table lists them with the phase that opened them)
+        for (int w = 0; w < kSolveWarps; ++w) {
+            if (open_unit[w].used > 0) units_of[w].push_back(std::move(open_unit[w]));
+            for (std::size_t k = 0; k < units_of[w].size(); ++k) {
+                const Unit& U = units_of[w][k];
+                const std::size_t w0 = static_cast<std::size_t>(pd.stream + pos / 8);
+                const std::size_t nw = static_cast<std::size_t>(pad16(U.used) / 8);
+                pools.stream.resize(w0 + nw, 0.0);
+                std::copy(U.words.begin(), U.words.begin() + static_cast<std::ptrdiff_t>(std::min(nw, U.words.size())),
+                          pools.stream.begin() + static_cast<std::ptrdiff_t>(w0));
+                if (tmpl) {
+                    pools.srcmap.resize(w0 + nw, kSrcCopy);
+                    std::copy(U.src.begin(), U.src.begin() + static_cast<std::ptrdiff_t>(std::min(nw, U.src.size())),
+                              pools.srcmap.begin() + static_cast<std::ptrdiff_t>(w0));
+                }
+                wunits[w].push_back(static_cast<std::int32_t>(pos / 16));
+                wunits[w].push_back(static_cast<std::int32_t>(U.used));
+                porder.insert(porder.end(), {static_cast<std::int32_t>(pos / 16), static_cast<std::int32_t>(U.used),
+                                             w | (U.opened << 8), static_cast<std::int32_t>(k)});
+                pos += pad16(U.used);
+            }
         }
         const std::int64_t total = pad16(pos);
         pools.stream.resize(static_cast<std::size_t>(pd.stream + total / 8), 0.0);

@@ -25,6 +25,10 @@ struct PartState {
     std::vector<double> T, X, Q;
     int ph = 0;
     bool split_done = false;
+    // per warp: step cursor (unit, 16-byte offset in it), steps done; the step stream runs on
+    // across phases (device_format.hpp)
+    int wu[kSolveWarps] = {}, wdone[kSolveWarps] = {};
+    std::uint32_t wcur[kSolveWarps] = {};
 };
 
 void run_phase(const SolvePools& sp, PartState& st) {
@@ -36,18 +40,22 @@ void run_phase(const SolvePools& sp, PartState& st) {
     const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
     for (int w = 0; w < kSolveWarps; ++w) {
         double acc[2][32] = {{0}};  // per sub-tile (a pair step's halves), per row
-        const int ua = st.ph == 0 ? 0 : sp.phases[pd.phases + (st.ph - 1) * kPhaseStride + kSolveWarps + w];
-        const int ub = row[kSolveWarps + w];
-        for (int u = ua; u < ub; ++u)
-        for (std::uint32_t cur = 0; cur != kNoTask;) {
-            const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + u)];
+        const int s_end = row[kSolveWarps + w];
+        while (st.wdone[w] < s_end) {
+            const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + st.wu[w])];
             const char* ubase = base + std::int64_t(ue[0]) * 16;
+            std::uint32_t& cur = st.wcur[w];
             TileTask hd[2];
             std::memcpy(&hd[0], ubase + std::int64_t(cur) * 16, 16);
             const bool pair = hd[0].flags & kTaskPair;
             if (pair) std::memcpy(&hd[1], ubase + std::int64_t(cur) * 16 + 16, 16);
             const char* tb = ubase + std::int64_t(cur) * 16 + (pair ? 32 : 16);
             cur = hd[0].next;
+            ++st.wdone[w];
+            if (cur == kNoTask) {  // unit consumed
+                ++st.wu[w];
+                cur = 0;
+            }
             const int nsub = pair ? 2 : 1;
             // step geometry (device_format.hpp): value stride S, iterations, list offsets
             int S = 0, im = 0;
@@ -106,67 +114,6 @@ void run_phase(const SolvePools& sp, PartState& st) {
 }
 
 }  // namespace
-
-// Task-shape statistics of the program (development aid).
-extern "C" int bddc_sim_program_stats(int cells, int k, int parts, int leaf_size) {
-    PoissonProblem pp = assemble_poisson(cells, cells, k, k);
-    ProblemData pb;
-    pb.constraints = build_constraints(pp.decomposition);
-    pb.decomposition = std::move(pp.decomposition);
-    pb.global_matrix = std::move(pp.global_matrix);
-    pb.local_matrices = std::move(pp.local_matrices);
-    pb.coords = std::move(pp.coords);
-    FactorOptions fo;
-    fo.leaf_size = leaf_size;
-    const BddcSetup setup = bddc_setup(pb.local_matrices, pb.decomposition, pb.constraints, pb.coords.data(), 8, fo);
-    const DeviceImage img = build_device_image(pb.decomposition, pb.constraints, pb.local_matrices,
-                                               pb.global_matrix, setup, parts);
-    const SolvePools& sp = img.solve;
-    const PartDesc& pd = sp.parts[parts * (pb.decomposition.n_subdomains / 2)];  // an interior subdomain
-    long cnt[4] = {0}, elems[4] = {0}, iters[4] = {0}, flat[4] = {0};
-    long rows_hist[33] = {0};
-    long critical = 0;
-    for (int ph = 0; ph < pd.n_phases; ++ph) {
-        const std::int32_t* row = &sp.phases[pd.phases + ph * kPhaseStride];
-        const bool bwd = row[2 * kSolveWarps] & kPhaseBackward;
-        const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
-        long crit = 0;
-        for (int w = 0; w < kSolveWarps; ++w) {
-          long wl = 0;
-          const int ua = ph == 0 ? 0 : sp.phases[pd.phases + (ph - 1) * kPhaseStride + kSolveWarps + w];
-          const int ub = row[kSolveWarps + w];
-          for (int u = ua; u < ub; ++u)
-          for (std::uint32_t cur = 0; cur != kNoTask;) {
-            const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + u)];
-            TileTask tk;
-            std::memcpy(&tk, base + std::int64_t(ue[0]) * 16 + std::int64_t(cur) * 16, 16);
-            cur = tk.next;
-            wl += tk.iters + 12;
-            const int kind = (bwd ? 2 : 0) + ((tk.flags & kTaskDiag) ? 1 : 0);
-            cnt[kind]++;
-            elems[kind] += tk.nrows * (1 << tk.groups) * tk.iters;
-            iters[kind] += tk.iters;
-            const int g = 32 / tk.nrows;
-            flat[kind] += tk.nrows * (1 << tk.groups) * tk.iters; (void)g;
-            rows_hist[tk.nrows]++;
-          }
-          crit = std::max(crit, wl);
-        }
-        critical += crit;
-    }
-    std::printf("critical path (sum over phases of the busiest warp's iterations+overhead): %ld\n", critical);
-    const char* names[4] = {"fwd-A", "fwd-B", "bwd-A", "bwd-B"};
-    std::printf("part stream %ld bytes, phases %d, tasks %ld\n", (long)pd.stream_bytes, pd.n_phases,
-                cnt[0] + cnt[1] + cnt[2] + cnt[3]);
-    for (int i = 0; i < 4; ++i)
-        std::printf("%s: tasks %ld elems %ld iters %ld lane-slots %ld lane-eff %.2f\n", names[i],
-                    cnt[i], elems[i], iters[i], flat[i], flat[i] ? double(elems[i]) / (32.0 * iters[i]) : 0.0);
-    std::printf("rows histogram:");
-    for (int r = 1; r <= 32; ++r)
-        if (rows_hist[r]) std::printf(" %d:%ld", r, rows_hist[r]);
-    std::printf("\n");
-    return 0;
-}
 
 // harm: 0 full program, 1 harmonic program, 2 head program (y0 -> ybuf, u0 -> out),
 // 3 harmonic program with y_in = ybuf (out = L^-T (y0 - L^-1 in)); the split hooks follow
