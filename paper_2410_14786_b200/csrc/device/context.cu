@@ -51,6 +51,40 @@ struct DBuf {
     }
 };
 
+// Setup scratch from the device's stream-ordered memory pool (cudaMallocAsync / cudaFreeAsync on
+// the setup stream): the pool keeps the memory (release threshold raised once per device), so a
+// later construction reuses it without a synchronising cudaMalloc / cudaFree of ~GBs.
+inline void keep_pool_memory(int device) {
+    static std::once_flag once[64];
+    std::call_once(once[device & 63], [device] {
+        cudaMemPool_t pool = nullptr;
+        BDDC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        std::uint64_t keep = ~std::uint64_t(0);
+        BDDC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    });
+}
+
+template <typename T>
+struct PBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    cudaStream_t s;
+    explicit PBuf(cudaStream_t stream) : s(stream) {}
+    PBuf(const PBuf&) = delete;
+    PBuf& operator=(const PBuf&) = delete;
+    ~PBuf() { if (p) cudaFreeAsync(p, s); }
+    void alloc(std::size_t count) {
+        if (p) BDDC_CUDA(cudaFreeAsync(p, s));
+        p = nullptr;
+        n = count;
+        if (count) BDDC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+    }
+    void upload(const std::vector<T>& v) {
+        alloc(std::max<std::size_t>(v.size(), 1));
+        if (!v.empty()) BDDC_CUDA(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+    }
+};
+
 struct Event {
     cudaEvent_t e = nullptr;
     Event() { BDDC_CUDA(cudaEventCreate(&e)); }
@@ -682,6 +716,7 @@ struct GpuContext::Impl {
         const auto t0 = std::chrono::steady_clock::now();
         SetupTimer tm;
         cudaStream_t s = stream;
+        keep_pool_memory(device);
         const Decomposition& d = pb.decomposition;
         const index_t nsub = d.n_subdomains;
         SolveProgram* pools[3] = {&prog, &harm, &head};
@@ -691,8 +726,8 @@ struct GpuContext::Impl {
 
         // ---- templates (word + source code per stream word), straight into one device buffer
         std::vector<std::array<std::int64_t, 3>> toff(ncls);
-        DBuf<double> tword;
-        DBuf<std::int32_t> tcode;
+        PBuf<double> tword(s);
+        PBuf<std::int32_t> tcode(s);
         {
             std::int64_t total = 0;
             for (std::size_t k = 0; k < ncls; ++k)
@@ -735,9 +770,9 @@ struct GpuContext::Impl {
             of[k].d = bd.size();
             bd.insert(bd.end(), C.c_val.begin(), C.c_val.end());
         }
-        DBuf<std::int32_t> pi;
-        DBuf<std::int64_t> pl;
-        DBuf<double> pdv;
+        PBuf<std::int32_t> pi(s);
+        PBuf<std::int64_t> pl(s);
+        PBuf<double> pdv(s);
         pi.upload(bi);
         pl.upload(bl);
         pdv.upload(bd);
@@ -774,8 +809,8 @@ struct GpuContext::Impl {
                     tot[t] = std::max(tot[t], need[k][t] + 1);
                 }
             }
-        DBuf<double> aval, fronts, Sb, Db, Mb, aci_dev;
-        DBuf<int> piv, status;
+        PBuf<double> aval(s), fronts(s), Sb(s), Db(s), Mb(s), aci_dev(s);
+        PBuf<int> piv(s), status(s);
         aval.alloc(tot[0]);
         fronts.alloc(tot[1]);
         Sb.alloc(tot[2]);
@@ -826,15 +861,16 @@ struct GpuContext::Impl {
             }
         }
         job0.back() = jobs.size();
-        DBuf<FillJob> jobs_dev;
-        DBuf<std::int64_t> outs_dev;
+        PBuf<FillJob> jobs_dev(s);
+        PBuf<std::int64_t> outs_dev(s);
         jobs_dev.upload(jobs);
         outs_dev.upload(outs);
         tm.mark("  templates, plans, scratch");
 
         double acc_t[4] = {};  // diagnostics: factor, schur + linv, fill, saddle
+        static const bool lap_on = std::getenv("BDDC_SETUP_TIMES") && std::atoi(std::getenv("BDDC_SETUP_TIMES")) >= 2;
         auto lap = [&](int k, std::chrono::steady_clock::time_point& t) {
-            if (!tm.on) return;
+            if (!lap_on) return;  // BDDC_SETUP_TIMES=2: per-kernel-kind laps (serialise the classes)
             BDDC_CUDA(cudaDeviceSynchronize());  // (diagnostics: serialises the class streams)
             const auto now = std::chrono::steady_clock::now();
             acc_t[k] += std::chrono::duration<double, std::milli>(now - t).count();
@@ -931,7 +967,7 @@ struct GpuContext::Impl {
                                          ": singular saddle system (zero pivot at step " + std::to_string(sb[3]) + ")");
             }
         }
-        if (tm.on)
+        if (lap_on)
             std::fprintf(stderr, "[setup]     factor %.1f, schur+linv %.1f, fill %.1f, saddle %.1f ms\n", acc_t[0],
                          acc_t[1], acc_t[2], acc_t[3]);
         tm.mark("  classes (factor, fill, saddle)");

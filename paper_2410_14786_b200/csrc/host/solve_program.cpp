@@ -20,12 +20,13 @@ constexpr double kPrunedJobsPerWarp = 0.0;
 struct Tile {
     TileTask t{};
     int jn = 0;                        // columns of this piece
-    std::vector<double> vals;
+    std::vector<double> vals;          // numeric mode (empty in template mode: the values are src codes)
     std::vector<std::int32_t> src;     // template mode: value sources (SolvePools::srcmap codes)
     std::vector<std::int32_t> idx;     // input index list (IN_INDEXED)
     std::vector<std::int32_t> outidx;  // output rows (PUSH, last piece)
+    std::int64_t nvals() const { return static_cast<std::int64_t>(vals.empty() ? src.size() : vals.size()); }
     std::int64_t bytes() const {
-        return pad16(static_cast<std::int64_t>(vals.size()) * 8) + pad16(static_cast<std::int64_t>(idx.size()) * 4) +
+        return pad16(nvals() * 8) + pad16(static_cast<std::int64_t>(idx.size()) * 4) +
                pad16(static_cast<std::int64_t>(outidx.size()) * 4);
     }
 };
@@ -75,8 +76,9 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
         T.t.nvalid = static_cast<std::uint8_t>(nvalid);
         T.t.flags = flags | (indexed ? kTaskInIndexed : 0) | (j0 == 0 ? kTaskFirst : 0) |
                     (j0 + jn >= ncols ? kTaskLast : 0);
-        T.vals.assign(static_cast<std::size_t>(iters) * k * G, 0.0);
-        if (tmpl) T.src.assign(T.vals.size(), kSrcZero);
+        const std::size_t nv = static_cast<std::size_t>(iters) * k * G;
+        if (tmpl) T.src.assign(nv, kSrcZero);
+        else T.vals.assign(nv, 0.0);
         for (int t = 0; t < iters; ++t)
             for (int g = 0; g < G; ++g) {
                 const int j = t * G + g;
@@ -84,7 +86,7 @@ Chunk make_chunk(int unit_bytes, int k, int ncols, Val val, bool indexed, InIdx 
                 for (int r = 0; r < k; ++r) {
                     const TileValue tv = val(r, j0 + j);
                     const std::size_t at = static_cast<std::size_t>(t) * k * G + r * G + g;
-                    T.vals[at] = tv.v;
+                    if (!tmpl) T.vals[at] = tv.v;
                     if (tmpl) T.src[at] = tv.src;
                 }
             }
@@ -112,13 +114,14 @@ Tile regroup(const Tile& T, int G2) {
     const int it2 = tile_iters(T.jn, G2);
     R.t.iters = static_cast<std::uint16_t>(it2);
     R.t.groups = static_cast<std::uint8_t>(__builtin_ctz(static_cast<unsigned>(G2)));
-    R.vals.assign(static_cast<std::size_t>(it2) * k * G2, 0.0);
-    if (!T.src.empty()) R.src.assign(R.vals.size(), kSrcZero);
+    const std::size_t nv = static_cast<std::size_t>(it2) * k * G2;
+    if (!T.src.empty()) R.src.assign(nv, kSrcZero);
+    if (!T.vals.empty()) R.vals.assign(nv, 0.0);
     for (int j = 0; j < T.jn; ++j)
         for (int r = 0; r < k; ++r) {
             const std::size_t o = static_cast<std::size_t>(j / G) * kG + r * G + j % G;
             const std::size_t n = static_cast<std::size_t>(j / G2) * k * G2 + r * G2 + j % G2;
-            R.vals[n] = T.vals[o];
+            if (!T.vals.empty()) R.vals[n] = T.vals[o];
             if (!T.src.empty()) R.src[n] = T.src[o];
         }
     if (!T.idx.empty()) {
@@ -136,12 +139,26 @@ int half_groups(int k) {
 
 // Bytes of a pair step (device_format.hpp): two headers, the interleaved values (iteration
 // stride kG_A + kG_B, max(iters) iterations), the two index lists, the two output-row lists.
-std::int64_t pair_bytes(const Tile& A, const Tile& B) {
+// A tile's shape at G2 column groups (header, index and output-list lengths) without its values:
+// the pairing decision is taken on shapes, only paired tiles are re-laid out (regroup).
+struct Shape {
+    TileTask t;
+    std::int64_t nidx, nout;
+};
+Shape shape_of(const Tile& T, int G2) {
+    Shape h{T.t, 0, static_cast<std::int64_t>(T.outidx.size())};
+    const int it2 = tile_iters(T.jn, G2);
+    h.t.iters = static_cast<std::uint16_t>(it2);
+    h.t.groups = static_cast<std::uint8_t>(__builtin_ctz(static_cast<unsigned>(G2)));
+    h.nidx = T.idx.empty() ? 0 : static_cast<std::int64_t>(it2) * G2;
+    return h;
+}
+
+std::int64_t pair_bytes(const Shape& A, const Shape& B) {
     const int ia = A.t.iters, ib = B.t.iters;
     const std::int64_t S = static_cast<std::int64_t>(A.t.nrows << A.t.groups) + (B.t.nrows << B.t.groups);
-    return 32 + pad16(std::max(ia, ib) * S * 8) + pad16(static_cast<std::int64_t>(A.idx.size()) * 4) +
-           pad16(static_cast<std::int64_t>(B.idx.size()) * 4) + pad16(static_cast<std::int64_t>(A.outidx.size()) * 4) +
-           pad16(static_cast<std::int64_t>(B.outidx.size()) * 4);
+    return 32 + pad16(std::max(ia, ib) * S * 8) + pad16(A.nidx * 4) + pad16(B.nidx * 4) + pad16(A.nout * 4) +
+           pad16(B.nout * 4);
 }
 
 }  // namespace
@@ -762,14 +779,14 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         solo.push_back(ph.jobs[c].size() == 1);
                     }
                 std::vector<int> mate(chs.size(), -1);
-                std::vector<std::vector<Tile>> half(chs.size());
+                std::vector<std::vector<Shape>> half(chs.size());
                 if (pair_tiles) {
                     std::vector<int> cand;
                     for (std::size_t i = 0; i < chs.size(); ++i) {
                         bool ok = !chs[i]->tiles.empty() && (solo[i] || !(ph.kind & kPhaseChained));
                         for (const Tile& t : chs[i]->tiles) ok = ok && t.t.nrows <= 16;
                         if (!ok) continue;
-                        for (const Tile& t : chs[i]->tiles) half[i].push_back(regroup(t, half_groups(t.t.nrows)));
+                        for (const Tile& t : chs[i]->tiles) half[i].push_back(shape_of(t, half_groups(t.t.nrows)));
                         cand.push_back(static_cast<int>(i));
                     }
                     constexpr std::uint8_t kShape = kTaskInIndexed | kTaskFirst | kTaskLast;
@@ -829,20 +846,20 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                             std::memcpy(dst, &hdr, 16);
                             std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
                             if (tmpl) std::copy(t.src.begin(), t.src.end(), srcw + 2);
-                            std::int64_t off = 16 + pad16(static_cast<std::int64_t>(t.vals.size()) * 8);
+                            std::int64_t off = 16 + pad16(t.nvals() * 8);
                             if (!t.idx.empty()) std::memcpy(dst + off, t.idx.data(), t.idx.size() * 4);
                             off += pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
                             if (!t.outidx.empty()) std::memcpy(dst + off, t.outidx.data(), t.outidx.size() * 4);
-                            pools.tile_values += static_cast<std::int64_t>(t.vals.size());
+                            pools.tile_values += t.nvals();
                             ++pools.n_tiles;
                         }
                         continue;
                     }
                     const std::size_t j = static_cast<std::size_t>(mate[i]);
                     for (std::size_t p = 0; p < half[i].size(); ++p) {
-                        const Tile& A = half[i][p];
-                        const Tile& B = half[j][p];
-                        auto [dst, srcw] = place(pair_bytes(A, B));
+                        const Tile A = regroup(chs[i]->tiles[p], half_groups(chs[i]->tiles[p].t.nrows));
+                        const Tile B = regroup(chs[j]->tiles[p], half_groups(chs[j]->tiles[p].t.nrows));
+                        auto [dst, srcw] = place(pair_bytes(half[i][p], half[j][p]));
                         TileTask ha = A.t, hb = B.t;
                         ha.next = kNoTask;
                         hb.next = 0;
@@ -856,12 +873,12 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         for (int t = 0; t < im; ++t) {
                             for (int l = 0; l < kga; ++l) {
                                 const std::size_t at = static_cast<std::size_t>(t) * S + l;
-                                V[at] = t < ia ? A.vals[static_cast<std::size_t>(t) * kga + l] : 0.0;
+                                if (!tmpl) V[at] = t < ia ? A.vals[static_cast<std::size_t>(t) * kga + l] : 0.0;
                                 if (tmpl) srcw[4 + at] = t < ia ? A.src[static_cast<std::size_t>(t) * kga + l] : kSrcZero;
                             }
                             for (int l = 0; l < kgb; ++l) {
                                 const std::size_t at = static_cast<std::size_t>(t) * S + kga + l;
-                                V[at] = t < ib ? B.vals[static_cast<std::size_t>(t) * kgb + l] : 0.0;
+                                if (!tmpl) V[at] = t < ib ? B.vals[static_cast<std::size_t>(t) * kgb + l] : 0.0;
                                 if (tmpl) srcw[4 + at] = t < ib ? B.src[static_cast<std::size_t>(t) * kgb + l] : kSrcZero;
                             }
                         }
