@@ -73,54 +73,32 @@ struct RegTable {
 
 // One tile GEMV (device_format.hpp): k <= 32 rows, G = 2^lg column groups, lane = r*G + g
 // owns row r and columns j = t*G + g; values are stored iteration-major, value(r, t*G + g)
-// at [t*S + r*G + g] (S = k*G), so every iteration is one contiguous, conflict-free
-// shared-memory read per lane. Written for a short issue path (most tiles hold ~5 values per
-// lane): no divergent guard around the loop (lanes beyond k*G read in-bounds slack and are
-// masked before the reduction), a 4-way body with predicated tails, pointer increments only.
-// The G partial sums of a row are reduced with an xor butterfly inside the row's lane group;
-// the row total accumulates into `acc` and is flushed by the group's first lane.
-// PAIR: a pair step (two half-warp tiles, device_format.hpp): lanes 16-31 run tile B with
-// its own header; the values interleave with stride S = kG_A + kG_B; each half loops over its
-// own iteration count.
-template <bool PAIR, bool PROF = false>
-__device__ __forceinline__ void tile_task(const int4 hA, const int4 hB, const unsigned char* tile, double* own,
-                                          double* other, double* Q, double& acc, int lane,
-                                          long long* tp = nullptr) {
+// at [t*S + voff + r*G + g], so every iteration is one contiguous, conflict-free shared-memory
+// read per lane. `h` is the lane's own step sub-header (a pair step: lanes 16-31 run tile B,
+// sl = lane - 16); it carries every field the lane needs, so decoding is a handful of bit
+// extractions. Written for a short issue path (most tiles hold ~5 values per lane): no
+// divergent guard around the loop (lanes beyond k*G read in-bounds slack and are masked
+// before the reduction), a 4-way body with predicated tails, pointer increments only. The
+// G partial sums of a row are reduced with an xor butterfly inside the row's lane group
+// (to the step's largest G, uniform over the warp); the row total accumulates into `acc` and
+// is flushed by the group's first lane.
+template <bool PROF = false>
+__device__ __forceinline__ void tile_task(const int4 h, const unsigned char* tile, int sl, double* own, double* other,
+                                          double* Q, double& acc, long long* tp = nullptr) {
     long long tq = PROF ? clock64() : 0;
 #define TILE_T(i) do { if constexpr (PROF) { const long long t_ = clock64(); tp[i] += t_ - tq; tq = t_; } } while (0)
-    const bool hi = PAIR && lane >= 16;
-    const int4 h = hi ? hB : hA;
-    const int sl = PAIR ? (lane & 15) : lane;
-    const int k = h.w & 0xff, lg = (h.w >> 8) & 0xff, flags = (h.w >> 16) & 0xff;
-    const int iters = static_cast<unsigned>(h.z) >> 16;
+    const unsigned w0 = h.x, w2 = h.z, w3 = h.w;
+    const int S = (w0 >> 11) & 63, gmax_lg = (w0 >> 25) & 7;
+    const int k = w2 & 63, lg = (w2 >> 6) & 7, flags = (w2 >> 9) & 255, iters = (w2 >> 17) & 511;
     const int G = 1 << lg, kG = k << lg;
     const int g = sl & (G - 1), r = sl >> lg;
     const double* in = (flags & kTaskInOwn) ? own : other;
-    int S = kG, itmax = iters, Gmax = G, ioff = 0, ibytes = 0, ooff = 0;
-    const bool indexed = flags & kTaskInIndexed;
-    if constexpr (PAIR) {
-        const int kA = hA.w & 0xff, lgA = (hA.w >> 8) & 0xff, itA = static_cast<unsigned>(hA.z) >> 16;
-        const int lgB = (hB.w >> 8) & 0xff, itB = static_cast<unsigned>(hB.z) >> 16;
-        const int kGA = kA << lgA;
-        S = kGA + ((hB.w & 0xff) << lgB);
-        itmax = max(itA, itB);
-        Gmax = 1 << max(lgA, lgB);
-        const int ia = indexed ? ((itA << lgA) * 4 + 15) & ~15 : 0;
-        ioff = hi ? ia : 0;
-        ibytes = indexed ? ia + (((itB << lgB) * 4 + 15) & ~15) : 0;
-        // B's output rows follow A's (A has a list when it is a push)
-        ooff = hi && (((hA.w >> 16) & (kTaskPush | kTaskLast)) == (kTaskPush | kTaskLast)) ? ((kA * 4 + 15) & ~15) : 0;
-    } else {
-        ibytes = indexed ? ((iters * G * 4 + 15) & ~15) : 0;
-    }
-    const int voff = PAIR && hi ? S - kG : 0;  // B's values start kG_A doubles into an iteration
-    const double* M = reinterpret_cast<const double*>(tile) + voff + sl;
-    const int vbytes = (itmax * S * 8 + 15) & ~15;
+    const double* M = reinterpret_cast<const double*>(tile) + (w3 & 31) + sl;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int full = iters & ~3, rem = iters & 3;
     TILE_T(0);
-    if (indexed) {
-        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + vbytes + ioff) + g;
+    if (flags & kTaskInIndexed) {
+        const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + (((w3 >> 5) & 255) << 4)) + g;
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], in[ix[0]], s0);
@@ -134,7 +112,7 @@ __device__ __forceinline__ void tile_task(const int4 hA, const int4 hB, const un
         if (rem > 1) s1 = fma(M[S], in[ix[G]], s1);
         if (rem > 2) s2 = fma(M[2 * S], in[ix[2 * G]], s2);
     } else {
-        const double* v = in + h.y + g;
+        const double* v = in + (h.y & 0xffff) + g;
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], v[0], s0);
@@ -148,28 +126,27 @@ __device__ __forceinline__ void tile_task(const int4 hA, const int4 hB, const un
         if (rem > 1) s1 = fma(M[S], v[G], s1);
         if (rem > 2) s2 = fma(M[2 * S], v[2 * G], s2);
     }
+    TILE_T(1);
     // per-lane partial sums accumulate over the pieces of a chunk (same k, hence same G and
     // lane -> row map); the row's lane group is reduced once, at its last piece (a pair's two
     // halves are in lockstep: both or neither are last)
-    TILE_T(1);
     acc = ((flags & kTaskFirst) ? 0.0 : acc) + (sl < kG ? (s0 + s1) + (s2 + s3) : 0.0);
     if (!(flags & kTaskLast)) return;
 #pragma unroll 1
-    for (int off = Gmax >> 1; off > 0; off >>= 1) {
+    for (int off = (1 << gmax_lg) >> 1; off > 0; off >>= 1) {
         const double o = __shfl_xor_sync(0xffffffffu, acc, off);
-        if (!PAIR || off < G) acc += o;
+        if (off < G) acc += o;
     }
     TILE_T(2);
     if (g == 0) {
-        const int nvalid = static_cast<unsigned>(h.w) >> 24;
         if (flags & kTaskPush) {
             if (r < k) {
-                const int o = reinterpret_cast<const std::int32_t*>(tile + vbytes + ibytes + ooff)[r];
+                const int o = reinterpret_cast<const std::int32_t*>(tile + (((w3 >> 13) & 255) << 4))[r];
                 if (flags & kTaskPartial) Q[o] += acc;
                 else own[o] -= acc;
             }
-        } else if (r < nvalid) {
-            const int out = (h.z & 0xffff) + r;
+        } else if (r < static_cast<int>(w2 >> 26)) {
+            const int out = (h.y >> 16) + r;
             if (flags & kTaskDiag) other[out] = acc;
             else own[out] -= acc;
         }
@@ -347,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     bool fresh = true;        // unit u not yet waited on
     std::uint32_t cur = 0;    // offset (16 B) of the next step in unit u
     const unsigned char* ubuf = my_ring;
-    int4 hdr4 = make_int4(0, 0, 0, 0), hdr4b = hdr4;
+    int4 hdr4 = make_int4(0, 0, 0, 0);  // the lane's sub-header of the next step
     bool split_done = !(MODE == 0 ? S.y_out : (MODE == 3 ? S.y_in : nullptr));
     // phase kind and end step count, looked up a phase ahead
     int nx_kind = pkind.get(0, gtable + 2 * kSolveWarps, kPhaseStride);
@@ -404,29 +381,28 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 }
                 ubuf = my_ring + s * unit;
                 cur = 0;
-                // a step's first 32 bytes: its header and, for a pair step, B's header (a single
-                // tile's first values otherwise; every tile holds at least 16 bytes of values)
-                hdr4 = *reinterpret_cast<const int4*>(ubuf);
-                hdr4b = *reinterpret_cast<const int4*>(ubuf + 16);
+                // the unit's first step: every lane reads sub-header A (for a single tile, the
+                // 16 bytes after it are values); lanes 16-31 of a pair step take B's
+                const int4 ha = *reinterpret_cast<const int4*>(ubuf);
+                const int4 hb = *reinterpret_cast<const int4*>(ubuf + 16);
+                hdr4 = ((ha.x >> 10) & 1) && lane >= 16 ? hb : ha;
                 fresh = false;
             }
             const long long t_tile0 = stats ? clock64() : 0;
             if (stats) ++n_tiles;
-            const int4 h = hdr4, hb = hdr4b;
-            const bool pair = (h.w >> 16) & kTaskPair;
+            const int4 h = hdr4;
+            const unsigned w0 = h.x;
+            const bool pair = (w0 >> 10) & 1;
             const unsigned char* tile = ubuf + (cur << 4) + (pair ? 32 : 16);
-            cur = static_cast<std::uint32_t>(h.x);
-            if (cur != kNoTask) {  // next headers early
-                hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4));
-                hdr4b = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + 16);
-            }
-            if (pair) tile_task<true, STATS>(h, hb, tile, own, other, Q, acc, lane, tprof);
-            else tile_task<false, STATS>(h, h, tile, own, other, Q, acc, lane, tprof);
-            if ((kind & kPhaseChained) && ((h.w >> 16) & kTaskLast))
+            cur = w0 & 0x1ff;
+            if (cur != kNoStep)  // the lane's sub-header of the next step, early
+                hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + (((w0 >> 9) & 1) && lane >= 16 ? 16 : 0));
+            tile_task<STATS>(h, tile, pair ? (lane & 15) : lane, own, other, Q, acc, tprof);
+            if ((kind & kPhaseChained) && ((h.z >> 9) & kTaskLast))
                 __syncwarp();  // a later tile of this warp's job reads what was just written
             ++done;
             if (stats) t_tiles += clock64() - t_tile0;
-            if (cur == kNoTask) {
+            if (cur == kNoStep) {
                 // unit u consumed: refill its slot with the unit nsl ahead
                 const long long t_r0 = stats ? clock64() : 0;
                 if (u + nsl < nunits) {

@@ -37,8 +37,8 @@
 // Pair steps: two independent tiles A and B with k <= 16 rows each run side by side, A on
 // lanes 0-15 and B on lanes 16-31 (lane - 16 = r*G_B + g), each with its own G (k*G <= 16),
 // iteration count, input, flags and outputs, so a warp pays one header decode, one loop and
-// one butterfly for both. Layout: header A (kTaskPair set; A.next links the unit), header B,
-// values iteration-major with stride S = k_A*G_A + k_B*G_B (A's lanes then B's), for
+// one butterfly for both. Layout: sub-header A, sub-header B (step header below), values
+// iteration-major with stride S = k_A*G_A + k_B*G_B (A's lanes then B's), for
 // max(iters_A, iters_B) iterations (the shorter tile's slots are zero and never read), then
 // A's and B's index lists (IN_INDEXED: both or neither; 16-byte aligned each), then A's and
 // B's output-row lists (those that have one). Chunks of several pieces are paired piece by
@@ -74,11 +74,10 @@ enum PhaseKind : std::int32_t {
     kPhaseChained = 4,  // a warp's later tiles read rows its earlier tiles wrote (subtree jobs)
 };
 
-// Each tile in a unit is preceded by its 16-byte header; `next` links the tiles of one
-// unit (offset in 16-byte units from the unit start), kNoTask ends the unit.
-constexpr std::uint32_t kNoTask = 0xffffffffu;
+// Builder-side description of one tile (host/solve_program.cpp); on the stream a tile is
+// described by a packed step sub-header (below).
 struct TileTask {
-    std::uint32_t next;     // offset (16-byte units, from the unit start) of the next tile, or kNoTask
+    std::uint32_t next;     // (builder: unused)
     std::uint32_t in_ref;   // first input local index (contiguous inputs)
     std::uint16_t out_base; // output chunk start (DIAG / PULL)
     std::uint16_t iters;    // ceil(columns / groups): inner-loop trip count
@@ -88,6 +87,53 @@ struct TileTask {
     std::uint8_t nvalid;    // rows written on flush
 };
 static_assert(sizeof(TileTask) == 16, "TileTask must stay 16 bytes");
+
+// On-stream step header: one 16-byte sub-header per tile of the step (a single tile: one; a
+// pair step: A, read by lanes 0-15, then B, read by lanes 16-31). Each sub-header holds
+// everything its lanes need (the step-wide fields duplicated), and carries the next step's
+// offset and pair flag, so a lane prefetches and decodes only its own 16 bytes:
+//   w0: [0:9) next step (16-byte units from the unit start; kNoStep ends the unit), [9] next
+//       step is a pair, [10] this step is a pair, [11:17) value stride S (values per
+//       iteration: k*G, or k_A*G_A + k_B*G_B), [17:25) value-section bytes / 16, [25:28) log2
+//       of the step's largest G
+//   w1: [0:16) in_ref, [16:32) out_base
+//   w2: [0:6) k, [6:9) log2 G, [9:17) flags, [17:26) iterations, [26:32) nvalid
+//   w3: [0:5) the tile's first value lane within S, [5:13) its index list offset / 16 and
+//       [13:21) its output-row list offset / 16, both from the tile data start
+constexpr std::uint32_t kNoStep = 0x1ff;
+struct StepFields {
+    std::uint32_t next = kNoStep, next_pair = 0, pair = 0, S = 0, vq = 0, gmax_lg = 0;
+    std::uint32_t in_ref = 0, out_base = 0;
+    std::uint32_t k = 0, lg = 0, flags = 0, iters = 0, nvalid = 0;
+    std::uint32_t voff = 0, ixq = 0, oq = 0;
+};
+inline void pack_step(const StepFields& f, std::uint32_t w[4]) {
+    w[0] = (f.next & 0x1ff) | (f.next_pair & 1) << 9 | (f.pair & 1) << 10 | (f.S & 63) << 11 | (f.vq & 255) << 17 |
+           (f.gmax_lg & 7) << 25;
+    w[1] = (f.in_ref & 0xffff) | (f.out_base & 0xffff) << 16;
+    w[2] = (f.k & 63) | (f.lg & 7) << 6 | (f.flags & 255) << 9 | (f.iters & 511) << 17 | (f.nvalid & 63) << 26;
+    w[3] = (f.voff & 31) | (f.ixq & 255) << 5 | (f.oq & 255) << 13;
+}
+inline StepFields unpack_step(const std::uint32_t w[4]) {
+    StepFields f;
+    f.next = w[0] & 0x1ff;
+    f.next_pair = (w[0] >> 9) & 1;
+    f.pair = (w[0] >> 10) & 1;
+    f.S = (w[0] >> 11) & 63;
+    f.vq = (w[0] >> 17) & 255;
+    f.gmax_lg = (w[0] >> 25) & 7;
+    f.in_ref = w[1] & 0xffff;
+    f.out_base = w[1] >> 16;
+    f.k = w[2] & 63;
+    f.lg = (w[2] >> 6) & 7;
+    f.flags = (w[2] >> 9) & 255;
+    f.iters = (w[2] >> 17) & 511;
+    f.nvalid = w[2] >> 26;
+    f.voff = w[3] & 31;
+    f.ixq = (w[3] >> 5) & 255;
+    f.oq = (w[3] >> 13) & 255;
+    return f;
+}
 
 // Bytes of one tile in the stream (16-byte aligned sections).
 inline constexpr int tile_iters(int ncols, int groups) { return (ncols + groups - 1) / groups; }

@@ -161,6 +161,22 @@ std::int64_t pair_bytes(const Shape& A, const Shape& B) {
            pad16(B.nout * 4);
 }
 
+// A tile's own fields of its step sub-header (the step-wide ones are set at emission); the
+// packed ranges are checked here.
+StepFields step_fields(const TileTask& t) {
+    if (t.iters > 511 || t.nrows > 32 || t.nvalid > 32 || t.in_ref > 0xffff)
+        throw std::logic_error("solve program: tile outside the step header ranges");
+    StepFields f;
+    f.in_ref = t.in_ref;
+    f.out_base = t.out_base;
+    f.k = t.nrows;
+    f.lg = t.groups;
+    f.flags = t.flags;
+    f.iters = t.iters;
+    f.nvalid = t.nvalid;
+    return f;
+}
+
 }  // namespace
 
 void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std::vector<index_t>& l2v, int sub,
@@ -745,6 +761,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             std::vector<double> words;
             std::vector<std::int32_t> src;  // template mode: srcmap codes of the words
             std::int64_t used = 0, last_hdr = -1;
+            bool last_pair = false;         // the previous step was a pair (two sub-headers to link)
             int opened = 0;                 // phase in which the unit was opened
         };
         std::vector<Unit> open_unit(kSolveWarps);
@@ -815,7 +832,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     }
                 }
                 // a step of nb bytes in this warp's open unit: {bytes, srcmap codes of its words}
-                auto place = [&](std::int64_t nb) {
+                auto place = [&](std::int64_t nb, bool pair) {
                     if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
                     Unit& U = open_unit[w];
                     if (U.used > 0 && U.used + nb > unit_bytes) {
@@ -827,9 +844,13 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     if (U.words.size() < need) U.words.resize(need, 0.0);
                     if (tmpl && U.src.size() < need) U.src.resize(need, kSrcCopy);
                     char* base = reinterpret_cast<char*>(U.words.data());
-                    if (U.last_hdr >= 0)
-                        reinterpret_cast<TileTask*>(base + U.last_hdr)->next = static_cast<std::uint32_t>(U.used / 16);
+                    if (U.last_hdr >= 0)  // link: the previous step's sub-header(s) name this step
+                        for (int h = 0; h < (U.last_pair ? 2 : 1); ++h) {
+                            std::uint32_t* w0 = reinterpret_cast<std::uint32_t*>(base + U.last_hdr + 16 * h);
+                            *w0 = (*w0 & ~0x3ffu) | static_cast<std::uint32_t>(U.used / 16) | (pair ? 1u << 9 : 0u);
+                        }
                     U.last_hdr = U.used;
+                    U.last_pair = pair;
                     char* dst = base + U.used;
                     std::int32_t* src = tmpl ? U.src.data() + U.used / 8 : nullptr;
                     U.used += nb;
@@ -840,10 +861,17 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     if (mate[i] >= 0 && mate[i] < static_cast<int>(i)) continue;  // emitted with its mate
                     if (mate[i] < 0) {
                         for (Tile& t : chs[i]->tiles) {
-                            auto [dst, srcw] = place(16 + t.bytes());
-                            TileTask hdr = t.t;
-                            hdr.next = kNoTask;
-                            std::memcpy(dst, &hdr, 16);
+                            auto [dst, srcw] = place(16 + t.bytes(), false);
+                            const std::int64_t vb = pad16(t.nvals() * 8), ib = pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
+                            StepFields f = step_fields(t.t);
+                            f.S = t.t.nrows << t.t.groups;
+                            f.vq = static_cast<std::uint32_t>(vb / 16);
+                            f.gmax_lg = t.t.groups;
+                            f.ixq = static_cast<std::uint32_t>(vb / 16);
+                            f.oq = static_cast<std::uint32_t>((vb + ib) / 16);
+                            std::uint32_t hw[4];
+                            pack_step(f, hw);
+                            std::memcpy(dst, hw, 16);
                             std::memcpy(dst + 16, t.vals.data(), t.vals.size() * 8);
                             if (tmpl) std::copy(t.src.begin(), t.src.end(), srcw + 2);
                             std::int64_t off = 16 + pad16(t.nvals() * 8);
@@ -859,16 +887,31 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     for (std::size_t p = 0; p < half[i].size(); ++p) {
                         const Tile A = regroup(chs[i]->tiles[p], half_groups(chs[i]->tiles[p].t.nrows));
                         const Tile B = regroup(chs[j]->tiles[p], half_groups(chs[j]->tiles[p].t.nrows));
-                        auto [dst, srcw] = place(pair_bytes(half[i][p], half[j][p]));
-                        TileTask ha = A.t, hb = B.t;
-                        ha.next = kNoTask;
-                        hb.next = 0;
-                        ha.flags |= kTaskPair;
-                        hb.flags |= kTaskPair;
-                        std::memcpy(dst, &ha, 16);
-                        std::memcpy(dst + 16, &hb, 16);
+                        auto [dst, srcw] = place(pair_bytes(half[i][p], half[j][p]), true);
                         const int kga = A.t.nrows << A.t.groups, kgb = B.t.nrows << B.t.groups, S = kga + kgb;
                         const int ia = A.t.iters, ib = B.t.iters, im = std::max(ia, ib);
+                        {
+                            const std::int64_t vb = pad16(static_cast<std::int64_t>(im) * S * 8);
+                            const std::int64_t iba = pad16(static_cast<std::int64_t>(A.idx.size()) * 4);
+                            const std::int64_t ibb = pad16(static_cast<std::int64_t>(B.idx.size()) * 4);
+                            const std::int64_t oba = pad16(static_cast<std::int64_t>(A.outidx.size()) * 4);
+                            StepFields fa = step_fields(A.t), fb = step_fields(B.t);
+                            for (StepFields* f : {&fa, &fb}) {
+                                f->pair = 1;
+                                f->S = static_cast<std::uint32_t>(S);
+                                f->vq = static_cast<std::uint32_t>(vb / 16);
+                                f->gmax_lg = std::max<std::uint32_t>(A.t.groups, B.t.groups);
+                            }
+                            fb.voff = static_cast<std::uint32_t>(kga);
+                            fa.ixq = static_cast<std::uint32_t>(vb / 16);
+                            fb.ixq = static_cast<std::uint32_t>((vb + iba) / 16);
+                            fa.oq = static_cast<std::uint32_t>((vb + iba + ibb) / 16);
+                            fb.oq = static_cast<std::uint32_t>((vb + iba + ibb + oba) / 16);
+                            std::uint32_t hw[8];
+                            pack_step(fa, hw);
+                            pack_step(fb, hw + 4);
+                            std::memcpy(dst, hw, 32);
+                        }
                         double* V = reinterpret_cast<double*>(dst + 32);
                         for (int t = 0; t < im; ++t) {
                             for (int l = 0; l < kga; ++l) {

@@ -45,41 +45,31 @@ void run_phase(const SolvePools& sp, PartState& st) {
             const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + st.wu[w])];
             const char* ubase = base + std::int64_t(ue[0]) * 16;
             std::uint32_t& cur = st.wcur[w];
-            TileTask hd[2];
-            std::memcpy(&hd[0], ubase + std::int64_t(cur) * 16, 16);
-            const bool pair = hd[0].flags & kTaskPair;
-            if (pair) std::memcpy(&hd[1], ubase + std::int64_t(cur) * 16 + 16, 16);
+            // step sub-headers (device_format.hpp): A, and B for a pair step; the tile data
+            // follows the sub-headers, every offset is read from the sub-header like the kernel
+            StepFields hd[2];
+            std::uint32_t hw[4];
+            std::memcpy(hw, ubase + std::int64_t(cur) * 16, 16);
+            hd[0] = unpack_step(hw);
+            const bool pair = hd[0].pair;
+            if (pair) {
+                std::memcpy(hw, ubase + std::int64_t(cur) * 16 + 16, 16);
+                hd[1] = unpack_step(hw);
+            }
             const char* tb = ubase + std::int64_t(cur) * 16 + (pair ? 32 : 16);
             cur = hd[0].next;
             ++st.wdone[w];
-            if (cur == kNoTask) {  // unit consumed
+            if (cur == kNoStep) {  // unit consumed
                 ++st.wu[w];
                 cur = 0;
             }
             const int nsub = pair ? 2 : 1;
-            // step geometry (device_format.hpp): value stride S, iterations, list offsets
-            int S = 0, im = 0;
             for (int q = 0; q < nsub; ++q) {
-                S += hd[q].nrows << hd[q].groups;
-                im = std::max<int>(im, hd[q].iters);
-            }
-            std::int64_t ioff[2] = {0, 0}, ooff[2] = {0, 0};
-            std::int64_t off = pad16i(im * S * 8);
-            for (int q = 0; q < nsub; ++q) {
-                ioff[q] = off;
-                if (hd[q].flags & kTaskInIndexed) off += pad16i(hd[q].iters * (1 << hd[q].groups) * 4);
-            }
-            for (int q = 0; q < nsub; ++q) {
-                ooff[q] = off;
-                if ((hd[q].flags & kTaskPush) && (hd[q].flags & kTaskLast)) off += pad16i(hd[q].nrows * 4);
-            }
-            int voff = 0;
-            for (int q = 0; q < nsub; ++q) {
-                const TileTask& task = hd[q];
-                const int k = task.nrows, G = 1 << task.groups, iters = task.iters;
+                const StepFields& task = hd[q];
+                const int k = task.k, G = 1 << task.lg, iters = task.iters, S = task.S, voff = task.voff;
                 const double* M = reinterpret_cast<const double*>(tb);
-                const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + ioff[q]);
-                const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(tb + ooff[q]);
+                const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tb + 16 * task.ixq);
+                const std::int32_t* ox = reinterpret_cast<const std::int32_t*>(tb + 16 * task.oq);
                 if (task.flags & kTaskFirst)
                     for (double& a : acc[q]) a = 0.0;
                 const std::vector<double>& in = (task.flags & kTaskInOwn) ? own : other;
@@ -94,20 +84,19 @@ void run_phase(const SolvePools& sp, PartState& st) {
                     for (int it = 0; it < iters; ++it)
                         for (int g = 0; g < G; ++g) {
                             const int j = it * G + g;
-                            const double v = (task.flags & kTaskInIndexed) ? fetch(ix[j]) : fetch(task.in_ref + j);
+                            const double v = (task.flags & kTaskInIndexed) ? fetch(ix[j]) : fetch(static_cast<int>(task.in_ref) + j);
                             s += M[it * S + voff + r * G + g] * v;
                         }
                     acc[q][r] += s;
                 }
                 if (task.flags & kTaskLast)
-                    for (int r = 0; r < task.nvalid; ++r) {
-                        if (task.flags & kTaskDiag) other.at(task.out_base + r) = acc[q][r];
+                    for (int r = 0; r < static_cast<int>(task.nvalid); ++r) {
+                        if (task.flags & kTaskDiag) other.at(static_cast<int>(task.out_base) + r) = acc[q][r];
                         else if (task.flags & kTaskPush) {
                             if (task.flags & kTaskPartial) st.Q.at(ox[r]) += acc[q][r];
                             else own.at(ox[r]) -= acc[q][r];
-                        } else own.at(task.out_base + r) -= acc[q][r];
+                        } else own.at(static_cast<int>(task.out_base) + r) -= acc[q][r];
                     }
-                voff += k * G;
             }
         }
     }

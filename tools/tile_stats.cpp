@@ -46,21 +46,22 @@ int main(int argc, char** argv) {
             for (int u = pd.warp_base[w]; u < pd.warp_base[w + 1]; ++u) {
                 const std::int32_t* ue = &pools.units[2 * (pd.units + u)];
                 const char* ub = base + std::int64_t(ue[0]) * 16;
-                for (std::uint32_t cur = 0; cur != kNoTask;) {
-                    TileTask t;
-                    std::memcpy(&t, ub + std::int64_t(cur) * 16, 16);
+                for (std::uint32_t cur = 0; cur != kNoStep;) {
+                    std::uint32_t hw[4];
+                    std::memcpy(hw, ub + std::int64_t(cur) * 16, 16);
+                    const StepFields t = unpack_step(hw);
                     ++nsteps;
-                    if (t.flags & kTaskPair) {  // a pair step: count its B tile too
+                    if (t.pair) {  // a pair step: count its B tile too
                         ++npairs;
-                        TileTask b;
-                        std::memcpy(&b, ub + std::int64_t(cur) * 16 + 16, 16);
+                        std::memcpy(hw, ub + std::int64_t(cur) * 16 + 16, 16);
+                        const StepFields b = unpack_step(hw);
                         ntile++;
-                        nval += (long long)b.iters * b.nrows * (1 << b.groups);
+                        nval += (long long)b.iters * b.k * (1 << b.lg);
                     }
                     cur = t.next;
-                    const int G = 1 << t.groups;
-                    const long long v = (long long)t.iters * t.nrows * G;
-                    auto& h = hist[{t.nrows, G, t.flags & (kTaskInIndexed | kTaskDiag | kTaskPush | kTaskPartial)}];
+                    const int G = 1 << t.lg;
+                    const long long v = (long long)t.iters * t.k * G;
+                    auto& h = hist[{(int)t.k, G, (int)(t.flags & (kTaskInIndexed | kTaskDiag | kTaskPush | kTaskPartial))}];
                     h.first++;
                     h.second += v;
                     auto& bi = by_iters[std::min<int>(t.iters, 64)];
