@@ -71,6 +71,27 @@ struct RegTable {
     }
 };
 
+// Checked build (make VARIANT=_checked EXTRA=-DBDDC_CHECKED; compute-sanitizer is closed on
+// this pool): every shared-memory access of a tile is bounds-checked against its part's
+// vectors and its unit, a violation traps with the step's coordinates.
+#ifdef BDDC_CHECKED
+#define SOLVE_CHECK(cond, code)                                                                          \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("interior solve check %d failed: cta %d warp %d lane %d\n", code, blockIdx.x,          \
+                   threadIdx.x >> 5, threadIdx.x & 31);                                                 \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define SOLVE_CHECK(cond, code) do { } while (0)
+#endif
+struct TileBounds {
+    int ldn_p;   // a part's vector stride: T[0, ldn_p), X[0, ldn_p) (T-relative indices < 2 ldn_p)
+    int n_top;   // Q entries
+    int room;    // bytes of the unit from the tile data start
+};
+
 // One tile GEMV (device_format.hpp): k <= 32 rows, G = 2^lg column groups, lane = r*G + g
 // owns row r and columns j = t*G + g; values are stored iteration-major, value(r, t*G + g)
 // at [t*S + voff + r*G + g], so every iteration is one contiguous, conflict-free shared-memory
@@ -84,7 +105,7 @@ struct RegTable {
 // is flushed by the group's first lane.
 template <bool PROF = false>
 __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* tile, int sl, double* own, double* other,
-                                          double* Q, double& acc, long long* tp = nullptr) {
+                                          double* Q, double& acc, const TileBounds& bnd, long long* tp = nullptr) {
     long long tq = PROF ? clock64() : 0;
 #define TILE_T(i) do { if constexpr (PROF) { const long long t_ = clock64(); tp[i] += t_ - tq; tq = t_; } } while (0)
     const unsigned w0 = h.x, w2 = h.z, w3 = h.w;
@@ -96,9 +117,15 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
     const double* M = reinterpret_cast<const double*>(tile) + (w3 & 31) + sl;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int full = iters & ~3, rem = iters & 3;
+    SOLVE_CHECK(((w0 >> 17) & 255) * 16 <= bnd.room && k >= 1 && k <= 32 && kG <= 32, 1);
+    SOLVE_CHECK(sl >= kG || iters == 0 || ((iters - 1) * S + static_cast<int>(w3 & 31) + sl + 1) * 8 <= static_cast<int>((w0 >> 17) & 255) * 16, 2);
     TILE_T(0);
     if (flags & kTaskInIndexed) {
         const std::int32_t* ix = reinterpret_cast<const std::int32_t*>(tile + (((w3 >> 5) & 255) << 4)) + g;
+        SOLVE_CHECK(static_cast<int>(((w3 >> 5) & 255) * 16) + iters * G * 4 <= bnd.room, 3);
+#ifdef BDDC_CHECKED
+        for (int t = 0; t < iters; ++t) SOLVE_CHECK(ix[t * G] >= 0 && ix[t * G] < 2 * bnd.ldn_p, 4);
+#endif
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], in[ix[0]], s0);
@@ -113,6 +140,7 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
         if (rem > 2) s2 = fma(M[2 * S], in[ix[2 * G]], s2);
     } else {
         const double* v = in + (h.y & 0xffff) + g;
+        SOLVE_CHECK(static_cast<int>(h.y & 0xffff) + iters * G <= bnd.ldn_p, 5);
 #pragma unroll 1
         for (int t = 0; t < full; t += 4) {
             s0 = fma(M[0], v[0], s0);
@@ -142,11 +170,14 @@ __device__ __forceinline__ void tile_task(const int4 h, const unsigned char* til
         if (flags & kTaskPush) {
             if (r < k) {
                 const int o = reinterpret_cast<const std::int32_t*>(tile + (((w3 >> 13) & 255) << 4))[r];
+                SOLVE_CHECK(static_cast<int>(((w3 >> 13) & 255) * 16) + k * 4 <= bnd.room, 6);
+                SOLVE_CHECK(o >= 0 && o < ((flags & kTaskPartial) ? bnd.n_top : bnd.ldn_p), 7);
                 if (flags & kTaskPartial) Q[o] += acc;
                 else own[o] -= acc;
             }
         } else if (r < static_cast<int>(w2 >> 26)) {
             const int out = (h.y >> 16) + r;
+            SOLVE_CHECK(out < bnd.ldn_p, 8);
             if (flags & kTaskDiag) other[out] = acc;
             else own[out] -= acc;
         }
@@ -393,11 +424,14 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             const int4 h = hdr4;
             const unsigned w0 = h.x;
             const bool pair = (w0 >> 10) & 1;
-            const unsigned char* tile = ubuf + (cur << 4) + (pair ? 32 : 16);
+            const int tile_off = static_cast<int>(cur << 4) + (pair ? 32 : 16);
+            const unsigned char* tile = ubuf + tile_off;
             cur = w0 & 0x1ff;
             if (cur != kNoStep)  // the lane's sub-header of the next step, early
                 hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + (((w0 >> 9) & 1) && lane >= 16 ? 16 : 0));
-            tile_task<STATS>(h, tile, pair ? (lane & 15) : lane, own, other, Q, acc, tprof);
+            SOLVE_CHECK(tile_off <= unit && (cur == kNoStep || static_cast<int>(cur << 4) < unit), 9);
+            tile_task<STATS>(h, tile, pair ? (lane & 15) : lane, own, other, Q, acc, TileBounds{ldn_p, n_top, unit - tile_off},
+                             tprof);
             if ((kind & kPhaseChained) && ((h.z >> 9) & kTaskLast))
                 __syncwarp();  // a later tile of this warp's job reads what was just written
             ++done;
