@@ -44,6 +44,7 @@ CASES = [
     {"BDDC_STEP": "1"},             # xpay / SpMV / update as one cooperative launch
     {"BDDC_K_FULL": "1"},           # row-major K_i, local_blocks CTAs per subdomain
     {"BDDC_PAIR_TILES": "0"},       # no pair steps in the interior-solve programs
+    {"BDDC_MAX_CHAIN": "0"},        # forward levels coloured into phases only
 ]
 
 
