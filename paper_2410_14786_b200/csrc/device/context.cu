@@ -1991,7 +1991,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         I.head_bwd_values = img.head.bwd_factor_values;
     }
     if (std::getenv("BDDC_SOLVE_STATS")) {
-        I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 8 + 256 + 5 * 256 * kSolveWarps + 8 + 4 * kSolveWarps);
+        I.dbg_buf.alloc(static_cast<std::size_t>(img.solve.parts.size()) * kSolveWarps * 8 + 256 + 5 * 256 * kSolveWarps + 8 + 4 * kSolveWarps + 512 * 6);
         BDDC_CUDA(cudaMemset(I.dbg_buf.p, 0, sizeof(long long) * I.dbg_buf.n));
     }
     upload_pod(I.subs, img.subs);

@@ -430,8 +430,20 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             if (cur != kNoStep)  // the lane's sub-header of the next step, early
                 hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + (((w0 >> 9) & 1) && lane >= 16 ? 16 : 0));
             SOLVE_CHECK(tile_off <= unit && (cur == kNoStep || static_cast<int>(cur << 4) < unit), 9);
+            long long tp_before[4];
+            if constexpr (STATS)
+                for (int i = 0; i < 4; ++i) tp_before[i] = tprof[i];
             tile_task<STATS>(h, tile, pair ? (lane & 15) : lane, own, other, Q, acc, TileBounds{ldn_p, n_top, unit - tile_off},
                              tprof);
+            if constexpr (STATS) {  // CTA 0, warp 0: its first 512 steps {phase, k|lg|iters, 4 sub-phase cycles}
+                if (blockIdx.x == 0 && warp == 0 && lane == 0 && done < 512) {
+                    long long* so = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 +
+                                    5 * 256 * kSolveWarps + 8 + 4 * kSolveWarps + done * 6;
+                    so[0] = ph;
+                    so[1] = static_cast<long long>(h.z);
+                    for (int i = 0; i < 4; ++i) so[2 + i] = tprof[i] - tp_before[i];
+                }
+            }
             if ((kind & kPhaseChained) && ((h.z >> 9) & kTaskLast))
                 __syncwarp();  // a later tile of this warp's job reads what was just written
             ++done;

@@ -55,3 +55,11 @@ tp = raw[nparts * W * 8 + 256 + 5 * 256 * W + 8: nparts * W * 8 + 256 + 5 * 256 
 print("CTA 0 tile sub-phase cycles per warp (decode, loop, reduction, flush):")
 for w_ in range(W):
     print("  warp", w_, [int(v) for v in tp[w_]])
+so = raw[nparts * W * 8 + 256 + 5 * 256 * W + 8 + 4 * W: nparts * W * 8 + 256 + 5 * 256 * W + 8 + 4 * W + 512 * 6].reshape(512, 6)
+print("CTA 0 warp 0 steps: phase k lg iters | decode loop reduction flush cycles")
+for st in so:
+    if st[1] == 0 and st[0] == 0 and st[2] == 0:
+        continue
+    z = int(st[1]) & 0xffffffff
+    print(f"  ph {int(st[0]):3d} k {z & 63:2d} lg {(z >> 6) & 7} it {(z >> 17) & 511:3d} flags {(z >> 9) & 255:3d} | "
+          f"{int(st[2]):5d} {int(st[3]):5d} {int(st[4]):5d} {int(st[5]):5d}")
