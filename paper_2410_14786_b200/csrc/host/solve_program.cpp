@@ -223,6 +223,9 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         if (bwdm[sidx]) pools.bwd_factor_values += v;
     }
     if (P != 1 && P != 2 && P != 4) throw std::invalid_argument("solve program: parts must be 1, 2 or 4");
+    // step sub-headers address a unit in 16-byte units with 9-bit step and 8-bit section offsets
+    if (unit_bytes < 256 || unit_bytes > 4096 || unit_bytes % 16)
+        throw std::invalid_argument("solve program: unit bytes must be a multiple of 16 in [256, 4096]");
 
     // ---- tree and group assignment (P = 2: halves below the top separator chain)
     std::vector<std::vector<index_t>> children(nsn);
