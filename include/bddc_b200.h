@@ -92,7 +92,9 @@ typedef struct {
     double coarse_abs_tolerance;   /* 0 */
     int32_t coarse_max_iterations; /* 500 */
     int32_t leaf_size;             /* nested-dissection leaf size (default 24) */
-    int32_t local_blocks;          /* CTAs per subdomain for the K_i GEMV (default 8) */
+    int32_t local_blocks;          /* CTAs per subdomain of the row-major K_i GEMV (default 8; only with
+                                      BDDC_K_FULL=1 - the default packed-symmetric K_i kernel runs a
+                                      2-CTA cluster per subdomain) */
     int32_t solve_parts;           /* CTAs (cluster size) per subdomain in the interior solve: 0 auto, 1, 2 */
     int32_t setup_mode;            /* BDDC_SETUP_DEVICE (default): factorisation, Schur complements, K_i,
                                       Phi, A_ci and A_c^-1 on the GPU; BDDC_SETUP_HOST: host numeric setup */
