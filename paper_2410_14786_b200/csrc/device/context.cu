@@ -51,40 +51,6 @@ struct DBuf {
     }
 };
 
-// Setup scratch from the device's stream-ordered memory pool (cudaMallocAsync / cudaFreeAsync on
-// the setup stream): the pool keeps the memory (release threshold raised once per device), so a
-// later construction reuses it without a synchronising cudaMalloc / cudaFree of ~GBs.
-inline void keep_pool_memory(int device) {
-    static std::once_flag once[64];
-    std::call_once(once[device & 63], [device] {
-        cudaMemPool_t pool = nullptr;
-        BDDC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        std::uint64_t keep = ~std::uint64_t(0);
-        BDDC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    });
-}
-
-template <typename T>
-struct PBuf {
-    T* p = nullptr;
-    std::size_t n = 0;
-    cudaStream_t s;
-    explicit PBuf(cudaStream_t stream) : s(stream) {}
-    PBuf(const PBuf&) = delete;
-    PBuf& operator=(const PBuf&) = delete;
-    ~PBuf() { if (p) cudaFreeAsync(p, s); }
-    void alloc(std::size_t count) {
-        if (p) BDDC_CUDA(cudaFreeAsync(p, s));
-        p = nullptr;
-        n = count;
-        if (count) BDDC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
-    }
-    void upload(const std::vector<T>& v) {
-        alloc(std::max<std::size_t>(v.size(), 1));
-        if (!v.empty()) BDDC_CUDA(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
-    }
-};
-
 struct Event {
     cudaEvent_t e = nullptr;
     Event() { BDDC_CUDA(cudaEventCreate(&e)); }
@@ -716,7 +682,6 @@ struct GpuContext::Impl {
         const auto t0 = std::chrono::steady_clock::now();
         SetupTimer tm;
         cudaStream_t s = stream;
-        keep_pool_memory(device);
         const Decomposition& d = pb.decomposition;
         const index_t nsub = d.n_subdomains;
         SolveProgram* pools[3] = {&prog, &harm, &head};
@@ -726,8 +691,8 @@ struct GpuContext::Impl {
 
         // ---- templates (word + source code per stream word), straight into one device buffer
         std::vector<std::array<std::int64_t, 3>> toff(ncls);
-        PBuf<double> tword(s);
-        PBuf<std::int32_t> tcode(s);
+        DBuf<double> tword;
+        DBuf<std::int32_t> tcode;
         {
             std::int64_t total = 0;
             for (std::size_t k = 0; k < ncls; ++k)
@@ -770,9 +735,9 @@ struct GpuContext::Impl {
             of[k].d = bd.size();
             bd.insert(bd.end(), C.c_val.begin(), C.c_val.end());
         }
-        PBuf<std::int32_t> pi(s);
-        PBuf<std::int64_t> pl(s);
-        PBuf<double> pdv(s);
+        DBuf<std::int32_t> pi;
+        DBuf<std::int64_t> pl;
+        DBuf<double> pdv;
         pi.upload(bi);
         pl.upload(bl);
         pdv.upload(bd);
@@ -809,8 +774,8 @@ struct GpuContext::Impl {
                     tot[t] = std::max(tot[t], need[k][t] + 1);
                 }
             }
-        PBuf<double> aval(s), fronts(s), Sb(s), Db(s), Mb(s), aci_dev(s);
-        PBuf<int> piv(s), status(s);
+        DBuf<double> aval, fronts, Sb, Db, Mb, aci_dev;
+        DBuf<int> piv, status;
         aval.alloc(tot[0]);
         fronts.alloc(tot[1]);
         Sb.alloc(tot[2]);
@@ -861,8 +826,8 @@ struct GpuContext::Impl {
             }
         }
         job0.back() = jobs.size();
-        PBuf<FillJob> jobs_dev(s);
-        PBuf<std::int64_t> outs_dev(s);
+        DBuf<FillJob> jobs_dev;
+        DBuf<std::int64_t> outs_dev;
         jobs_dev.upload(jobs);
         outs_dev.upload(outs);
         tm.mark("  templates, plans, scratch");
