@@ -453,10 +453,15 @@ def run_ours(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": workload(cfg, world)["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload(cfg, world), "iterations": rep.iterations,
-        "final_relative_residual": rep.final_relative_residual, "setup_seconds": m["setup_s"],
+        # steady-state construction (the second in the process); the first one also pays the
+        # process's one-time CUDA costs (lazy kernel-module loads, first allocations) and is
+        # reported beside it
+        "final_relative_residual": rep.final_relative_residual,
+        "setup_seconds": m["setup_repeat"] if m["setup_repeat"] is not None else m["setup_s"],
         "setup": {"mode": "device (GPU setup, SURVEY.md §8 f1)", "first_construction_s": m["setup_s"],
                   "repeat_construction_s": m["setup_repeat"], "device_kernels_s": m["st"]["setup_device_seconds"],
-                  "setup_classes": m["st"]["unique_subdomains"]},
+                  "setup_classes": m["st"]["unique_subdomains"],
+                  "setup_seconds_is": "repeat construction" if m["setup_repeat"] is not None else "first construction"},
     }
     if ks:
         line["roofline"] = dict(ks["roofline"], traffic=traffic, peak_source=peak_src)
