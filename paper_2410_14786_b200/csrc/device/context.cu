@@ -145,7 +145,7 @@ const char* const kEnvSwitches[] = {
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
-    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP", "BDDC_MAX_CHAIN"};
+    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP", "BDDC_MAX_CHAIN", "BDDC_QUAD_TILES"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.

@@ -412,29 +412,29 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 }
                 ubuf = my_ring + s * unit;
                 cur = 0;
-                // the unit's first step: every lane reads sub-header A (for a single tile, the
-                // 16 bytes after it are values); lanes 16-31 of a pair step take B's
-                const int4 ha = *reinterpret_cast<const int4*>(ubuf);
-                const int4 hb = *reinterpret_cast<const int4*>(ubuf + 16);
-                hdr4 = ((ha.x >> 10) & 1) && lane >= 16 ? hb : ha;
+                // the unit's first step: every lane reads sub-header A; in a group step the
+                // lanes of the other sub-tiles then read their own
+                hdr4 = *reinterpret_cast<const int4*>(ubuf);
+                const int nl0 = static_cast<unsigned>(hdr4.x) >> 30;
+                if (nl0) hdr4 = *reinterpret_cast<const int4*>(ubuf + 16 * (lane >> (5 - nl0)));
                 fresh = false;
             }
             const long long t_tile0 = stats ? clock64() : 0;
             if (stats) ++n_tiles;
             const int4 h = hdr4;
             const unsigned w0 = h.x;
-            const bool pair = (w0 >> 10) & 1;
-            const int tile_off = static_cast<int>(cur << 4) + (pair ? 32 : 16);
+            const int nsub_lg = w0 >> 30;  // sub-tiles: 1, 2 or 4, on 32 >> nsub_lg lanes each
+            const int tile_off = static_cast<int>(cur << 4) + (16 << nsub_lg);
             const unsigned char* tile = ubuf + tile_off;
             cur = w0 & 0x1ff;
             if (cur != kNoStep)  // the lane's sub-header of the next step, early
-                hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + (((w0 >> 9) & 1) && lane >= 16 ? 16 : 0));
+                hdr4 = *reinterpret_cast<const int4*>(ubuf + (cur << 4) + 16 * (lane >> (5 - ((w0 >> 28) & 3))));
             SOLVE_CHECK(tile_off <= unit && (cur == kNoStep || static_cast<int>(cur << 4) < unit), 9);
             long long tp_before[4];
             if constexpr (STATS)
                 for (int i = 0; i < 4; ++i) tp_before[i] = tprof[i];
-            tile_task<STATS>(h, tile, pair ? (lane & 15) : lane, own, other, Q, acc, TileBounds{ldn_p, n_top, unit - tile_off},
-                             tprof);
+            tile_task<STATS>(h, tile, lane & ((32 >> nsub_lg) - 1), own, other, Q, acc,
+                             TileBounds{ldn_p, n_top, unit - tile_off}, tprof);
             if constexpr (STATS) {  // CTA 0, warp 0: its first 512 steps {phase, k|lg|iters, 4 sub-phase cycles}
                 if (blockIdx.x == 0 && warp == 0 && lane == 0 && done < 512) {
                     long long* so = S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 +

@@ -34,8 +34,9 @@
 // Input column j is in[in_ref + j] (contiguous) or in[idx[j]] (IN_INDEXED).
 // Pushes of one phase never share a target row (supernodes are coloured per height).
 //
-// Pair steps: two independent tiles A and B with k <= 16 rows each run side by side, A on
-// lanes 0-15 and B on lanes 16-31 (lane - 16 = r*G_B + g), each with its own G (k*G <= 16),
+// Group steps (pairs and quads): two independent tiles A and B with k <= 16 rows each run side
+// by side, A on lanes 0-15 and B on lanes 16-31 (lane - 16 = r*G_B + g), each with its own G
+// (k*G <= 16); likewise four tiles of k <= 8 rows on the four 8-lane quarters (k*G <= 8),
 // iteration count, input, flags and outputs, so a warp pays one header decode, one loop and
 // one butterfly for both. Layout: sub-header A, sub-header B (step header below), values
 // iteration-major with stride S = k_A*G_A + k_B*G_B (A's lanes then B's), for
@@ -92,24 +93,25 @@ static_assert(sizeof(TileTask) == 16, "TileTask must stay 16 bytes");
 // pair step: A, read by lanes 0-15, then B, read by lanes 16-31). Each sub-header holds
 // everything its lanes need (the step-wide fields duplicated), and carries the next step's
 // offset and pair flag, so a lane prefetches and decodes only its own 16 bytes:
-//   w0: [0:9) next step (16-byte units from the unit start; kNoStep ends the unit), [9] next
-//       step is a pair, [10] this step is a pair, [11:17) value stride S (values per
-//       iteration: k*G, or k_A*G_A + k_B*G_B), [17:25) value-section bytes / 16, [25:28) log2
-//       of the step's largest G
+//   w0: [0:9) next step (16-byte units from the unit start; kNoStep ends the unit),
+//       [11:17) value stride S (values per iteration: k*G, or the sub-tiles' sum), [17:25)
+//       value-section bytes / 16, [25:28) log2 of the step's largest G, [28:30) log2 of the
+//       next step's sub-tile count, [30:32) log2 of this step's sub-tile count (1, 2 or 4: the
+//       sub-tile of lane l is l / (32 >> that), its 16-byte sub-header at that index)
 //   w1: [0:16) in_ref, [16:32) out_base
 //   w2: [0:6) k, [6:9) log2 G, [9:17) flags, [17:26) iterations, [26:32) nvalid
 //   w3: [0:5) the tile's first value lane within S, [5:13) its index list offset / 16 and
 //       [13:21) its output-row list offset / 16, both from the tile data start
 constexpr std::uint32_t kNoStep = 0x1ff;
 struct StepFields {
-    std::uint32_t next = kNoStep, next_pair = 0, pair = 0, S = 0, vq = 0, gmax_lg = 0;
+    std::uint32_t next = kNoStep, next_nsub_lg = 0, nsub_lg = 0, S = 0, vq = 0, gmax_lg = 0;
     std::uint32_t in_ref = 0, out_base = 0;
     std::uint32_t k = 0, lg = 0, flags = 0, iters = 0, nvalid = 0;
     std::uint32_t voff = 0, ixq = 0, oq = 0;
 };
 inline void pack_step(const StepFields& f, std::uint32_t w[4]) {
-    w[0] = (f.next & 0x1ff) | (f.next_pair & 1) << 9 | (f.pair & 1) << 10 | (f.S & 63) << 11 | (f.vq & 255) << 17 |
-           (f.gmax_lg & 7) << 25;
+    w[0] = (f.next & 0x1ff) | (f.S & 63) << 11 | (f.vq & 255) << 17 | (f.gmax_lg & 7) << 25 | (f.next_nsub_lg & 3) << 28 |
+           (f.nsub_lg & 3) << 30;
     w[1] = (f.in_ref & 0xffff) | (f.out_base & 0xffff) << 16;
     w[2] = (f.k & 63) | (f.lg & 7) << 6 | (f.flags & 255) << 9 | (f.iters & 511) << 17 | (f.nvalid & 63) << 26;
     w[3] = (f.voff & 31) | (f.ixq & 255) << 5 | (f.oq & 255) << 13;
@@ -117,8 +119,8 @@ inline void pack_step(const StepFields& f, std::uint32_t w[4]) {
 inline StepFields unpack_step(const std::uint32_t w[4]) {
     StepFields f;
     f.next = w[0] & 0x1ff;
-    f.next_pair = (w[0] >> 9) & 1;
-    f.pair = (w[0] >> 10) & 1;
+    f.next_nsub_lg = (w[0] >> 28) & 3;
+    f.nsub_lg = (w[0] >> 30) & 3;
     f.S = (w[0] >> 11) & 63;
     f.vq = (w[0] >> 17) & 255;
     f.gmax_lg = (w[0] >> 25) & 7;

@@ -131,9 +131,10 @@ Tile regroup(const Tile& T, int G2) {
     return R;
 }
 
-int half_groups(int k) {
+// G of a tile of k rows on a sub-tile of `lanes` lanes (k*G <= lanes)
+int lane_groups(int k, int lanes) {
     int G = 1;
-    while (k * G * 2 <= 16) G *= 2;
+    while (k * G * 2 <= lanes) G *= 2;
     return G;
 }
 
@@ -154,11 +155,17 @@ Shape shape_of(const Tile& T, int G2) {
     return h;
 }
 
-std::int64_t pair_bytes(const Shape& A, const Shape& B) {
-    const int ia = A.t.iters, ib = B.t.iters;
-    const std::int64_t S = static_cast<std::int64_t>(A.t.nrows << A.t.groups) + (B.t.nrows << B.t.groups);
-    return 32 + pad16(std::max(ia, ib) * S * 8) + pad16(A.nidx * 4) + pad16(B.nidx * 4) + pad16(A.nout * 4) +
-           pad16(B.nout * 4);
+// bytes of a group step (device_format.hpp): the sub-headers, the interleaved values for the
+// longest sub-tile's iterations, the index lists, the output-row lists
+std::int64_t group_bytes(const std::vector<const Shape*>& g) {
+    int im = 0;
+    std::int64_t S = 0, lists = 0;
+    for (const Shape* h : g) {
+        im = std::max<int>(im, h->t.iters);
+        S += h->t.nrows << h->t.groups;
+        lists += pad16(h->nidx * 4) + pad16(h->nout * 4);
+    }
+    return 16 * static_cast<std::int64_t>(g.size()) + pad16(im * S * 8) + lists;
 }
 
 // A tile's own fields of its step sub-header (the step-wide ones are set at emission); the
@@ -462,6 +469,8 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
         // forward levels: pushes sharing target rows chained into one warp job (up to kMaxChain
         // chunks) instead of coloured into phases; BDDC_MAX_CHAIN=0: colouring only (experiments)
         static const std::size_t kMaxChain = std::getenv("BDDC_MAX_CHAIN") ? std::atoi(std::getenv("BDDC_MAX_CHAIN")) : 8;
+        // BDDC_QUAD_TILES=0: no quads (pairs only); BDDC_PAIR_TILES=0: no group steps (experiments)
+        static const bool quad_tiles = !std::getenv("BDDC_QUAD_TILES") || std::atoi(std::getenv("BDDC_QUAD_TILES")) != 0;
         // BDDC_PAIR_TILES=0: no pair steps (experiments)
         static const bool pair_tiles = !std::getenv("BDDC_PAIR_TILES") || std::atoi(std::getenv("BDDC_PAIR_TILES")) != 0;
         static const int min_kr = std::getenv("BDDC_MIN_CHUNK_ROWS") ? std::atoi(std::getenv("BDDC_MIN_CHUNK_ROWS")) : 8;
@@ -764,7 +773,7 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
             std::vector<double> words;
             std::vector<std::int32_t> src;  // template mode: srcmap codes of the words
             std::int64_t used = 0, last_hdr = -1;
-            bool last_pair = false;         // the previous step was a pair (two sub-headers to link)
+            int last_nsub_lg = 0;           // the previous step's sub-headers to link: 1 << this
             int opened = 0;                 // phase in which the unit was opened
         };
         std::vector<Unit> open_unit(kSolveWarps);
@@ -798,44 +807,64 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         chs.push_back(&ch);
                         solo.push_back(ph.jobs[c].size() == 1);
                     }
-                std::vector<int> mate(chs.size(), -1);
-                std::vector<std::vector<Shape>> half(chs.size());
+                // groups: quads of chunks whose tiles have <= 8 rows (8-lane quarters), then pairs
+                // of <= 16 rows (half-warps); the members of a group match piece by piece in count,
+                // FIRST / LAST / indexed flags, and every group step fits a unit
+                std::vector<int> grp(chs.size(), -1);              // group of a chunk
+                std::vector<std::vector<int>> groups;              // member chunks
+                std::vector<std::vector<std::vector<Shape>>> gshape;  // per group: per member: pieces
                 if (pair_tiles) {
-                    std::vector<int> cand;
-                    for (std::size_t i = 0; i < chs.size(); ++i) {
-                        bool ok = !chs[i]->tiles.empty() && (solo[i] || !(ph.kind & kPhaseChained));
-                        for (const Tile& t : chs[i]->tiles) ok = ok && t.t.nrows <= 16;
-                        if (!ok) continue;
-                        for (const Tile& t : chs[i]->tiles) half[i].push_back(shape_of(t, half_groups(t.t.nrows)));
-                        cand.push_back(static_cast<int>(i));
-                    }
                     constexpr std::uint8_t kShape = kTaskInIndexed | kTaskFirst | kTaskLast;
-                    auto shape_less = [&](int a, int b) {
-                        const auto& A = half[a];
-                        const auto& B = half[b];
-                        if (A.size() != B.size()) return A.size() < B.size();
-                        for (std::size_t q = 0; q < A.size(); ++q)
-                            if ((A[q].t.flags & kShape) != (B[q].t.flags & kShape))
-                                return (A[q].t.flags & kShape) < (B[q].t.flags & kShape);
-                        for (std::size_t q = 0; q < A.size(); ++q)
-                            if (A[q].t.iters != B[q].t.iters) return A[q].t.iters < B[q].t.iters;
-                        return a < b;
-                    };
-                    std::sort(cand.begin(), cand.end(), shape_less);
-                    for (std::size_t q = 0; q + 1 < cand.size();) {
-                        const int a = cand[q], b = cand[q + 1];
-                        bool ok = half[a].size() == half[b].size();
-                        for (std::size_t p = 0; ok && p < half[a].size(); ++p)
-                            ok = (half[a][p].t.flags & kShape) == (half[b][p].t.flags & kShape) &&
-                                 pair_bytes(half[a][p], half[b][p]) <= unit_bytes;
-                        if (!ok) { ++q; continue; }
-                        mate[a] = b;
-                        mate[b] = a;
-                        q += 2;
+                    for (int lanes : {8, 16}) {
+                        if (lanes == 8 && !quad_tiles) continue;
+                        const int n = 32 / lanes;
+                        std::vector<int> cand;
+                        std::vector<std::vector<Shape>> sh(chs.size());
+                        for (std::size_t i = 0; i < chs.size(); ++i) {
+                            if (grp[i] >= 0) continue;
+                            bool ok = !chs[i]->tiles.empty() && (solo[i] || !(ph.kind & kPhaseChained));
+                            for (const Tile& t : chs[i]->tiles) ok = ok && t.t.nrows <= lanes;
+                            if (!ok) continue;
+                            for (const Tile& t : chs[i]->tiles) sh[i].push_back(shape_of(t, lane_groups(t.t.nrows, lanes)));
+                            cand.push_back(static_cast<int>(i));
+                        }
+                        auto same_shape = [&](int a, int b) {
+                            if (sh[a].size() != sh[b].size()) return false;
+                            for (std::size_t q = 0; q < sh[a].size(); ++q)
+                                if ((sh[a][q].t.flags & kShape) != (sh[b][q].t.flags & kShape)) return false;
+                            return true;
+                        };
+                        std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+                            if (sh[a].size() != sh[b].size()) return sh[a].size() < sh[b].size();
+                            for (std::size_t q = 0; q < sh[a].size(); ++q)
+                                if ((sh[a][q].t.flags & kShape) != (sh[b][q].t.flags & kShape))
+                                    return (sh[a][q].t.flags & kShape) < (sh[b][q].t.flags & kShape);
+                            for (std::size_t q = 0; q < sh[a].size(); ++q)
+                                if (sh[a][q].t.iters != sh[b][q].t.iters) return sh[a][q].t.iters < sh[b][q].t.iters;
+                            return a < b;
+                        });
+                        for (std::size_t q = 0; q + n <= cand.size();) {
+                            bool ok = true;
+                            for (int m = 1; ok && m < n; ++m) ok = same_shape(cand[q], cand[q + m]);
+                            for (std::size_t p = 0; ok && p < sh[cand[q]].size(); ++p) {
+                                std::vector<const Shape*> g;
+                                for (int m = 0; m < n; ++m) g.push_back(&sh[cand[q + m]][p]);
+                                ok = group_bytes(g) <= unit_bytes;
+                            }
+                            if (!ok) { ++q; continue; }
+                            groups.emplace_back();
+                            gshape.emplace_back();
+                            for (int m = 0; m < n; ++m) {
+                                grp[cand[q + m]] = static_cast<int>(groups.size()) - 1;
+                                groups.back().push_back(cand[q + m]);
+                                gshape.back().push_back(sh[cand[q + m]]);
+                            }
+                            q += n;
+                        }
                     }
                 }
                 // a step of nb bytes in this warp's open unit: {bytes, srcmap codes of its words}
-                auto place = [&](std::int64_t nb, bool pair) {
+                auto place = [&](std::int64_t nb, int nsub_lg) {
                     if (nb > unit_bytes) throw std::logic_error("solve program: tile larger than a unit");
                     Unit& U = open_unit[w];
                     if (U.used > 0 && U.used + nb > unit_bytes) {
@@ -847,13 +876,14 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     if (U.words.size() < need) U.words.resize(need, 0.0);
                     if (tmpl && U.src.size() < need) U.src.resize(need, kSrcCopy);
                     char* base = reinterpret_cast<char*>(U.words.data());
-                    if (U.last_hdr >= 0)  // link: the previous step's sub-header(s) name this step
-                        for (int h = 0; h < (U.last_pair ? 2 : 1); ++h) {
+                    if (U.last_hdr >= 0)  // link: the previous step's sub-headers name this step
+                        for (int h = 0; h < (1 << U.last_nsub_lg); ++h) {
                             std::uint32_t* w0 = reinterpret_cast<std::uint32_t*>(base + U.last_hdr + 16 * h);
-                            *w0 = (*w0 & ~0x3ffu) | static_cast<std::uint32_t>(U.used / 16) | (pair ? 1u << 9 : 0u);
+                            *w0 = (*w0 & ~(0x1ffu | 3u << 28)) | static_cast<std::uint32_t>(U.used / 16) |
+                                  static_cast<std::uint32_t>(nsub_lg) << 28;
                         }
                     U.last_hdr = U.used;
-                    U.last_pair = pair;
+                    U.last_nsub_lg = nsub_lg;
                     char* dst = base + U.used;
                     std::int32_t* src = tmpl ? U.src.data() + U.used / 8 : nullptr;
                     U.used += nb;
@@ -861,10 +891,10 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                     return std::make_pair(dst, src);
                 };
                 for (std::size_t i = 0; i < chs.size(); ++i) {
-                    if (mate[i] >= 0 && mate[i] < static_cast<int>(i)) continue;  // emitted with its mate
-                    if (mate[i] < 0) {
+                    if (grp[i] >= 0 && groups[grp[i]][0] != static_cast<int>(i)) continue;  // emitted with its group
+                    if (grp[i] < 0) {
                         for (Tile& t : chs[i]->tiles) {
-                            auto [dst, srcw] = place(16 + t.bytes(), false);
+                            auto [dst, srcw] = place(16 + t.bytes(), 0);
                             const std::int64_t vb = pad16(t.nvals() * 8), ib = pad16(static_cast<std::int64_t>(t.idx.size()) * 4);
                             StepFields f = step_fields(t.t);
                             f.S = t.t.nrows << t.t.groups;
@@ -886,59 +916,68 @@ void build_solve_program(const InteriorFactor& F, const CsrMatrix& A, const std:
                         }
                         continue;
                     }
-                    const std::size_t j = static_cast<std::size_t>(mate[i]);
-                    for (std::size_t p = 0; p < half[i].size(); ++p) {
-                        const Tile A = regroup(chs[i]->tiles[p], half_groups(chs[i]->tiles[p].t.nrows));
-                        const Tile B = regroup(chs[j]->tiles[p], half_groups(chs[j]->tiles[p].t.nrows));
-                        auto [dst, srcw] = place(pair_bytes(half[i][p], half[j][p]), true);
-                        const int kga = A.t.nrows << A.t.groups, kgb = B.t.nrows << B.t.groups, S = kga + kgb;
-                        const int ia = A.t.iters, ib = B.t.iters, im = std::max(ia, ib);
-                        {
-                            const std::int64_t vb = pad16(static_cast<std::int64_t>(im) * S * 8);
-                            const std::int64_t iba = pad16(static_cast<std::int64_t>(A.idx.size()) * 4);
-                            const std::int64_t ibb = pad16(static_cast<std::int64_t>(B.idx.size()) * 4);
-                            const std::int64_t oba = pad16(static_cast<std::int64_t>(A.outidx.size()) * 4);
-                            StepFields fa = step_fields(A.t), fb = step_fields(B.t);
-                            for (StepFields* f : {&fa, &fb}) {
-                                f->pair = 1;
-                                f->S = static_cast<std::uint32_t>(S);
-                                f->vq = static_cast<std::uint32_t>(vb / 16);
-                                f->gmax_lg = std::max<std::uint32_t>(A.t.groups, B.t.groups);
-                            }
-                            fb.voff = static_cast<std::uint32_t>(kga);
-                            fa.ixq = static_cast<std::uint32_t>(vb / 16);
-                            fb.ixq = static_cast<std::uint32_t>((vb + iba) / 16);
-                            fa.oq = static_cast<std::uint32_t>((vb + iba + ibb) / 16);
-                            fb.oq = static_cast<std::uint32_t>((vb + iba + ibb + oba) / 16);
-                            std::uint32_t hw[8];
-                            pack_step(fa, hw);
-                            pack_step(fb, hw + 4);
-                            std::memcpy(dst, hw, 32);
+                    // a group step per piece: sub-tiles side by side on 32 / n lanes each
+                    const std::vector<int>& members = groups[grp[i]];
+                    const int n = static_cast<int>(members.size());
+                    const int nsub_lg = n == 4 ? 2 : 1;
+                    for (std::size_t p = 0; p < chs[i]->tiles.size(); ++p) {
+                        std::vector<Tile> T;
+                        std::vector<const Shape*> shp;
+                        for (int m = 0; m < n; ++m) {
+                            const Tile& src = chs[members[m]]->tiles[p];
+                            T.push_back(regroup(src, lane_groups(src.t.nrows, 32 / n)));
+                            shp.push_back(&gshape[grp[i]][m][p]);
                         }
-                        double* V = reinterpret_cast<double*>(dst + 32);
-                        for (int t = 0; t < im; ++t) {
-                            for (int l = 0; l < kga; ++l) {
-                                const std::size_t at = static_cast<std::size_t>(t) * S + l;
-                                if (!tmpl) V[at] = t < ia ? A.vals[static_cast<std::size_t>(t) * kga + l] : 0.0;
-                                if (tmpl) srcw[4 + at] = t < ia ? A.src[static_cast<std::size_t>(t) * kga + l] : kSrcZero;
-                            }
-                            for (int l = 0; l < kgb; ++l) {
-                                const std::size_t at = static_cast<std::size_t>(t) * S + kga + l;
-                                if (!tmpl) V[at] = t < ib ? B.vals[static_cast<std::size_t>(t) * kgb + l] : 0.0;
-                                if (tmpl) srcw[4 + at] = t < ib ? B.src[static_cast<std::size_t>(t) * kgb + l] : kSrcZero;
-                            }
+                        auto [dst, srcw] = place(group_bytes(shp), nsub_lg);
+                        int S = 0, im = 0;
+                        std::uint32_t glmax = 0;
+                        std::vector<int> kg(n), voff(n);
+                        for (int m = 0; m < n; ++m) {
+                            kg[m] = T[m].t.nrows << T[m].t.groups;
+                            voff[m] = S;
+                            S += kg[m];
+                            im = std::max<int>(im, T[m].t.iters);
+                            glmax = std::max<std::uint32_t>(glmax, T[m].t.groups);
                         }
-                        std::int64_t off = 32 + pad16(static_cast<std::int64_t>(im) * S * 8);
-                        for (const Tile* T : {&A, &B}) {
-                            if (!T->idx.empty()) std::memcpy(dst + off, T->idx.data(), T->idx.size() * 4);
-                            off += pad16(static_cast<std::int64_t>(T->idx.size()) * 4);
+                        const std::int64_t vb = pad16(static_cast<std::int64_t>(im) * S * 8);
+                        std::int64_t off = vb;
+                        std::vector<StepFields> f(n);
+                        for (int m = 0; m < n; ++m) {  // index lists after the values
+                            f[m] = step_fields(T[m].t);
+                            f[m].ixq = static_cast<std::uint32_t>(off / 16);
+                            off += pad16(static_cast<std::int64_t>(T[m].idx.size()) * 4);
                         }
-                        for (const Tile* T : {&A, &B}) {
-                            if (!T->outidx.empty()) std::memcpy(dst + off, T->outidx.data(), T->outidx.size() * 4);
-                            off += pad16(static_cast<std::int64_t>(T->outidx.size()) * 4);
+                        for (int m = 0; m < n; ++m) {  // then the output-row lists
+                            f[m].oq = static_cast<std::uint32_t>(off / 16);
+                            off += pad16(static_cast<std::int64_t>(T[m].outidx.size()) * 4);
+                        }
+                        for (int m = 0; m < n; ++m) {
+                            f[m].nsub_lg = static_cast<std::uint32_t>(nsub_lg);
+                            f[m].S = static_cast<std::uint32_t>(S);
+                            f[m].vq = static_cast<std::uint32_t>(vb / 16);
+                            f[m].gmax_lg = glmax;
+                            f[m].voff = static_cast<std::uint32_t>(voff[m]);
+                            std::uint32_t hw[4];
+                            pack_step(f[m], hw);
+                            std::memcpy(dst + 16 * m, hw, 16);
+                        }
+                        char* tile = dst + 16 * n;
+                        double* V = reinterpret_cast<double*>(tile);
+                        const std::size_t w0 = static_cast<std::size_t>(2 * n);  // value words after the sub-headers
+                        for (int m = 0; m < n; ++m)
+                            for (int t = 0; t < im; ++t)
+                                for (int l = 0; l < kg[m]; ++l) {
+                                    const std::size_t at = static_cast<std::size_t>(t) * S + voff[m] + l;
+                                    const bool in = t < T[m].t.iters;
+                                    if (!tmpl) V[at] = in ? T[m].vals[static_cast<std::size_t>(t) * kg[m] + l] : 0.0;
+                                    if (tmpl) srcw[w0 + at] = in ? T[m].src[static_cast<std::size_t>(t) * kg[m] + l] : kSrcZero;
+                                }
+                        for (int m = 0; m < n; ++m) {
+                            if (!T[m].idx.empty()) std::memcpy(tile + 16 * f[m].ixq, T[m].idx.data(), T[m].idx.size() * 4);
+                            if (!T[m].outidx.empty()) std::memcpy(tile + 16 * f[m].oq, T[m].outidx.data(), T[m].outidx.size() * 4);
                         }
                         pools.tile_values += static_cast<std::int64_t>(im) * S;
-                        pools.n_tiles += 2;
+                        pools.n_tiles += n;
                     }
                 }
                 row[kSolveWarps + w] = steps_of[w];

@@ -39,31 +39,30 @@ void run_phase(const SolvePools& sp, PartState& st) {
     std::vector<double>& other = (kind & kPhaseBackward) ? st.T : st.X;
     const char* base = reinterpret_cast<const char*>(sp.stream.data() + pd.stream);
     for (int w = 0; w < kSolveWarps; ++w) {
-        double acc[2][32] = {{0}};  // per sub-tile (a pair step's halves), per row
+        double acc[4][32] = {{0}};  // per sub-tile (a group step's 1, 2 or 4), per row
         const int s_end = row[kSolveWarps + w];
         while (st.wdone[w] < s_end) {
             const std::int32_t* ue = &sp.units[2 * (pd.units + pd.warp_base[w] + st.wu[w])];
             const char* ubase = base + std::int64_t(ue[0]) * 16;
             std::uint32_t& cur = st.wcur[w];
-            // step sub-headers (device_format.hpp): A, and B for a pair step; the tile data
-            // follows the sub-headers, every offset is read from the sub-header like the kernel
-            StepFields hd[2];
+            // step sub-headers (device_format.hpp): one per sub-tile (1, 2 or 4); the tile data
+            // follows them, every offset is read from the sub-header like the kernel
+            StepFields hd[4];
             std::uint32_t hw[4];
             std::memcpy(hw, ubase + std::int64_t(cur) * 16, 16);
             hd[0] = unpack_step(hw);
-            const bool pair = hd[0].pair;
-            if (pair) {
-                std::memcpy(hw, ubase + std::int64_t(cur) * 16 + 16, 16);
-                hd[1] = unpack_step(hw);
+            const int nsub = 1 << hd[0].nsub_lg;
+            for (int q = 1; q < nsub; ++q) {
+                std::memcpy(hw, ubase + std::int64_t(cur) * 16 + 16 * q, 16);
+                hd[q] = unpack_step(hw);
             }
-            const char* tb = ubase + std::int64_t(cur) * 16 + (pair ? 32 : 16);
+            const char* tb = ubase + std::int64_t(cur) * 16 + 16 * nsub;
             cur = hd[0].next;
             ++st.wdone[w];
             if (cur == kNoStep) {  // unit consumed
                 ++st.wu[w];
                 cur = 0;
             }
-            const int nsub = pair ? 2 : 1;
             for (int q = 0; q < nsub; ++q) {
                 const StepFields& task = hd[q];
                 const int k = task.k, G = 1 << task.lg, iters = task.iters, S = task.S, voff = task.voff;

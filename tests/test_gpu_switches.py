@@ -45,6 +45,7 @@ CASES = [
     {"BDDC_K_FULL": "1"},           # row-major K_i, local_blocks CTAs per subdomain
     {"BDDC_PAIR_TILES": "0"},       # no pair steps in the interior-solve programs
     {"BDDC_MAX_CHAIN": "0"},        # forward levels coloured into phases only
+    {"BDDC_QUAD_TILES": "0"},       # pairs only (no 8-lane quads)
 ]
 
 

@@ -51,12 +51,14 @@ int main(int argc, char** argv) {
                     std::memcpy(hw, ub + std::int64_t(cur) * 16, 16);
                     const StepFields t = unpack_step(hw);
                     ++nsteps;
-                    if (t.pair) {  // a pair step: count its B tile too
+                    if (t.nsub_lg) {  // a group step: count its other tiles too
                         ++npairs;
-                        std::memcpy(hw, ub + std::int64_t(cur) * 16 + 16, 16);
-                        const StepFields b = unpack_step(hw);
-                        ntile++;
-                        nval += (long long)b.iters * b.k * (1 << b.lg);
+                        for (int q = 1; q < (1 << t.nsub_lg); ++q) {
+                            std::memcpy(hw, ub + std::int64_t(cur) * 16 + 16 * q, 16);
+                            const StepFields b = unpack_step(hw);
+                            ntile++;
+                            nval += (long long)b.iters * b.k * (1 << b.lg);
+                        }
                     }
                     cur = t.next;
                     const int G = 1 << t.lg;
@@ -72,7 +74,7 @@ int main(int argc, char** argv) {
                 }
             }
     }
-    std::printf("tiles %lld values %lld (%.1f per tile), warp steps %lld (%lld pair steps)\n", ntile, nval,
+    std::printf("tiles %lld values %lld (%.1f per tile), warp steps %lld (%lld group steps)\n", ntile, nval,
                 double(nval) / ntile, nsteps, npairs);
     std::printf("%4s %3s %5s %8s %10s %8s\n", "k", "G", "flags", "tiles", "values", "v/tile");
     for (auto& [key, c] : hist)
