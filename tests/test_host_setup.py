@@ -2,7 +2,9 @@
 matrix against the reference (tests/golden), plus the reference's setup identities
 (test_bddc.cpp:56-125, 371-402) and the device-program builder via its CPU simulator."""
 import ctypes as C
+import json
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -198,3 +200,39 @@ def test_gpu_setup_templates_reproduce_host_programs(sim, cx, cy, kx, ky, parts,
     err = C.create_string_buffer(512)
     bad = sim.bddc_sim_template_check(cx, cy, kx, ky, parts, leaf, coords, err, 512)
     assert bad == 0, err.value
+
+
+VARIANT_SCRIPT = r"""
+import ctypes as C, json, os, sys
+import numpy as np
+sys.path.insert(0, ROOT); sys.path.insert(0, ROOT + "/oracle")
+import bddc_oracle as o
+sim = C.CDLL(os.path.join(ROOT, "tests", "native", "libbddc_sim.so"))
+dp = C.POINTER(C.c_double)
+out = {}
+for k, m, parts, leaf in ((3, 32, 2, 24), (4, 16, 2, 8), (3, 32, 1, 16)):
+    prob, cs, b = o.poisson_setup(k, m)
+    P = o.Preconditioner(prob.global_matrix, prob.local_matrices, prob.decomposition, cs)
+    ref = P.interior_correction(b)
+    z = np.zeros_like(b)
+    err = C.create_string_buffer(512)
+    rc = sim.bddc_sim_interior_solve(k * m, k * m, k, k, parts, leaf, 1, b.ctypes.data_as(dp), z.ctypes.data_as(dp), err, 512)
+    out[f"{k}/{m}/{parts}/{leaf}"] = [rc, err.value.decode(), float(np.abs(z - ref).max() / np.abs(ref).max())]
+print(json.dumps(out))
+""".replace("ROOT", repr(ROOT))
+
+
+@pytest.mark.parametrize("env", [{"BDDC_PAIR_TILES": "0"}, {"BDDC_QUAD_TILES": "0"}, {"BDDC_MAX_CHAIN": "0"},
+                                 {"BDDC_MAX_CHAIN": "100"}, {"BDDC_MIN_CHUNK_ROWS": "4"}],
+                         ids=lambda e: ",".join(f"{a}={b}" for a, b in e.items()))
+def test_program_shape_switches_keep_the_solve(sim, env):
+    # the builder's shape switches (group steps, chained levels, chunk rows; read once per
+    # process) change the program, never the solve: the CPU interpreter reproduces the oracle
+    import subprocess
+    r = subprocess.run([sys.executable, "-c", VARIANT_SCRIPT], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for case, (rc, msg, e) in res.items():
+        assert rc == 0, (case, msg)
+        assert e <= 1e-12, (case, e)
