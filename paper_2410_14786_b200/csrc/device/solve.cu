@@ -191,6 +191,8 @@ template <int MODE, int CLUSTER, bool STATS>
 __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const SolveParams S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     pdl_trigger();
+    const long long t_entry = STATS ? clock64() : 0;  // CTA 0 prologue / epilogue markers (STATS)
+    long long* const mkp = STATS ? S.stats + static_cast<long long>(gridDim.x) * kSolveWarps * 8 + 256 + 2 * 256 * kSolveWarps : nullptr;
     double rz = 0.0;  // MODE 3 with dot_part: this thread's share of r.z
     const PartDesc& pdr = S.parts[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     // everything above reads only the program (immutable): it overlaps the predecessor's tail
     // under programmatic dependent launch; from here on the inputs are the predecessors'
     pdl_wait();
+    if (STATS && blockIdx.x == 0 && tid == 0) mkp[4] = clock64() - t_entry;  // predecessor done
     if (skip_launch(S.skip)) {  // uniform over the cluster: every CTA reads the same flag
         for (int u = 0; u < nsl && u < nunits; ++u) mbar_wait(&my_bars[u], 0);  // drain the prefetch
         return;
@@ -348,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
 
     constexpr bool stats = STATS;
     long long t_start = stats ? clock64() : 0, t_wait = 0, t_bar = 0, t_refill = 0, t_tiles = 0, n_tiles = 0;
+    if (stats && blockIdx.x == 0 && tid == 0) mkp[5] = t_start - t_entry;  // prologue (incl. the wait for the predecessor)
     long long tprof[4] = {0, 0, 0, 0};  // STATS: decode, loop, reduction, flush cycles
     double acc = 0.0;
     int u = 0;                // this warp's current unit (ring slot u & (nsl - 1))
@@ -507,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         }
     }
 
+    if (stats && blockIdx.x == 0 && tid == 0) mkp[6] = clock64() - t_entry;  // phase loop done
     if (stats && lane == 0) {
         long long* o = S.stats + (static_cast<long long>(blockIdx.x) * kSolveWarps + warp) * 8;
         o[0] = clock64() - t_start;
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
         rz = block_sum<kThreads>(rz, red);
         if (tid == 0) S.dot_part[blockIdx.x] = rz;
     }
+    if (stats && blockIdx.x == 0 && tid == 0) mkp[7] = clock64() - t_entry;  // through the epilogue
     if (CLUSTER > 1) cluster_sync_all();  // keep our Q alive until the partner is done
     if (MODE == 0 || MODE == 3) publish<kThreads>(S.pub);  // after the cluster barrier: non-last CTAs return
 }

@@ -42,6 +42,8 @@ for ph in range(nph):
     print(f"{ph:3d} {dur:6d} {bm:9d} {bmean:10.0f} {int(nt[ph].max()):9d} {nt[ph].mean():10.1f} "
           f"{int(wt[ph].max()):9d} {wt[ph].mean():9.0f} {int(tt[ph][pw[ph].argmax()]):9d} {int(rf[ph][pw[ph].argmax()]):9d}")
 mk = raw[nparts * W * 8 + 256 + 2 * 256 * W: nparts * W * 8 + 256 + 2 * 256 * W + 8]
+print("CTA 0 since kernel entry: predecessor done", mk[4], "prologue done", mk[5], "phase loop done", mk[6],
+      "epilogue done", mk[7])
 print("markers (cycles since start): before cluster sync", mk[0], "after", mk[1], "after combine", mk[2],
       "after split switch", mk[3], "| timeline at the combine phase end", [int(t) for t in tl[:nph] if 0 < t <= mk[0]][-1:])
 print(f"sum: duration {tot_dur}, sum of busiest warps {tot_max}, sum of mean busy {tot_mean:.0f}")
