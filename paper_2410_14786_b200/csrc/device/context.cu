@@ -215,7 +215,7 @@ struct GpuContext::Impl {
     // interface data
     DBuf<SubdomainDesc> subs;
     DBuf<std::int32_t> iface_dof, iface_gid, iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col,
-        gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col;
+        gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col, iface_own4;
     DBuf<double> iface_w, kmat, phig, phi, gi_row_val, coarse_inv, lrow_val, weights_local;
     // coarse matrix (CG mode)
     DBuf<std::int32_t> Ac_ptr, Ac_col;
@@ -500,6 +500,7 @@ struct GpuContext::Impl {
         P.iface_writer = iface_writer.p;
         P.gi_own_ptr = gi_own_ptr.p;
         P.gi_own_ref = gi_own_ref.p;
+        P.iface_own4 = iface_own4.p;
         P.hbuf = hbuf.p;
         P.in = in;
         P.out = out;
@@ -1988,6 +1989,20 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     tm.mark("subdomain / K / Phi buffers");
     I.gi_own_ptr.upload(img.gi_own_ptr);
     I.gi_own_ref.upload(img.gi_own_ref);
+    {
+        // each local interface slot's owners as one int4 (the interior solve's z_G gather)
+        std::vector<std::int32_t> own4(4 * std::max<std::size_t>(img.iface_gid.size(), 1), -1);
+        for (std::size_t k = 0; k < img.iface_gid.size(); ++k) {
+            const int gid = img.iface_gid[k];
+            const int o0 = img.gi_own_ptr[gid], o1 = img.gi_own_ptr[gid + 1];
+            if (o1 - o0 > 4) {
+                own4[4 * k] = -2 - gid;
+                continue;
+            }
+            for (int o = o0; o < o1; ++o) own4[4 * k + (o - o0)] = img.gi_own_ref[o];
+        }
+        I.iface_own4.upload(own4);
+    }
     I.dof_own_ptr.upload(img.dof_own_ptr);
     I.dof_own_ref.upload(img.dof_own_ref);
     I.c_own_ptr.upload(img.c_own_ptr);

@@ -305,11 +305,32 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             if (MODE == 1 || MODE == 3) {
                 // z_G = sum over the subdomains sharing the dof of their h, ascending
                 // subdomain (reference prolong_add order, preconditioner.cpp:168-169,189-190)
-                const int gid = S.iface_gid[sd.iface + g];
                 z = 0.0;
                 const bool ll = MODE == 3 && S.ll_h;  // peers' h_i from the LL buffer (multi-GPU, fused)
                 const std::uint32_t tag = ll ? ll_tag(S.seq_h) : 0u;
-                const int o0 = S.gi_own_ptr[gid], o1 = S.gi_own_ptr[gid + 1];
+                // the writer's output slot and r entry, loaded alongside the owners' h (independent)
+                const bool writes = pdr.rank == 0 && S.iface_writer[sd.iface + g];
+                const int dof = writes ? S.iface_dof[sd.iface + g] : 0;
+                const double rdot = MODE == 3 && writes && S.dot_part && dof < S.n_dot ? S.dot_r[dof] : 0.0;
+                // the slot's owners (<= 4): their h slots in one 16-byte load, no owner-list walk
+                const int4 o4 = __ldg(reinterpret_cast<const int4*>(S.iface_own4) + sd.iface + g);
+                int o0 = 0, o1 = 0;
+                if (o4.x <= -2) {  // more than four owners: the owner list of global dof -2 - x
+                    o0 = S.gi_own_ptr[-2 - o4.x];
+                    o1 = S.gi_own_ptr[-1 - o4.x];
+                } else {
+                    const int ref[4] = {o4.x, o4.y, o4.z, o4.w};
+                    double h[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        h[t] = ref[t] < 0 ? 0.0
+                               : (ll && ref[t] >= S.ll_h_base)
+                                   ? ll_get(S.ll_h + 2 * static_cast<std::int64_t>(ref[t] - S.ll_h_base), tag)
+                                   : S.hbuf[ref[t]];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (ref[t] >= 0) z += h[t];
+                }
                 for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
                     int ref[4];
                     double h[4];
@@ -325,10 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                     for (int t = 0; t < 4; ++t)
                         if (ref[t] >= 0) z += h[t];
                 }
-                if (pdr.rank == 0 && S.iface_writer[sd.iface + g]) {
-                    const int dof = S.iface_dof[sd.iface + g];
+                if (writes) {
                     S.out[dof] = z;
-                    if (MODE == 3 && S.dot_part && dof < S.n_dot) rz += S.dot_r[dof] * z;
+                    if (MODE == 3 && S.dot_part && dof < S.n_dot) rz += rdot * z;
                 }
             } else {
                 z = S.hbuf[sd.hbuf + g];

@@ -26,6 +26,9 @@ struct SolveParams {
     const std::int32_t* iface_dof;
     const std::int32_t* iface_writer;
     const std::int32_t* gi_own_ptr;
+    // per local interface slot: the hbuf slots of its owners (ascending subdomain, -1 padded) as
+    // an int4; x <= -2: more than four owners, the owner list of global interface dof -2 - x
+    const std::int32_t* iface_own4;
     const std::int32_t* gi_own_ref;
     const double* hbuf;
     const double* in;
