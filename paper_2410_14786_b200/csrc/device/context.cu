@@ -1964,7 +1964,12 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.iface_dof.upload(img.iface_dof);
     I.iface_w.upload(img.iface_w);
     I.iface_gid.upload(img.iface_gid);
-    I.iface_writer.upload(img.iface_writer);
+    {
+        // the solve kernel reads the written dof directly: the slot's dof if it is the writer, -1
+        std::vector<std::int32_t> wdof(img.iface_writer.size());
+        for (std::size_t k = 0; k < wdof.size(); ++k) wdof[k] = img.iface_writer[k] ? img.iface_dof[k] : -1;
+        I.iface_writer.upload(wdof);
+    }
     if (img.device_values) {  // written by the device setup
         I.kmat.alloc(std::max<std::int64_t>(img.kmat_total, 1));
         I.phig.alloc(std::max<std::int64_t>(img.phig_total, 1));

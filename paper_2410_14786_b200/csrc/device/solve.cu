@@ -274,18 +274,19 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
     const std::int32_t* gmap = S.gmap + pdr.gmap;
     const int n_loc = pdr.n_loc, n_top = pdr.n_top;
     // rhs gather: four independent index/value loads in flight per thread
-    for (int l0 = tid; l0 < ldn_p; l0 += 4 * kThreads) {
-        int gi[4];
+    constexpr int kInRows = MODE == 3 ? 4 : 12;  // rows per thread per round (MODE 3: no gather)
+    for (int l0 = tid; l0 < ldn_p; l0 += kInRows * kThreads) {
+        int gi[kInRows];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kInRows; ++q) {
             const int l = l0 + q * kThreads;
-            gi[q] = l < n_loc ? __ldg(gmap + l) : -1;
+            gi[q] = MODE != 3 && l < n_loc ? __ldg(gmap + l) : -1;
         }
-        double gv[4];
+        double gv[kInRows];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) gv[q] = (MODE != 3 && gi[q] >= 0) ? S.in[gi[q]] : 0.0;
+        for (int q = 0; q < kInRows; ++q) gv[q] = (MODE != 3 && gi[q] >= 0) ? S.in[gi[q]] : 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kInRows; ++q) {
             const int l = l0 + q * kThreads;
             if (l < ldn_p) {
                 T[l] = gv[q];
@@ -309,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
                 const bool ll = MODE == 3 && S.ll_h;  // peers' h_i from the LL buffer (multi-GPU, fused)
                 const std::uint32_t tag = ll ? ll_tag(S.seq_h) : 0u;
                 // the writer's output slot and r entry, loaded alongside the owners' h (independent)
-                const bool writes = pdr.rank == 0 && S.iface_writer[sd.iface + g];
-                const int dof = writes ? S.iface_dof[sd.iface + g] : 0;
+                const int dof = pdr.rank == 0 ? S.iface_writer[sd.iface + g] : -1;  // written dof or -1
+                const bool writes = dof >= 0;
                 const double rdot = MODE == 3 && writes && S.dot_part && dof < S.n_dot ? S.dot_r[dof] : 0.0;
                 // the slot's owners (<= 4): their h slots in one 16-byte load, no owner-list walk
                 const int4 o4 = __ldg(reinterpret_cast<const int4*>(S.iface_own4) + sd.iface + g);
@@ -546,21 +547,28 @@ __global__ void __launch_bounds__(kThreads, 1) interior_solve_kernel(const Solve
             for (int i = 0; i < 4; ++i) tpo[warp * 4 + i] = tprof[i];
         }
     }
-    for (int l0 = tid; l0 < pdr.n_write; l0 += 4 * kThreads) {
-        int gi[4];
+    // output: twelve rows per thread per round, all their index loads, then all their r loads,
+    // in flight together (two dependent global levels per round; r.z keeps its row order)
+    constexpr int kOutRows = 12;
+    for (int l0 = tid; l0 < pdr.n_write; l0 += kOutRows * kThreads) {
+        int gi[kOutRows];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kOutRows; ++q) {
             const int l = l0 + q * kThreads;
             gi[q] = l < pdr.n_write ? __ldg(gmap + l) : -1;
         }
+        double dr[kOutRows];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kOutRows; ++q)
+            dr[q] = MODE == 3 && S.dot_part && gi[q] >= 0 && gi[q] < S.n_dot ? S.dot_r[gi[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kOutRows; ++q)
             if (gi[q] >= 0) {
                 if (MODE == 3) {
                     // z_I = u0 - extension, or (split apply) the backward sweep's result itself
                     const double z = S.y_in ? T[l0 + q * kThreads] : S.u0[gi[q]] - T[l0 + q * kThreads];
                     S.out[gi[q]] = z;
-                    if (S.dot_part && gi[q] < S.n_dot) rz += S.dot_r[gi[q]] * z;
+                    if (S.dot_part && gi[q] < S.n_dot) rz += dr[q] * z;
                 } else {
                     S.out[gi[q]] = T[l0 + q * kThreads];
                 }

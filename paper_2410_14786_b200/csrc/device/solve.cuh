@@ -24,7 +24,7 @@ struct SolveParams {
     const double* couple_val;
     const std::int32_t* iface_gid;
     const std::int32_t* iface_dof;
-    const std::int32_t* iface_writer;
+    const std::int32_t* iface_writer;  // per local interface slot: the dof it writes (its writer), else -1
     const std::int32_t* gi_own_ptr;
     // per local interface slot: the hbuf slots of its owners (ascending subdomain, -1 padded) as
     // an int4; x <= -2: more than four owners, the owner list of global interface dof -2 - x
