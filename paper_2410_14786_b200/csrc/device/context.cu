@@ -214,6 +214,7 @@ struct GpuContext::Impl {
     SolveLaunch launch;
     // interface data
     DBuf<SubdomainDesc> subs;
+    DBuf<std::int32_t> slot_rows;  // per local interface slot: {begin, end} of its global A_GI row
     DBuf<std::int32_t> iface_dof, iface_gid, iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col,
         gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col, iface_own4;
     DBuf<double> iface_w, kmat, phig, phi, gi_row_val, coarse_inv, lrow_val, weights_local;
@@ -555,6 +556,7 @@ struct GpuContext::Impl {
         P.iface_w = iface_w.p;
         P.iface_gid = iface_gid.p;
         P.gi_row_ptr = gi_row_ptr.p;
+        P.slot_rows = slot_rows.p;
         P.gi_row_col = gi_row_col.p;
         P.gi_row_val = gi_row_val.p;
         P.kmat = kmat.p;
@@ -1989,6 +1991,14 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.lrow_val.upload(img.lrow_val);
     I.gi_dof.upload(img.gi_dof);
     I.gi_row_ptr.upload(img.gi_row_ptr);
+    {
+        std::vector<std::int32_t> sr(2 * std::max<std::size_t>(img.iface_gid.size(), 1), 0);
+        for (std::size_t k = 0; k < img.iface_gid.size(); ++k) {
+            sr[2 * k] = img.gi_row_ptr[img.iface_gid[k]];
+            sr[2 * k + 1] = img.gi_row_ptr[img.iface_gid[k] + 1];
+        }
+        I.slot_rows.upload(sr);
+    }
     I.gi_row_col.upload(img.gi_row_col);
     I.gi_row_val.upload(img.gi_row_val);
     tm.mark("subdomain / K / Phi buffers");

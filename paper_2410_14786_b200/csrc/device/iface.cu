@@ -27,11 +27,14 @@ iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const d
     const SubdomainDesc& sd = P.subs[blockIdx.x];
     const int ng = sd.n_iface, np = sd.n_primal;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-        const int gid = P.iface_gid[sd.iface + g];
+        // the slot's A_GI row range, its r entry and weight: independent loads, issued together
+        const int2 er = __ldg(reinterpret_cast<const int2*>(P.slot_rows) + sd.iface + g);
+        const double rg = r[P.iface_dof[sd.iface + g]];
+        const double wg = P.iface_w[sd.iface + g];
         double acc = 0.0;
         // four entries per round: their column / value / u0 loads issue back to back; the sum
         // stays sequential in CSR order
-        const int e0 = P.gi_row_ptr[gid], e1 = P.gi_row_ptr[gid + 1];
+        const int e0 = er.x, e1 = er.y;
         for (int e = e0; e < e1; e += 4) {
             int col[4];
             double val[4], u[4];
@@ -50,7 +53,7 @@ iface_restrict_kernel(const IfaceParams P, const double* __restrict__ r, const d
             for (int q = 0; q < 4; ++q)
                 if (col[q] >= 0) acc += val[q] * u[q];
         }
-        const double v = P.iface_w[sd.iface + g] * (r[P.iface_dof[sd.iface + g]] - acc);
+        const double v = wg * (rg - acc);
         sg[g] = v;
         P.gbuf[sd.hbuf + g] = v;
     }

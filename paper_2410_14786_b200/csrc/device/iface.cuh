@@ -25,6 +25,7 @@ struct IfaceParams {
     const double* iface_w;
     const std::int32_t* iface_gid;
     const std::int32_t* gi_row_ptr;
+    const std::int32_t* slot_rows;  // per local interface slot: its global A_GI row range {begin, end}
     const std::int32_t* gi_row_col;
     const double* gi_row_val;
     // dense blocks. kpacked: K_i stored as its upper triangle of 32 x 32 tiles (iface.cu,
