@@ -216,7 +216,7 @@ struct GpuContext::Impl {
     DBuf<SubdomainDesc> subs;
     DBuf<std::int32_t> slot_rows;  // per local interface slot: {begin, end} of its global A_GI row
     DBuf<std::int32_t> iface_dof, iface_gid, iface_writer, primal, local_dofs, gi_dof, gi_row_ptr, gi_row_col,
-        gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col, iface_own4;
+        gi_own_ptr, gi_own_ref, dof_own_ptr, dof_own_ref, c_own_ptr, c_own_ref, lrow_ptr, lrow_col, iface_own4, c_own4;
     DBuf<double> iface_w, kmat, phig, phi, gi_row_val, coarse_inv, lrow_val, weights_local;
     // coarse matrix (CG mode)
     DBuf<std::int32_t> Ac_ptr, Ac_col;
@@ -568,6 +568,7 @@ struct GpuContext::Impl {
         P.n_coarse = n_coarse;
         P.c_own_ptr = c_own_ptr.p;
         P.c_own_ref = c_own_ref.p;
+        P.c_own4 = c_own4.p;
         P.coarse_inv = coarse_inv.p;
         if (coop_coarse) {
             P.rc_g = rc_g.p;
@@ -2022,6 +2023,19 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     I.dof_own_ref.upload(img.dof_own_ref);
     I.c_own_ptr.upload(img.c_own_ptr);
     I.c_own_ref.upload(img.c_own_ref);
+    {
+        const std::size_t nc = img.c_own_ptr.empty() ? 0 : img.c_own_ptr.size() - 1;
+        std::vector<std::int32_t> c4(4 * std::max<std::size_t>(nc, 1), -1);
+        for (std::size_t q = 0; q < nc; ++q) {
+            const int o0 = img.c_own_ptr[q], o1 = img.c_own_ptr[q + 1];
+            if (o1 - o0 > 4) {
+                c4[4 * q] = -2;
+                continue;
+            }
+            for (int o = o0; o < o1; ++o) c4[4 * q + (o - o0)] = img.c_own_ref[o];
+        }
+        I.c_own4.upload(c4);
+    }
     I.rc_g.alloc(std::max(img.n_coarse, 1));
     I.coarse_ctr.alloc(1);
     BDDC_CUDA(cudaMemset(I.coarse_ctr.p, 0, sizeof(unsigned long long)));

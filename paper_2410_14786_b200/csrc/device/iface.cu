@@ -109,7 +109,29 @@ constexpr int kLocalRows = BDDC_LOCAL_ROWS;  // rows per warp in flight (2 * kLo
 // subdomain's x_c rows, and every warp finishes its rows with Phi_G x_c.
 __device__ __forceinline__ double coarse_entry(const IfaceParams& P, int q, std::uint32_t tag_c) {
     double acc = 0.0;
-    const int o0 = P.c_own_ptr[q], o1 = P.c_own_ptr[q + 1];
+    int o0 = 0, o1 = 0;
+    if (P.c_own4) {  // the entry's owners (<= 4) in one 16-byte load: no owner-list walk
+        const int4 o4 = __ldg(reinterpret_cast<const int4*>(P.c_own4) + q);
+        if (o4.x <= -2) {  // more than four owners: the owner list
+            o0 = P.c_own_ptr[q];
+            o1 = P.c_own_ptr[q + 1];
+        } else {
+            const int ref[4] = {o4.x, o4.y, o4.z, o4.w};
+            double c[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                c[t] = ref[t] < 0 ? 0.0
+                       : (P.ll_c && (ref[t] < P.c_own_lo || ref[t] >= P.c_own_hi))
+                           ? ll_get(P.ll_c + 2 * static_cast<std::int64_t>(ref[t]), tag_c)
+                           : P.cbuf[ref[t]];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (ref[t] >= 0) acc += c[t];
+        }
+    } else {
+        o0 = P.c_own_ptr[q];
+        o1 = P.c_own_ptr[q + 1];
+    }
     for (int o = o0; o < o1; o += 4) {  // the owners' loads of a round back to back
         int ref[4];
         double c[4];

@@ -41,6 +41,9 @@ struct IfaceParams {
     int n_coarse;
     const std::int32_t* c_own_ptr;
     const std::int32_t* c_own_ref;
+    // per coarse dof: its owners' cbuf slots (ascending subdomain, -1 padded) as an int4; x <= -2:
+    // more than four owners (the owner list); null: owner lists only
+    const std::int32_t* c_own4;
     const double* coarse_inv;
     // scratch
     double* gbuf;   // w * r'_G per (subdomain, gamma)
