@@ -51,6 +51,63 @@ struct DBuf {
     }
 };
 
+// Non-owning view into a scratch block.
+template <typename T>
+struct Span {
+    T* p = nullptr;
+    std::size_t n = 0;
+};
+
+// The device setup's numeric scratch (supernode fronts, Schur blocks, saddle matrices: ~1-2 GB at
+// C2) as one block that is kept for the process's next setup on the same device, like a caching
+// allocator: freeing and re-mapping GBs costs 20-200 ms of host time per construction, more than
+// the setup's kernels. BDDC_SETUP_SCRATCH_CACHE=0 frees it after every setup.
+std::mutex g_scratch_mu;
+std::vector<std::pair<char*, std::size_t>> g_scratch(64, {nullptr, 0});
+
+struct SetupScratch {
+    char* p = nullptr;
+    std::size_t bytes = 0;
+    int dev = 0;
+    SetupScratch(int device, std::size_t need) : dev(device) {
+        char* stale = nullptr;
+        {
+            std::lock_guard<std::mutex> g(g_scratch_mu);
+            auto& c = g_scratch.at(static_cast<std::size_t>(dev));
+            if (c.first && c.second >= need) {
+                p = c.first;
+                bytes = c.second;
+            } else {
+                stale = c.first;
+            }
+            if (p || stale) c = {nullptr, 0};
+        }
+        if (stale) BDDC_CUDA(cudaFree(stale));
+        if (!p) {
+            bytes = need;
+            BDDC_CUDA(cudaMalloc(&p, bytes));
+        }
+    }
+    SetupScratch(const SetupScratch&) = delete;
+    SetupScratch& operator=(const SetupScratch&) = delete;
+    ~SetupScratch() {
+        static const bool keep = !(std::getenv("BDDC_SETUP_SCRATCH_CACHE") && std::atoi(std::getenv("BDDC_SETUP_SCRATCH_CACHE")) == 0);
+        cudaDeviceSynchronize();  // no setup work may still use the block
+        char* drop = p;
+        if (keep) {
+            std::lock_guard<std::mutex> g(g_scratch_mu);
+            auto& c = g_scratch[static_cast<std::size_t>(dev)];
+            if (!c.first || c.second < bytes) {
+                std::swap(c.first, drop);
+                std::swap(c.second, bytes);
+            }
+        }
+        if (drop) cudaFree(drop);
+    }
+    template <typename T>
+    Span<T> span(std::size_t off, std::size_t n) const { return {reinterpret_cast<T*>(p + off), n}; }
+};
+
 struct Event {
     cudaEvent_t e = nullptr;
     Event() { BDDC_CUDA(cudaEventCreate(&e)); }
@@ -145,7 +202,8 @@ const char* const kEnvSwitches[] = {
     "BDDC_DIR_SPMV", "BDDC_PDL", "BDDC_PROFILE_STRIDE", "BDDC_ZERO_COPY", "BDDC_HOST_THREADS",
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
-    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP", "BDDC_MAX_CHAIN", "BDDC_QUAD_TILES"};
+    "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP", "BDDC_MAX_CHAIN", "BDDC_QUAD_TILES",
+    "BDDC_SETUP_SCRATCH_CACHE"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
@@ -778,15 +836,28 @@ struct GpuContext::Impl {
                     tot[t] = std::max(tot[t], need[k][t] + 1);
                 }
             }
-        DBuf<double> aval, fronts, Sb, Db, Mb, aci_dev;
-        DBuf<int> piv, status;
-        aval.alloc(tot[0]);
-        fronts.alloc(tot[1]);
-        Sb.alloc(tot[2]);
-        Db.alloc(tot[3]);
-        Mb.alloc(tot[4]);
-        piv.alloc(tot[5]);
-        status.alloc(4 * batches.size());
+        std::vector<std::int64_t> aci_off(nsub);
+        std::int64_t aci_total = 0;
+        for (index_t i = 0; i < nsub; ++i) {
+            aci_off[i] = aci_total;
+            aci_total += static_cast<std::int64_t>(setup.subs[i].n_primal) * setup.subs[i].n_primal;
+        }
+        // one scratch block, 256-byte aligned pieces
+        std::size_t sbytes = 0;
+        auto carve = [&sbytes](std::size_t b) {
+            const std::size_t o = sbytes;
+            sbytes += (b + 255) & ~std::size_t(255);
+            return o;
+        };
+        const std::size_t n_aci = static_cast<std::size_t>(std::max<std::int64_t>(aci_total, 1));
+        const std::size_t o_aval = carve(8 * tot[0]), o_fronts = carve(8 * tot[1]), o_S = carve(8 * tot[2]),
+                          o_D = carve(8 * tot[3]), o_M = carve(8 * tot[4]), o_aci = carve(8 * n_aci),
+                          o_piv = carve(4 * tot[5]), o_status = carve(16 * batches.size());
+        SetupScratch scratch(device, sbytes);
+        const Span<double> aval = scratch.span<double>(o_aval, tot[0]), fronts = scratch.span<double>(o_fronts, tot[1]),
+                           Sb = scratch.span<double>(o_S, tot[2]), Db = scratch.span<double>(o_D, tot[3]),
+                           Mb = scratch.span<double>(o_M, tot[4]), aci_dev = scratch.span<double>(o_aci, n_aci);
+        const Span<int> piv = scratch.span<int>(o_piv, tot[5]), status = scratch.span<int>(o_status, 4 * batches.size());
         BDDC_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int) * status.n, s));
         struct Streams {
             std::vector<cudaStream_t> v;
@@ -800,13 +871,6 @@ struct GpuContext::Impl {
         BDDC_CUDA(cudaEventRecord(ready.e, s));
         for (cudaStream_t q : cs.v) BDDC_CUDA(cudaStreamWaitEvent(q, ready.e, 0));
         // ---- jobs of every batch: fills and saddle output offsets
-        std::vector<std::int64_t> aci_off(nsub);
-        std::int64_t aci_total = 0;
-        for (index_t i = 0; i < nsub; ++i) {
-            aci_off[i] = aci_total;
-            aci_total += static_cast<std::int64_t>(setup.subs[i].n_primal) * setup.subs[i].n_primal;
-        }
-        aci_dev.alloc(std::max<std::int64_t>(aci_total, 1));
         std::vector<std::vector<const DeviceImage::Fill*>> fill_of(nprog, std::vector<const DeviceImage::Fill*>(nsub));
         for (int q = 0; q < nprog; ++q)
             for (const auto& f : img.fills[q]) fill_of[q][f.sub] = &f;

@@ -16,6 +16,7 @@ for name, args, kw in [("c2", (800, 8), {}), ("c5", (352, 8), dict(kappa_decades
             pre = Preconditioner(p, setup=setup)
             dt = time.time() - t
             st = pre.stats()
+            print("  ", name, setup, "ctor %.3f s" % dt, flush=True)
             if best is None or st["setup_seconds"] < best[1]["setup_seconds"]:
                 best = (dt, st)
             del pre
