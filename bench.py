@@ -368,11 +368,13 @@ def measure(cfg: str, D: Dist, steps: int, warmup: int, clocks_on: bool = True) 
         xh, rh = pre.pcg(b_pin, opts, precondition=precondition, out=x_pin)
     torch.cuda.synchronize()
     D.barrier()
+    gc.disable()
     t0 = time.perf_counter()
     for _ in range(steps):
         xh, rh = pre.pcg(b_pin, opts, precondition=precondition, out=x_pin)
-    D.barrier()
     e2e_local = (time.perf_counter() - t0) / steps
+    gc.enable()
+    D.barrier()
     it = rh.iterations
     h2d = 8 * n_local
     d2h = 8 * n_rows + 8 * it + 8 * it + 8 * max(0, it - 1) + 32 * (it + 1)  # x, history, alpha, beta, scalars

@@ -10,3 +10,7 @@ PCG=1 NAPPLY=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read
   --clock-control none --csv --log-file gpurun_out/kernels.csv python tools/profile_apply.py > gpurun_out/ncu1.log 2>&1; echo "ncu list rc $?"
 PCG=0 NAPPLY=3 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:interior_solve_kernel<\\(int\\)(0|3)," -s 2 -c 2 \
   -o gpurun_out/interior_full python tools/profile_apply.py > gpurun_out/ncu2.log 2>&1; echo "ncu full rc $?"
+# the bench command's own launch list: the BDDC-PCG kernels (the setup kernels filtered out by name)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  -k "regex:^(interior_solve_kernel|iface_|spmv_dot|update_kernel|xpay_kernel|init_rho|dot_kernel|finalize_kernel|coarse_)" \
+  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extra > gpurun_out/ncu3.log 2>&1; echo "ncu bench list rc $?"

@@ -28,13 +28,16 @@ def launches(path):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi, ui = h.index("Metric Name"), h.index("Metric Unit")
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9}
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in rows[hdr + 1:]:
-        if len(r) <= vi:
+        # one row per (launch, metric): only the duration rows count (a log with DRAM metrics too)
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].replace("(anonymous namespace)::", "").replace("unnamed>::", "")
         name = name.split("(")[0]
-        tot[name] += float(r[vi].replace(",", ""))
+        tot[name] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)  # ns
         cnt[name] += 1
     T = sum(tot.values())
     out = ["| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
@@ -71,8 +74,8 @@ def main():
     if os.path.exists(lpath):
         with open(os.path.join(ROOT, "profiles", f"{tag}_launches.md"), "w") as f:
             f.write(f"# {tag}: device time per kernel (ncu gpu__time_duration.sum, --clock-control none)\n\n")
-            f.write("Cold-cache, serialised launches of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`;\n"
-                    "compare shares, not absolutes.\n\n")
+            cmd = os.environ.get("NCU_CMD", "python bench.py --steps 2 --warmup 3 --no-cpu-baseline")
+            f.write(f"Cold-cache, serialised launches of `{cmd}`;\ncompare shares, not absolutes.\n\n")
             f.write(launches(lpath) + "\n")
     if fpath and os.path.exists(fpath):
         recs = full(fpath)
