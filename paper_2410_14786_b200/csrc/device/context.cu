@@ -451,7 +451,10 @@ struct GpuContext::Impl {
     index_t n_global = 0, n_rows = 0, n_owned = 0;
     std::string symmetry_error;  // distributed: global symmetry check done once at creation
     // host entry points: the rank-local layout as runs {local, global, length} of consecutive
-    // indices (split at n_rows), copied through a pinned staging buffer
+    // indices (split at n_rows, and into pieces of at most kRunPiece entries: a warp copies one
+    // piece, so a rank whose rows are one contiguous block of the global vector still spreads
+    // its PCIe reads over the whole GPU), copied through a pinned staging buffer
+    static constexpr index_t kRunPiece = 1024;
     std::vector<std::array<index_t, 3>> runs;
     double* stage = nullptr;
     void build_runs() {
@@ -459,7 +462,7 @@ struct GpuContext::Impl {
         const index_t n = static_cast<index_t>(l2g.size());
         for (index_t l = 0; l < n;) {
             index_t e = l + 1;
-            while (e < n && e != n_rows && l2g[e] == l2g[e - 1] + 1) ++e;
+            while (e < n && e != n_rows && e - l < kRunPiece && l2g[e] == l2g[e - 1] + 1) ++e;
             runs.push_back({l, l2g[l], e - l});
             l = e;
         }
@@ -773,6 +776,7 @@ struct GpuContext::Impl {
                                               sizeof(std::int32_t) * T.srcmap.size(), cudaMemcpyHostToDevice, s));
                 }
         }
+        tm.mark("    templates upload");
         // ---- every class's plan in three blobs (int32 / int64 / double) with per-class offsets
         std::vector<std::int32_t> bi;
         std::vector<std::int64_t> bl;
@@ -803,6 +807,7 @@ struct GpuContext::Impl {
         pi.upload(bi);
         pl.upload(bl);
         pdv.upload(bd);
+        tm.mark("    plan blobs upload");
         // ---- batches: members per batch from a scratch budget. When every class's first batch
         // fits the budget at once, the classes get disjoint scratch and a stream each and run
         // concurrently (their pipelines are independent); otherwise they share the scratch in turn.
@@ -859,6 +864,7 @@ struct GpuContext::Impl {
                            Mb = scratch.span<double>(o_M, tot[4]), aci_dev = scratch.span<double>(o_aci, n_aci);
         const Span<int> piv = scratch.span<int>(o_piv, tot[5]), status = scratch.span<int>(o_status, 4 * batches.size());
         BDDC_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int) * status.n, s));
+        tm.mark("    scratch");
         struct Streams {
             std::vector<cudaStream_t> v;
             ~Streams() {
