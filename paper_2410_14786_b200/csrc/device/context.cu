@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <thread>
@@ -743,7 +745,46 @@ struct GpuContext::Impl {
     // (one interior solve per primal column, all subdomains at once). A handful of allocations
     // in total: every class's plan goes up in one blob per element type, the scratch buffers are
     // sized for the largest batch and reused, the jobs of all batches go up at once.
-    void device_setup(const std::vector<SetupClass>& classes, const DeviceImage& img) {
+    // every class x program template (stream words + source codes) in two device buffers; run on
+    // a host thread of its own while the device image is built (a pageable copy of ~100 MB)
+    struct Templates {
+        DBuf<double> word;
+        DBuf<std::int32_t> code;
+        std::vector<std::array<std::int64_t, 3>> off;
+        std::exception_ptr error;
+    };
+    static void upload_templates(const std::vector<SetupClass>& classes, int device, Templates& T) {
+        try {
+            BDDC_CUDA(cudaSetDevice(device));
+            cudaStream_t us = nullptr;
+            BDDC_CUDA(cudaStreamCreateWithFlags(&us, cudaStreamNonBlocking));
+            const std::size_t ncls = classes.size();
+            T.off.assign(ncls, {});
+            std::int64_t total = 0;
+            for (std::size_t k = 0; k < ncls; ++k)
+                for (int q = 0; q < 3; ++q) {
+                    T.off[k][q] = total;
+                    total += static_cast<std::int64_t>(classes[k].prog[q].stream.size());
+                }
+            T.word.alloc(std::max<std::int64_t>(total, 1));
+            T.code.alloc(std::max<std::int64_t>(total, 1));
+            for (std::size_t k = 0; k < ncls; ++k)
+                for (int q = 0; q < 3; ++q) {
+                    const SolvePools& P = classes[k].prog[q];
+                    if (P.stream.empty()) continue;
+                    BDDC_CUDA(cudaMemcpyAsync(T.word.p + T.off[k][q], P.stream.data(), sizeof(double) * P.stream.size(),
+                                              cudaMemcpyHostToDevice, us));
+                    BDDC_CUDA(cudaMemcpyAsync(T.code.p + T.off[k][q], P.srcmap.data(),
+                                              sizeof(std::int32_t) * P.srcmap.size(), cudaMemcpyHostToDevice, us));
+                }
+            BDDC_CUDA(cudaStreamSynchronize(us));
+            cudaStreamDestroy(us);
+        } catch (...) {
+            T.error = std::current_exception();
+        }
+    }
+
+    void device_setup(const std::vector<SetupClass>& classes, const DeviceImage& img, const Templates& T) {
         const auto t0 = std::chrono::steady_clock::now();
         SetupTimer tm;
         cudaStream_t s = stream;
@@ -754,28 +795,10 @@ struct GpuContext::Impl {
         while (nprog < 3 && !img.fills[nprog].empty()) ++nprog;
         const std::size_t ncls = classes.size();
 
-        // ---- templates (word + source code per stream word), straight into one device buffer
-        std::vector<std::array<std::int64_t, 3>> toff(ncls);
-        DBuf<double> tword;
-        DBuf<std::int32_t> tcode;
-        {
-            std::int64_t total = 0;
-            for (std::size_t k = 0; k < ncls; ++k)
-                for (int q = 0; q < nprog; ++q) {
-                    toff[k][q] = total;
-                    total += static_cast<std::int64_t>(classes[k].prog[q].stream.size());
-                }
-            tword.alloc(std::max<std::int64_t>(total, 1));
-            tcode.alloc(std::max<std::int64_t>(total, 1));
-            for (std::size_t k = 0; k < ncls; ++k)
-                for (int q = 0; q < nprog; ++q) {
-                    const SolvePools& T = classes[k].prog[q];
-                    BDDC_CUDA(cudaMemcpyAsync(tword.p + toff[k][q], T.stream.data(), sizeof(double) * T.stream.size(),
-                                              cudaMemcpyHostToDevice, s));
-                    BDDC_CUDA(cudaMemcpyAsync(tcode.p + toff[k][q], T.srcmap.data(),
-                                              sizeof(std::int32_t) * T.srcmap.size(), cudaMemcpyHostToDevice, s));
-                }
-        }
+        // ---- templates (word + source code per stream word): uploaded by upload_templates
+        const auto& toff = T.off;
+        const DBuf<double>& tword = T.word;
+        const DBuf<std::int32_t>& tcode = T.code;
         tm.mark("    templates upload");
         // ---- every class's plan in three blobs (int32 / int64 / double) with per-class offsets
         std::vector<std::int32_t> bi;
@@ -1964,11 +1987,28 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     int spw = 0;
     tm.mark("host numeric setup (host path)");
     std::vector<SetupClass> classes;
+    std::unique_ptr<Impl::Templates> tmpl;
+    // joined before the classes go away, also when the setup throws
+    struct Joiner {
+        std::thread t;
+        bool joinable() const { return t.joinable(); }
+        void join() { t.join(); }
+        Joiner& operator=(std::thread&& o) {
+            t = std::move(o);
+            return *this;
+        }
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } tup;
     for (;; unit = units[++ui]) {
         if (on_device) {
+            if (tup.joinable()) tup.join();  // a previous unit size's upload still reads the classes
             classes = plan_gpu_setup(I.pb.local_matrices, d, I.pb.constraints, coords, fo, parts, unit,
                                      I.opt.harmonic, workers);
             tm.mark("  class plan (symbolic, templates)");
+            tmpl = std::make_unique<Impl::Templates>();
+            tup = std::thread(Impl::upload_templates, std::cref(classes), I.device, std::ref(*tmpl));
             img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
                                      unit, I.plan.get(), I.opt.harmonic, &classes);
             tm.mark("  device image");
@@ -2187,7 +2227,9 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         if (!(p2p_env && std::atoi(p2p_env) == 0)) I.setup_peer_links(img);
     }
     tm.mark("uploads + buffers");
-    if (on_device) I.device_setup(classes, img);
+    if (tup.joinable()) tup.join();
+    if (tmpl && tmpl->error) std::rethrow_exception(tmpl->error);
+    if (on_device) I.device_setup(classes, img, *tmpl);
     tm.mark("device numeric setup");
     if (I.kpacked) I.pack_k(img);
     I.finish_coarse(dist);
