@@ -2,6 +2,7 @@
 // status codes; messages are kept verbatim for bddc_last_error().
 #include "../../include/bddc_b200.h"
 
+#include <memory>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -15,7 +16,9 @@
 using namespace bddc_b200;
 
 struct bddc_problem {
-    ProblemData data;
+    // filled at creation, read-only afterwards: GPU contexts share it instead of copying it
+    std::shared_ptr<ProblemData> shared = std::make_shared<ProblemData>();
+    ProblemData& data = *shared;
     std::vector<double> rhs;
     // flattened storage backing bddc_problem_get_view
     std::vector<bddc_csr_view> local_views, constraint_views;
@@ -390,7 +393,7 @@ int bddc_gpu_create(const bddc_problem* p, const bddc_gpu_options* opt, bddc_gpu
     return guarded([&] {
         if (!p || !out) throw std::invalid_argument("bddc_gpu_create: null argument");
         auto c = std::make_unique<bddc_gpu_ctx>();
-        c->ctx = std::make_unique<GpuContext>(p->data, to_gpu(opt));
+        c->ctx = std::make_unique<GpuContext>(std::shared_ptr<const ProblemData>(p->shared), to_gpu(opt));
         *out = c.release();
     });
 }
@@ -417,7 +420,7 @@ int bddc_gpu_create_dist(const bddc_problem* p, const bddc_gpu_options* opt, con
         if (dist->subdomain_rank)
             spec.sub_rank.assign(dist->subdomain_rank, dist->subdomain_rank + p->data.decomposition.n_subdomains);
         auto c = std::make_unique<bddc_gpu_ctx>();
-        c->ctx = std::make_unique<GpuContext>(p->data, to_gpu(opt), &spec);
+        c->ctx = std::make_unique<GpuContext>(std::shared_ptr<const ProblemData>(p->shared), to_gpu(opt), &spec);
         *out = c.release();
     });
 }

@@ -84,6 +84,8 @@ enum class Stage : int { interior = 0, coarse = 1, local = 2, static_condensatio
 class GpuContext {
 public:
     GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpec* dist = nullptr);
+    // shares the (immutable) problem instead of copying it
+    GpuContext(std::shared_ptr<const ProblemData> problem, const GpuOptions& opt, const DistSpec* dist = nullptr);
     ~GpuContext();
     GpuContext(const GpuContext&) = delete;
     GpuContext& operator=(const GpuContext&) = delete;

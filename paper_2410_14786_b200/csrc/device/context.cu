@@ -228,7 +228,9 @@ constexpr index_t kDenseCoarseMax = 4096;
 }  // namespace
 
 struct GpuContext::Impl {
-    ProblemData pb;
+    // the problem, shared with the caller's handle (read-only: no per-construction deep copy)
+    std::shared_ptr<const ProblemData> pbs;
+    const ProblemData& pb() const { return *pbs; }
     GpuOptions opt;
     BddcSetup setup;
     int device = 0;
@@ -612,7 +614,7 @@ struct GpuContext::Impl {
         IfaceParams P{};
         P.skip = apply_skip;
         P.subs = subs.p;
-        P.n_subdomains = pb.decomposition.n_subdomains;
+        P.n_subdomains = pb().decomposition.n_subdomains;
         P.max_iface = max_iface;
         P.max_primal = max_primal;
         P.iface_dof = iface_dof.p;
@@ -647,8 +649,8 @@ struct GpuContext::Impl {
     StageParams stage_params() const {
         StageParams P{};
         P.subs = subs.p;
-        P.n_subdomains = pb.decomposition.n_subdomains;
-        P.n_vector = pb.decomposition.global_dofs;
+        P.n_subdomains = pb().decomposition.n_subdomains;
+        P.n_vector = pb().decomposition.global_dofs;
         P.max_primal = max_primal;
         P.local_dofs = local_dofs.p;
         P.phi = phi.p;
@@ -788,7 +790,7 @@ struct GpuContext::Impl {
         const auto t0 = std::chrono::steady_clock::now();
         SetupTimer tm;
         cudaStream_t s = stream;
-        const Decomposition& d = pb.decomposition;
+        const Decomposition& d = pb().decomposition;
         const index_t nsub = d.n_subdomains;
         SolveProgram* pools[3] = {&prog, &harm, &head};
         int nprog = 0;
@@ -969,7 +971,7 @@ struct GpuContext::Impl {
             for (int v : C.sn_nc) max_nc = std::max(max_nc, v);
             av.resize(static_cast<std::size_t>(Bt.nb) * C.nnz);
             for (int b = 0; b < Bt.nb; ++b) {
-                const CsrMatrix& A = pb.local_matrices[C.members[Bt.m0 + b]];
+                const CsrMatrix& A = pb().local_matrices[C.members[Bt.m0 + b]];
                 std::copy(A.values.begin(), A.values.end(), av.begin() + static_cast<std::ptrdiff_t>(b) * C.nnz);
             }
             // (pageable source: the call returns once av is staged, so the next batch may refill it)
@@ -1057,7 +1059,7 @@ struct GpuContext::Impl {
     // A_c from every subdomain's A_ci (gathered over the ranks), then its dense inverse (device
     // setup: on the GPU; host setup: setup.cpp) unless the coarse CG is in effect
     void finish_coarse(const DistSpec* dist) {
-        const index_t nc = pb.constraints.n_coarse;
+        const index_t nc = pb().constraints.n_coarse;
         const bool host_inverse = opt.coarse_mode == 0 && !opt.setup_on_device;
         if (plan) {
             // gather the padded per-rank blocks over NCCL, then assemble in ascending global
@@ -1094,7 +1096,7 @@ struct GpuContext::Impl {
         } else {
             std::vector<const std::vector<double>*> blocks(setup.subs.size());
             for (std::size_t i = 0; i < blocks.size(); ++i) blocks[i] = &setup.subs[i].aci;
-            assemble_coarse(setup, blocks, pb.constraints.primal_maps, nc, host_inverse);
+            assemble_coarse(setup, blocks, pb().constraints.primal_maps, nc, host_inverse);
         }
         if (opt.coarse_mode == 0) {
             if (opt.setup_on_device) {
@@ -1190,7 +1192,7 @@ struct GpuContext::Impl {
     }
 
     void ensure_pcg(int max_it) {
-        const index_t n = pb.decomposition.global_dofs;
+        const index_t n = pb().decomposition.global_dofs;
         if (!x.p) {
             for (DBuf<double>* b : {&x, &r, &z, &p, &q, &p_alt}) b->alloc(n);
             const int g = pcg_grid_for(dist() ? n_rows : n);
@@ -1220,7 +1222,7 @@ struct GpuContext::Impl {
 
     PcgDevice pcg_device(const SolverOpts& o, double* xd, double* rd, double* zd) const {
         PcgDevice D{};
-        D.n = dist() ? n_rows : pb.decomposition.global_dofs;
+        D.n = dist() ? n_rows : pb().decomposition.global_dofs;
         D.n_dot = dist() ? n_owned : D.n;
         D.n_dir = D.n;  // pcg() widens it to the halo when z's halo arrives with r.z
         D.grid = pcg_grid_for(D.n);
@@ -1507,7 +1509,7 @@ struct GpuContext::Impl {
     double first_nonfinite_global(const double* v, cudaStream_t s) {
         DBuf<int> bad;
         bad.alloc(1);
-        device_first_nonfinite(dist() ? static_cast<int>(n_owned) : static_cast<int>(pb.decomposition.global_dofs), v,
+        device_first_nonfinite(dist() ? static_cast<int>(n_owned) : static_cast<int>(pb().decomposition.global_dofs), v,
                                bad.p, s);
         int idx = 0;
         BDDC_CUDA(cudaMemcpyAsync(&idx, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1538,9 +1540,9 @@ struct GpuContext::Impl {
         if (dist()) {
             if (!symmetry_error.empty()) throw std::invalid_argument(symmetry_error);
         } else {
-            sampled_symmetry_check(pb.global_matrix);
+            sampled_symmetry_check(pb().global_matrix);
         }
-        const index_t n = pb.decomposition.global_dofs;
+        const index_t n = pb().decomposition.global_dofs;
         ensure_pcg(o.max_iterations);
         SolveResult rep;
         double* xd = xout;
@@ -1906,7 +1908,11 @@ struct GpuContext::Impl {
     }
 };
 
-GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpec* dist) {
+GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpec* dist)
+    : GpuContext(std::make_shared<const ProblemData>(std::move(problem)), opt, dist) {}
+
+GpuContext::GpuContext(std::shared_ptr<const ProblemData> problem, const GpuOptions& opt, const DistSpec* dist) {
+    if (!problem) throw std::invalid_argument("bddc setup: null problem");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
@@ -1914,21 +1920,21 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     BDDC_CUDA(cudaSetDevice(opt.device));
     impl_.reset(new Impl);
     Impl& I = *impl_;
-    I.n_global = problem.decomposition.global_dofs;
+    I.n_global = problem->decomposition.global_dofs;
     if (dist && dist->world > 1) {
         try {
-            sampled_symmetry_check(problem.global_matrix);
+            sampled_symmetry_check(problem->global_matrix);
         } catch (const std::invalid_argument& e) {
             I.symmetry_error = e.what();
         }
         I.plan = std::make_unique<RankPlan>(make_rank_plan(
-            problem, dist->rank, dist->world, dist->sub_rank.empty() ? nullptr : dist->sub_rank.data()));
-        I.pb = std::move(I.plan->local);
+            *problem, dist->rank, dist->world, dist->sub_rank.empty() ? nullptr : dist->sub_rank.data()));
+        I.pbs = std::make_shared<const ProblemData>(std::move(I.plan->local));
         I.plan->local = ProblemData{};
         I.n_rows = I.plan->n_rows;
         I.n_owned = I.plan->n_owned;
     } else {
-        I.pb = std::move(problem);
+        I.pbs = std::move(problem);
     }
     I.opt = opt;
     I.device = opt.device;
@@ -1938,11 +1944,11 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
             "BDDC_NO_EXCHANGE=1 skips every inter-GPU exchange (timing experiments, wrong results); "
             "it needs BDDC_EXPERIMENTS=1");
     // the dense replicated A_c^-1 only up to kDenseCoarseMax coarse dofs; the coarse CG beyond
-    if (I.opt.coarse_mode == 0 && I.pb.constraints.n_coarse > kDenseCoarseMax) I.opt.coarse_mode = 1;
+    if (I.opt.coarse_mode == 0 && I.pb().constraints.n_coarse > kDenseCoarseMax) I.opt.coarse_mode = 1;
     BDDC_CUDA(cudaSetDevice(I.device));
-    const Decomposition& d = I.pb.decomposition;
-    if (static_cast<index_t>(I.pb.local_matrices.size()) != d.n_subdomains ||
-        static_cast<index_t>(I.pb.constraints.constraint_matrices.size()) != d.n_subdomains)
+    const Decomposition& d = I.pb().decomposition;
+    if (static_cast<index_t>(I.pb().local_matrices.size()) != d.n_subdomains ||
+        static_cast<index_t>(I.pb().constraints.constraint_matrices.size()) != d.n_subdomains)
         throw std::invalid_argument("bddc setup: subdomain count mismatch");
     const int workers = opt.workers > 0 ? opt.workers : std::max(1u, std::thread::hardware_concurrency());
     FactorOptions fo;
@@ -1950,7 +1956,7 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     const auto t_setup0 = std::chrono::steady_clock::now();
     SetupTimer tm;
     const bool on_device = I.opt.setup_on_device;
-    const index_t* coords = I.pb.coords.empty() ? nullptr : I.pb.coords.data();
+    const index_t* coords = I.pb().coords.empty() ? nullptr : I.pb().coords.data();
     if (I.plan) I.comm = std::make_unique<Comm>(dist->nccl_id, dist->rank, dist->world);
     if (on_device) {
         // GPU setup: the host keeps only the per-subdomain sizes (the class planner below does the
@@ -1958,13 +1964,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
         I.setup.subs.resize(d.n_subdomains);
         for (index_t i = 0; i < d.n_subdomains; ++i) {
             SubdomainSetup& S = I.setup.subs[i];
-            S.n_local = I.pb.local_matrices[i].nrows;
+            S.n_local = I.pb().local_matrices[i].nrows;
             S.n_interior = d.interior_counts[i];
             S.n_iface = S.n_local - S.n_interior;
-            S.n_primal = I.pb.constraints.constraint_matrices[i].nrows;
+            S.n_primal = I.pb().constraints.constraint_matrices[i].nrows;
         }
     } else {
-        I.setup = bddc_setup(I.pb.local_matrices, d, I.pb.constraints, coords, workers, fo, /*assemble=*/false,
+        I.setup = bddc_setup(I.pb().local_matrices, d, I.pb().constraints, coords, workers, fo, /*assemble=*/false,
                              /*dense_inverse=*/false);
     }
     int nsm = 148;
@@ -2004,16 +2010,16 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     for (;; unit = units[++ui]) {
         if (on_device) {
             if (tup.joinable()) tup.join();  // a previous unit size's upload still reads the classes
-            classes = plan_gpu_setup(I.pb.local_matrices, d, I.pb.constraints, coords, fo, parts, unit,
+            classes = plan_gpu_setup(I.pb().local_matrices, d, I.pb().constraints, coords, fo, parts, unit,
                                      I.opt.harmonic, workers);
             tm.mark("  class plan (symbolic, templates)");
             tmpl = std::make_unique<Impl::Templates>();
             tup = std::thread(Impl::upload_templates, std::cref(classes), I.device, std::ref(*tmpl));
-            img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
+            img = build_device_image(d, I.pb().constraints, I.pb().local_matrices, I.pb().global_matrix, I.setup, parts,
                                      unit, I.plan.get(), I.opt.harmonic, &classes);
             tm.mark("  device image");
         } else {
-            img = build_device_image(d, I.pb.constraints, I.pb.local_matrices, I.pb.global_matrix, I.setup, parts,
+            img = build_device_image(d, I.pb().constraints, I.pb().local_matrices, I.pb().global_matrix, I.setup, parts,
                                      unit, I.plan.get(), I.opt.harmonic);
         }
         const std::size_t fixed = interior_solve_smem(img.solve.max_loc, img.solve.max_top, img.max_iface, unit, 0);
@@ -2156,13 +2162,13 @@ GpuContext::GpuContext(ProblemData problem, const GpuOptions& opt, const DistSpe
     }
     I.coarse_status.alloc(4);
     tm.mark("  coarse-owner maps, weights");
-    I.A_ptr.upload(I.pb.global_matrix.row_offsets);
-    I.A_col.upload(I.pb.global_matrix.col_indices);
-    I.A_val.upload(I.pb.global_matrix.values);
+    I.A_ptr.upload(I.pb().global_matrix.row_offsets);
+    I.A_col.upload(I.pb().global_matrix.col_indices);
+    I.A_val.upload(I.pb().global_matrix.values);
     {
         // sliced ELL copy for the PCG SpMV: slices of 32 rows, width = the slice's longest row,
         // entries column-major within the slice in CSR order (padding never read: row lengths)
-        const CsrMatrix& A = I.pb.global_matrix;
+        const CsrMatrix& A = I.pb().global_matrix;
         const index_t nr = A.nrows, ns = (nr + 31) / 32;
         std::vector<std::int64_t> off(static_cast<std::size_t>(ns) + 1, 0);
         std::vector<std::uint16_t> len(static_cast<std::size_t>(ns) * 32, 0);
@@ -2249,7 +2255,7 @@ GpuContext::~GpuContext() {
 
 void dist_nccl_id(char out[128]) { nccl_unique_id(out); }
 
-index_t GpuContext::n() const { return impl_->pb.decomposition.global_dofs; }
+index_t GpuContext::n() const { return impl_->pb().decomposition.global_dofs; }
 index_t GpuContext::n_global() const { return impl_->n_global; }
 index_t GpuContext::n_owned() const { return impl_->dist() ? impl_->n_owned : n(); }
 index_t GpuContext::n_rows() const { return impl_->dist() ? impl_->n_rows : n(); }
@@ -2271,7 +2277,7 @@ void GpuContext::apply_device(const double* r, double* z, void* stream) {
 void GpuContext::apply_host(const double* r, double* z) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
-    const index_t n = I.pb.decomposition.global_dofs;
+    const index_t n = I.pb().decomposition.global_dofs;
     ensure_finite(r, I.n_global, "bddc apply");
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {
@@ -2304,7 +2310,7 @@ void GpuContext::apply_host(const double* r, double* z) {
 SolveResult GpuContext::pcg_host(const double* b, const SolverOpts& o, double* x, bool precondition) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
-    const index_t n = I.pb.decomposition.global_dofs;
+    const index_t n = I.pb().decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) {  // non-finite rhs entries: found on the devices, agreed over the ranks (pcg)
         const void* bm = mapped_host_pointer(b);
@@ -2341,7 +2347,7 @@ SolveResult GpuContext::pcg_device(const double* b, const SolverOpts& o, double*
 void GpuContext::stage_host(Stage st, const double* in0, const double* in1, const double* in2, double* out) {
     std::lock_guard<std::mutex> lk(impl_->mu);
     Impl& I = *impl_;
-    const index_t n = I.pb.decomposition.global_dofs;
+    const index_t n = I.pb().decomposition.global_dofs;
     BDDC_CUDA(cudaSetDevice(I.device));
     if (I.dist()) throw std::invalid_argument("stage hooks are single-GPU parity hooks");
     cudaStream_t s = I.stream;
@@ -2391,7 +2397,7 @@ void GpuContext::stage_host(Stage st, const double* in0, const double* in1, cons
 }
 
 const BddcSetup& GpuContext::setup() const { return impl_->setup; }
-const ProblemData& GpuContext::problem() const { return impl_->pb; }
+const ProblemData& GpuContext::problem() const { return impl_->pb(); }
 double GpuContext::setup_seconds() const { return impl_->setup.seconds; }
 double GpuContext::setup_device_seconds() const { return impl_->setup_device_s; }
 
@@ -2429,7 +2435,7 @@ std::int64_t GpuContext::interior_pass_bytes() const { return impl_->solve_strea
 int GpuContext::solve_parts() const { return impl_->launch.cluster; }
 std::int64_t GpuContext::apply_bytes() const {
     const Impl& I = *impl_;
-    const std::int64_t n = I.pb.decomposition.global_dofs;
+    const std::int64_t n = I.pb().decomposition.global_dofs;
     // algorithmic FP64 bytes: the two interior solves (forward + backward over every factor
     // value; the harmonic extension's forward sweep only over its active supernodes), K_i,
     // Phi_G (restrict + prolong), the coarse inverse, interface rows and coupling, plus vector
