@@ -137,3 +137,31 @@ def test_cluster_saddle_inverse_is_bitwise_the_global_one(gpu):
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert res[0] == res[1]
+
+
+def test_repeated_setups_share_scratch_and_problem(gpu):
+    """Constructions of different sizes in one process (the cached setup scratch block grows and
+    is reused; every context shares its problem's data): each preconditioner's blocks and apply
+    are bitwise those of the first construction of the same problem, also after the problem
+    handle that built an earlier context is gone."""
+    small = Problem.poisson(128, 4, rhs_seed=3)
+    big = Problem.poisson(352, 8, kappa_decades=2.0, kappa_seed=0x5EED, rhs_seed=5)
+    r_small = np.random.default_rng(1).standard_normal(small.global_dofs)
+    first = Preconditioner(small)
+    z0 = first.apply(r_small)
+    b0 = [first.subdomain_blocks(i)[2] for i in range(small.n_subdomains)]
+    second = Preconditioner(big)  # larger scratch: the cached block is replaced
+    r_big = np.random.default_rng(2).standard_normal(big.global_dofs)
+    zb = second.apply(r_big)
+    del first
+    third = Preconditioner(small)  # the larger cached block is reused
+    assert np.array_equal(third.apply(r_small), z0)
+    assert all(np.array_equal(third.subdomain_blocks(i)[2], b0[i]) for i in range(small.n_subdomains))
+    # a context outlives the Python problem object that built it (shared problem data)
+    tmp = Problem.poisson(352, 8, kappa_decades=2.0, kappa_seed=0x5EED, rhs_seed=5)
+    fourth = Preconditioner(tmp)
+    fourth.problem = None
+    del tmp
+    assert np.array_equal(fourth.apply(r_big), zb)
+    del second
+    assert np.array_equal(fourth.apply(r_big), zb)

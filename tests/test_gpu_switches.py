@@ -46,6 +46,7 @@ CASES = [
     {"BDDC_PAIR_TILES": "0"},       # no pair steps in the interior-solve programs
     {"BDDC_MAX_CHAIN": "0"},        # forward levels coloured into phases only
     {"BDDC_QUAD_TILES": "0"},       # pairs only (no 8-lane quads)
+    {"BDDC_SETUP_SCRATCH_CACHE": "0"},  # setup scratch freed after every setup
 ]
 
 
