@@ -236,7 +236,9 @@ void bddc_rank_plan_destroy(bddc_rank_plan* plan);
 /* ---- GPU hot path ----
  * On a distributed context the host entry points take GLOBAL vectors and each rank writes
  * the entries of its own subdomains; the *_device entry points take rank-local vectors
- * (bddc_gpu_layout). Every rank must make the same calls in the same order. */
+ * (bddc_gpu_layout). Every rank must make the same calls in the same order.
+ * A context shares the problem's (immutable) data with the handle it was created from: the
+ * problem handle may be destroyed before the context, the data lives until both are gone. */
 int bddc_gpu_create(const bddc_problem* p, const bddc_gpu_options* opt, bddc_gpu_ctx** out);
 int bddc_gpu_apply(bddc_gpu_ctx* ctx, const double* r, double* z);
 int bddc_gpu_apply_device(bddc_gpu_ctx* ctx, const double* r_dev, double* z_dev, void* cuda_stream);
