@@ -36,6 +36,11 @@ extern std::atomic<std::int64_t> g_kernel_launches;
 // (pdl_trigger) and waits for its predecessor (pdl_wait: that grid complete, its memory
 // visible; transitively every earlier grid) before it reads or writes anything a
 // predecessor touches. Both are no-ops for kernels launched without the attribute.
+// GPU-scope acquire-release fence: what the ticket / arrival-counter patterns (writes, fence,
+// relaxed atomic; relaxed read, fence, reads) need. __threadfence() is fence.sc.gpu
+// (MEMBAR.SC.GPU), a sequentially consistent fence that costs more on the critical path.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();  // BDDC_PDL=1 turns the attribute on

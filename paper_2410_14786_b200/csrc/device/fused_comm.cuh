@@ -96,7 +96,7 @@ __device__ __forceinline__ bool publish(const Publish& P) {
     const std::uint32_t tag = last == 0xffffffffu ? 1u : last + 1u;  // never 0 (the buffers start zeroed)
     __syncthreads();  // this CTA's outputs are written
     if (threadIdx.x == 0) {
-        __threadfence();  // local writes only (the peer stores follow: no wait for NVLink acks)
+        fence_acq_rel_gpu();  // local writes only (the peer stores follow: no wait for NVLink acks)
         last_s = atomicAdd(P.ticket, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
     }
     __syncthreads();
@@ -113,7 +113,7 @@ __device__ __forceinline__ bool publish(const Publish& P) {
         if (P.trace) trace_event(P.trace, P.kid * 4 + 2, t_in);
     }
     if (P.part) {
-        __threadfence();  // every other CTA's partial is visible to the last one
+        fence_acq_rel_gpu();  // every other CTA's partial is visible to the last one
         double v = 0.0;
 #pragma unroll 8  // independent loads in flight; the sum order is unchanged
         for (int i = threadIdx.x; i < P.grid; i += THREADS) v += __ldcg(P.part + i);

@@ -234,7 +234,7 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
         for (int q = q0 + lane; q < q1; q += 32) P.rc_g[q] = coarse_entry(P, q, tag_c);
         __syncwarp();
         if (lane == 0) {
-            __threadfence();
+            fence_acq_rel_gpu();
             atomicAdd(P.coarse_ctr, 1ull);
         }
     } else {
@@ -254,7 +254,7 @@ iface_local_kernel(const IfaceParams P, int blocks_per_sub, int with_coarse) {
             const unsigned long long target = (seen + gridDim.x - 1) / gridDim.x * gridDim.x;
             while (*reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr) < target) {
             }
-            __threadfence();
+            fence_acq_rel_gpu();
         }
         __syncthreads();
         for (int q = threadIdx.x; q < nc; q += blockDim.x) rc[q] = __ldcg(P.rc_g + q);
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kSymThreads) iface_local_sym_kernel(const Ifac
             const int q0 = static_cast<int>(static_cast<long long>(nc) * blockIdx.x / gridDim.x);
             const int q1 = static_cast<int>(static_cast<long long>(nc) * (blockIdx.x + 1) / gridDim.x);
             for (int q = q0 + threadIdx.x; q < q1; q += kSymThreads) P.rc_g[q] = coarse_entry(P, q, tag_c);
-            __threadfence();  // each writer's entries visible GPU-wide before the CTA arrives
+            fence_acq_rel_gpu();  // each writer's entries visible GPU-wide before the CTA arrives
         } else {
             for (int q = threadIdx.x; q < nc; q += kSymThreads) rc[q] = coarse_entry(P, q, tag_c);
         }
@@ -428,13 +428,13 @@ __global__ void __launch_bounds__(kSymThreads) iface_local_sym_kernel(const Ifac
     SYM_T(3);
     if (with_coarse == 2 && P.coarse_ctr) {
         if (threadIdx.x == 0) {  // grid barrier (monotonic counter, see iface_local_kernel)
-            __threadfence();
+            fence_acq_rel_gpu();
             atomicAdd(P.coarse_ctr, 1ull);
             const unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr);
             const unsigned long long target = (seen + gridDim.x - 1) / gridDim.x * gridDim.x;
             while (*reinterpret_cast<volatile unsigned long long*>(P.coarse_ctr) < target) {
             }
-            __threadfence();
+            fence_acq_rel_gpu();
         }
         __syncthreads();
         for (int q = threadIdx.x; q < nc; q += blockDim.x) rc[q] = __ldcg(P.rc_g + q);

@@ -247,7 +247,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         unsigned int v;
         do {
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevic
 __device__ __forceinline__ void grid_sync_mono(unsigned long long* ctr) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         const unsigned long long v = atomicAdd(ctr, 1ull);
         const unsigned long long target = (v / gridDim.x + 1) * gridDim.x;
         unsigned long long c;
