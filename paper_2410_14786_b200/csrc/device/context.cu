@@ -205,7 +205,7 @@ const char* const kEnvSwitches[] = {
     "BDDC_UNIT_BYTES", "BDDC_MIN_CHUNK_ROWS", "BDDC_TILE_COST", "BDDC_JOBS_PER_WARP", "BDDC_SOLVE_STATS",
     "BDDC_EXCH_STATS", "BDDC_FUSED_TRACE", "BDDC_NO_EXCHANGE", "BDDC_EXPERIMENTS", "BDDC_SETUP_TIMES",
     "BDDC_PRUNED_JOBS", "BDDC_PLAIN_LOOP", "BDDC_SADDLE_GLOBAL", "BDDC_PAIR_TILES", "BDDC_K_FULL", "BDDC_STEP", "BDDC_MAX_CHAIN", "BDDC_QUAD_TILES",
-    "BDDC_SETUP_SCRATCH_CACHE"};
+    "BDDC_SETUP_SCRATCH_CACHE", "BDDC_ELL16"};
 constexpr int kNumEnvSwitches = sizeof(kEnvSwitches) / sizeof(kEnvSwitches[0]);
 
 // Diagnostics (BDDC_SETUP_TIMES=1): wall time of each setup phase on stderr.
@@ -289,6 +289,7 @@ struct GpuContext::Impl {
     DBuf<std::int64_t> ell_off;  // the global (rank) matrix as sliced ELL (PcgDevice)
     DBuf<std::uint16_t> ell_len;
     DBuf<std::int32_t> ell_col;
+    DBuf<std::int16_t> ell_d16;  // column offsets from the row, when they all fit (else empty)
     DBuf<double> ell_val;
     // scratch
     DBuf<double> U, gbuf, hbuf, cbuf, xc, lbuf, vin, vout, vtmp, vtmp2;
@@ -1232,6 +1233,7 @@ struct GpuContext::Impl {
         D.ell_off = ell_off.p;
         D.ell_len = ell_len.p;
         D.ell_col = ell_col.p;
+        D.ell_d16 = ell_d16.p;
         D.ell_val = ell_val.p;
         D.x = xd;
         D.r = rd;
@@ -2190,8 +2192,19 @@ GpuContext::GpuContext(std::shared_ptr<const ProblemData> problem, const GpuOpti
         I.ell_val.alloc(words);
         BDDC_CUDA(cudaMemsetAsync(I.ell_col.p, 0, sizeof(std::int32_t) * words, I.stream));
         BDDC_CUDA(cudaMemsetAsync(I.ell_val.p, 0, sizeof(double) * words, I.stream));
+        // 16-bit column offsets (half the column bytes of the SpMV) unless one does not fit
+        I.ell_d16.alloc(words);
+        DBuf<int> over;
+        over.alloc(1);
+        BDDC_CUDA(cudaMemsetAsync(I.ell_d16.p, 0, sizeof(std::int16_t) * words, I.stream));
+        BDDC_CUDA(cudaMemsetAsync(over.p, 0, sizeof(int), I.stream));
         device_csr_to_sliced_ell(static_cast<int>(nr), I.A_ptr.p, I.A_col.p, I.A_val.p, I.ell_off.p, I.ell_col.p,
-                                 I.ell_val.p, I.stream);
+                                 I.ell_val.p, I.ell_d16.p, over.p, I.stream);
+        int over_h = 0;
+        BDDC_CUDA(cudaMemcpyAsync(&over_h, over.p, sizeof(int), cudaMemcpyDeviceToHost, I.stream));
+        BDDC_CUDA(cudaStreamSynchronize(I.stream));
+        const char* e16 = std::getenv("BDDC_ELL16");
+        if (over_h || (e16 && std::atoi(e16) == 0)) I.ell_d16.alloc(0);
     }
     tm.mark("  global matrix, sliced ELL");
     const std::size_t n = d.global_dofs;

@@ -24,6 +24,19 @@ __device__ __forceinline__ double sum_ranks(const PcgDevice& D, const double* re
     return block_sum<kVecThreads>(v, scratch);
 }
 
+// column of sliced-ELL entry k of row i: 32-bit columns, or 16-bit offsets from the row (the
+// kernels are instantiated for both; the launch picks the matrix's)
+__device__ __forceinline__ int ell_column(const std::int32_t* __restrict__ c, std::int64_t k, int) { return c[k]; }
+__device__ __forceinline__ int ell_column(const std::int16_t* __restrict__ c, std::int64_t k, int i) {
+    return i + static_cast<int>(c[k]);
+}
+template <typename COL>
+__device__ __forceinline__ const COL* ell_cols(const PcgDevice& D);
+template <>
+__device__ __forceinline__ const std::int32_t* ell_cols<std::int32_t>(const PcgDevice& D) { return D.ell_col; }
+template <>
+__device__ __forceinline__ const std::int16_t* ell_cols<std::int16_t>(const PcgDevice& D) { return D.ell_d16; }
+
 __global__ void __launch_bounds__(kVecThreads) dot_kernel(int n, const double* __restrict__ a,
                                                           const double* __restrict__ b, double* part) {
     __shared__ double scratch[kVecThreads / 32];
@@ -41,6 +54,7 @@ __global__ void __launch_bounds__(kVecThreads) finalize_kernel(const double* par
     if (threadIdx.x == 0) *out = take_sqrt ? sqrt(v) : v;
 }
 
+template <typename COL>
 __global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
     pdl_trigger();
@@ -51,7 +65,7 @@ __global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevic
     double acc = 0.0;
     // sliced ELL: a warp's 32 rows are one slice, so every entry load of the warp is one
     // contiguous 256-byte (values) / 128-byte (columns) access
-    const std::int32_t* __restrict__ ec = D.ell_col;
+    const COL* __restrict__ ec = ell_cols<COL>(D);
     const double* __restrict__ ev = D.ell_val;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
         const std::int64_t base = D.ell_off[i >> 5] + (i & 31);
@@ -61,14 +75,14 @@ __global__ void __launch_bounds__(kVecThreads, 4) spmv_dot_kernel(const PcgDevic
         for (; j + 3 < len; j += 4) {  // four entries' loads in flight; the sum stays in CSR order
             const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
             const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
-            const double x0 = p[ec[base + 32 * j]], x1 = p[ec[base + 32 * (j + 1)]];
-            const double x2 = p[ec[base + 32 * (j + 2)]], x3 = p[ec[base + 32 * (j + 3)]];
+            const double x0 = p[ell_column(ec, base + 32 * j, i)], x1 = p[ell_column(ec, base + 32 * (j + 1), i)];
+            const double x2 = p[ell_column(ec, base + 32 * (j + 2), i)], x3 = p[ell_column(ec, base + 32 * (j + 3), i)];
             y += v0 * x0;
             y += v1 * x1;
             y += v2 * x2;
             y += v3 * x3;
         }
-        for (; j < len; ++j) y += ev[base + 32 * j] * p[ec[base + 32 * j]];
+        for (; j < len; ++j) y += ev[base + 32 * j] * p[ell_column(ec, base + 32 * j, i)];
         q[i] = y;
         if (i < D.n_dot) acc = fma(p[i], y, acc);
     }
@@ -266,11 +280,12 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
 // launch-per-kernel loop, so the iterates are bitwise identical. The vectors change inside the
 // launch and are read through the coherent path (no __restrict__ / non-coherent loads); only
 // the matrix is. scal[4] = iterations done.
+template <typename COL>
 __global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevice D, int max_it, unsigned int* bar) {
     __shared__ double scratch[kVecThreads / 32];
     unsigned int target = 0;
     const int stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
-    const std::int32_t* __restrict__ ec = D.ell_col;
+    const COL* __restrict__ ec = ell_cols<COL>(D);
     const double* __restrict__ ev = D.ell_val;
     double* q = D.q;
     double* x = D.x;
@@ -292,14 +307,16 @@ __global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevic
             for (; j + 3 < len; j += 4) {
                 const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
                 const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
-                const double x0 = p_at(ec[base + 32 * j]), x1 = p_at(ec[base + 32 * (j + 1)]);
-                const double x2 = p_at(ec[base + 32 * (j + 2)]), x3 = p_at(ec[base + 32 * (j + 3)]);
+                const double x0 = p_at(ell_column(ec, base + 32 * j, i));
+                const double x1 = p_at(ell_column(ec, base + 32 * (j + 1), i));
+                const double x2 = p_at(ell_column(ec, base + 32 * (j + 2), i));
+                const double x3 = p_at(ell_column(ec, base + 32 * (j + 3), i));
                 y += v0 * x0;
                 y += v1 * x1;
                 y += v2 * x2;
                 y += v3 * x3;
             }
-            for (; j < len; ++j) y += ev[base + 32 * j] * p_at(ec[base + 32 * j]);
+            for (; j < len; ++j) y += ev[base + 32 * j] * p_at(ell_column(ec, base + 32 * j, i));
             const double pi = p_at(i);
             pn[i] = pi;
             q[i] = y;
@@ -373,6 +390,7 @@ __device__ __forceinline__ void grid_sync_mono(unsigned long long* ctr) {
 // grid's last CTA, which also advances the iteration counter). Grid barriers between the phases
 // instead of kernel boundaries; every expression and fixed-order partial sum is the per-kernel
 // loop's, so the iterates are bitwise identical to it.
+template <typename COL>
 __global__ void __launch_bounds__(kVecThreads, 4) pcg_step_kernel(const PcgDevice D, unsigned long long* bar) {
     __shared__ double scratch[kVecThreads / 32];
     const int km1 = *D.iter, k = km1 + 1;
@@ -396,7 +414,7 @@ __global__ void __launch_bounds__(kVecThreads, 4) pcg_step_kernel(const PcgDevic
         // phase 1: q = A p (sliced ELL, CSR order), p.q
         const double* p = D.p;
         double* q = D.q;
-        const std::int32_t* __restrict__ ec = D.ell_col;
+        const COL* __restrict__ ec = ell_cols<COL>(D);
         const double* __restrict__ ev = D.ell_val;
         double acc = 0.0;
         for (int i = i0; i < D.n; i += stride) {
@@ -407,14 +425,16 @@ __global__ void __launch_bounds__(kVecThreads, 4) pcg_step_kernel(const PcgDevic
             for (; j + 3 < len; j += 4) {
                 const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
                 const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
-                const double x0 = p[ec[base + 32 * j]], x1 = p[ec[base + 32 * (j + 1)]];
-                const double x2 = p[ec[base + 32 * (j + 2)]], x3 = p[ec[base + 32 * (j + 3)]];
+                const double x0 = p[ell_column(ec, base + 32 * j, i)];
+                const double x1 = p[ell_column(ec, base + 32 * (j + 1), i)];
+                const double x2 = p[ell_column(ec, base + 32 * (j + 2), i)];
+                const double x3 = p[ell_column(ec, base + 32 * (j + 3), i)];
                 y += v0 * x0;
                 y += v1 * x1;
                 y += v2 * x2;
                 y += v3 * x3;
             }
-            for (; j < len; ++j) y += ev[base + 32 * j] * p[ec[base + 32 * j]];
+            for (; j < len; ++j) y += ev[base + 32 * j] * p[ell_column(ec, base + 32 * j, i)];
             q[i] = y;
             if (i < D.n_dot) acc = fma(p[i], y, acc);
         }
@@ -481,14 +501,20 @@ __global__ void __launch_bounds__(kVecThreads) csr_to_ell_kernel(int n, const st
                                                                 const std::int32_t* __restrict__ col,
                                                                 const double* __restrict__ val,
                                                                 const std::int64_t* __restrict__ off,
-                                                                std::int32_t* ell_col, double* ell_val) {
+                                                                std::int32_t* ell_col, double* ell_val,
+                                                                std::int16_t* d16, int* overflow) {
+    bool over = false;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const std::int64_t base = off[i >> 5] + (i & 31);
         for (int e = ptr[i], j = 0; e < ptr[i + 1]; ++e, ++j) {
             ell_col[base + 32 * j] = col[e];
             ell_val[base + 32 * j] = val[e];
+            const int d = col[e] - i;
+            over |= d < -32768 || d > 32767;
+            if (d16) d16[base + 32 * j] = static_cast<std::int16_t>(d);
         }
     }
+    if (over && overflow) atomicOr(overflow, 1);
 }
 
 int vec_grid(int n) { return std::max(1, std::min((n + kVecThreads - 1) / kVecThreads, 148 * 4)); }
@@ -504,7 +530,8 @@ void pcg_finalize(const PcgDevice& D, const double* part, int slot, bool take_sq
     BDDC_LAUNCHED();
 }
 void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
-    launch_pdl(spmv_dot_kernel, D.grid, kVecThreads, 0, s, D);
+    if (D.ell_d16) launch_pdl(spmv_dot_kernel<std::int16_t>, D.grid, kVecThreads, 0, s, D);
+    else launch_pdl(spmv_dot_kernel<std::int32_t>, D.grid, kVecThreads, 0, s, D);
     BDDC_LAUNCHED();
 }
 void pcg_dir_spmv(const PcgDevice& D, cudaStream_t s) {
@@ -546,16 +573,17 @@ void device_first_nonfinite(int n, const double* x, int* dev_result, cudaStream_
 
 int pcg_grid_for(int n) { return vec_grid(n); }
 void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
-                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s) {
+                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, std::int16_t* d16,
+                              int* overflow, cudaStream_t s) {
     if (n <= 0) return;
-    csr_to_ell_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, off, ell_col, ell_val);
+    csr_to_ell_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(n, ptr, col, val, off, ell_col, ell_val, d16, overflow);
     BDDC_LAUNCHED();
 }
 bool pcg_step_fits(int grid) {
     int dev = 0, sms = 0, per_sm = 0;
     BDDC_CUDA(cudaGetDevice(&dev));
     BDDC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_step_kernel, kVecThreads, 0));
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_step_kernel<std::int32_t>, kVecThreads, 0));
     return grid <= per_sm * sms;
 }
 void pcg_step(const PcgDevice& D, unsigned long long* barrier, cudaStream_t s) {
@@ -568,14 +596,15 @@ void pcg_step(const PcgDevice& D, unsigned long long* barrier, cudaStream_t s) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BDDC_CUDA(cudaLaunchKernelEx(&cfg, pcg_step_kernel, D, barrier));
+    BDDC_CUDA(D.ell_d16 ? cudaLaunchKernelEx(&cfg, pcg_step_kernel<std::int16_t>, D, barrier)
+                             : cudaLaunchKernelEx(&cfg, pcg_step_kernel<std::int32_t>, D, barrier));
     BDDC_LAUNCHED();
 }
 bool pcg_plain_loop_fits(int grid) {
     int dev = 0, sms = 0, per_sm = 0;
     BDDC_CUDA(cudaGetDevice(&dev));
     BDDC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plain_cg_kernel, kVecThreads, 0));
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plain_cg_kernel<std::int32_t>, kVecThreads, 0));
     return grid <= per_sm * sms;
 }
 void pcg_plain_loop(const PcgDevice& D, int max_iterations, unsigned int* barrier, cudaStream_t s) {
@@ -589,7 +618,8 @@ void pcg_plain_loop(const PcgDevice& D, int max_iterations, unsigned int* barrie
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BDDC_CUDA(cudaLaunchKernelEx(&cfg, plain_cg_kernel, D, max_iterations, barrier));
+    BDDC_CUDA(D.ell_d16 ? cudaLaunchKernelEx(&cfg, plain_cg_kernel<std::int16_t>, D, max_iterations, barrier)
+                             : cudaLaunchKernelEx(&cfg, plain_cg_kernel<std::int32_t>, D, max_iterations, barrier));
     BDDC_LAUNCHED();
 }
 

@@ -21,6 +21,9 @@ struct PcgDevice {
     const std::int64_t* ell_off;
     const std::uint16_t* ell_len;
     const std::int32_t* ell_col;
+    // the same columns as 16-bit offsets from the row (column = row + offset) when every entry's
+    // offset fits (2D stencils: about one grid line); null: ell_col
+    const std::int16_t* ell_d16;
     const double* ell_val;
     double* x;
     double* r;
@@ -84,8 +87,10 @@ void device_axpby(int n, double a, const double* x, double b, const double* y, d
                   cudaStream_t s);  // out = a x + b y
 int pcg_grid_for(int n);
 // sliced ELL from CSR (entry j of row i at off[i / 32] + 32 j + i % 32, CSR order kept)
+// (and, with d16, the column offsets col - row as int16; *overflow set when one does not fit)
 void device_csr_to_sliced_ell(int n, const std::int32_t* ptr, const std::int32_t* col, const double* val,
-                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, cudaStream_t s);
+                              const std::int64_t* off, std::int32_t* ell_col, double* ell_val, std::int16_t* d16,
+                              int* overflow, cudaStream_t s);
 // plain CG (no preconditioner, one GPU) as one cooperative launch over D.grid CTAs: iterations
 // 1..max_iterations from rho[0] and p = r; scal[1..4] = rel, converged, error code, iterations
 // one BDDC-PCG iteration's xpay + SpMV + update (+ fused check) on one GPU as one cooperative

@@ -47,6 +47,7 @@ CASES = [
     {"BDDC_MAX_CHAIN": "0"},        # forward levels coloured into phases only
     {"BDDC_QUAD_TILES": "0"},       # pairs only (no 8-lane quads)
     {"BDDC_SETUP_SCRATCH_CACHE": "0"},  # setup scratch freed after every setup
+    {"BDDC_ELL16": "0"},            # 32-bit ELL columns instead of 16-bit row offsets
 ]
 
 
@@ -136,13 +137,15 @@ def test_plain_cg_one_launch_matches_kernel_loop(gpu):
     # bitwise identical, at convergence and at the iteration cap, and "not SPD" is raised alike
     env = {k: v for k, v in os.environ.items() if not k.startswith("BDDC_")}
     res = []
-    for extra in ({}, {"BDDC_PLAIN_LOOP": "0"}):
+    # (and 16-bit ELL column offsets give the 32-bit columns' iterates bit for bit)
+    for extra in ({}, {"BDDC_PLAIN_LOOP": "0"}, {"BDDC_ELL16": "0"}):
         r = subprocess.run([sys.executable, "-c", PLAIN_SCRIPT], env={**env, **extra}, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    one, loop = res
+    one, loop, col32 = res
     assert one == loop
+    assert one == col32
     assert one["c2/10000"][0] == 1649 and one["c2/10000"][1]
     assert one["c2/7"][0] == 7 and not one["c2/7"][1] and len(one["c2/7"][2]) == 8
     assert "matrix not SPD" in one["neg"]
