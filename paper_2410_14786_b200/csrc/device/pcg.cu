@@ -114,6 +114,7 @@ __device__ __forceinline__ void check_scalar(const PcgDevice& D, int it, double 
 // xpay_kernel, so the iterates are bitwise those of the unfused loop); the distributed halo of
 // z comes from the LL buffer. The iteration counter is advanced by the grid's last CTA, after
 // every CTA has read it.
+template <typename COL>
 __global__ void __launch_bounds__(kVecThreads) dir_spmv_kernel(const PcgDevice D) {
     __shared__ double scratch[kVecThreads / 32];
     pdl_trigger();
@@ -135,9 +136,27 @@ __global__ void __launch_bounds__(kVecThreads) dir_spmv_kernel(const PcgDevice D
         return km1 > 0 ? zj + beta * po[j] : zj;
     };
     double acc = 0.0;
+    const COL* __restrict__ ec = ell_cols<COL>(D);
+    const double* __restrict__ ev = D.ell_val;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+        // sliced ELL (CSR order), four entries' loads in flight
+        const std::int64_t base = D.ell_off[i >> 5] + (i & 31);
+        const int len = D.ell_len[i];
         double y = 0.0;
-        for (int e = D.A_ptr[i]; e < D.A_ptr[i + 1]; ++e) y += D.A_val[e] * p_at(D.A_col[e]);
+        int j = 0;
+        for (; j + 3 < len; j += 4) {
+            const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
+            const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
+            const double x0 = p_at(ell_column(ec, base + 32 * j, i));
+            const double x1 = p_at(ell_column(ec, base + 32 * (j + 1), i));
+            const double x2 = p_at(ell_column(ec, base + 32 * (j + 2), i));
+            const double x3 = p_at(ell_column(ec, base + 32 * (j + 3), i));
+            y += v0 * x0;
+            y += v1 * x1;
+            y += v2 * x2;
+            y += v3 * x3;
+        }
+        for (; j < len; ++j) y += ev[base + 32 * j] * p_at(ell_column(ec, base + 32 * j, i));
         const double pi = p_at(i);
         pn[i] = pi;
         D.q[i] = y;
@@ -535,7 +554,8 @@ void pcg_spmv_dot(const PcgDevice& D, cudaStream_t s) {
     BDDC_LAUNCHED();
 }
 void pcg_dir_spmv(const PcgDevice& D, cudaStream_t s) {
-    launch_pdl(dir_spmv_kernel, D.grid, kVecThreads, 0, s, D);
+    if (D.ell_d16) launch_pdl(dir_spmv_kernel<std::int16_t>, D.grid, kVecThreads, 0, s, D);
+    else launch_pdl(dir_spmv_kernel<std::int32_t>, D.grid, kVecThreads, 0, s, D);
     BDDC_LAUNCHED();
 }
 void pcg_update(const PcgDevice& D, int it, cudaStream_t s) {
