@@ -332,6 +332,15 @@ __global__ void __launch_bounds__(kVecThreads, 4) plain_cg_kernel(const PcgDevic
             const int len = D.ell_len[i];
             double y = 0.0;
             int j = 0;
+            for (; j + 7 < len; j += 8) {  // eight entries' loads in flight, CSR-order sum
+                double v[8], x[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) v[t] = ev[base + 32 * (j + t)];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) x[t] = p_at(ell_column(ec, base + 32 * (j + t), i));
+#pragma unroll
+                for (int t = 0; t < 8; ++t) y += v[t] * x[t];
+            }
             for (; j + 3 < len; j += 4) {
                 const double v0 = ev[base + 32 * j], v1 = ev[base + 32 * (j + 1)];
                 const double v2 = ev[base + 32 * (j + 2)], v3 = ev[base + 32 * (j + 3)];
